@@ -1,0 +1,205 @@
+/*
+ * dqn_b200.h -- C ABI of libdqn_b200.so, the B200 (sm_100a) implementation of
+ * the CytonRL / deepq learner hot path.
+ *
+ * The reference (/root/reference/pkg/src/deepq) has no FFI: its boundary is
+ * the duck-typed Python API that ``learn_step`` consumes.  Every entry point
+ * below replaces one reference method and names it (file:line).  The Python
+ * mirror in paper_1804_05834_b200/ binds these with ctypes (INTEGRATION.md
+ * shows the binding a deepq maintainer would add).
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers on the current device unless the name
+ *    says ``host``.  Scalars are passed by value.  The caller owns every
+ *    buffer; the library never allocates or frees caller memory.
+ *  - ``stream`` is a cudaStream_t; all work is asynchronous on it, nothing
+ *    synchronises the device, and every call is legal inside CUDA-graph
+ *    capture.
+ *  - Return value: 0 (DQN_OK) or a dqn_status; ``dqn_last_error()`` holds a
+ *    thread-local message.  Faults only detectable on the device (an index out
+ *    of range, zero total priority, a non-finite gradient) are OR-ed into a
+ *    caller-provided int32 ``flags`` word (DQN_FLAG_*); the host reads it
+ *    lazily and raises the reference's exception (errors.py:4-41).
+ */
+#ifndef DQN_B200_H
+#define DQN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DQN_OK = 0,
+  DQN_ERR_INVALID_ARG = 1,   /* ValueError */
+  DQN_ERR_GEOMETRY = 2,      /* GeometryError (layers.py:182-190) */
+  DQN_ERR_INDEX = 3,         /* IndexError (replay.py:157,239) */
+  DQN_ERR_EMPTY = 4,         /* ValueError: empty replay (replay.py:120,219) */
+  DQN_ERR_ZERO_TOTAL = 5,    /* ValueError: zero total (replay.py:171,222) */
+  DQN_ERR_NONFINITE = 6,     /* NonFiniteError (network.py:102, optim.py:40) */
+  DQN_ERR_CUDA = 7,
+  DQN_ERR_UNSUPPORTED = 8    /* ConfigError */
+} dqn_status;
+
+/* device flag bits (int32 word written by kernels, read lazily by the host) */
+#define DQN_FLAG_INDEX          0x1  /* update_priorities index out of range */
+#define DQN_FLAG_ZERO_TOTAL     0x2  /* sample from a zero-mass tree */
+#define DQN_FLAG_NONFINITE_GRAD 0x4  /* RmsProp.step finite scan failed: no update applied */
+#define DQN_FLAG_NONFINITE_OUT  0x8  /* network output non-finite */
+#define DQN_FLAG_BAD_PRIORITY   0x10 /* SumTree.set with negative / non-finite value */
+
+const char *dqn_last_error(void);
+int dqn_abi_version(void);
+/* 1 if this library was built with the tcgen05 (sm_100a UMMA) conv trunk */
+int dqn_has_tcgen05(void);
+/* kernels launched (or captured) through this library so far, all threads */
+int64_t dqn_launch_count(void);
+
+/* ------------------------------------------------------------------ replay */
+
+/* Synthetic frames: bytes = splitmix64(counter_base | (slot*words + w)),
+ * little-endian, for slots [slot0, slot0+nslots).  Test / bench input
+ * generator (no reference counterpart; mirrors synth.frames on the host). */
+int dqn_ring_fill_hash(void *stream, uint8_t *frames, int64_t slot0, int64_t nslots,
+                       int64_t slot_bytes, uint64_t counter_base);
+
+/* ReplayMemory._gather (replay.py:104-115): fancy-index gather of k slots.
+ * states/next_states are [capacity][slot_bytes] byte rings (u8 frames or raw
+ * float32 states).  Any output pointer may be NULL to skip it. */
+int dqn_ring_gather(void *stream, const uint8_t *states, const uint8_t *next_states,
+                    int64_t slot_bytes, const int64_t *actions, const double *rewards,
+                    const uint8_t *terminals, const int64_t *idx, int32_t k,
+                    uint8_t *out_states, uint8_t *out_next_states, int64_t *out_actions,
+                    double *out_rewards, uint8_t *out_terminals);
+
+/* PrioritizedReplay.sample (replay.py:215-229) + SumTree.find (167-181):
+ * stratified queries q_j = (j + u_j) * (total / k), clipped descent, P = leaf
+ * / total, w = (size * P)^-beta / max w.  ``beta`` and ``size`` (the ring's
+ * fill count) are device scalars so a captured graph follows them.  Bit-exact with the reference given u. */
+int dqn_tree_sample(void *stream, const double *nodes, int32_t depth, const int64_t *size,
+                    const double *u, int32_t k, const double *beta, int64_t *idx,
+                    double *prob, double *weight, int32_t *flags);
+
+/* SumTree.find alone (replay.py:167-181) for arbitrary query masses. */
+int dqn_tree_find(void *stream, const double *nodes, int32_t depth, const double *queries,
+                  int64_t n, int64_t *idx, int32_t *flags);
+
+/* PrioritizedReplay.update_priorities (replay.py:232-241): in batch order,
+ * leaf_i = (|td_i| + eps)^alpha (last write wins), ancestors recomputed from
+ * children; *max_p = max(*max_p, max(|td|+eps)).  An index outside [0,*size)
+ * stops the update at that position (leaves before it stay written, as in the
+ * reference), sets DQN_FLAG_INDEX and leaves max_p untouched. */
+int dqn_tree_update(void *stream, double *nodes, int32_t depth, const int64_t *size,
+                    const int64_t *idx, const double *td, int32_t k, double alpha,
+                    double eps, double *max_p, int32_t *flags);
+
+/* PrioritizedReplay.store's tree half (replay.py:207-210) for n consecutive
+ * ring slots starting at ``slot`` (wrapping at capacity): leaf = max_p^alpha. */
+int dqn_tree_store(void *stream, double *nodes, int32_t depth, int64_t capacity,
+                   int64_t slot, int64_t n, const double *max_p, double alpha);
+
+/* SumTree.set for k leaves (replay.py:155-165), batch order, last wins. */
+int dqn_tree_set(void *stream, double *nodes, int32_t depth, int64_t capacity,
+                 const int64_t *idx, const double *values, int32_t k, int32_t *flags);
+
+/* Recompute every internal node bottom-up (bulk load). */
+int dqn_tree_rebuild(void *stream, double *nodes, int32_t depth);
+
+/* ----------------------------------------------------------------- network */
+
+#define DQN_MAX_LAYERS 8
+
+typedef enum { DQN_LAYER_CONV = 0, DQN_LAYER_LINEAR = 1, DQN_LAYER_DUELING = 2 } dqn_layer_kind;
+
+/* One parameterised layer (layers.py:115-330) with an optional fused ReLU
+ * (layers.py:99-112).  Linear layers use in_h = in_w = 1, in_c = features.
+ * Offsets are in floats into the flat parameter (and gradient) buffers, laid
+ * out in the reference registry order (network.py:74-84). */
+typedef struct {
+  int32_t kind, relu;
+  int32_t in_h, in_w, in_c;
+  int32_t out_h, out_w, out_c;
+  int32_t fh, fw, sh, sw;
+  int64_t w_off, b_off;    /* conv/linear weight+bias; dueling: value branch */
+  int64_t w2_off, b2_off;  /* dueling: advantage branch */
+} dqn_layer_desc;
+
+typedef struct {
+  int32_t n_layers;
+  int32_t input_u8;        /* 1: input bytes x = f32(u8)/255 (envs.py:300-311); 0: float32 */
+  int32_t algo;            /* 0: auto (tcgen05 trunk when the geometry has a kernel), 1: SIMT only */
+  int32_t reserved;
+  dqn_layer_desc layer[DQN_MAX_LAYERS];
+} dqn_net_desc;
+
+/* Activations for one batch extent (layers.py:65-77 bindings).  act[l] is
+ * layer l's output after its fused ReLU; dact[l] is the gradient w.r.t. layer
+ * l's pre-activation output.  ``scratch`` holds split-K partial sums; size it
+ * with dqn_net_scratch_floats. */
+typedef struct {
+  int32_t batch, pad_;
+  const void *x;
+  float *act[DQN_MAX_LAYERS];
+  float *dact[DQN_MAX_LAYERS];
+  float *dx;               /* input gradient (NULL = skip, as the learner does) */
+  float *scratch;
+  int64_t scratch_floats;
+} dqn_binding;
+
+int64_t dqn_net_scratch_floats(const dqn_net_desc *net, int32_t batch);
+
+/* Network.forward (network.py:90-104): all layers front to back. */
+int dqn_net_forward(void *stream, const dqn_net_desc *net, const float *params,
+                    const dqn_binding *bind, int32_t *flags);
+
+/* Network.backward (network.py:106-117): dq is the [batch][n_actions] output
+ * gradient; fills dact[] (and dx when non-NULL). */
+int dqn_net_backward(void *stream, const dqn_net_desc *net, const float *params,
+                     const dqn_binding *bind, const float *dq);
+
+/* Network.calculate_gradient (network.py:119-126): grads += dW, db for every
+ * layer (deterministic fixed-order reductions, no float atomics). */
+int dqn_net_wgrad(void *stream, const dqn_net_desc *net, float *grads,
+                  const dqn_binding *bind);
+
+/* One phase of one layer (0 forward, 1 backward to the layer's input,
+ * 2 wgrad) -- the unit the bench times for its roofline line. */
+int dqn_net_layer(void *stream, const dqn_net_desc *net, const float *params, float *grads,
+                  const dqn_binding *bind, int32_t layer, int32_t phase, int32_t *flags);
+
+/* ---------------------------------------------------------- loss / optim */
+
+#define DQN_TD_DOUBLE 0x1
+#define DQN_TD_HUBER 0x2
+#define DQN_TD_REWARD_CLIP 0x4
+
+/* compute_target_double / compute_target_dqn (agent.py:58-73) and the loss
+ * block of learn_step (agent.py:110-124): argmax (first max), y = r + (t ? 0 :
+ * gamma * Q_tg), delta = y - f64(Q_on(s,a)) in fp64, squared or Huber loss,
+ * dq = f32(-w * delta) at (j, a_j) and 0 elsewhere.  q_next_online may be NULL
+ * when !(flags & DQN_TD_DOUBLE).  stats[0] = sum|delta|, stats[1] = sum loss. */
+int dqn_td_loss(void *stream, const float *q_online, const float *q_next_online,
+                const float *q_next_target, const int64_t *actions, const double *rewards,
+                const uint8_t *terminals, const double *weights, int32_t batch,
+                int32_t n_actions, double gamma, int32_t flags, double *targets,
+                double *td, double *losses, float *dq, double *stats);
+
+/* RmsProp.step (optim.py:36-47) over a flat buffer: finite scan of all grads,
+ * then (only if all finite) acc = acc*rho; acc += (1-rho)*g*g;
+ * w -= (lr*g)/(sqrt(acc)+eps); g = 0 -- fp32, no FMA, bit-exact given g.
+ * A non-finite gradient sets DQN_FLAG_NONFINITE_GRAD and applies nothing. */
+int dqn_rmsprop_step(void *stream, float *w, float *g, float *acc, int64_t n,
+                     float lr, float rho, float one_minus_rho, float eps, int32_t *flags);
+
+/* clip_gradients (optim.py:61-75): fp64 global L2 norm into *norm_out; if
+ * norm > max_norm, g *= f32(max_norm / norm). */
+int dqn_clip_gradients(void *stream, float *g, int64_t n, double max_norm, double *norm_out);
+
+/* sync_target (optim.py:78-89): bitwise copy of the flat parameter buffer. */
+int dqn_sync_target(void *stream, float *dst, const float *src, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DQN_B200_H */

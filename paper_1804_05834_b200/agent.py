@@ -1,0 +1,254 @@
+"""The learner update on the GPU: ``learn_step`` and the target helpers
+(deepq/agent.py:58-132) with the reference's signatures.
+
+``learn_step(online, target, memory, optimizer, config, step, rng)`` takes the
+replay draws from the caller's ``rng`` on the host exactly as the reference
+does (``rng.random(k)`` for PER, ``rng.integers(0, size, k)`` for uniform),
+copies them to HBM, runs the whole update on the device and returns a
+``TdResult`` of host numpy arrays.  Per (networks, memory, optimizer, config)
+tuple a ``_StepPlan`` owns the device buffers; after the first (eager) call
+the update is captured into one CUDA graph and replayed, so a step costs one
+graph launch plus two small copies (draws in, TdResult out).
+
+Device pipeline of one update:
+  dqn_tree_sample -> dqn_ring_gather (s and s' into one [2k] batch)
+  -> online forward on [s; s'] -> target forward on s' -> dqn_td_loss
+  (argmax, bootstrap, delta, loss, output grad written straight into the
+  online net's y.grad) -> backward (conv1 dX skipped) -> wgrad
+  -> [clip] -> dqn_tree_update -> dqn_rmsprop_step.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import NonFiniteError
+from .network import _FORWARD, _GRAD, Network
+from .optim import RmsProp, clip_gradients, sync_target  # noqa: F401  (re-export)
+from .replay import PrioritizedReplay, ReplayMemory, SampleBatch
+
+
+@dataclass
+class TdResult:
+    targets: np.ndarray
+    td_errors: np.ndarray
+    losses: np.ndarray
+
+    @property
+    def mean_abs_td(self) -> float:
+        return float(np.mean(np.abs(self.td_errors)))
+
+    @property
+    def mean_loss(self) -> float:
+        return float(np.mean(self.losses))
+
+
+def _td_flags(config) -> int:
+    f = 0
+    if getattr(config, "double", True):
+        f |= _lib.TD_DOUBLE
+    if getattr(config, "huber", False):
+        f |= _lib.TD_HUBER
+    if getattr(config, "reward_clip", False):
+        f |= _lib.TD_REWARD_CLIP
+    return f
+
+
+def _targets_only(batch: SampleBatch, online, target, gamma: float, double: bool):
+    torch = _lib.require_cuda()
+    k = len(batch)
+    q_tg = target.forward(batch.next_states).contiguous().clone()
+    if double:
+        q_on2 = online.forward(batch.next_states).contiguous().clone()
+    else:
+        q_on2 = q_tg
+    out = [torch.empty(k, dtype=torch.float64, device="cuda") for _ in range(3)]
+    dq = torch.empty_like(q_tg)
+    acts = torch.zeros(k, dtype=torch.int64, device="cuda")
+    r = batch.rewards.to(device="cuda", dtype=torch.float64).contiguous()
+    t = batch.terminals.to(device="cuda", dtype=torch.bool).contiguous()
+    w = torch.ones(k, dtype=torch.float64, device="cuda")
+    _lib.call("dqn_td_loss", _lib.stream_ptr(), q_on2.data_ptr(), q_on2.data_ptr(),
+              q_tg.data_ptr(), acts.data_ptr(), r.data_ptr(), t.data_ptr(), w.data_ptr(), k,
+              q_tg.shape[1], float(gamma), _lib.TD_DOUBLE if double else 0,
+              out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr(), dq.data_ptr(), None)
+    return out[0]
+
+
+def compute_target_dqn(batch: SampleBatch, target_net, gamma: float):
+    """``y = r + gamma * max_a Q_target(s', a)``, ``y = r`` on terminals (agent.py:58-63)."""
+    return _targets_only(batch, None, target_net, gamma, False)
+
+
+def compute_target_double(batch: SampleBatch, online_net, target_net, gamma: float):
+    """Online net picks a* (first max), target net evaluates it (agent.py:66-73)."""
+    return _targets_only(batch, online_net, target_net, gamma, True)
+
+
+class _StepPlan:
+    """Device buffers (and, after warm-up, the CUDA graph) of one learner
+    configuration."""
+
+    def __init__(self, online: Network, target: Network, memory, optimizer: RmsProp, config):
+        torch = _lib.require_cuda()
+        self.online, self.target, self.memory, self.opt = online, target, memory, optimizer
+        self.per = isinstance(memory, PrioritizedReplay)
+        self.ring: ReplayMemory = memory.memory if self.per else memory
+        self.k = k = int(config.batch_size)
+        self.double = bool(getattr(config, "double", True))
+        self.gamma = float(config.gamma)
+        self.flags_td = _td_flags(config)
+        self.grad_clip = float(getattr(config, "grad_clip", 0.0))
+        self.nA = online.output_shape[-1]
+        dev = "cuda"
+        ring = self.ring
+        self.x = torch.empty((2 * k,) + ring.state_shape, dtype=ring.states.dtype, device=dev)
+        self.a = torch.empty(k, dtype=torch.int64, device=dev)
+        self.r = torch.empty(k, dtype=torch.float64, device=dev)
+        self.t = torch.empty(k, dtype=torch.bool, device=dev)
+        self.idx = torch.empty(k, dtype=torch.int64, device=dev)
+        self.prob = torch.empty(k, dtype=torch.float64, device=dev)
+        self.w = torch.ones(k, dtype=torch.float64, device=dev)
+        # inputs: u[k] + beta (PER) | indices[k] (uniform); pinned staging
+        self.d_in = torch.zeros(k + 1, dtype=torch.float64, device=dev)
+        self.h_in = torch.zeros(k + 1, dtype=torch.float64).pin_memory()
+        self.h_idx = torch.zeros(k, dtype=torch.int64).pin_memory()
+        # outputs: targets | td | losses | stats(2)  + flags
+        self.d_out = torch.zeros(3 * k + 2, dtype=torch.float64, device=dev)
+        self.h_out = torch.zeros(3 * k + 2, dtype=torch.float64).pin_memory()
+        self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.h_flags = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.norm = torch.zeros(1, dtype=torch.float64, device=dev)
+        on_rows = 2 * k if self.double else k
+        self.on_bind = online.binding(on_rows)
+        self.on_view = online.prefix_binding(self.on_bind, k) if self.double else self.on_bind
+        self.tg_bind = target.binding(k)
+        self.graph = None
+        self.calls = 0
+        self.h2d_bytes = (k + 1) * 8 if self.per else k * 8
+        self.d2h_bytes = (3 * k + 2) * 8 + 4
+
+    # -- the device pipeline ----------------------------------------------
+    def enqueue(self, io: bool = True) -> None:
+        """Enqueue one update; ``io`` adds the pinned host copies of the
+        draws (in) and TdResult + flags (out)."""
+        torch = _lib.require_cuda()
+        st = _lib.stream_ptr()
+        k, ring = self.k, self.ring
+        if self.per:
+            self.d_in.copy_(self.h_in, non_blocking=True)
+            self.memory.sample_indices(self.d_in[:k], k, self.d_in[k:], self.idx, self.prob,
+                                       self.w, self.flags)
+        else:
+            self.idx.copy_(self.h_idx, non_blocking=True)
+        ring.gather_into(self.idx, k, self.x[:k], self.x[k:], self.a, self.r, self.t)
+        on, tg = self.online, self.target
+        if self.double:
+            on.forward_into(self.x, self.on_bind)
+        else:
+            on.forward_into(self.x[:k], self.on_bind)
+        tg.forward_into(self.x[k:], self.tg_bind)
+        nA = self.nA
+        q_on = self.on_bind.act[-1]
+        out = self.d_out
+        _lib.call("dqn_td_loss", st, q_on.data_ptr(),
+                  q_on[k * nA:].data_ptr() if self.double else None,
+                  self.tg_bind.act[-1].data_ptr(), self.a.data_ptr(), self.r.data_ptr(),
+                  self.t.data_ptr(), self.w.data_ptr(), k, nA, self.gamma, self.flags_td,
+                  out[:k].data_ptr(), out[k:2 * k].data_ptr(), out[2 * k:3 * k].data_ptr(),
+                  self.on_view.dact[-1].data_ptr(), out[3 * k:].data_ptr())
+        self.on_view.x = self.x[:k]
+        self.on_view.struct.x = self.x.data_ptr()
+        on.backward_from(self.on_view, need_input_grad=False)
+        on.wgrad_into(self.on_view)
+        if self.grad_clip > 0.0:
+            _lib.call("dqn_clip_gradients", st, on.flat_grads.data_ptr(), on.n_flat,
+                      self.grad_clip, self.norm.data_ptr())
+        if self.per:
+            self.memory.update_priorities_dev(self.idx, out[k:2 * k], k, self.flags)
+        self.opt.enqueue_step(self.flags)
+        if io:
+            self.h_out.copy_(out, non_blocking=True)
+            self.h_flags.copy_(self.flags, non_blocking=True)
+        del torch
+
+    def run(self, use_graph: bool) -> None:
+        torch = _lib.require_cuda()
+        if use_graph and self.graph is None and self.calls >= 1:
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    self.enqueue()
+            torch.cuda.current_stream().wait_stream(s)
+            self.graph = g
+        if use_graph and self.graph is not None:
+            self.graph.replay()
+        else:
+            self.enqueue()
+        self.calls += 1
+
+
+_PLANS: dict = {}
+USE_GRAPH = os.environ.get("DQN_B200_GRAPH", "1") != "0"
+
+
+def _plan_for(online, target, memory, optimizer, config) -> _StepPlan:
+    key = (id(online), id(target), id(memory), id(optimizer), int(config.batch_size),
+           bool(getattr(config, "double", True)), float(config.gamma), _td_flags(config),
+           float(getattr(config, "grad_clip", 0.0)))
+    p = _PLANS.get(key)
+    if p is None or p.online is not online or p.memory is not memory:
+        p = _StepPlan(online, target, memory, optimizer, config)
+        _PLANS[key] = p
+    return p
+
+
+def learn_step_enqueue(plan: _StepPlan, step: int, rng: np.random.Generator) -> None:
+    """Stage this step's draws and launch the update without waiting."""
+    k = plan.k
+    if plan.per:
+        hin = plan.h_in.numpy()
+        hin[:k] = rng.random(k)
+        hin[k] = plan.memory.beta(step)
+    else:
+        plan.h_idx.numpy()[:] = rng.integers(0, plan.ring.size, size=k)
+    plan.run(USE_GRAPH)
+
+
+def learn_step_collect(plan: _StepPlan) -> TdResult:
+    torch = _lib.require_cuda()
+    torch.cuda.current_stream().synchronize()
+    k = plan.k
+    f = int(plan.h_flags.numpy()[0])
+    if f:
+        plan.flags.zero_()
+        if f & _lib.FLAG_ZERO_TOTAL:
+            raise ValueError("zero total priority; nothing can be sampled")
+        if f & _lib.FLAG_NONFINITE_OUT:
+            raise NonFiniteError("non-finite network output")
+        if f & _lib.FLAG_INDEX:
+            raise IndexError("transition index out of range")
+        if f & _lib.FLAG_BAD_PRIORITY:
+            raise ValueError("priority must be finite and >= 0")
+        if f & _lib.FLAG_NONFINITE_GRAD:
+            raise NonFiniteError("non-finite gradient; step aborted")
+    h = plan.h_out.numpy()
+    plan.online._set_current(plan.on_view, _GRAD)
+    plan.target._set_current(plan.tg_bind, _FORWARD)
+    return TdResult(targets=h[:k].copy(), td_errors=h[k:2 * k].copy(), losses=h[2 * k:3 * k].copy())
+
+
+def learn_step(online: Network, target: Network, memory, optimizer: RmsProp, config, step: int,
+               rng: np.random.Generator) -> TdResult:
+    """One optimisation step (agent.py:91-132) on the GPU."""
+    if memory.size == 0:
+        raise ValueError("cannot sample from an empty replay memory")
+    plan = _plan_for(online, target, memory, optimizer, config)
+    learn_step_enqueue(plan, step, rng)
+    return learn_step_collect(plan)

@@ -1,0 +1,52 @@
+// Shared helpers for libdqn_b200: error plumbing and exact-arithmetic
+// intrinsics.  Parity-critical code uses explicit __d*_rn / __f*_rn so that
+// nvcc never contracts a mul+add into an FMA the reference did not do.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+
+#include "../../include/dqn_b200.h"
+
+namespace dqn {
+
+void set_error(const char *fmt, ...);
+void note_launch();   // counts kernel launches issued by the library (dqn_launch_count)
+
+inline int cuda_status(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return DQN_OK;
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return DQN_ERR_CUDA;
+}
+
+// After a launch: report configuration errors without synchronising.
+inline int launch_status(const char *what) {
+  return cuda_status(cudaGetLastError(), what);
+}
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+__device__ __forceinline__ void raise_flag(int32_t *flags, int32_t bit) {
+  if (flags) atomicOr(flags, bit);
+}
+
+constexpr int kNumSMs = 148;
+
+}  // namespace dqn
+
+#define DQN_CHECK_ARG(cond, ...)              \
+  do {                                        \
+    if (!(cond)) {                            \
+      dqn::set_error(__VA_ARGS__);            \
+      return DQN_ERR_INVALID_ARG;             \
+    }                                         \
+  } while (0)
+
+#define DQN_LAUNCH_CHECK(what)                 \
+  do {                                         \
+    int _st = dqn::launch_status(what);        \
+    if (_st != DQN_OK) return _st;             \
+    dqn::note_launch();                        \
+  } while (0)

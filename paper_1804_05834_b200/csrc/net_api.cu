@@ -1,0 +1,132 @@
+// C-ABI entry points of the network phases (network.py:90-126).  Layers are
+// dispatched to the tcgen05 trunk kernels when one exists for the geometry
+// (trunk_tc.cu), otherwise to the generic SIMT kernels (net_simt.cu).
+#include "common.cuh"
+
+#include <string.h>
+
+#include <atomic>
+
+namespace dqn {
+
+int simt_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
+                       const dqn_binding *b, int32_t *flags);
+int simt_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
+                        const dqn_binding *b);
+int simt_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
+                     const dqn_binding *b);
+int64_t simt_scratch_floats(const dqn_net_desc *net, int batch);
+int simt_validate(const dqn_net_desc *net);
+
+namespace {
+thread_local char g_err[512] = "";
+std::atomic<long long> g_launches{0};
+}
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+}  // namespace dqn
+
+using namespace dqn;
+
+extern "C" const char *dqn_last_error(void) { return g_err; }
+extern "C" int dqn_abi_version(void) { return 1; }
+extern "C" int dqn_has_tcgen05(void) { return 0; }
+extern "C" int64_t dqn_launch_count(void) { return g_launches.load(); }
+
+extern "C" int64_t dqn_net_scratch_floats(const dqn_net_desc *net, int32_t batch) {
+  if (simt_validate(net) != DQN_OK || batch < 1) return -1;
+  return simt_scratch_floats(net, batch);
+}
+
+static int check_binding(const dqn_net_desc *net, const dqn_binding *b) {
+  int st = simt_validate(net);
+  if (st) return st;
+  if (!b || b->batch < 1 || !b->x) {
+    set_error("binding: batch/input missing");
+    return DQN_ERR_INVALID_ARG;
+  }
+  if (b->scratch_floats < simt_scratch_floats(net, b->batch)) {
+    set_error("binding: scratch too small (%lld < %lld floats)", (long long)b->scratch_floats,
+              (long long)simt_scratch_floats(net, b->batch));
+    return DQN_ERR_INVALID_ARG;
+  }
+  for (int l = 0; l < net->n_layers; ++l)
+    if (!b->act[l]) {
+      set_error("binding: act[%d] missing", l);
+      return DQN_ERR_INVALID_ARG;
+    }
+  return DQN_OK;
+}
+
+extern "C" int dqn_net_forward(void *stream, const dqn_net_desc *net, const float *params,
+                               const dqn_binding *bind, int32_t *flags) {
+  int st = check_binding(net, bind);
+  if (st) return st;
+  for (int l = 0; l < net->n_layers; ++l) {
+    st = simt_layer_forward(as_stream(stream), net, l, params, bind, flags);
+    if (st) return st;
+  }
+  return DQN_OK;
+}
+
+extern "C" int dqn_net_backward(void *stream, const dqn_net_desc *net, const float *params,
+                                const dqn_binding *bind, const float *dq) {
+  int st = check_binding(net, bind);
+  if (st) return st;
+  const int L = net->n_layers;
+  for (int l = 0; l < L; ++l)
+    if (!bind->dact[l]) {
+      set_error("binding: dact[%d] missing", l);
+      return DQN_ERR_INVALID_ARG;
+    }
+  cudaStream_t s = as_stream(stream);
+  // y.grad = dq (network.py:112)
+  if (dq != bind->dact[L - 1]) {
+    st = cuda_status(cudaMemcpyAsync(bind->dact[L - 1], dq,
+                                     sizeof(float) * bind->batch * net->layer[L - 1].out_c,
+                                     cudaMemcpyDeviceToDevice, s),
+                     "backward: copy dq");
+    if (st) return st;
+  }
+  for (int l = L - 1; l >= 0; --l) {
+    st = simt_layer_backward(s, net, l, params, bind);
+    if (st) return st;
+  }
+  return DQN_OK;
+}
+
+extern "C" int dqn_net_wgrad(void *stream, const dqn_net_desc *net, float *grads,
+                             const dqn_binding *bind) {
+  int st = check_binding(net, bind);
+  if (st) return st;
+  for (int l = net->n_layers - 1; l >= 0; --l) {
+    st = simt_layer_wgrad(as_stream(stream), net, l, grads, bind);
+    if (st) return st;
+  }
+  return DQN_OK;
+}
+
+extern "C" int dqn_net_layer(void *stream, const dqn_net_desc *net, const float *params,
+                             float *grads, const dqn_binding *bind, int32_t layer, int32_t phase,
+                             int32_t *flags) {
+  int st = check_binding(net, bind);
+  if (st) return st;
+  if (layer < 0 || layer >= net->n_layers) {
+    set_error("net_layer: layer %d out of range", layer);
+    return DQN_ERR_INVALID_ARG;
+  }
+  switch (phase) {
+    case 0: return simt_layer_forward(as_stream(stream), net, layer, params, bind, flags);
+    case 1: return simt_layer_backward(as_stream(stream), net, layer, params, bind);
+    case 2: return simt_layer_wgrad(as_stream(stream), net, layer, grads, bind);
+    default: set_error("net_layer: bad phase %d", phase); return DQN_ERR_INVALID_ARG;
+  }
+}

@@ -1,0 +1,675 @@
+// Generic-geometry Q-network kernels (SIMT fp32).  These cover every layer
+// geometry the reference accepts (layers.py:163-330: NHWC valid convolution,
+// linear with implicit flatten, ReLU, dueling head) and are the parity
+// baseline for the tcgen05 trunk in trunk_tc.cu.
+//
+// Reference call sites replaced:
+//   ConvolutionLayer.forward       layers.py:226-233 -> conv_fwd_kernel (implicit GEMM, no im2col buffer)
+//   ConvolutionLayer.backward      layers.py:235-248 -> conv_dgrad_kernel (gather form: no col2im scatter, no atomics)
+//   ConvolutionLayer.calculate_gradient layers.py:250-255 -> wgrad_kernel + wgrad_reduce_kernel
+//   LinearLayer.*                  layers.py:148-160 -> same kernels with 1x1 geometry
+//   ReluLayer                      layers.py:108-112 -> fused into epilogues (fwd) / masks (bwd)
+//   DuelingHeadLayer               layers.py:302-330 -> head_fwd/head_bwd/head_wgrad kernels
+//
+// Determinism (reference tests test_layers.py:60-67, test_network.py:95-103):
+// every reduction has a fixed order that does not depend on the batch size
+// of OTHER rows; split-K partials are summed in split order; no float atomics.
+#include "common.cuh"
+
+#include <algorithm>
+
+namespace dqn {
+namespace {
+
+constexpr int BM = 64;
+constexpr int BK = 16;
+constexpr int APAD = 4;
+
+struct Geo {
+  int H, W, C;       // input
+  int OH, OW, N;     // output
+  int fh, fw, sh, sw;
+};
+
+__device__ __forceinline__ float lift(uint8_t v) { return __fdiv_rn((float)v, 255.0f); }
+__device__ __forceinline__ float lift(float v) { return v; }
+
+// 4x4 register micro-tile update from one BK slice in shared memory.
+template <int BN>
+__device__ __forceinline__ void micro_mma(const float (*As)[BM + APAD], const float (*Bs)[BN + APAD],
+                                          int ty, int tx, float acc[4][4]) {
+#pragma unroll
+  for (int kk = 0; kk < BK; ++kk) {
+    const float4 a = *reinterpret_cast<const float4 *>(&As[kk][ty * 4]);
+    const float4 b = *reinterpret_cast<const float4 *>(&Bs[kk][tx * 4]);
+    const float av[4] = {a.x, a.y, a.z, a.w};
+    const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+  }
+}
+
+// ----------------------------------------------------------- forward GEMM
+// y[m, n] = relu( sum_k x_im2col[m, k] * W[k, n] + b[n] ),  m = (img, oy, ox),
+// k = (i, j, c) in the (fh, fw, cin, cout) filter order of layers.py:198-199.
+template <typename InT, int BN>
+__global__ void __launch_bounds__(BM *BN / 16)
+conv_fwd_kernel(const InT *__restrict__ x, const float *__restrict__ w,
+                const float *__restrict__ bias, float *__restrict__ y,
+                float *__restrict__ partial, Geo g, int M, int K, int klen, int relu) {
+  constexpr int THREADS = BM * BN / 16;
+  __shared__ __align__(16) float As[BK][BM + APAD];
+  __shared__ __align__(16) float Bs[BK][BN + APAD];
+  __shared__ int64_t s_row[BM];
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / 4), ty = tid / (BN / 4);
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int kbeg = blockIdx.z * klen, kend = min(K, kbeg + klen);
+  const int P = g.OH * g.OW;
+  for (int r = tid; r < BM; r += THREADS) {
+    const int m = m0 + r;
+    int64_t off = -1;
+    if (m < M) {
+      const int img = m / P, p = m % P;
+      const int oy = p / g.OW, ox = p % g.OW;
+      off = (int64_t)img * g.H * g.W * g.C + ((int64_t)oy * g.sh * g.W + (int64_t)ox * g.sw) * g.C;
+    }
+    s_row[r] = off;
+  }
+  __syncthreads();
+  const int rowlen = g.fw * g.C;        // (j, c) are contiguous in NHWC
+  float acc[4][4] = {};
+  for (int k0 = kbeg; k0 < kend; k0 += BK) {
+#pragma unroll
+    for (int q = 0; q < BM * BK / THREADS; ++q) {
+      const int e = tid + q * THREADS;
+      const int kk = e % BK, mm = e / BK;
+      const int k = k0 + kk;
+      float v = 0.f;
+      const int64_t ro = s_row[mm];
+      if (k < kend && ro >= 0) {
+        const int i = k / rowlen, rem = k - i * rowlen;
+        v = lift(x[ro + (int64_t)i * g.W * g.C + rem]);
+      }
+      As[kk][mm] = v;
+    }
+#pragma unroll
+    for (int q = 0; q < BK * BN / THREADS; ++q) {
+      const int e = tid + q * THREADS;
+      const int nn = e % BN, kk = e / BN;
+      const int k = k0 + kk, n = n0 + nn;
+      Bs[kk][nn] = (k < kend && n < g.N) ? w[(int64_t)k * g.N + n] : 0.f;
+    }
+    __syncthreads();
+    micro_mma<BN>(As, Bs, ty, tx, acc);
+    __syncthreads();
+  }
+  const bool split = gridDim.z > 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= g.N) continue;
+      if (split) {
+        partial[((int64_t)blockIdx.z * M + m) * g.N + n] = acc[i][j];
+      } else {
+        float v = __fadd_rn(acc[i][j], bias[n]);
+        if (relu) v = fmaxf(v, 0.f);
+        y[(int64_t)m * g.N + n] = v;
+      }
+    }
+  }
+}
+
+// Fixed-order split-K reduction + bias + ReLU.
+__global__ void splitk_bias_kernel(const float *__restrict__ partial, int splits, int64_t MN,
+                                   int N, const float *__restrict__ bias, float *__restrict__ y,
+                                   int relu) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < MN;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float s = partial[e];
+    for (int z = 1; z < splits; ++z) s = __fadd_rn(s, partial[(int64_t)z * MN + e]);
+    float v = __fadd_rn(s, bias[e % N]);
+    if (relu) v = fmaxf(v, 0.f);
+    y[e] = v;
+  }
+}
+
+// ------------------------------------------------------------- dgrad GEMM
+// dx[m_in, c] = sum_{i,j,co} dy[img, (y-i)/sh, (x-j)/sw, co] * W[i, j, c, co]
+// over the taps whose output position exists (gather form of the col2im
+// scatter of layers.py:240-248).  Optional ReLU mask of the layer below:
+// out = (act_in > 0) ? dx : 0  (layers.py:112).
+template <int BN>
+__global__ void __launch_bounds__(BM *BN / 16)
+conv_dgrad_kernel(const float *__restrict__ dy, const float *__restrict__ w,
+                  const float *__restrict__ mask_act, float *__restrict__ dx, Geo g, int Min) {
+  constexpr int THREADS = BM * BN / 16;
+  __shared__ __align__(16) float As[BK][BM + APAD];
+  __shared__ __align__(16) float Bs[BK][BN + APAD];
+  __shared__ int64_t s_base[BM];
+  __shared__ int s_y[BM], s_x[BM];
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / 4), ty = tid / (BN / 4);
+  const int m0 = blockIdx.x * BM, c0 = blockIdx.y * BN;
+  const int Pin = g.H * g.W;
+  const int K = g.fh * g.fw * g.N;
+  for (int r = tid; r < BM; r += THREADS) {
+    const int m = m0 + r;
+    if (m < Min) {
+      const int img = m / Pin, p = m % Pin;
+      s_base[r] = (int64_t)img * g.OH * g.OW * g.N;
+      s_y[r] = p / g.W;
+      s_x[r] = p % g.W;
+    } else {
+      s_base[r] = -1;
+      s_y[r] = 0;
+      s_x[r] = 0;
+    }
+  }
+  __syncthreads();
+  const int tapN = g.fw * g.N;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int q = 0; q < BM * BK / THREADS; ++q) {
+      const int e = tid + q * THREADS;
+      const int kk = e % BK, mm = e / BK;
+      const int k = k0 + kk;
+      float v = 0.f;
+      if (k < K && s_base[mm] >= 0) {
+        const int i = k / tapN, rem = k - i * tapN;
+        const int j = rem / g.N, co = rem - j * g.N;
+        const int yy = s_y[mm] - i, xx = s_x[mm] - j;
+        if (yy >= 0 && xx >= 0 && yy % g.sh == 0 && xx % g.sw == 0) {
+          const int oy = yy / g.sh, ox = xx / g.sw;
+          if (oy < g.OH && ox < g.OW)
+            v = dy[s_base[mm] + ((int64_t)oy * g.OW + ox) * g.N + co];
+        }
+      }
+      As[kk][mm] = v;
+    }
+#pragma unroll
+    for (int q = 0; q < BK * BN / THREADS; ++q) {
+      const int e = tid + q * THREADS;
+      const int nn = e % BN, kk = e / BN;
+      const int k = k0 + kk, c = c0 + nn;
+      float v = 0.f;
+      if (k < K && c < g.C) {
+        const int i = k / tapN, rem = k - i * tapN;
+        const int j = rem / g.N, co = rem - j * g.N;
+        v = w[(((int64_t)i * g.fw + j) * g.C + c) * g.N + co];
+      }
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+    micro_mma<BN>(As, Bs, ty, tx, acc);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= Min) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + tx * 4 + j;
+      if (c >= g.C) continue;
+      const int64_t o = (int64_t)m * g.C + c;
+      float v = acc[i][j];
+      if (mask_act != nullptr && !(mask_act[o] > 0.f)) v = 0.f;
+      dx[o] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------- wgrad GEMM
+// partial[z, r, n] = sum_{m in split z} x_im2col[m, r] * dy[m, n]; the
+// blocks of row tile 0 also produce partial column sums of dy (bias grads).
+template <typename InT, int BN>
+__global__ void __launch_bounds__(BM *BN / 16)
+wgrad_kernel(const InT *__restrict__ x, const float *__restrict__ dy, float *__restrict__ partial,
+             float *__restrict__ bpartial, Geo g, int M, int R, int mlen) {
+  constexpr int THREADS = BM * BN / 16;
+  __shared__ __align__(16) float As[BK][BM + APAD];
+  __shared__ __align__(16) float Bs[BK][BN + APAD];
+  __shared__ int64_t s_koff[BM];
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / 4), ty = tid / (BN / 4);
+  const int r0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int mbeg = blockIdx.z * mlen, mend = min(M, mbeg + mlen);
+  const int P = g.OH * g.OW;
+  const int rowlen = g.fw * g.C;
+  for (int rr = tid; rr < BM; rr += THREADS) {
+    const int r = r0 + rr;
+    int64_t off = -1;
+    if (r < R) {
+      const int i = r / rowlen, rem = r - i * rowlen;
+      off = (int64_t)i * g.W * g.C + rem;
+    }
+    s_koff[rr] = off;
+  }
+  __syncthreads();
+  const bool do_bias = (blockIdx.x == 0) && (ty == 0);
+  float bsum[4] = {0.f, 0.f, 0.f, 0.f};
+  float acc[4][4] = {};
+  for (int mk = mbeg; mk < mend; mk += BK) {
+    // A slice: rows r (BM), reduction m (BK)
+#pragma unroll
+    for (int q = 0; q < BM * BK / THREADS; ++q) {
+      const int e = tid + q * THREADS;
+      const int rr = e % BM, kk = e / BM;
+      const int m = mk + kk;
+      float v = 0.f;
+      if (m < mend && s_koff[rr] >= 0) {
+        const int img = m / P, p = m - img * P;
+        const int oy = p / g.OW, ox = p - oy * g.OW;
+        const int64_t ro =
+            (int64_t)img * g.H * g.W * g.C + ((int64_t)oy * g.sh * g.W + (int64_t)ox * g.sw) * g.C;
+        v = lift(x[ro + s_koff[rr]]);
+      }
+      As[kk][rr] = v;
+    }
+#pragma unroll
+    for (int q = 0; q < BK * BN / THREADS; ++q) {
+      const int e = tid + q * THREADS;
+      const int nn = e % BN, kk = e / BN;
+      const int m = mk + kk, n = n0 + nn;
+      Bs[kk][nn] = (m < mend && n < g.N) ? dy[(int64_t)m * g.N + n] : 0.f;
+    }
+    __syncthreads();
+    micro_mma<BN>(As, Bs, ty, tx, acc);
+    if (do_bias) {
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bsum[j] = __fadd_rn(bsum[j], Bs[kk][tx * 4 + j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + ty * 4 + i;
+    if (r >= R) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n < g.N) partial[((int64_t)blockIdx.z * R + r) * g.N + n] = acc[i][j];
+    }
+  }
+  if (do_bias) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n < g.N) bpartial[(int64_t)blockIdx.z * g.N + n] = bsum[j];
+    }
+  }
+}
+
+// grad += sum_z partial[z]  (fixed order); bias likewise.
+__global__ void wgrad_reduce_kernel(const float *__restrict__ partial,
+                                    const float *__restrict__ bpartial, int splits, int64_t RN,
+                                    int N, float *__restrict__ gw, float *__restrict__ gb) {
+  const int64_t total = RN + N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < RN) {
+      float s = partial[e];
+      for (int z = 1; z < splits; ++z) s = __fadd_rn(s, partial[(int64_t)z * RN + e]);
+      gw[e] = __fadd_rn(gw[e], s);
+    } else {
+      const int n = (int)(e - RN);
+      float s = bpartial[n];
+      for (int z = 1; z < splits; ++z) s = __fadd_rn(s, bpartial[(int64_t)z * N + n]);
+      gb[n] = __fadd_rn(gb[n], s);
+    }
+  }
+}
+
+// -------------------------------------------------------------- the head
+// One CTA per sample row: V/A (or plain linear) dot products over F features,
+// fixed-order tree reduction in shared memory.
+constexpr int kHeadThreads = 128;
+constexpr int kMaxHeadOut = 33;   // 1 value + up to 32 actions
+
+__global__ void __launch_bounds__(kHeadThreads)
+head_fwd_kernel(const float *__restrict__ x, int F, const float *__restrict__ wv,
+                const float *__restrict__ bv, const float *__restrict__ wa,
+                const float *__restrict__ ba, int nA, int dueling, float *__restrict__ q,
+                int32_t *flags) {
+  __shared__ float red[kMaxHeadOut][kHeadThreads];
+  const int row = blockIdx.x, t = threadIdx.x;
+  const float *xr = x + (int64_t)row * F;
+  const int nout = dueling ? nA + 1 : nA;
+  float part[kMaxHeadOut];
+#pragma unroll
+  for (int o = 0; o < kMaxHeadOut; ++o) part[o] = 0.f;
+  for (int f = t; f < F; f += kHeadThreads) {
+    const float xv = xr[f];
+    if (dueling) {
+      part[0] = fmaf(xv, wv[f], part[0]);
+      for (int a = 0; a < nA; ++a) part[a + 1] = fmaf(xv, wa[(int64_t)f * nA + a], part[a + 1]);
+    } else {
+      for (int a = 0; a < nA; ++a) part[a] = fmaf(xv, wa[(int64_t)f * nA + a], part[a]);
+    }
+  }
+  for (int o = 0; o < nout; ++o) red[o][t] = part[o];
+  __syncthreads();
+  for (int s = kHeadThreads / 2; s > 0; s >>= 1) {
+    if (t < s)
+      for (int o = 0; o < nout; ++o) red[o][t] = __fadd_rn(red[o][t], red[o][t + s]);
+    __syncthreads();
+  }
+  if (t == 0) {
+    bool bad = false;
+    if (dueling) {
+      // layers.py:302-310: y = V; y += A; y -= mean(A)
+      const float v = __fadd_rn(red[0][0], bv[0]);
+      float adv[kMaxHeadOut];
+      float sum = 0.f;
+      for (int a = 0; a < nA; ++a) {
+        adv[a] = __fadd_rn(red[a + 1][0], ba[a]);
+        sum = __fadd_rn(sum, adv[a]);
+      }
+      const float mean = __fdiv_rn(sum, (float)nA);
+      for (int a = 0; a < nA; ++a) {
+        const float qa = __fsub_rn(__fadd_rn(v, adv[a]), mean);
+        bad |= !isfinite(qa);
+        q[(int64_t)row * nA + a] = qa;
+      }
+    } else {
+      for (int a = 0; a < nA; ++a) {
+        const float qa = __fadd_rn(red[a][0], ba[a]);
+        bad |= !isfinite(qa);
+        q[(int64_t)row * nA + a] = qa;
+      }
+    }
+    if (bad) raise_flag(flags, DQN_FLAG_NONFINITE_OUT);
+  }
+}
+
+// Head backward (layers.py:312-323): gv = sum_a g, ga = g - gv/nA,
+// dx = gv*Wv^T + ga*Wa^T (plain head: g*W^T), masked by the input ReLU.
+__global__ void head_bwd_kernel(const float *__restrict__ dq, int B, int nA, int dueling,
+                                const float *__restrict__ wv, const float *__restrict__ wa, int F,
+                                const float *__restrict__ mask_act, float *__restrict__ dx) {
+  const int64_t total = (int64_t)B * F;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(e / F), f = (int)(e % F);
+    const float *g = dq + (int64_t)row * nA;
+    float v;
+    if (dueling) {
+      float gv = 0.f;
+      for (int a = 0; a < nA; ++a) gv = __fadd_rn(gv, g[a]);
+      const float gvn = __fdiv_rn(gv, (float)nA);
+      float s = 0.f;
+      for (int a = 0; a < nA; ++a) s = fmaf(__fsub_rn(g[a], gvn), wa[(int64_t)f * nA + a], s);
+      v = __fadd_rn(__fmul_rn(gv, wv[f]), s);
+    } else {
+      float s = 0.f;
+      for (int a = 0; a < nA; ++a) s = fmaf(g[a], wa[(int64_t)f * nA + a], s);
+      v = s;
+    }
+    if (mask_act != nullptr && !(mask_act[e] > 0.f)) v = 0.f;
+    dx[e] = v;
+  }
+}
+
+// Head wgrad (layers.py:325-330): thread per (f, out); fixed row order.
+__global__ void head_wgrad_kernel(const float *__restrict__ x, const float *__restrict__ dq, int B,
+                                  int F, int nA, int dueling, float *__restrict__ gwv,
+                                  float *__restrict__ gbv, float *__restrict__ gwa,
+                                  float *__restrict__ gba) {
+  const int nout = dueling ? nA + 1 : nA;
+  const int64_t total = (int64_t)(F + 1) * nout;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int f = (int)(e / nout), o = (int)(e % nout);   // f == F -> bias row
+    float s = 0.f;
+    for (int r = 0; r < B; ++r) {
+      const float *g = dq + (int64_t)r * nA;
+      float gr;
+      if (dueling) {
+        float gv = 0.f;
+        for (int a = 0; a < nA; ++a) gv = __fadd_rn(gv, g[a]);
+        gr = (o == 0) ? gv : __fsub_rn(g[o - 1], __fdiv_rn(gv, (float)nA));
+      } else {
+        gr = g[o];
+      }
+      const float xv = (f < F) ? x[(int64_t)r * F + f] : 1.f;
+      s = fmaf(xv, gr, s);
+    }
+    if (dueling) {
+      if (o == 0) {
+        if (f < F) gwv[f] = __fadd_rn(gwv[f], s); else gbv[0] = __fadd_rn(gbv[0], s);
+      } else {
+        if (f < F) gwa[(int64_t)f * nA + o - 1] = __fadd_rn(gwa[(int64_t)f * nA + o - 1], s);
+        else gba[o - 1] = __fadd_rn(gba[o - 1], s);
+      }
+    } else {
+      if (f < F) gwa[(int64_t)f * nA + o] = __fadd_rn(gwa[(int64_t)f * nA + o], s);
+      else gba[o] = __fadd_rn(gba[o], s);
+    }
+  }
+}
+
+// ------------------------------------------------------------ host plans
+
+inline Geo geo_of(const dqn_layer_desc &L) {
+  Geo g;
+  g.H = L.in_h; g.W = L.in_w; g.C = L.in_c;
+  g.OH = L.out_h; g.OW = L.out_w; g.N = L.out_c;
+  g.fh = L.fh; g.fw = L.fw; g.sh = L.sh; g.sw = L.sw;
+  return g;
+}
+
+inline bool is_head(const dqn_net_desc *net, int l) {
+  const dqn_layer_desc &L = net->layer[l];
+  return L.kind == DQN_LAYER_DUELING || (l == net->n_layers - 1 && L.kind == DQN_LAYER_LINEAR &&
+                                         L.out_c <= kMaxHeadOut - 1);
+}
+
+// split-K factor of a forward GEMM.  It depends on the reduction length
+// only, never on the batch, so every output row is computed in the same order
+// whatever batch it arrives in (batch-rebinding bit-exactness,
+// test_network.py:95-103).
+inline int fwd_splits(int /*M*/, int /*N*/, int K, int /*BN*/) {
+  if (K >= 2048) return 8;
+  if (K >= 1024) return 4;
+  return 1;
+}
+
+inline int wgrad_splits(int R, int N, int M, int BN) {
+  const int tiles = ((R + BM - 1) / BM) * ((N + BN - 1) / BN);
+  int s = 1;
+  while (tiles * s < 2 * kNumSMs && M / (s + 1) >= 8 * BK) ++s;
+  return s;
+}
+
+inline int pick_bn(int N) { return N <= 32 ? 32 : 64; }
+
+inline int64_t fwd_scratch(const dqn_layer_desc &L, int batch) {
+  if (L.kind == DQN_LAYER_DUELING) return 0;
+  const int M = batch * L.out_h * L.out_w, K = L.fh * L.fw * L.in_c;
+  const int s = fwd_splits(M, L.out_c, K, pick_bn(L.out_c));
+  return s > 1 ? (int64_t)s * M * L.out_c : 0;
+}
+
+inline int64_t wgrad_scratch(const dqn_layer_desc &L, int batch) {
+  if (L.kind == DQN_LAYER_DUELING) return 0;
+  const int M = batch * L.out_h * L.out_w, R = L.fh * L.fw * L.in_c;
+  const int s = wgrad_splits(R, L.out_c, M, pick_bn(L.out_c));
+  return (int64_t)s * R * L.out_c + (int64_t)s * L.out_c;
+}
+
+template <typename InT>
+int launch_fwd(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *params,
+               float *y, float *scratch, int batch) {
+  Geo g = geo_of(L);
+  const int M = batch * g.OH * g.OW, K = g.fh * g.fw * g.C;
+  const int bn = pick_bn(g.N);
+  const int s = fwd_splits(M, g.N, K, bn);
+  int klen = (K + s - 1) / s;
+  klen = (klen + BK - 1) / BK * BK;
+  const int splits = (K + klen - 1) / klen;
+  dim3 grid((M + BM - 1) / BM, (g.N + bn - 1) / bn, splits);
+  const float *w = params + L.w_off, *b = params + L.b_off;
+  if (bn == 32)
+    conv_fwd_kernel<InT, 32><<<grid, BM * 32 / 16, 0, st>>>(x, w, b, y, scratch, g, M, K, klen, L.relu);
+  else
+    conv_fwd_kernel<InT, 64><<<grid, BM * 64 / 16, 0, st>>>(x, w, b, y, scratch, g, M, K, klen, L.relu);
+  DQN_LAUNCH_CHECK("conv_fwd");
+  if (splits > 1) {
+    const int64_t MN = (int64_t)M * g.N;
+    splitk_bias_kernel<<<(int)std::min<int64_t>((MN + 255) / 256, 148 * 8), 256, 0, st>>>(
+        scratch, splits, MN, g.N, b, y, L.relu);
+    DQN_LAUNCH_CHECK("splitk_bias");
+  }
+  return DQN_OK;
+}
+
+template <typename InT>
+int launch_wgrad(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *dy,
+                 float *grads, float *scratch, int batch) {
+  Geo g = geo_of(L);
+  const int M = batch * g.OH * g.OW, R = g.fh * g.fw * g.C;
+  const int bn = pick_bn(g.N);
+  const int s = wgrad_splits(R, g.N, M, bn);
+  int mlen = (M + s - 1) / s;
+  mlen = (mlen + BK - 1) / BK * BK;
+  const int splits = (M + mlen - 1) / mlen;
+  float *partial = scratch;
+  float *bpartial = scratch + (int64_t)splits * R * g.N;
+  dim3 grid((R + BM - 1) / BM, (g.N + bn - 1) / bn, splits);
+  if (bn == 32)
+    wgrad_kernel<InT, 32><<<grid, BM * 32 / 16, 0, st>>>(x, dy, partial, bpartial, g, M, R, mlen);
+  else
+    wgrad_kernel<InT, 64><<<grid, BM * 64 / 16, 0, st>>>(x, dy, partial, bpartial, g, M, R, mlen);
+  DQN_LAUNCH_CHECK("wgrad");
+  const int64_t RN = (int64_t)R * g.N;
+  wgrad_reduce_kernel<<<(int)std::min<int64_t>((RN + g.N + 255) / 256, 148 * 8), 256, 0, st>>>(
+      partial, bpartial, splits, RN, g.N, grads + L.w_off, grads + L.b_off);
+  DQN_LAUNCH_CHECK("wgrad_reduce");
+  return DQN_OK;
+}
+
+int launch_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *params,
+                 const float *mask_act, float *dx, int batch) {
+  Geo g = geo_of(L);
+  const int Min = batch * g.H * g.W;
+  const int bn = pick_bn(g.C);
+  dim3 grid((Min + BM - 1) / BM, (g.C + bn - 1) / bn, 1);
+  const float *w = params + L.w_off;
+  if (bn == 32)
+    conv_dgrad_kernel<32><<<grid, BM * 32 / 16, 0, st>>>(dy, w, mask_act, dx, g, Min);
+  else
+    conv_dgrad_kernel<64><<<grid, BM * 64 / 16, 0, st>>>(dy, w, mask_act, dx, g, Min);
+  DQN_LAUNCH_CHECK("conv_dgrad");
+  return DQN_OK;
+}
+
+int validate(const dqn_net_desc *net) {
+  if (!net || net->n_layers < 1 || net->n_layers > DQN_MAX_LAYERS) {
+    set_error("net: bad layer count");
+    return DQN_ERR_GEOMETRY;
+  }
+  for (int l = 0; l < net->n_layers; ++l) {
+    const dqn_layer_desc &L = net->layer[l];
+    if (L.kind == DQN_LAYER_DUELING && l != net->n_layers - 1) {
+      set_error("net: dueling head must be last");
+      return DQN_ERR_GEOMETRY;
+    }
+    if (is_head(net, l) && L.out_c > kMaxHeadOut - 1) {
+      set_error("net: at most %d actions", kMaxHeadOut - 1);
+      return DQN_ERR_UNSUPPORTED;
+    }
+  }
+  return DQN_OK;
+}
+
+}  // namespace
+
+// Called by dqn_net_forward for layers the tcgen05 trunk does not own.
+int simt_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
+                       const dqn_binding *b, int32_t *flags) {
+  const dqn_layer_desc &L = net->layer[l];
+  const void *in = (l == 0) ? b->x : b->act[l - 1];
+  if (is_head(net, l)) {
+    const int F = L.in_h * L.in_w * L.in_c;
+    const bool duel = L.kind == DQN_LAYER_DUELING;
+    if (l == 0 && net->input_u8) {
+      set_error("head cannot read u8 input");
+      return DQN_ERR_UNSUPPORTED;
+    }
+    head_fwd_kernel<<<b->batch, kHeadThreads, 0, st>>>(
+        (const float *)in, F, duel ? params + L.w_off : nullptr, duel ? params + L.b_off : nullptr,
+        duel ? params + L.w2_off : params + L.w_off, duel ? params + L.b2_off : params + L.b_off,
+        L.out_c, duel, b->act[l], flags);
+    DQN_LAUNCH_CHECK("head_fwd");
+    return DQN_OK;
+  }
+  if (l == 0 && net->input_u8)
+    return launch_fwd<uint8_t>(st, L, (const uint8_t *)in, params, b->act[l], b->scratch, b->batch);
+  return launch_fwd<float>(st, L, (const float *)in, params, b->act[l], b->scratch, b->batch);
+}
+
+int simt_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
+                        const dqn_binding *b) {
+  // produces the gradient w.r.t. layer l's INPUT: dact[l-1] (masked by the
+  // ReLU fused into layer l-1) or dx for l == 0.
+  const dqn_layer_desc &L = net->layer[l];
+  float *out = (l == 0) ? b->dx : b->dact[l - 1];
+  if (out == nullptr) return DQN_OK;
+  const float *mask = (l > 0 && net->layer[l - 1].relu) ? b->act[l - 1] : nullptr;
+  if (is_head(net, l)) {
+    const int F = L.in_h * L.in_w * L.in_c;
+    const bool duel = L.kind == DQN_LAYER_DUELING;
+    const int64_t total = (int64_t)b->batch * F;
+    head_bwd_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, st>>>(
+        b->dact[l], b->batch, L.out_c, duel, duel ? params + L.w_off : nullptr,
+        duel ? params + L.w2_off : params + L.w_off, F, mask, out);
+    DQN_LAUNCH_CHECK("head_bwd");
+    return DQN_OK;
+  }
+  return launch_dgrad(st, L, b->dact[l], params, mask, out, b->batch);
+}
+
+int simt_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
+                     const dqn_binding *b) {
+  const dqn_layer_desc &L = net->layer[l];
+  const void *in = (l == 0) ? b->x : b->act[l - 1];
+  if (is_head(net, l)) {
+    const int F = L.in_h * L.in_w * L.in_c;
+    const bool duel = L.kind == DQN_LAYER_DUELING;
+    const int nout = duel ? L.out_c + 1 : L.out_c;
+    const int64_t total = (int64_t)(F + 1) * nout;
+    head_wgrad_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(
+        (const float *)in, b->dact[l], b->batch, F, L.out_c, duel,
+        duel ? grads + L.w_off : nullptr, duel ? grads + L.b_off : nullptr,
+        duel ? grads + L.w2_off : grads + L.w_off, duel ? grads + L.b2_off : grads + L.b_off);
+    DQN_LAUNCH_CHECK("head_wgrad");
+    return DQN_OK;
+  }
+  if (l == 0 && net->input_u8)
+    return launch_wgrad<uint8_t>(st, L, (const uint8_t *)in, b->dact[l], grads, b->scratch, b->batch);
+  return launch_wgrad<float>(st, L, (const float *)in, b->dact[l], grads, b->scratch, b->batch);
+}
+
+int64_t simt_scratch_floats(const dqn_net_desc *net, int batch) {
+  int64_t m = 0;
+  for (int l = 0; l < net->n_layers; ++l) {
+    if (is_head(net, l)) continue;
+    m = std::max(m, fwd_scratch(net->layer[l], batch));
+    m = std::max(m, wgrad_scratch(net->layer[l], batch));
+  }
+  return m;
+}
+
+int simt_validate(const dqn_net_desc *net) { return validate(net); }
+
+}  // namespace dqn

@@ -1,0 +1,490 @@
+// Replay side of the learner hot path: the uint8 frame ring gather and the
+// fp64 proportional-priority sum tree.
+//
+// Reference: /root/reference/pkg/src/deepq/replay.py
+//   ReplayMemory._gather          replay.py:104-115   -> ring_gather_kernel
+//   SumTree.set / find            replay.py:155-181   -> tree_* kernels
+//   PrioritizedReplay.sample      replay.py:215-229   -> tree_sample_kernel
+//   PrioritizedReplay.update_priorities  232-241      -> tree_update_kernel
+//   PrioritizedReplay.store       replay.py:207-210   -> tree_store_kernel
+//
+// HBM layout: the heap keeps the reference's 1-indexed layout
+// (nodes[0] unused, leaf i at nodes[2^depth + i], replay.py:141-143), fp64,
+// 16 MiB at 1M leaves.  Tree arithmetic uses __dadd_rn/__dmul_rn/__ddiv_rn so
+// internal nodes, query masses and sampled indices are bit-identical to the
+// reference given the same uniforms.
+#include "common.cuh"
+
+#include <math.h>
+
+#include <mutex>
+
+namespace dqn {
+namespace {
+
+// ------------------------------------------------------------- frame ring
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void ring_fill_hash_kernel(uint64_t *__restrict__ out, int64_t total_words,
+                                      int64_t first_word, uint64_t base) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < total_words; i += stride) out[i] = splitmix64(base | (uint64_t)(first_word + i));
+}
+
+// One CTA copies a 16 KiB chunk of one sampled slot (state or next state).
+// 16-byte vector loads, four in flight per thread; slot strides are
+// multiples of 16 B for the Atari ring (28,224 B).
+constexpr int kGatherThreads = 256;
+constexpr int kGatherUnroll = 4;
+constexpr int kGatherChunk = kGatherThreads * kGatherUnroll;  // int4 per CTA
+
+__global__ void __launch_bounds__(kGatherThreads)
+ring_gather_vec_kernel(const int4 *__restrict__ states, const int4 *__restrict__ next_states,
+                       int64_t slot_vecs, const int64_t *__restrict__ idx,
+                       int4 *__restrict__ out_s, int4 *__restrict__ out_s2) {
+  const int j = blockIdx.y;
+  const int which = blockIdx.z;
+  const int4 *src = which ? next_states : states;
+  int4 *dst = which ? out_s2 : out_s;
+  if (dst == nullptr) return;
+  const int64_t slot = __ldg(idx + j);
+  const int4 *s = src + slot * slot_vecs;
+  int4 *d = dst + (int64_t)j * slot_vecs;
+  const int64_t base = (int64_t)blockIdx.x * kGatherChunk + threadIdx.x;
+  int4 v[kGatherUnroll];
+#pragma unroll
+  for (int u = 0; u < kGatherUnroll; ++u) {
+    int64_t e = base + u * kGatherThreads;
+    if (e < slot_vecs) v[u] = __ldg(s + e);
+  }
+#pragma unroll
+  for (int u = 0; u < kGatherUnroll; ++u) {
+    int64_t e = base + u * kGatherThreads;
+    if (e < slot_vecs) d[e] = v[u];
+  }
+}
+
+__global__ void ring_gather_bytes_kernel(const uint8_t *__restrict__ states,
+                                         const uint8_t *__restrict__ next_states,
+                                         int64_t slot_bytes, const int64_t *__restrict__ idx,
+                                         uint8_t *__restrict__ out_s, uint8_t *__restrict__ out_s2) {
+  const int j = blockIdx.y;
+  const int which = blockIdx.z;
+  const uint8_t *src = which ? next_states : states;
+  uint8_t *dst = which ? out_s2 : out_s;
+  if (dst == nullptr) return;
+  const int64_t slot = idx[j];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < slot_bytes;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[j * slot_bytes + e] = src[slot * slot_bytes + e];
+}
+
+__global__ void ring_gather_meta_kernel(const int64_t *__restrict__ actions,
+                                        const double *__restrict__ rewards,
+                                        const uint8_t *__restrict__ terminals,
+                                        const int64_t *__restrict__ idx, int k,
+                                        int64_t *out_a, double *out_r, uint8_t *out_t) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  int64_t s = idx[j];
+  if (out_a) out_a[j] = actions[s];
+  if (out_r) out_r[j] = rewards[s];
+  if (out_t) out_t[j] = terminals[s];
+}
+
+// --------------------------------------------------------------- sum tree
+
+// SumTree.find descent for one query mass (replay.py:172-181).
+__device__ __forceinline__ int64_t tree_descend(const double *__restrict__ nodes, int depth,
+                                                double q, double hi) {
+  q = fmin(fmax(q, 1e-300), hi);            // np.clip(q, 1e-300, nextafter(total, 0))
+  int64_t n = 1;
+  for (int l = 0; l < depth; ++l) {
+    const int64_t left = n << 1;
+    const double ls = __ldg(nodes + left);
+    const bool right = q > ls;
+    if (right) q = __dsub_rn(q, ls);          // q -= left_sum * go_right
+    n = left + (right ? 1 : 0);
+  }
+  return n - (int64_t(1) << depth);
+}
+
+// PrioritizedReplay.sample for k <= blockDim (one CTA): stratified masses,
+// descent, probabilities, IS weights and their batch-max normalisation.
+__global__ void tree_sample_kernel(const double *__restrict__ nodes, int depth,
+                                   const int64_t *__restrict__ size_p,
+                                   const double *__restrict__ u, int k,
+                                   const double *__restrict__ beta_p, int64_t *__restrict__ idx,
+                                   double *__restrict__ prob, double *__restrict__ weight,
+                                   int32_t *flags) {
+  __shared__ double red[32];
+  const int j = threadIdx.x;
+  const double total = nodes[1];
+  if (!(total > 0.0)) {                        // replay.py:221-222
+    if (j == 0) raise_flag(flags, DQN_FLAG_ZERO_TOTAL);
+    if (j < k) { idx[j] = 0; prob[j] = 0.0; weight[j] = 0.0; }
+    return;
+  }
+  const double beta = *beta_p;
+  const int64_t size = *size_p;
+  const double hi = nextafter(total, 0.0);
+  const double seg = __ddiv_rn(total, (double)k);                 // segment = total / k
+  double w = 0.0;
+  if (j < k) {
+    const double q = __dmul_rn(__dadd_rn((double)j, u[j]), seg);  // (arange + u) * seg
+    const int64_t i = tree_descend(nodes, depth, q, hi);
+    const double p = __ddiv_rn(nodes[(int64_t(1) << depth) + i], total);
+    w = pow(__dmul_rn((double)size, p), -beta);                   // (size * P)^-beta
+    idx[j] = i;
+    prob[j] = p;
+  }
+  // block max of w (order-free, exact)
+  double m = w;
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((j & 31) == 0) red[j >> 5] = m;
+  __syncthreads();
+  if (j < 32) {
+    double v = (j < (int)((blockDim.x + 31) >> 5)) ? red[j] : 0.0;
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (j == 0) red[0] = v;
+  }
+  __syncthreads();
+  if (j < k) weight[j] = __ddiv_rn(w, red[0]);                    // w /= w.max()
+}
+
+// Large-k variant, pass 1: per-query descent, raw weights, per-CTA max.
+__global__ void tree_sample_raw_kernel(const double *__restrict__ nodes, int depth,
+                                       const int64_t *__restrict__ size_p,
+                                       const double *__restrict__ u, int k,
+                                       const double *__restrict__ beta_p, int64_t *__restrict__ idx,
+                                       double *__restrict__ prob, double *__restrict__ weight,
+                                       double *__restrict__ block_max, int32_t *flags) {
+  __shared__ double red[32];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const double total = nodes[1];
+  if (!(total > 0.0)) {
+    if (j == 0) raise_flag(flags, DQN_FLAG_ZERO_TOTAL);
+    if (threadIdx.x == 0) block_max[blockIdx.x] = 1.0;
+    if (j < k) { idx[j] = 0; prob[j] = 0.0; weight[j] = 0.0; }
+    return;
+  }
+  const double beta = *beta_p;
+  const int64_t size = *size_p;
+  const double seg = __ddiv_rn(total, (double)k);
+  double w = 0.0;
+  if (j < k) {
+    const double q = __dmul_rn(__dadd_rn((double)j, u[j]), seg);
+    const int64_t i = tree_descend(nodes, depth, q, nextafter(total, 0.0));
+    const double p = __ddiv_rn(nodes[(int64_t(1) << depth) + i], total);
+    w = pow(__dmul_rn((double)size, p), -beta);
+    idx[j] = i;
+    prob[j] = p;
+    weight[j] = w;
+  }
+  double m = w;
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = red[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) v = fmax(v, red[i]);
+    block_max[blockIdx.x] = v;
+  }
+}
+
+__global__ void tree_sample_norm_kernel(double *__restrict__ weight, int k,
+                                        const double *__restrict__ block_max, int nblocks) {
+  __shared__ double mx;
+  if (threadIdx.x == 0) {
+    double v = block_max[0];
+    for (int i = 1; i < nblocks; ++i) v = fmax(v, block_max[i]);
+    mx = v;
+  }
+  __syncthreads();
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x)
+    weight[j] = __ddiv_rn(weight[j], mx);
+}
+
+__global__ void tree_find_kernel(const double *__restrict__ nodes, int depth,
+                                 const double *__restrict__ q, int64_t n, int64_t *__restrict__ idx,
+                                 int32_t *flags) {
+  const double total = nodes[1];
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (!(total > 0.0)) {
+    if (j == 0) raise_flag(flags, DQN_FLAG_ZERO_TOTAL);
+    return;
+  }
+  const double hi = nextafter(total, 0.0);
+  for (; j < n; j += (int64_t)gridDim.x * blockDim.x) idx[j] = tree_descend(nodes, depth, q[j], hi);
+}
+
+constexpr int kTreeThreads = 1024;
+
+// Recompute the ancestors of the leaves in leaf_ids[0..n) level by level.
+// Each internal node is a pure function of its two children, so duplicate
+// writers store identical bits and the result equals the reference's
+// sequential set() calls.
+__device__ void tree_fix_ancestors(double *nodes, int depth, const int64_t *leaf_node, int n) {
+  for (int l = 1; l <= depth; ++l) {
+    __syncthreads();
+    if ((int)threadIdx.x < n) {
+      const int64_t a = leaf_node[threadIdx.x] >> l;
+      nodes[a] = __dadd_rn(nodes[2 * a], nodes[2 * a + 1]);
+    }
+  }
+  __syncthreads();
+}
+
+// update_priorities (replay.py:232-241) and set (155-165).  mode 0: leaf
+// value = (|td| + eps)^alpha; mode 1: leaf value = td (raw SumTree.set).
+// One CTA walks the batch in chunks of 1024 in batch order.
+__global__ void __launch_bounds__(kTreeThreads)
+tree_update_kernel(double *__restrict__ nodes, int depth, const int64_t *__restrict__ limit_p,
+                   int64_t limit_v,
+                   const int64_t *__restrict__ idx, const double *__restrict__ td, int k,
+                   double alpha, double eps, double *__restrict__ max_p, int32_t *flags,
+                   int mode) {
+  __shared__ int64_t s_node[kTreeThreads];
+  __shared__ int s_first_bad;
+  __shared__ double s_red[32];
+  const int t = threadIdx.x;
+  const int64_t limit = limit_p ? *limit_p : limit_v;
+  // the reference raises before update_priorities when the step already
+  // failed (empty/zero-mass sample, non-finite network output)
+  if (flags && (*flags & (DQN_FLAG_ZERO_TOTAL | DQN_FLAG_NONFINITE_OUT))) return;
+  if (t == 0) s_first_bad = k;
+  __syncthreads();
+  // first invalid position in batch order (index range, then value)
+  for (int j = t; j < k; j += blockDim.x) {
+    const int64_t i = idx[j];
+    bool bad = (i < 0 || i >= limit);
+    if (!bad) {
+      double v = (mode == 0) ? __dadd_rn(fabs(td[j]), eps) : td[j];
+      if (mode == 0) v = pow(v, alpha);
+      bad = !(v >= 0.0) || isinf(v);
+    }
+    if (bad) atomicMin(&s_first_bad, j);
+  }
+  __syncthreads();
+  const int kk = s_first_bad;
+  const int64_t base = int64_t(1) << depth;
+  for (int c0 = 0; c0 < kk; c0 += blockDim.x) {
+    const int n = min((int)blockDim.x, kk - c0);
+    const int j = c0 + t;
+    if (t < n) s_node[t] = base + idx[j];
+    __syncthreads();
+    if (t < n) {
+      // last write wins inside the chunk; later chunks run after this one
+      bool last = true;
+      for (int o = t + 1; o < n; ++o)
+        if (s_node[o] == s_node[t]) { last = false; break; }
+      if (last) {
+        double v = (mode == 0) ? pow(__dadd_rn(fabs(td[j]), eps), alpha) : td[j];
+        nodes[s_node[t]] = v;
+      }
+    }
+    tree_fix_ancestors(nodes, depth, s_node, n);
+  }
+  if (kk < k) {
+    if (t == 0)
+      raise_flag(flags, (idx[kk] < 0 || idx[kk] >= limit) ? DQN_FLAG_INDEX : DQN_FLAG_BAD_PRIORITY);
+    return;                                   // reference raises: max_p untouched
+  }
+  if (mode == 0 && max_p != nullptr) {
+    double m = -INFINITY;
+    for (int j = t; j < k; j += blockDim.x) m = fmax(m, __dadd_rn(fabs(td[j]), eps));
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((t & 31) == 0) s_red[t >> 5] = m;
+    __syncthreads();
+    if (t == 0) {
+      double v = s_red[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, s_red[w]);
+      const double cur = *max_p;
+      if (v > cur) *max_p = v;                // max(self.max_priority, p.max())
+    }
+  }
+}
+
+// store (replay.py:207-210): n consecutive slots get max_p^alpha.
+__global__ void __launch_bounds__(kTreeThreads)
+tree_store_kernel(double *__restrict__ nodes, int depth, int64_t capacity, int64_t slot,
+                  int64_t n, const double *__restrict__ max_p, double alpha) {
+  __shared__ int64_t s_node[kTreeThreads];
+  const int t = threadIdx.x;
+  const double v = pow(*max_p, alpha);
+  const int64_t base = int64_t(1) << depth;
+  const int64_t m = n < capacity ? n : capacity;   // later wraps overwrite the same slot value
+  for (int64_t c0 = 0; c0 < m; c0 += blockDim.x) {
+    const int cn = (int)min((int64_t)blockDim.x, m - c0);
+    if (t < cn) {
+      s_node[t] = base + (slot + c0 + t) % capacity;
+      nodes[s_node[t]] = v;
+    }
+    tree_fix_ancestors(nodes, depth, s_node, cn);
+  }
+}
+
+__global__ void tree_level_kernel(double *__restrict__ nodes, int64_t lo, int64_t hi) {
+  for (int64_t a = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < hi;
+       a += (int64_t)gridDim.x * blockDim.x)
+    nodes[a] = __dadd_rn(nodes[2 * a], nodes[2 * a + 1]);
+}
+
+inline int grid_for(int64_t n, int threads, int cap = 148 * 16) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+}  // namespace
+}  // namespace dqn
+
+using namespace dqn;
+
+extern "C" int dqn_ring_fill_hash(void *stream, uint8_t *frames, int64_t slot0, int64_t nslots,
+                                  int64_t slot_bytes, uint64_t counter_base) {
+  DQN_CHECK_ARG(frames && slot_bytes % 8 == 0 && nslots >= 0, "ring_fill_hash: bad args");
+  const int64_t words = slot_bytes / 8;
+  const int64_t total = nslots * words;
+  if (total == 0) return DQN_OK;
+  ring_fill_hash_kernel<<<grid_for(total, 256, 148 * 64), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<uint64_t *>(frames + slot0 * slot_bytes), total, slot0 * words,
+      counter_base);
+  DQN_LAUNCH_CHECK("ring_fill_hash");
+  return DQN_OK;
+}
+
+extern "C" int dqn_ring_gather(void *stream, const uint8_t *states, const uint8_t *next_states,
+                               int64_t slot_bytes, const int64_t *actions, const double *rewards,
+                               const uint8_t *terminals, const int64_t *idx, int32_t k,
+                               uint8_t *out_states, uint8_t *out_next_states,
+                               int64_t *out_actions, double *out_rewards,
+                               uint8_t *out_terminals) {
+  DQN_CHECK_ARG(idx && k >= 0 && slot_bytes > 0, "ring_gather: bad args");
+  if (k == 0) return DQN_OK;
+  cudaStream_t st = as_stream(stream);
+  if (out_states || out_next_states) {
+    const bool vec = slot_bytes % 16 == 0 && ((uintptr_t)states % 16 == 0) &&
+                     ((uintptr_t)next_states % 16 == 0) && ((uintptr_t)out_states % 16 == 0) &&
+                     ((uintptr_t)out_next_states % 16 == 0);
+    if (vec) {
+      const int64_t vecs = slot_bytes / 16;
+      dim3 grid((unsigned)((vecs + kGatherChunk - 1) / kGatherChunk), (unsigned)k, 2);
+      ring_gather_vec_kernel<<<grid, kGatherThreads, 0, st>>>(
+          reinterpret_cast<const int4 *>(states), reinterpret_cast<const int4 *>(next_states),
+          vecs, idx, reinterpret_cast<int4 *>(out_states),
+          reinterpret_cast<int4 *>(out_next_states));
+    } else {
+      dim3 grid((unsigned)((slot_bytes + 255) / 256 < 64 ? (slot_bytes + 255) / 256 : 64),
+                (unsigned)k, 2);
+      ring_gather_bytes_kernel<<<grid, 256, 0, st>>>(states, next_states, slot_bytes, idx,
+                                                     out_states, out_next_states);
+    }
+    DQN_LAUNCH_CHECK("ring_gather");
+  }
+  if (out_actions || out_rewards || out_terminals) {
+    ring_gather_meta_kernel<<<(k + 255) / 256, 256, 0, st>>>(actions, rewards, terminals, idx, k,
+                                                            out_actions, out_rewards,
+                                                            out_terminals);
+    DQN_LAUNCH_CHECK("ring_gather_meta");
+  }
+  return DQN_OK;
+}
+
+extern "C" int dqn_tree_sample(void *stream, const double *nodes, int32_t depth, const int64_t *size,
+                               const double *u, int32_t k, const double *beta, int64_t *idx,
+                               double *prob, double *weight, int32_t *flags) {
+  DQN_CHECK_ARG(nodes && size && u && beta && idx && prob && weight && k >= 1 && depth >= 1 &&
+                    depth < 40,
+                "tree_sample: bad args");
+  cudaStream_t st = as_stream(stream);
+  if (k <= 1024) {
+    int threads = ((k + 31) / 32) * 32;
+    tree_sample_kernel<<<1, threads, 0, st>>>(nodes, depth, size, u, k, beta, idx, prob, weight,
+                                              flags);
+    DQN_LAUNCH_CHECK("tree_sample");
+    return DQN_OK;
+  }
+  // Large batches (sampler microbenchmarks; the learner uses k <= 1024): the
+  // normaliser needs a grid-wide max, so two passes with per-CTA maxima in a
+  // process-wide scratch grown outside any graph capture.
+  static std::mutex mu;
+  static double *scratch = nullptr;
+  static int scratch_n = 0;
+  const int threads = 256;
+  const int blocks = (k + threads - 1) / threads;
+  std::lock_guard<std::mutex> lock(mu);
+  if (scratch_n < blocks) {
+    if (scratch) cudaFree(scratch);
+    int st_ = cuda_status(cudaMalloc(&scratch, sizeof(double) * blocks), "tree_sample scratch");
+    if (st_) return st_;
+    scratch_n = blocks;
+  }
+  tree_sample_raw_kernel<<<blocks, threads, 0, st>>>(nodes, depth, size, u, k, beta, idx, prob,
+                                                     weight, scratch, flags);
+  DQN_LAUNCH_CHECK("tree_sample_raw");
+  tree_sample_norm_kernel<<<grid_for(k, 256), 256, 0, st>>>(weight, k, scratch, blocks);
+  DQN_LAUNCH_CHECK("tree_sample_norm");
+  return DQN_OK;
+}
+
+extern "C" int dqn_tree_find(void *stream, const double *nodes, int32_t depth,
+                             const double *queries, int64_t n, int64_t *idx, int32_t *flags) {
+  DQN_CHECK_ARG(nodes && queries && idx && n >= 0 && depth >= 1, "tree_find: bad args");
+  if (n == 0) return DQN_OK;
+  tree_find_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(nodes, depth, queries, n, idx,
+                                                                     flags);
+  DQN_LAUNCH_CHECK("tree_find");
+  return DQN_OK;
+}
+
+extern "C" int dqn_tree_update(void *stream, double *nodes, int32_t depth, const int64_t *size,
+                               const int64_t *idx, const double *td, int32_t k, double alpha,
+                               double eps, double *max_p, int32_t *flags) {
+  DQN_CHECK_ARG(nodes && size && idx && td && k >= 0 && depth >= 1, "tree_update: bad args");
+  if (k == 0) return DQN_OK;
+  tree_update_kernel<<<1, kTreeThreads, 0, as_stream(stream)>>>(nodes, depth, size, 0, idx, td, k,
+                                                                alpha, eps, max_p, flags, 0);
+  DQN_LAUNCH_CHECK("tree_update");
+  return DQN_OK;
+}
+
+extern "C" int dqn_tree_set(void *stream, double *nodes, int32_t depth, int64_t capacity,
+                            const int64_t *idx, const double *values, int32_t k, int32_t *flags) {
+  DQN_CHECK_ARG(nodes && idx && values && k >= 0 && depth >= 1, "tree_set: bad args");
+  if (k == 0) return DQN_OK;
+  tree_update_kernel<<<1, kTreeThreads, 0, as_stream(stream)>>>(nodes, depth, nullptr, capacity, idx,
+                                                                values, k, 0.0, 0.0, nullptr,
+                                                                flags, 1);
+  DQN_LAUNCH_CHECK("tree_set");
+  return DQN_OK;
+}
+
+extern "C" int dqn_tree_store(void *stream, double *nodes, int32_t depth, int64_t capacity,
+                              int64_t slot, int64_t n, const double *max_p, double alpha) {
+  DQN_CHECK_ARG(nodes && max_p && capacity >= 1 && slot >= 0 && slot < capacity && n >= 0,
+                "tree_store: bad args");
+  if (n == 0) return DQN_OK;
+  tree_store_kernel<<<1, kTreeThreads, 0, as_stream(stream)>>>(nodes, depth, capacity, slot, n,
+                                                               max_p, alpha);
+  DQN_LAUNCH_CHECK("tree_store");
+  return DQN_OK;
+}
+
+extern "C" int dqn_tree_rebuild(void *stream, double *nodes, int32_t depth) {
+  DQN_CHECK_ARG(nodes && depth >= 1 && depth < 40, "tree_rebuild: bad args");
+  for (int l = depth - 1; l >= 0; --l) {
+    const int64_t lo = int64_t(1) << l, hi = int64_t(1) << (l + 1);
+    tree_level_kernel<<<grid_for(hi - lo, 256), 256, 0, as_stream(stream)>>>(nodes, lo, hi);
+    DQN_LAUNCH_CHECK("tree_rebuild");
+  }
+  return DQN_OK;
+}

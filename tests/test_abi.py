@@ -1,0 +1,48 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library loads and
+exports every entry point include/dqn_b200.h declares (no compute calls)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent.parent
+HEADER = REPO / "include" / "dqn_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z0-9_]+\s*\*?\s*(dqn_[a-z0-9_]+)\(", text, re.M)))
+
+
+def test_header_declares_the_hot_path():
+    syms = declared_symbols()
+    for must in ["dqn_ring_gather", "dqn_tree_sample", "dqn_tree_update", "dqn_net_forward",
+                 "dqn_net_backward", "dqn_net_wgrad", "dqn_td_loss", "dqn_rmsprop_step",
+                 "dqn_sync_target"]:
+        assert must in syms
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1804_05834_b200 import _lib
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(declared_symbols()) == set(_lib.EXPORTED)
+    assert lib.dqn_abi_version() == 1
+
+
+def test_struct_layouts_match_header():
+    from paper_1804_05834_b200 import _lib
+    # dqn_layer_desc: 12 int32 + 4 int64 = 80 bytes; net desc: 16 + 8*80
+    assert ctypes.sizeof(_lib.LayerDesc) == 80
+    assert ctypes.sizeof(_lib.NetDesc) == 16 + 8 * 80
+    assert ctypes.sizeof(_lib.Binding) == 8 + 8 + 16 * 8 + 8 + 8 + 8
+
+
+def test_product_path_refuses_without_gpu(monkeypatch):
+    import pytest
+    import torch
+    from paper_1804_05834_b200 import _lib
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _lib.require_cuda()

@@ -1,0 +1,138 @@
+"""GPU parity of the Q-network phases against the CPU oracle (norm-wise,
+fp32): forward, backward (input grads), wgrad, for the Atari trunk with both
+heads, the desk preset and a tiny float-input net; plus determinism and the
+reference's geometry / phase-order errors."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import deepq_oracle as O
+from tests.helpers import rel_norm
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+TOL = 1e-5      # fp32 re-ordered sums vs numpy/BLAS
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1804_05834_b200 as P
+    return P
+
+
+def _pair(P, trunk_name, shape, nA, dueling, seed=3):
+    o_trunk = {"atari": O.ATARI_TRUNK, "desk": O.DESK_TRUNK}[trunk_name]
+    on = P.build_network(trunk_name, shape, nA, dueling)
+    P.init_params(on, seed)
+    ref = O.QNet(o_trunk, shape, nA, dueling)
+    ref.init(seed)
+    for n, t in on.named_tensors():
+        assert np.array_equal(t.values.cpu().numpy(), ref.params[n]), n   # init is bit-exact
+    return on, ref
+
+
+@pytest.mark.parametrize("dueling", [True, False])
+def test_atari_forward_backward_wgrad(P, dueling):
+    from paper_1804_05834_b200 import synth
+    on, ref = _pair(P, "atari", (84, 84, 4), 4, dueling)
+    # perturb biases so ReLU masks are non-trivial
+    rng = np.random.default_rng(0)
+    for n, t in on.named_tensors():
+        if n.endswith("bias"):
+            v = (rng.standard_normal(t.shape) * 0.01).astype(np.float32)
+            t.values.copy_(torch.as_tensor(v, device="cuda"))
+            ref.params[n][...] = v
+    x8 = synth.frames(4, 0, np.arange(16))
+    q = on.forward(torch.as_tensor(x8, device="cuda")).cpu().numpy()
+    xf = O.Ring.lift(x8)
+    qr = ref.forward(xf)
+    assert rel_norm(q, qr) < TOL
+    g = rng.standard_normal(q.shape).astype(np.float32)
+    dx = on.backward(g).cpu().numpy()
+    dxr = ref.backward(g)
+    assert rel_norm(dx, dxr) < TOL
+    on.calculate_gradient()
+    ref.wgrad()
+    for n, t in on.named_tensors():
+        assert rel_norm(t.grad.cpu().numpy(), ref.grads[n]) < TOL, n
+
+
+def test_desk_and_float_input(P):
+    on, ref = _pair(P, "desk", (24, 24, 4), 3, True, seed=2)
+    x = np.random.default_rng(1).random((5, 24, 24, 4), dtype=np.float32)
+    q = on.forward(x).cpu().numpy()
+    assert rel_norm(q, ref.forward(x)) < TOL
+    g = np.random.default_rng(2).standard_normal(q.shape).astype(np.float32)
+    assert rel_norm(on.backward(g).cpu().numpy(), ref.backward(g)) < TOL
+    on.calculate_gradient()
+    ref.wgrad()
+    for n, t in on.named_tensors():
+        assert rel_norm(t.grad.cpu().numpy(), ref.grads[n]) < TOL, n
+
+
+def test_tiny_custom_trunk(P):
+    trunk = [P.LayerSpec("convolution", {"filters": 2, "filter_h": 2, "filter_w": 2,
+                                         "stride_h": 2, "stride_w": 2}),
+             P.LayerSpec.relu(), P.LayerSpec.linear(8), P.LayerSpec.relu()]
+    on = P.build_network(trunk, (6, 6, 2), 3, True)
+    P.init_params(on, 5)
+    ref = O.QNet([("conv", 2, 2, 2), ("relu",), ("fc", 8), ("relu",)], (6, 6, 2), 3, True)
+    ref.init(5)
+    x = np.random.default_rng(3).random((4, 6, 6, 2), dtype=np.float32)
+    assert rel_norm(on.forward(x).cpu().numpy(), ref.forward(x)) < TOL
+
+
+def test_shape_chain_and_registry(P):
+    net = P.build_network("atari", (84, 84, 4), 4, dueling=False)
+    shapes = net.layer_output_shapes()
+    assert shapes[0] == (20, 20, 32) and shapes[2] == (9, 9, 64) and shapes[4] == (7, 7, 64)
+    assert shapes[6] == (512,) and shapes[-1] == (4,)
+    fc1 = [v for v in net.layers if v.name == "fc1"][0]
+    assert fc1.in_features == 3136
+    names = [n for n, _ in P.build_network("atari", (84, 84, 4), 6, True).named_tensors()]
+    assert names == ["conv1.weight", "conv1.bias", "conv2.weight", "conv2.bias", "conv3.weight",
+                     "conv3.bias", "fc1.weight", "fc1.bias", "duel.value.weight", "duel.value.bias",
+                     "duel.advantage.weight", "duel.advantage.bias"]
+    n_params = sum(t.size for _, t in P.build_network("atari", (84, 84, 4), 4, True).named_tensors())
+    assert n_params == 1_686_693
+
+
+def test_determinism_and_batch_independence(P):
+    from paper_1804_05834_b200 import synth
+    net = P.build_network("atari", (84, 84, 4), 4, True)
+    P.init_params(net, 1)
+    x = torch.as_tensor(synth.frames(9, 0, np.arange(64)), device="cuda")
+    q64 = net.forward(x).clone()
+    q64b = net.forward(x).clone()
+    assert torch.equal(q64, q64b)
+    q8 = net.forward(x[:8]).clone()
+    assert torch.equal(q8, q64[:8])       # a row's Q does not depend on its batch
+
+
+def test_errors(P):
+    with pytest.raises(P.GeometryError):
+        P.build_network("atari", (30, 30, 4), 4, dueling=False)
+    with pytest.raises(P.GeometryError):
+        P.build_network("atari", (4, 4, 4), 4, dueling=False)
+    with pytest.raises(P.GeometryError):
+        P.build_network("desk", (24, 24, 4), 1, dueling=False)
+    with pytest.raises(ValueError):
+        P.trunk_layers("mega")
+    with pytest.raises(P.ConfigError):
+        P.build_network("desk", (24, 24, 4), 3, False, dtype=np.float64)
+    net = P.build_network("desk", (24, 24, 4), 3, dueling=False)
+    with pytest.raises(P.PhaseOrderError):
+        net.backward(np.zeros((1, 3), np.float32))
+    with pytest.raises(P.GeometryError):
+        net.forward(np.zeros((1, 24, 24, 3), dtype=np.float32))
+    net.forward(np.zeros((2, 24, 24, 4), np.float32))
+    with pytest.raises(P.PhaseOrderError):
+        net.calculate_gradient()
+    net.params()[0].weight.values.fill_(float("nan"))
+    with pytest.raises(P.NonFiniteError):
+        net.forward(np.ones((1, 24, 24, 4), np.float32))
