@@ -54,11 +54,15 @@ __device__ __forceinline__ void micro_mma(const float (*As)[BM + APAD], const fl
 // ----------------------------------------------------------- forward GEMM
 // y[m, n] = relu( sum_k x_im2col[m, k] * W[k, n] + b[n] ),  m = (img, oy, ox),
 // k = (i, j, c) in the (fh, fw, cin, cout) filter order of layers.py:198-199.
-template <typename InT, int BN>
+// TB: B is stored transposed (W[n, k], the dgrad operand W^T); bias may be
+// NULL; ``mask`` (optional) zeroes outputs whose mask value is <= 0 (ReLU
+// backward of the layer below, layers.py:112).
+template <typename InT, int BN, bool TB>
 __global__ void __launch_bounds__(BM *BN / 16)
 conv_fwd_kernel(const InT *__restrict__ x, const float *__restrict__ w,
                 const float *__restrict__ bias, float *__restrict__ y,
-                float *__restrict__ partial, Geo g, int M, int K, int klen, int relu) {
+                float *__restrict__ partial, Geo g, int M, int K, int klen, int relu,
+                const float *__restrict__ mask) {
   constexpr int THREADS = BM * BN / 16;
   __shared__ __align__(16) float As[BK][BM + APAD];
   __shared__ __align__(16) float Bs[BK][BN + APAD];
@@ -98,9 +102,15 @@ conv_fwd_kernel(const InT *__restrict__ x, const float *__restrict__ w,
 #pragma unroll
     for (int q = 0; q < BK * BN / THREADS; ++q) {
       const int e = tid + q * THREADS;
-      const int nn = e % BN, kk = e / BN;
-      const int k = k0 + kk, n = n0 + nn;
-      Bs[kk][nn] = (k < kend && n < g.N) ? w[(int64_t)k * g.N + n] : 0.f;
+      if (TB) {                                   // coalesce along k
+        const int kk = e % BK, nn = e / BK;
+        const int k = k0 + kk, n = n0 + nn;
+        Bs[kk][nn] = (k < kend && n < g.N) ? w[(int64_t)n * K + k] : 0.f;
+      } else {
+        const int nn = e % BN, kk = e / BN;
+        const int k = k0 + kk, n = n0 + nn;
+        Bs[kk][nn] = (k < kend && n < g.N) ? w[(int64_t)k * g.N + n] : 0.f;
+      }
     }
     __syncthreads();
     micro_mma<BN>(As, Bs, ty, tx, acc);
@@ -118,112 +128,60 @@ conv_fwd_kernel(const InT *__restrict__ x, const float *__restrict__ w,
       if (split) {
         partial[((int64_t)blockIdx.z * M + m) * g.N + n] = acc[i][j];
       } else {
-        float v = __fadd_rn(acc[i][j], bias[n]);
-        if (relu) v = fmaxf(v, 0.f);
-        y[(int64_t)m * g.N + n] = v;
+        float v = bias ? __fadd_rn(acc[i][j], bias[n]) : acc[i][j];
+        if (relu && v < 0.f) v = 0.f;   // np.maximum(x, 0) keeps NaN
+        const int64_t o = (int64_t)m * g.N + n;
+        if (mask && !(mask[o] > 0.f)) v = 0.f;
+        y[o] = v;
       }
     }
   }
 }
 
-// Fixed-order split-K reduction + bias + ReLU.
+// Fixed-order split-K reduction + bias + ReLU (+ mask).
 __global__ void splitk_bias_kernel(const float *__restrict__ partial, int splits, int64_t MN,
                                    int N, const float *__restrict__ bias, float *__restrict__ y,
-                                   int relu) {
+                                   int relu, const float *__restrict__ mask) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < MN;
        e += (int64_t)gridDim.x * blockDim.x) {
     float s = partial[e];
     for (int z = 1; z < splits; ++z) s = __fadd_rn(s, partial[(int64_t)z * MN + e]);
-    float v = __fadd_rn(s, bias[e % N]);
-    if (relu) v = fmaxf(v, 0.f);
+    float v = bias ? __fadd_rn(s, bias[e % N]) : s;
+    if (relu && v < 0.f) v = 0.f;   // np.maximum(x, 0) keeps NaN
+    if (mask && !(mask[e] > 0.f)) v = 0.f;
     y[e] = v;
   }
 }
 
-// ------------------------------------------------------------- dgrad GEMM
-// dx[m_in, c] = sum_{i,j,co} dy[img, (y-i)/sh, (x-j)/sw, co] * W[i, j, c, co]
-// over the taps whose output position exists (gather form of the col2im
-// scatter of layers.py:240-248).  Optional ReLU mask of the layer below:
-// out = (act_in > 0) ? dx : 0  (layers.py:112).
-template <int BN>
-__global__ void __launch_bounds__(BM *BN / 16)
-conv_dgrad_kernel(const float *__restrict__ dy, const float *__restrict__ w,
-                  const float *__restrict__ mask_act, float *__restrict__ dx, Geo g, int Min) {
-  constexpr int THREADS = BM * BN / 16;
-  __shared__ __align__(16) float As[BK][BM + APAD];
-  __shared__ __align__(16) float Bs[BK][BN + APAD];
-  __shared__ int64_t s_base[BM];
-  __shared__ int s_y[BM], s_x[BM];
-  const int tid = threadIdx.x;
-  const int tx = tid % (BN / 4), ty = tid / (BN / 4);
-  const int m0 = blockIdx.x * BM, c0 = blockIdx.y * BN;
-  const int Pin = g.H * g.W;
-  const int K = g.fh * g.fw * g.N;
-  for (int r = tid; r < BM; r += THREADS) {
-    const int m = m0 + r;
-    if (m < Min) {
-      const int img = m / Pin, p = m % Pin;
-      s_base[r] = (int64_t)img * g.OH * g.OW * g.N;
-      s_y[r] = p / g.W;
-      s_x[r] = p % g.W;
-    } else {
-      s_base[r] = -1;
-      s_y[r] = 0;
-      s_x[r] = 0;
-    }
-  }
-  __syncthreads();
-  const int tapN = g.fw * g.N;
-  float acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += BK) {
-#pragma unroll
-    for (int q = 0; q < BM * BK / THREADS; ++q) {
-      const int e = tid + q * THREADS;
-      const int kk = e % BK, mm = e / BK;
-      const int k = k0 + kk;
-      float v = 0.f;
-      if (k < K && s_base[mm] >= 0) {
-        const int i = k / tapN, rem = k - i * tapN;
-        const int j = rem / g.N, co = rem - j * g.N;
-        const int yy = s_y[mm] - i, xx = s_x[mm] - j;
-        if (yy >= 0 && xx >= 0 && yy % g.sh == 0 && xx % g.sw == 0) {
-          const int oy = yy / g.sh, ox = xx / g.sw;
-          if (oy < g.OH && ox < g.OW)
-            v = dy[s_base[mm] + ((int64_t)oy * g.OW + ox) * g.N + co];
-        }
+// col2im as a gather (layers.py:240-248 scatter-adds one strided slice per
+// filter tap): dx[img, y, x, c] = sum over taps (i ascending, j ascending)
+// with y = oy*sh + i, x = ox*sw + j of dpatch[(img, oy, ox), (i, j, c)] --
+// the same per-element summation order as the reference's tap loop, no
+// atomics.  Optional ReLU mask of the layer below.
+__global__ void col2im_kernel(const float *__restrict__ dpatch, Geo g, int64_t total,
+                              const float *__restrict__ mask, float *__restrict__ dx) {
+  const int R = g.fh * g.fw * g.C;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % g.C);
+    int64_t t = e / g.C;
+    const int x = (int)(t % g.W);
+    t /= g.W;
+    const int y = (int)(t % g.H);
+    const int img = (int)(t / g.H);
+    float s = 0.f;
+    for (int i = y % g.sh; i < g.fh; i += g.sh) {
+      const int oy = (y - i) / g.sh;
+      if (y - i < 0 || oy >= g.OH) continue;
+      for (int j = x % g.sw; j < g.fw; j += g.sw) {
+        const int ox = (x - j) / g.sw;
+        if (x - j < 0 || ox >= g.OW) continue;
+        const int64_t m = ((int64_t)img * g.OH + oy) * g.OW + ox;
+        s = __fadd_rn(s, dpatch[m * R + (i * g.fw + j) * g.C + c]);
       }
-      As[kk][mm] = v;
     }
-#pragma unroll
-    for (int q = 0; q < BK * BN / THREADS; ++q) {
-      const int e = tid + q * THREADS;
-      const int nn = e % BN, kk = e / BN;
-      const int k = k0 + kk, c = c0 + nn;
-      float v = 0.f;
-      if (k < K && c < g.C) {
-        const int i = k / tapN, rem = k - i * tapN;
-        const int j = rem / g.N, co = rem - j * g.N;
-        v = w[(((int64_t)i * g.fw + j) * g.C + c) * g.N + co];
-      }
-      Bs[kk][nn] = v;
-    }
-    __syncthreads();
-    micro_mma<BN>(As, Bs, ty, tx, acc);
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + ty * 4 + i;
-    if (m >= Min) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = c0 + tx * 4 + j;
-      if (c >= g.C) continue;
-      const int64_t o = (int64_t)m * g.C + c;
-      float v = acc[i][j];
-      if (mask_act != nullptr && !(mask_act[o] > 0.f)) v = 0.f;
-      dx[o] = v;
-    }
+    if (mask && !(mask[e] > 0.f)) s = 0.f;
+    dx[e] = s;
   }
 }
 
@@ -479,8 +437,8 @@ inline bool is_head(const dqn_net_desc *net, int l) {
 // whatever batch it arrives in (batch-rebinding bit-exactness,
 // test_network.py:95-103).
 inline int fwd_splits(int /*M*/, int /*N*/, int K, int /*BN*/) {
-  if (K >= 2048) return 8;
-  if (K >= 1024) return 4;
+  if (K >= 2048) return 16;
+  if (K >= 512) return 4;
   return 1;
 }
 
@@ -493,11 +451,22 @@ inline int wgrad_splits(int R, int N, int M, int BN) {
 
 inline int pick_bn(int N) { return N <= 32 ? 32 : 64; }
 
+inline int64_t gemm_scratch(int M, int N, int K) {
+  const int s = fwd_splits(M, N, K, pick_bn(N));
+  return s > 1 ? (int64_t)s * M * N : 0;
+}
+
 inline int64_t fwd_scratch(const dqn_layer_desc &L, int batch) {
   if (L.kind == DQN_LAYER_DUELING) return 0;
-  const int M = batch * L.out_h * L.out_w, K = L.fh * L.fw * L.in_c;
-  const int s = fwd_splits(M, L.out_c, K, pick_bn(L.out_c));
-  return s > 1 ? (int64_t)s * M * L.out_c : 0;
+  return gemm_scratch(batch * L.out_h * L.out_w, L.out_c, L.fh * L.fw * L.in_c);
+}
+
+// dgrad = GEMM dY * W^T (conv: into a dpatch buffer, then col2im gather)
+inline int64_t dgrad_scratch(const dqn_layer_desc &L, int batch) {
+  if (L.kind == DQN_LAYER_DUELING) return 0;
+  const int M = batch * L.out_h * L.out_w, R = L.fh * L.fw * L.in_c;
+  const bool conv = L.kind == DQN_LAYER_CONV;
+  return (conv ? (int64_t)M * R : 0) + gemm_scratch(M, R, L.out_c);
 }
 
 inline int64_t wgrad_scratch(const dqn_layer_desc &L, int batch) {
@@ -507,30 +476,40 @@ inline int64_t wgrad_scratch(const dqn_layer_desc &L, int batch) {
   return (int64_t)s * R * L.out_c + (int64_t)s * L.out_c;
 }
 
-template <typename InT>
-int launch_fwd(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *params,
-               float *y, float *scratch, int batch) {
-  Geo g = geo_of(L);
-  const int M = batch * g.OH * g.OW, K = g.fh * g.fw * g.C;
+// C[M, g.N] = A_im2col(x; g)[M, K] * B[K, g.N] (B transposed when TB), with
+// optional bias / ReLU / mask epilogue; fixed K-only split-K.
+template <typename InT, bool TB>
+int launch_gemm(cudaStream_t st, const InT *x, const Geo &g, const float *w, const float *bias,
+                const float *mask, int relu, float *y, float *scratch, int M, int K) {
   const int bn = pick_bn(g.N);
   const int s = fwd_splits(M, g.N, K, bn);
   int klen = (K + s - 1) / s;
   klen = (klen + BK - 1) / BK * BK;
   const int splits = (K + klen - 1) / klen;
   dim3 grid((M + BM - 1) / BM, (g.N + bn - 1) / bn, splits);
-  const float *w = params + L.w_off, *b = params + L.b_off;
   if (bn == 32)
-    conv_fwd_kernel<InT, 32><<<grid, BM * 32 / 16, 0, st>>>(x, w, b, y, scratch, g, M, K, klen, L.relu);
+    conv_fwd_kernel<InT, 32, TB><<<grid, BM * 32 / 16, 0, st>>>(x, w, bias, y, scratch, g, M, K,
+                                                                klen, relu, mask);
   else
-    conv_fwd_kernel<InT, 64><<<grid, BM * 64 / 16, 0, st>>>(x, w, b, y, scratch, g, M, K, klen, L.relu);
-  DQN_LAUNCH_CHECK("conv_fwd");
+    conv_fwd_kernel<InT, 64, TB><<<grid, BM * 64 / 16, 0, st>>>(x, w, bias, y, scratch, g, M, K,
+                                                                klen, relu, mask);
+  DQN_LAUNCH_CHECK("gemm");
   if (splits > 1) {
     const int64_t MN = (int64_t)M * g.N;
     splitk_bias_kernel<<<(int)std::min<int64_t>((MN + 255) / 256, 148 * 8), 256, 0, st>>>(
-        scratch, splits, MN, g.N, b, y, L.relu);
+        scratch, splits, MN, g.N, bias, y, relu, mask);
     DQN_LAUNCH_CHECK("splitk_bias");
   }
   return DQN_OK;
+}
+
+template <typename InT>
+int launch_fwd(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *params,
+               float *y, float *scratch, int batch) {
+  Geo g = geo_of(L);
+  const int M = batch * g.OH * g.OW, K = g.fh * g.fw * g.C;
+  return launch_gemm<InT, false>(st, x, g, params + L.w_off, params + L.b_off, nullptr, L.relu,
+                                 y, scratch, M, K);
 }
 
 template <typename InT>
@@ -558,18 +537,29 @@ int launch_wgrad(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const f
   return DQN_OK;
 }
 
+// dX = dY * W^T: linear layers write dX directly (masked); convolutions form
+// dpatch[M, R] then gather it back with col2im.
 int launch_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *params,
-                 const float *mask_act, float *dx, int batch) {
+                 const float *mask_act, float *dx, float *scratch, int batch) {
   Geo g = geo_of(L);
-  const int Min = batch * g.H * g.W;
-  const int bn = pick_bn(g.C);
-  dim3 grid((Min + BM - 1) / BM, (g.C + bn - 1) / bn, 1);
+  const int M = batch * g.OH * g.OW, R = g.fh * g.fw * g.C;
+  // dY viewed as a 1x1 "image" of Cout channels per output pixel
+  Geo a;
+  a.H = a.W = a.OH = a.OW = 1;
+  a.C = g.N;
+  a.N = R;
+  a.fh = a.fw = a.sh = a.sw = 1;
   const float *w = params + L.w_off;
-  if (bn == 32)
-    conv_dgrad_kernel<32><<<grid, BM * 32 / 16, 0, st>>>(dy, w, mask_act, dx, g, Min);
-  else
-    conv_dgrad_kernel<64><<<grid, BM * 64 / 16, 0, st>>>(dy, w, mask_act, dx, g, Min);
-  DQN_LAUNCH_CHECK("conv_dgrad");
+  if (L.kind == DQN_LAYER_LINEAR)
+    return launch_gemm<float, true>(st, dy, a, w, nullptr, mask_act, 0, dx, scratch, M, g.N);
+  float *dpatch = scratch;
+  int rc = launch_gemm<float, true>(st, dy, a, w, nullptr, nullptr, 0, dpatch,
+                                    scratch + (int64_t)M * R, M, g.N);
+  if (rc) return rc;
+  const int64_t total = (int64_t)batch * g.H * g.W * g.C;
+  col2im_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+      dpatch, g, total, mask_act, dx);
+  DQN_LAUNCH_CHECK("col2im");
   return DQN_OK;
 }
 
@@ -636,7 +626,7 @@ int simt_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const f
     DQN_LAUNCH_CHECK("head_bwd");
     return DQN_OK;
   }
-  return launch_dgrad(st, L, b->dact[l], params, mask, out, b->batch);
+  return launch_dgrad(st, L, b->dact[l], params, mask, out, b->scratch, b->batch);
 }
 
 int simt_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
@@ -666,6 +656,7 @@ int64_t simt_scratch_floats(const dqn_net_desc *net, int batch) {
     if (is_head(net, l)) continue;
     m = std::max(m, fwd_scratch(net->layer[l], batch));
     m = std::max(m, wgrad_scratch(net->layer[l], batch));
+    m = std::max(m, dgrad_scratch(net->layer[l], batch));
   }
   return m;
 }

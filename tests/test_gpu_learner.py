@@ -96,7 +96,8 @@ def test_one_step_parity(P, name):
     compare_weights(on, o_on, TOL)
     if kw["per"]:
         got = mem.tree.nodes.cpu().numpy()
-        assert rel_norm(got, o_mem.tree.nodes) < 1e-9
+        # leaves are (|delta|+eps)^alpha of an fp32-network delta: norm-wise
+        assert rel_norm(got, o_mem.tree.nodes) < 1e-5
         chk = O.HeapTree(o_mem.tree.capacity)
         chk.nodes[:] = got
         chk.rebuild()
