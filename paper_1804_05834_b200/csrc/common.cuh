@@ -34,6 +34,21 @@ __device__ __forceinline__ void raise_flag(int32_t *flags, int32_t bit) {
 
 constexpr int kNumSMs = 148;
 
+// Layer geometry in NHWC terms (linear layers: H = W = OH = OW = 1).
+struct Geo {
+  int H, W, C;       // input
+  int OH, OW, N;     // output
+  int fh, fw, sh, sw;
+};
+
+inline Geo geo_of(const dqn_layer_desc &L) {
+  Geo g;
+  g.H = L.in_h; g.W = L.in_w; g.C = L.in_c;
+  g.OH = L.out_h; g.OW = L.out_w; g.N = L.out_c;
+  g.fh = L.fh; g.fw = L.fw; g.sh = L.sh; g.sw = L.sw;
+  return g;
+}
+
 }  // namespace dqn
 
 #define DQN_CHECK_ARG(cond, ...)              \

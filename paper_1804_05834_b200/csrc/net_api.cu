@@ -17,6 +17,40 @@ int simt_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *gra
                      const dqn_binding *b);
 int64_t simt_scratch_floats(const dqn_net_desc *net, int batch);
 int simt_validate(const dqn_net_desc *net);
+bool tc_layer_supported(const dqn_net_desc *net, int l);
+int64_t tc_scratch_floats(const dqn_net_desc *net, int batch);
+int tc_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
+                     const dqn_binding *b);
+int tc_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
+                      const dqn_binding *b);
+int tc_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
+                   const dqn_binding *b);
+
+// tcgen05 trunk for supported geometries unless the descriptor asks for SIMT
+static bool use_tc(const dqn_net_desc *net, int l) {
+  return net->algo != 1 && tc_layer_supported(net, l);
+}
+
+static int64_t scratch_need(const dqn_net_desc *net, int batch) {
+  const int64_t a = simt_scratch_floats(net, batch), b = tc_scratch_floats(net, batch);
+  return a > b ? a : b;
+}
+
+static int layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
+                         const dqn_binding *b, int32_t *flags) {
+  if (use_tc(net, l)) return tc_layer_forward(st, net, l, params, b);
+  return simt_layer_forward(st, net, l, params, b, flags);
+}
+static int layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
+                          const dqn_binding *b) {
+  if (use_tc(net, l)) return tc_layer_backward(st, net, l, params, b);
+  return simt_layer_backward(st, net, l, params, b);
+}
+static int layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
+                       const dqn_binding *b) {
+  if (use_tc(net, l)) return tc_layer_wgrad(st, net, l, grads, b);
+  return simt_layer_wgrad(st, net, l, grads, b);
+}
 
 namespace {
 thread_local char g_err[512] = "";
@@ -38,12 +72,12 @@ using namespace dqn;
 
 extern "C" const char *dqn_last_error(void) { return g_err; }
 extern "C" int dqn_abi_version(void) { return 1; }
-extern "C" int dqn_has_tcgen05(void) { return 0; }
+extern "C" int dqn_has_tcgen05(void) { return 1; }
 extern "C" int64_t dqn_launch_count(void) { return g_launches.load(); }
 
 extern "C" int64_t dqn_net_scratch_floats(const dqn_net_desc *net, int32_t batch) {
   if (simt_validate(net) != DQN_OK || batch < 1) return -1;
-  return simt_scratch_floats(net, batch);
+  return scratch_need(net, batch);
 }
 
 static int check_binding(const dqn_net_desc *net, const dqn_binding *b) {
@@ -53,9 +87,9 @@ static int check_binding(const dqn_net_desc *net, const dqn_binding *b) {
     set_error("binding: batch/input missing");
     return DQN_ERR_INVALID_ARG;
   }
-  if (b->scratch_floats < simt_scratch_floats(net, b->batch)) {
+  if (b->scratch_floats < scratch_need(net, b->batch)) {
     set_error("binding: scratch too small (%lld < %lld floats)", (long long)b->scratch_floats,
-              (long long)simt_scratch_floats(net, b->batch));
+              (long long)scratch_need(net, b->batch));
     return DQN_ERR_INVALID_ARG;
   }
   for (int l = 0; l < net->n_layers; ++l)
@@ -71,7 +105,7 @@ extern "C" int dqn_net_forward(void *stream, const dqn_net_desc *net, const floa
   int st = check_binding(net, bind);
   if (st) return st;
   for (int l = 0; l < net->n_layers; ++l) {
-    st = simt_layer_forward(as_stream(stream), net, l, params, bind, flags);
+    st = layer_forward(as_stream(stream), net, l, params, bind, flags);
     if (st) return st;
   }
   return DQN_OK;
@@ -97,7 +131,7 @@ extern "C" int dqn_net_backward(void *stream, const dqn_net_desc *net, const flo
     if (st) return st;
   }
   for (int l = L - 1; l >= 0; --l) {
-    st = simt_layer_backward(s, net, l, params, bind);
+    st = layer_backward(s, net, l, params, bind);
     if (st) return st;
   }
   return DQN_OK;
@@ -108,7 +142,7 @@ extern "C" int dqn_net_wgrad(void *stream, const dqn_net_desc *net, float *grads
   int st = check_binding(net, bind);
   if (st) return st;
   for (int l = net->n_layers - 1; l >= 0; --l) {
-    st = simt_layer_wgrad(as_stream(stream), net, l, grads, bind);
+    st = layer_wgrad(as_stream(stream), net, l, grads, bind);
     if (st) return st;
   }
   return DQN_OK;
@@ -124,9 +158,9 @@ extern "C" int dqn_net_layer(void *stream, const dqn_net_desc *net, const float 
     return DQN_ERR_INVALID_ARG;
   }
   switch (phase) {
-    case 0: return simt_layer_forward(as_stream(stream), net, layer, params, bind, flags);
-    case 1: return simt_layer_backward(as_stream(stream), net, layer, params, bind);
-    case 2: return simt_layer_wgrad(as_stream(stream), net, layer, grads, bind);
+    case 0: return layer_forward(as_stream(stream), net, layer, params, bind, flags);
+    case 1: return layer_backward(as_stream(stream), net, layer, params, bind);
+    case 2: return layer_wgrad(as_stream(stream), net, layer, grads, bind);
     default: set_error("net_layer: bad phase %d", phase); return DQN_ERR_INVALID_ARG;
   }
 }

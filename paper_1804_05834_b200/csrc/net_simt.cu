@@ -25,11 +25,6 @@ constexpr int BM = 64;
 constexpr int BK = 16;
 constexpr int APAD = 4;
 
-struct Geo {
-  int H, W, C;       // input
-  int OH, OW, N;     // output
-  int fh, fw, sh, sw;
-};
 
 __device__ __forceinline__ float lift(uint8_t v) { return __fdiv_rn((float)v, 255.0f); }
 __device__ __forceinline__ float lift(float v) { return v; }
@@ -418,13 +413,6 @@ __global__ void head_wgrad_kernel(const float *__restrict__ x, const float *__re
 
 // ------------------------------------------------------------ host plans
 
-inline Geo geo_of(const dqn_layer_desc &L) {
-  Geo g;
-  g.H = L.in_h; g.W = L.in_w; g.C = L.in_c;
-  g.OH = L.out_h; g.OW = L.out_w; g.N = L.out_c;
-  g.fh = L.fh; g.fw = L.fw; g.sh = L.sh; g.sw = L.sw;
-  return g;
-}
 
 inline bool is_head(const dqn_net_desc *net, int l) {
   const dqn_layer_desc &L = net->layer[l];
@@ -583,6 +571,23 @@ int validate(const dqn_net_desc *net) {
 }
 
 }  // namespace
+
+int launch_splitk_reduce(cudaStream_t st, const float *partial, int splits, int64_t MN, int N,
+                         const float *bias, float *y, int relu, const float *mask) {
+  splitk_bias_kernel<<<(int)std::min<int64_t>((MN + 255) / 256, 148 * 8), 256, 0, st>>>(
+      partial, splits, MN, N, bias, y, relu, mask);
+  DQN_LAUNCH_CHECK("splitk_reduce");
+  return DQN_OK;
+}
+
+int launch_col2im(cudaStream_t st, const float *dpatch, const Geo &g, int batch,
+                  const float *mask, float *dx) {
+  const int64_t total = (int64_t)batch * g.H * g.W * g.C;
+  col2im_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+      dpatch, g, total, mask, dx);
+  DQN_LAUNCH_CHECK("col2im");
+  return DQN_OK;
+}
 
 // Called by dqn_net_forward for layers the tcgen05 trunk does not own.
 int simt_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,

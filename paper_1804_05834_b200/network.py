@@ -17,6 +17,7 @@ ConfigError (no CPU fallback).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -237,7 +238,8 @@ class Network:
         d = _lib.NetDesc()
         d.n_layers = len(self._units)
         d.input_u8 = 1 if input_u8 else 0
-        d.algo = 0
+        # DQN_B200_ALGO=simt forces the generic SIMT kernels (A/B diagnostics)
+        d.algo = 1 if os.environ.get("DQN_B200_ALGO", "") == "simt" else 0
         for i, u in enumerate(self._units):
             L = d.layer[i]
             L.kind, L.relu = u["kind"], u["relu"]
