@@ -156,14 +156,15 @@ __global__ void splitk_bias_kernel(const float *__restrict__ partial, int splits
 __global__ void col2im_kernel(const float *__restrict__ dpatch, Geo g, int64_t total,
                               const float *__restrict__ mask, float *__restrict__ dx) {
   const int R = g.fh * g.fw * g.C;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e % g.C);
-    int64_t t = e / g.C;
-    const int x = (int)(t % g.W);
+  // element index fits 32 bits for any learner batch (checked by the caller)
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (int)total;
+       e += gridDim.x * blockDim.x) {
+    const int c = e % g.C;
+    int t = e / g.C;
+    const int x = t % g.W;
     t /= g.W;
-    const int y = (int)(t % g.H);
-    const int img = (int)(t / g.H);
+    const int y = t % g.H;
+    const int img = t / g.H;
     float s = 0.f;
     for (int i = y % g.sh; i < g.fh; i += g.sh) {
       const int oy = (y - i) / g.sh;
@@ -373,30 +374,53 @@ __global__ void head_bwd_kernel(const float *__restrict__ dq, int B, int nA, int
   }
 }
 
-// Head wgrad (layers.py:325-330): thread per (f, out); fixed row order.
-__global__ void head_wgrad_kernel(const float *__restrict__ x, const float *__restrict__ dq, int B,
-                                  int F, int nA, int dueling, float *__restrict__ gwv,
-                                  float *__restrict__ gbv, float *__restrict__ gwa,
-                                  float *__restrict__ gba) {
+// Head wgrad (layers.py:325-330): a CTA owns 128 consecutive input features
+// (feature F = the bias row); per 64-row chunk the branch gradients
+// (gv = sum_a g, ga = g - gv/nA) and the feature tile are staged in shared
+// memory, then every thread reduces its feature over rows in fixed order.
+constexpr int kHeadRows = 64;
+__global__ void __launch_bounds__(128)
+head_wgrad_kernel(const float *__restrict__ x, const float *__restrict__ dq, int B, int F, int nA,
+                  int dueling, float *__restrict__ gwv, float *__restrict__ gbv,
+                  float *__restrict__ gwa, float *__restrict__ gba) {
+  __shared__ float xs[kHeadRows][128];
+  __shared__ float gs[kHeadRows][kMaxHeadOut];
   const int nout = dueling ? nA + 1 : nA;
-  const int64_t total = (int64_t)(F + 1) * nout;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int f = (int)(e / nout), o = (int)(e % nout);   // f == F -> bias row
-    float s = 0.f;
-    for (int r = 0; r < B; ++r) {
-      const float *g = dq + (int64_t)r * nA;
-      float gr;
+  const int t = threadIdx.x;
+  const int f = blockIdx.x * 128 + t;
+  float acc[kMaxHeadOut];
+#pragma unroll
+  for (int o = 0; o < kMaxHeadOut; ++o) acc[o] = 0.f;
+  for (int r0 = 0; r0 < B; r0 += kHeadRows) {
+    const int nr = min(kHeadRows, B - r0);
+    __syncthreads();
+    for (int r = 0; r < nr; ++r)
+      xs[r][t] = (f < F) ? x[(int64_t)(r0 + r) * F + f] : 1.f;
+    for (int r = t; r < nr; r += 128) {
+      const float *g = dq + (int64_t)(r0 + r) * nA;
       if (dueling) {
         float gv = 0.f;
         for (int a = 0; a < nA; ++a) gv = __fadd_rn(gv, g[a]);
-        gr = (o == 0) ? gv : __fsub_rn(g[o - 1], __fdiv_rn(gv, (float)nA));
+        gs[r][0] = gv;
+        const float gvn = __fdiv_rn(gv, (float)nA);
+        for (int a = 0; a < nA; ++a) gs[r][a + 1] = __fsub_rn(g[a], gvn);
       } else {
-        gr = g[o];
+        for (int a = 0; a < nA; ++a) gs[r][a] = g[a];
       }
-      const float xv = (f < F) ? x[(int64_t)r * F + f] : 1.f;
-      s = fmaf(xv, gr, s);
     }
+    __syncthreads();
+    for (int r = 0; r < nr; ++r) {
+      const float xv = xs[r][t];
+#pragma unroll
+      for (int o = 0; o < kMaxHeadOut; ++o)
+        if (o < nout) acc[o] = fmaf(xv, gs[r][o], acc[o]);
+    }
+  }
+  if (f > F) return;
+#pragma unroll
+  for (int o = 0; o < kMaxHeadOut; ++o) {
+    if (o >= nout) break;
+    const float s = acc[o];
     if (dueling) {
       if (o == 0) {
         if (f < F) gwv[f] = __fadd_rn(gwv[f], s); else gbv[0] = __fadd_rn(gbv[0], s);
@@ -641,9 +665,7 @@ int simt_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *gra
   if (is_head(net, l)) {
     const int F = L.in_h * L.in_w * L.in_c;
     const bool duel = L.kind == DQN_LAYER_DUELING;
-    const int nout = duel ? L.out_c + 1 : L.out_c;
-    const int64_t total = (int64_t)(F + 1) * nout;
-    head_wgrad_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(
+    head_wgrad_kernel<<<(F + 1 + 127) / 128, 128, 0, st>>>(
         (const float *)in, b->dact[l], b->batch, F, L.out_c, duel,
         duel ? grads + L.w_off : nullptr, duel ? grads + L.b_off : nullptr,
         duel ? grads + L.w2_off : grads + L.w_off, duel ? grads + L.b2_off : grads + L.b_off);

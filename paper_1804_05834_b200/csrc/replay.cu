@@ -106,7 +106,23 @@ __device__ __forceinline__ int64_t tree_descend(const double *__restrict__ nodes
                                                 double q, double hi) {
   q = fmin(fmax(q, 1e-300), hi);            // np.clip(q, 1e-300, nextafter(total, 0))
   int64_t n = 1;
-  for (int l = 0; l < depth; ++l) {
+  int l = 0;
+  // two levels per dependent round trip: the left child and both left
+  // grandchildren are loaded together, then the two compare/subtract steps
+  // run exactly as the reference's per-level loop (same operations, order)
+  for (; l + 2 <= depth; l += 2) {
+    const double ls = __ldg(nodes + 2 * n);               // nodes[2n]
+    const double lls = __ldg(nodes + 4 * n);              // nodes[4n]   (left-left)
+    const double rls = __ldg(nodes + 4 * n + 2);          // nodes[4n+2] (right-left)
+    const bool r1 = q > ls;
+    if (r1) q = __dsub_rn(q, ls);
+    const int64_t c = 2 * n + (r1 ? 1 : 0);
+    const double ls2 = r1 ? rls : lls;
+    const bool r2 = q > ls2;
+    if (r2) q = __dsub_rn(q, ls2);
+    n = 2 * c + (r2 ? 1 : 0);
+  }
+  for (; l < depth; ++l) {
     const int64_t left = n << 1;
     const double ls = __ldg(nodes + left);
     const bool right = q > ls;
@@ -312,6 +328,87 @@ tree_update_kernel(double *__restrict__ nodes, int depth, const int64_t *__restr
   }
 }
 
+// update_priorities for learner-sized batches (k <= kSmallK): the same
+// result as tree_update_kernel without a global-memory round trip per level.
+// A node touched this step is (left + right) of children that are either
+// touched too (their new value is published in shared memory) or untouched
+// (their old value can be loaded up front, all levels in parallel).
+constexpr int kSmallK = 256;
+constexpr int kMaxDepth = 32;
+
+__global__ void __launch_bounds__(kSmallK)
+tree_update_small_kernel(double *__restrict__ nodes, int depth, const int64_t *__restrict__ limit_p,
+                         const int64_t *__restrict__ idx, const double *__restrict__ td, int k,
+                         double alpha, double eps, double *__restrict__ max_p, int32_t *flags) {
+  __shared__ int64_t s_node[kSmallK];
+  __shared__ double s_val[kSmallK];
+  __shared__ int s_first_bad;
+  __shared__ double s_red[kSmallK / 32];
+  const int t = threadIdx.x;
+  if (flags && (*flags & (DQN_FLAG_ZERO_TOTAL | DQN_FLAG_NONFINITE_OUT))) return;
+  const int64_t limit = *limit_p;
+  if (t == 0) s_first_bad = k;
+  __syncthreads();
+  int64_t leaf = 0;
+  double v = 0.0, p = -INFINITY;
+  if (t < k) {
+    leaf = idx[t];
+    p = __dadd_rn(fabs(td[t]), eps);                    // |td| + eps
+    bool bad = leaf < 0 || leaf >= limit;
+    if (!bad) {
+      v = pow(p, alpha);                                 // raw ** alpha
+      bad = !(v >= 0.0) || isinf(v);
+    }
+    if (bad) atomicMin(&s_first_bad, t);
+  }
+  __syncthreads();
+  const int kk = s_first_bad;
+  const int64_t node = (int64_t(1) << depth) + leaf;
+  s_node[t] = t < kk ? node : -1;
+  __syncthreads();
+  bool act = t < kk;
+  for (int o = t + 1; act && o < kk; ++o)                // last write wins
+    if (s_node[o] == node) act = false;
+  double sib[kMaxDepth];
+#pragma unroll
+  for (int l = 0; l < kMaxDepth; ++l)
+    if (l < depth) sib[l] = act ? nodes[(node >> l) ^ 1] : 0.0;
+  if (act) nodes[node] = v;
+  double cur = v;
+#pragma unroll
+  for (int l = 0; l < kMaxDepth; ++l) {
+    if (l >= depth) break;
+    __syncthreads();
+    s_node[t] = act ? (node >> l) : -1;
+    s_val[t] = cur;
+    __syncthreads();
+    if (act) {
+      const int64_t me = node >> l, other = me ^ 1;
+      double sv = sib[l];
+      for (int o = 0; o < kk; ++o)
+        if (s_node[o] == other) sv = s_val[o];
+      cur = (me & 1) ? __dadd_rn(sv, cur) : __dadd_rn(cur, sv);   // left + right
+      nodes[me >> 1] = cur;
+    }
+  }
+  if (kk < k) {
+    if (t == kk)
+      raise_flag(flags, (leaf < 0 || leaf >= limit) ? DQN_FLAG_INDEX : DQN_FLAG_BAD_PRIORITY);
+    return;
+  }
+  if (max_p != nullptr) {
+    double m = p;
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((t & 31) == 0) s_red[t >> 5] = m;
+    __syncthreads();
+    if (t == 0) {
+      double mx = s_red[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, s_red[w]);
+      if (mx > *max_p) *max_p = mx;
+    }
+  }
+}
+
 // store (replay.py:207-210): n consecutive slots get max_p^alpha.
 __global__ void __launch_bounds__(kTreeThreads)
 tree_store_kernel(double *__restrict__ nodes, int depth, int64_t capacity, int64_t slot,
@@ -451,6 +548,12 @@ extern "C" int dqn_tree_update(void *stream, double *nodes, int32_t depth, const
                                double eps, double *max_p, int32_t *flags) {
   DQN_CHECK_ARG(nodes && size && idx && td && k >= 0 && depth >= 1, "tree_update: bad args");
   if (k == 0) return DQN_OK;
+  if (k <= kSmallK && depth <= kMaxDepth) {
+    tree_update_small_kernel<<<1, ((k + 31) / 32) * 32, 0, as_stream(stream)>>>(
+        nodes, depth, size, idx, td, k, alpha, eps, max_p, flags);
+    DQN_LAUNCH_CHECK("tree_update_small");
+    return DQN_OK;
+  }
   tree_update_kernel<<<1, kTreeThreads, 0, as_stream(stream)>>>(nodes, depth, size, 0, idx, td, k,
                                                                 alpha, eps, max_p, flags, 0);
   DQN_LAUNCH_CHECK("tree_update");

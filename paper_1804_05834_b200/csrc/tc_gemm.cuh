@@ -29,7 +29,12 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 32;               // fp32 elements per stage (4 MMA k-steps of 8)
-constexpr int kThreads = 128;
+constexpr int kThreads = 256;          // 8 warps: all gather; warps w, w+4 share TMEM lanes
+
+#ifndef DQN_TC_PIECES
+#define DQN_TC_PIECES 2
+#endif
+constexpr int kPieces = DQN_TC_PIECES;  // tf32 pieces per fp32 operand (2: hi/lo, 3: h/m/l)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -134,6 +139,11 @@ __device__ __forceinline__ void store_split(uint32_t base, uint32_t level_stride
   const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
   const float4 r = make_float4(__fsub_rn(v.x, h.x), __fsub_rn(v.y, h.y), __fsub_rn(v.z, h.z),
                                __fsub_rn(v.w, h.w));
+  if (kPieces == 2) {          // hi/lo: lo keeps up to 13 bits, the MMA reads its top 11
+    st_shared_v4(base, h);
+    st_shared_v4(base + level_stride, r);
+    return;
+  }
   const float4 m = make_float4(tf32_hi(r.x), tf32_hi(r.y), tf32_hi(r.z), tf32_hi(r.w));
   const float4 l = make_float4(__fsub_rn(r.x, m.x), __fsub_rn(r.y, m.y), __fsub_rn(r.z, m.z),
                                __fsub_rn(r.w, m.w));
@@ -176,7 +186,7 @@ constexpr int tmem_cols(int bn) { return bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 1
 
 // pipeline depth that fits ~200 KB of operand stages
 constexpr int auto_stages(int bn, bool split_a, bool split_b) {
-  const int bytes = (split_a ? 3 : 1) * BM * BK * 4 + (split_b ? 3 : 1) * bn * BK * 4;
+  const int bytes = (split_a ? kPieces : 1) * BM * BK * 4 + (split_b ? kPieces : 1) * bn * BK * 4;
   const int s = (200 * 1024) / bytes;
   return s > 4 ? 4 : (s < 1 ? 1 : s);
 }
@@ -195,7 +205,7 @@ template <class Pol>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const int nacc) {
   constexpr int BN = Pol::BN, STAGES = Pol::STAGES;
   constexpr int A_BYTES = Smem<BN>::A_BYTES, B_BYTES = Smem<BN>::B_BYTES;
-  constexpr int NA = Pol::SPLIT_A ? 3 : 1, NB = Pol::SPLIT_B ? 3 : 1;
+  constexpr int NA = Pol::SPLIT_A ? kPieces : 1, NB = Pol::SPLIT_B ? kPieces : 1;
   constexpr int STAGE_BYTES = NA * A_BYTES + NB * B_BYTES;
   // accumulator pairs: [a] holds the h*h chain, [nacc + a] the small pieces
   constexpr bool TWO = Pol::SPLIT_A || Pol::SPLIT_B;
@@ -291,14 +301,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
     __syncthreads();
     if (threadIdx.x == 0) {
       tc_fence_after();
-#pragma unroll
       const uint32_t dbig = tmem + (uint32_t)((kb % nacc) * BN);
       const uint32_t dsmall = dbig + (uint32_t)(nacc * BN);
+#pragma unroll
       for (int ks = 0; ks < BK / 8; ++ks) {
         bool first_big = (kb < nacc && ks == 0), first_small = first_big;
-        // piece products with significance 2^0, 2^-11, 2^-22: (ia, ib), ia + ib <= 2
+        // piece products with significance 2^0, 2^-11, 2^-22: (ia, ib), ia + ib < kPieces
 #pragma unroll
-        for (int sum = 0; sum <= 2; ++sum)
+        for (int sum = 0; sum < kPieces; ++sum)
 #pragma unroll
           for (int ia = 0; ia <= sum; ++ia) {
             const int ib = sum - ia;
@@ -321,10 +331,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   // epilogue: TMEM -> registers -> smem (row-major staging) -> coalesced stores
   float *stage = reinterpret_cast<float *>(smem);
   constexpr int ES = Smem<BN>::EPI_STRIDE;
-  const int r = warp * 32 + lane;
+  // warps w and w+4 read the same TMEM lane quarter (w % 4) and split the
+  // 16-column chunks between them
+  const int quarter = warp & 3, half = warp >> 2;
+  const int r = quarter * 32 + lane;
   const int nused = nk < nacc ? nk : nacc;
 #pragma unroll 1
-  for (int c = 0; c < BN; c += 16) {
+  for (int c = 16 * half; c < BN; c += 32) {
     float v[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = 0.f;
@@ -334,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
       const int a = TWO ? (q < nacc ? nacc + q : q - nacc) : q;   // smalls, then bigs
       if ((a % nacc) >= nused) continue;
       float t[16];
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(a * BN + c), t);
+      tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(a * BN + c), t);
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], t[j]);
     }
@@ -359,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
 
 template <class Pol>
 inline int smem_bytes() {
-  constexpr int NA = Pol::SPLIT_A ? 3 : 1, NB = Pol::SPLIT_B ? 3 : 1;
+  constexpr int NA = Pol::SPLIT_A ? kPieces : 1, NB = Pol::SPLIT_B ? kPieces : 1;
   constexpr int pipe = Pol::STAGES * (NA * Smem<Pol::BN>::A_BYTES + NB * Smem<Pol::BN>::B_BYTES);
   constexpr int epi = Smem<Pol::BN>::EPI_BYTES;
   return pipe > epi ? pipe : epi;
