@@ -1,22 +1,28 @@
 // tcgen05 (5th-gen tensor core) implicit-GEMM engine for sm_100a.
 //
-// One CTA = 4 warps computes a 128 x BN tile of C = A * B^T (A: M x K,
+// One CTA = 8 warps computes a 128 x BN tile of C = A * B^T (A: M x K,
 // B: N x K in "math" orientation) with the accumulator in TMEM:
-//   * all 128 threads gather operand chunks (16 B = 4 fp32) from global
+//   * all 256 threads gather operand chunks (16 B = 4 fp32) from global
 //     memory through a Policy (im2col addressing, transposed weights, ...),
-//     split each value exactly into three tf32 pieces (x = h + m + l) and
-//     store them into shared memory in the canonical no-swizzle K-major UMMA
-//     layout (core matrices of 8 rows x 16 B);
-//   * thread 0 issues tcgen05.mma.kind::tf32 (M=128, N=BN, K=8) for the six
-//     significant piece products hh, hm, mh, mm, hl, lh (fp32-grade products;
-//     one bf16/tf32 pass misses the 1e-3 one-step parity
-//     bar, and 3xTF32 (hi/lo) leaves RMSprop-amplified bias errors near it) --
-//     and
-//     tcgen05.commit's an mbarrier per pipeline stage, so the gather of
-//     stage s+1 overlaps the MMAs of stage s;
-//   * the epilogue reads TMEM with tcgen05.ld (warp w owns lanes 32w..32w+31
-//     = tile rows) and hands 16 consecutive columns per thread to the
-//     Policy (bias / ReLU / mask / split-K partial / gradient accumulate).
+//     one k-block ahead in registers, split each value exactly into tf32
+//     pieces (x = hi + lo; kPieces = 3 gives h + m + l) and store them into
+//     shared memory in the canonical no-swizzle K-major UMMA layout (core
+//     matrices of 8 rows x 16 B);
+//   * thread 0 issues tcgen05.mma.kind::tf32 (M=128, N=BN, K=8) for the
+//     significant piece products (hi*hi, hi*lo, lo*hi: "3xTF32") and
+//     tcgen05.commit's an mbarrier per pipeline stage, so the gather of stage
+//     s+1 overlaps the MMAs of stage s;
+//   * accuracy: SURVEY.md App. A -- one bf16/tf32 pass misses the 1e-3
+//     one-step parity bar.  Measured here, the residual error of 3xTF32 is
+//     dominated by the tensor pipe's accumulation rounding, not by the
+//     dropped lo*lo term, so hi*hi and the small products go to separate
+//     TMEM accumulators and the K loop round-robins k-blocks over `nacc`
+//     accumulator pairs; the epilogue sums them in fp32 (~3e-7 rel. vs fp32
+//     SIMT per GEMM);
+//   * the epilogue reads TMEM with tcgen05.ld (warps w and w+4 own lanes
+//     32(w%4)..+31 = tile rows and split the columns), stages the tile
+//     row-major in shared memory and hands coalesced float4s to the Policy
+//     (bias / ReLU / mask / split-K partial / gradient accumulate).
 // Operands that are exact in tf32 (uint8 pixels) use one piece.
 #pragma once
 

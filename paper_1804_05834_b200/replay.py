@@ -88,6 +88,17 @@ def _to_device(x, dtype):
     return torch.as_tensor(np.asarray(x), device="cuda").to(dtype)
 
 
+def _frames(x, dtype):
+    """States for the ring.  Float frames produced by the reference's
+    preprocess_frame are f32(u8)/255 (envs.py:300-311); rounding x*255 maps
+    them back to the exact byte, so a u8 ring reproduces them bit-for-bit."""
+    torch = _torch()
+    t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x))
+    if dtype == torch.uint8 and t.dtype.is_floating_point:
+        t = torch.round(t.to(torch.float64) * 255.0).clamp_(0, 255)
+    return t.to(device="cuda", dtype=dtype)
+
+
 class ReplayMemory:
     """FIFO ring with uniform with-replacement sampling (replay.py:74-124)."""
 
@@ -123,8 +134,8 @@ class ReplayMemory:
     def store(self, transition: Transition) -> int:
         """Insert at the cursor, evicting the oldest (replay.py:91-102)."""
         i = self.cursor
-        self.states[i] = _to_device(transition.state, self.states.dtype).reshape(self.state_shape)
-        self.next_states[i] = _to_device(transition.next_state, self.states.dtype).reshape(self.state_shape)
+        self.states[i] = _frames(transition.state, self.states.dtype).reshape(self.state_shape)
+        self.next_states[i] = _frames(transition.next_state, self.states.dtype).reshape(self.state_shape)
         self.actions[i] = int(transition.action)
         self.rewards[i] = float(transition.reward)
         self.terminals[i] = bool(transition.terminal)
@@ -138,8 +149,8 @@ class ReplayMemory:
         n = len(actions)
         slots = (self.cursor + np.arange(n)) % self.capacity
         sl = torch.as_tensor(slots, device="cuda")
-        self.states[sl] = _to_device(states, self.states.dtype).reshape((n,) + self.state_shape)
-        self.next_states[sl] = _to_device(next_states, self.states.dtype).reshape((n,) + self.state_shape)
+        self.states[sl] = _frames(states, self.states.dtype).reshape((n,) + self.state_shape)
+        self.next_states[sl] = _frames(next_states, self.states.dtype).reshape((n,) + self.state_shape)
         self.actions[sl] = _to_device(actions, torch.int64)
         self.rewards[sl] = _to_device(rewards, torch.float64)
         self.terminals[sl] = _to_device(terminals, torch.bool)
