@@ -525,6 +525,20 @@ def learn_step(online: QNet, target: QNet, mem, opt: RmsPropState, cfg: LearnCfg
         else:
             idx = np.asarray(indices, dtype=np.int64)
             batch = ring.gather(idx, np.full(k, 1.0 / ring.size), np.ones(k))
+    out = learn_on_batch(online, target, batch, cfg)
+    if cfg.grad_clip > 0.0:
+        clip_grads(online, cfg.grad_clip)
+    if per:
+        mem.update_priorities(batch.indices, np.abs(out["td_errors"]))
+    opt.step()
+    return out
+
+
+def learn_on_batch(online: QNet, target: QNet, batch: Batch, cfg: LearnCfg) -> dict:
+    """agent.py:102-126 for a given batch: targets, TD errors, losses, output
+    gradient, backward and gradient accumulation (no optimizer, no priority
+    update).  Used directly by the sharded (data-parallel) restatement."""
+    k = len(batch.actions)
     if cfg.reward_clip:
         batch.rewards = np.clip(batch.rewards, -1.0, 1.0)
     y = td_targets(batch, online, target, cfg.gamma, cfg.double)
@@ -544,10 +558,5 @@ def learn_step(online: QNet, target: QNet, mem, opt: RmsPropState, cfg: LearnCfg
     online.backward(out_grad)
     online.wgrad()
     grads = {kk: v.copy() for kk, v in online.grads.items()}
-    if cfg.grad_clip > 0.0:
-        clip_grads(online, cfg.grad_clip)
-    if per:
-        mem.update_priorities(batch.indices, np.abs(delta))
-    opt.step()
     return dict(batch=batch, targets=y, td_errors=delta, losses=losses, q=q,
                 out_grad=out_grad, grads=grads)

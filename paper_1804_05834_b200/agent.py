@@ -146,6 +146,20 @@ class _StepPlan:
         else:
             self.idx.copy_(self.h_idx, non_blocking=True)
         ring.gather_into(self.idx, k, self.x[:k], self.x[k:], self.a, self.r, self.t)
+        self.enqueue_learn()
+        if self.per:
+            self.memory.update_priorities_dev(self.idx, self.d_out[k:2 * k], k, self.flags)
+        self.opt.enqueue_step(self.flags)
+        if io:
+            self.h_out.copy_(self.d_out, non_blocking=True)
+            self.h_flags.copy_(self.flags, non_blocking=True)
+        del torch
+
+    def enqueue_learn(self) -> None:
+        """Targets, TD loss, backward and wgrad from the batch already in
+        self.x ([s; s']), self.a/r/t and IS weights self.w."""
+        st = _lib.stream_ptr()
+        k = self.k
         on, tg = self.online, self.target
         if self.double:
             on.forward_into(self.x, self.on_bind)
@@ -168,13 +182,6 @@ class _StepPlan:
         if self.grad_clip > 0.0:
             _lib.call("dqn_clip_gradients", st, on.flat_grads.data_ptr(), on.n_flat,
                       self.grad_clip, self.norm.data_ptr())
-        if self.per:
-            self.memory.update_priorities_dev(self.idx, out[k:2 * k], k, self.flags)
-        self.opt.enqueue_step(self.flags)
-        if io:
-            self.h_out.copy_(out, non_blocking=True)
-            self.h_flags.copy_(self.flags, non_blocking=True)
-        del torch
 
     def run(self, use_graph: bool) -> None:
         torch = _lib.require_cuda()

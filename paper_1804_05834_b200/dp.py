@@ -1,0 +1,236 @@
+"""Data-parallel prioritized-replay learner (BASELINE cfg5).
+
+The reference has no distributed mode; its comparator is
+one ``learn_step`` at the global batch K = k * N.  This
+module defines the sharded algorithm and runs it over ``torch.distributed``
+(NCCL on GPUs, gloo on CPU for the tests).  Per learner step, with N ranks
+and per-rank batch k:
+
+1. shards: global transition g lives on rank g % N at local slot g // N
+   (round-robin insertion); each rank owns an fp64 sum tree over its shard;
+2. ``all_gather`` of the shard totals t_r; T = sum_r t_r in rank order, so
+   every rank holds bit-identical T and prefix masses c_r;
+3. global stratification (replay.py:215-229 over the union of shards):
+   q_j = (j + u_j) * (T / K) for j < K with the SAME uniforms on every rank
+   (a common generator); query j belongs to the first shard r with
+   q_j <= c_r + t_r, and its owner descends its own tree with the local mass
+   q_j - c_r (clipped like SumTree.find, replay.py:172-173);
+4. ``all_reduce`` (sum; every entry has exactly one non-zero writer) of the
+   table (owner, local index, leaf priority); P_j = leaf_j / T and
+   w_j = (size * P_j)^-beta / max_j w_j are then computed identically on
+   every rank with numpy (the reference's own np.power semantics);
+5. rank r learns strata j in [r k, (r+1) k): the owners ship those
+   transitions with ``all_to_all_single`` (variable splits);
+6. the loss is a sum over the batch, so ``all_reduce`` (sum) of the per-rank
+   gradients equals the gradient of the global batch (agent.py:110-131);
+7. ``all_gather`` of the TD errors; every owner applies
+   ``update_priorities`` to its leaves in global batch order (last write
+   wins, replay.py:237-240) and every rank updates max_priority with the max
+   over all K errors, so shards stay consistent;
+8. every rank applies the same RMSprop update to identical gradients.
+
+For N = 1 this is exactly ``learn_step`` (same queries, same clip, same
+descent).  The per-rank compute is a ``Backend``: the device backend
+(``DeviceBackend``) runs the libdqn_b200 kernels; the CPU tests plug in the
+oracle.  The host orchestration here is plain numpy + torch.distributed.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+
+# ---------------------------------------------------------------------------
+# sharding math (host, numpy; identical on every rank)
+# ---------------------------------------------------------------------------
+
+def shard_of(g, world: int):
+    """(rank, local slot) of global transition g (round-robin insertion)."""
+    g = np.asarray(g, dtype=np.int64)
+    return g % world, g // world
+
+
+def global_slot(rank: int, local, world: int):
+    return np.asarray(local, dtype=np.int64) * world + rank
+
+
+def global_total(totals: np.ndarray) -> float:
+    """T = t_0 + t_1 + ... in rank order (fp64, sequential)."""
+    s = 0.0
+    for t in np.asarray(totals, dtype=np.float64):
+        s = s + float(t)
+    return s
+
+
+def stratified_queries(totals: np.ndarray, K: int, u: np.ndarray):
+    """Owner rank and local query mass of each of the K strata."""
+    totals = np.asarray(totals, dtype=np.float64)
+    T = global_total(totals)
+    if not T > 0.0:
+        raise ValueError("zero total priority; nothing can be sampled")
+    seg = T / K
+    q = (np.arange(K) + np.asarray(u, dtype=np.float64)) * seg
+    q = np.minimum(np.maximum(q, 1e-300), np.nextafter(T, 0.0))
+    prefix = np.zeros(len(totals) + 1)
+    acc = 0.0
+    for r, t in enumerate(totals):
+        acc = acc + float(t)
+        prefix[r + 1] = acc
+    # first shard whose cumulative mass reaches q (q <= prefix[r+1])
+    owner = np.searchsorted(prefix[1:], q, side="left")
+    owner = np.minimum(owner, len(totals) - 1)
+    # skip empty shards (possible only through rounding at a boundary)
+    for j in np.nonzero(totals[owner] <= 0.0)[0]:
+        r = owner[j]
+        while r < len(totals) - 1 and totals[r] <= 0.0:
+            r += 1
+        owner[j] = r
+    q_local = q - prefix[owner]
+    return owner.astype(np.int64), q_local, T
+
+
+def is_weights(leaf: np.ndarray, T: float, size_total: int, beta: float):
+    """replay.py:227-229 over the global batch."""
+    prob = np.asarray(leaf, dtype=np.float64) / T
+    w = np.power(size_total * prob, -beta)
+    return prob, w / w.max()
+
+
+@dataclass
+class ExchangePlan:
+    """Who sends which strata to whom (all ranks compute the same plan)."""
+    send_counts: list       # to each destination
+    recv_counts: list       # from each source
+    send_strata: np.ndarray  # strata this rank ships, grouped by destination, j order
+    recv_order: np.ndarray  # batch position b -> row in the receive buffer
+
+
+def exchange_plan(owner: np.ndarray, rank: int, world: int, k: int) -> ExchangePlan:
+    K = len(owner)
+    dest = np.arange(K) // k                       # stratum j is learned by rank j // k
+    send_strata = np.nonzero(owner == rank)[0]
+    send_strata = send_strata[np.argsort(dest[send_strata], kind="stable")]
+    send_counts = [int(np.sum((owner == rank) & (dest == d))) for d in range(world)]
+    mine = np.arange(rank * k, (rank + 1) * k)
+    recv_counts = [int(np.sum(owner[mine] == s)) for s in range(world)]
+    # receive buffer = concat over sources s of (my strata owned by s, in j order)
+    offsets = np.concatenate([[0], np.cumsum(recv_counts)[:-1]]).astype(np.int64)
+    recv_order = np.empty(k, dtype=np.int64)
+    seen = [0] * world
+    for b, j in enumerate(mine):
+        s = int(owner[j])
+        recv_order[b] = offsets[s] + seen[s]
+        seen[s] += 1
+    return ExchangePlan(send_counts, recv_counts, send_strata, recv_order)
+
+
+# ---------------------------------------------------------------------------
+# the orchestrator
+# ---------------------------------------------------------------------------
+
+class Backend:
+    """Per-rank compute of one sharded learner step (see DeviceBackend)."""
+
+    def shard_total(self) -> float: ...
+    def shard_size(self) -> int: ...
+    def max_priority(self) -> float: ...
+    def descend(self, q_local: np.ndarray) -> tuple: ...          # -> (local idx, leaf)
+    def pack(self, local_idx: np.ndarray): ...                     # -> dict of tensors
+    def learn(self, batch: dict, weights: np.ndarray): ...         # -> td (k,) np; grads computed
+    def grads(self): ...                                           # flat grad tensor (in place)
+    def apply_update(self, local_idx: np.ndarray, td: np.ndarray, max_p: float) -> None: ...
+    def optimizer_step(self) -> None: ...
+
+
+@dataclass
+class DpStepResult:
+    indices: np.ndarray        # global transition ids of the K strata
+    weights: np.ndarray        # IS weights of the K strata
+    td_errors: np.ndarray      # K TD errors (global batch order)
+    owner: np.ndarray
+
+
+class DataParallelLearner:
+    """Runs the sharded step over a torch.distributed process group."""
+
+    def __init__(self, backend: Backend, k: int, alpha: float, eps: float,
+                 comm_device: str = "cpu", group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.b = backend
+        self.k = int(k)
+        self.alpha, self.eps = float(alpha), float(eps)
+        self.dev = comm_device
+        # the global running max raw priority = max over the shards' maxima
+        self.max_p = float(self._all_gather(
+            np.array([backend.max_priority()], dtype=np.float64)).max())
+
+    # -- collectives on host-side numpy values -------------------------------
+    def _all_gather(self, arr: np.ndarray) -> np.ndarray:
+        import torch
+        t = torch.as_tensor(np.ascontiguousarray(arr), device=self.dev)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return np.concatenate([o.cpu().numpy() for o in out])
+
+    def _all_reduce_sum(self, arr: np.ndarray) -> np.ndarray:
+        import torch
+        t = torch.as_tensor(np.ascontiguousarray(arr), device=self.dev)
+        self.dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
+    def step(self, u: np.ndarray, beta: float) -> DpStepResult:
+        """One global update; ``u`` = rng.random(K) from a generator shared by
+        all ranks, ``beta`` = the annealed exponent for this step."""
+        import torch
+        k, N, r = self.k, self.world, self.rank
+        K = k * N
+        totals = self._all_gather(np.array([self.b.shard_total()], dtype=np.float64))
+        sizes = self._all_gather(np.array([self.b.shard_size()], dtype=np.int64))
+        owner, q_local, T = stratified_queries(totals, K, u)
+        mine = np.nonzero(owner == r)[0]
+        table = np.zeros((K, 2), dtype=np.float64)       # (local index, leaf), owner writes
+        if len(mine):
+            idx, leaf = self.b.descend(q_local[mine])
+            table[mine, 0] = idx
+            table[mine, 1] = leaf
+        table = self._all_reduce_sum(table)
+        local_idx = table[:, 0].astype(np.int64)
+        prob, w = is_weights(table[:, 1], T, int(sizes.sum()), beta)
+        # ship the strata to the ranks that learn them
+        plan = exchange_plan(owner, r, N, k)
+        packed = self.b.pack(local_idx[plan.send_strata])
+        batch = {}
+        for name, t in packed.items():
+            send = t.reshape(len(plan.send_strata), -1) if t.dim() > 1 else t.reshape(-1, 1)
+            send = send.to(self.dev).contiguous()
+            recv = torch.empty((k,) + tuple(send.shape[1:]), dtype=send.dtype, device=self.dev)
+            self.dist.all_to_all_single(recv, send, plan.recv_counts, plan.send_counts,
+                                        group=self.group)
+            recv = recv[torch.as_tensor(plan.recv_order, device=self.dev)]
+            batch[name] = recv.reshape((k,) + tuple(t.shape[1:])) if t.dim() > 1 else recv.reshape(k)
+        mw = w[r * k:(r + 1) * k]
+        td_local = self.b.learn(batch, mw)
+        g = self.b.grads()
+        gd = g if str(g.device).startswith(self.dev.split(":")[0]) else g.to(self.dev)
+        self.dist.all_reduce(gd, group=self.group)
+        if gd is not g:
+            g.copy_(gd)
+        td = self._all_gather(np.asarray(td_local, dtype=np.float64))
+        # owners update their leaves in global batch order; max over all K
+        self.max_p = max(self.max_p, float((np.abs(td) + self.eps).max()))
+        if len(mine):
+            self.b.apply_update(local_idx[mine], np.abs(td[mine]), self.max_p)
+        self.b.optimizer_step()
+        gidx = global_slot(owner, local_idx, N)
+        return DpStepResult(indices=gidx, weights=w, td_errors=td, owner=owner)
+
+
+def max_priority_leaf(max_p: float, alpha: float) -> float:
+    return math.pow(max_p, alpha)
