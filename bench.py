@@ -16,9 +16,11 @@ Our arm (default) prints ONE JSON line on rank 0:
   cpu_baseline  the CPU oracle port of the reference learn_step on this
              host's cores for a bounded sample.
 ``--impl reference`` times that CPU path alone and prints its own line.
-Under torchrun (N > 1) every rank runs an independent replica (population of
-seeds, no communication; SURVEY.md §8(e) "replicas only") and rank 0 reports
-the max-over-ranks device time.
+Under torchrun (N > 1) the default is the cfg5 data-parallel learner
+(paper_1804_05834_b200/dp.py: replay sharded across the ranks, global
+stratified PER over all-gathered shard totals, per-GPU batch 32, NCCL
+gradient all-reduce); ``--mode replicas`` runs independent learners instead
+(population of seeds).  Rank 0 reports the max-over-ranks time.
 """
 
 from __future__ import annotations
@@ -449,6 +451,79 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_dp(args):
+    """cfg5: data-parallel learner, replay sharded over the ranks (capacity /
+    N each), global stratified PER over shard totals, per-rank batch 32,
+    NCCL gradient all-reduce (paper_1804_05834_b200/dp.py).  value = batch-32
+    learner updates/s summed over the GPUs (= transitions/s / 32)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1804_05834_b200 as P
+    from paper_1804_05834_b200 import _lib, dp
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl")
+    c = CONFIGS["cfg4"]
+    cap = (args.capacity or c["capacity"]) // world
+    k = args.batch
+    cfg = P.RunConfig(batch_size=k, double=True, dueling=True, beta_end_step=50_000_000)
+    on = P.build_network("atari", (84, 84, 4), 4, True)
+    tg = P.build_network("atari", (84, 84, 4), 4, True)
+    P.init_params(on, np.random.SeedSequence([1, 3]))          # identical on every rank
+    P.sync_target(on, tg)
+    opt = P.RmsProp(on, cfg.learning_rate, cfg.rms_decay, cfg.rms_epsilon)
+    mem = P.PrioritizedReplay(cap, (84, 84, 4), P.PriorityConfig(0.6, 0.01, cfg.beta_schedule()))
+    mem.fill_synthetic(100 + rank, cap)
+    learner = dp.DataParallelLearner(dp.DeviceBackend(on, tg, mem, opt, cfg), k, 0.6, 0.01, "cuda")
+    rng = np.random.default_rng(np.random.SeedSequence([1, 2]))  # common draws on all ranks
+    step0 = 50_000
+    for s in range(args.warmup):
+        learner.step(rng.random(k * world), mem.beta(step0 + s))
+    n0 = _lib.lib.dqn_launch_count()
+    learner.step(rng.random(k * world), mem.beta(step0 + args.warmup))
+    launches = int(_lib.lib.dqn_launch_count() - n0)
+    stream = torch.cuda.current_stream()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(stream)
+        t0 = time.perf_counter()
+        for s in range(args.steps):
+            learner.step(rng.random(k * world), mem.beta(step0 + 100 + s))
+            if (s + 1) % TARGET_SYNC_UPDATES == 0:
+                P.sync_target(on, tg)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    ms = max(e0.elapsed_time(e1), wall * 1e3)
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = world * args.steps / (ms / 1e3)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT + " (batch-32 updates, all GPUs)",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (hash-generated u8 frames per shard, random-init nets)",
+            "config": {"workload": "cfg5 Dueling+Double+PER data-parallel, replay sharded",
+                       "capacity": cap * world, "global_batch": k * world, "per_gpu_batch": k,
+                       "parallelism": f"dp{world} (sharded PER, NCCL allreduce)"},
+            "transitions_per_sec": value * k,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 8 * (k * world + 1),
+                    "d2h_bytes_per_step": 8 * 3 * k * world,
+                    "path": "dp.DataParallelLearner.step (host-orchestrated, every step)"},
+            "gpu_launches": launches * args.steps, "launches_per_step": launches,
+            "clocks": clk.summary(), "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -460,11 +535,17 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", default="auto", choices=["auto", "single", "replicas", "dp"],
+                    help="auto: single GPU at N=1, data-parallel (cfg5) under torchrun; "
+                         "replicas: independent learners per GPU (population of seeds)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world = dist_env()[1]
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "dp" or (args.mode == "auto" and world > 1):
+        run_dp(args)
     else:
         run_ours(args)
 

@@ -234,3 +234,69 @@ class DataParallelLearner:
 
 def max_priority_leaf(max_p: float, alpha: float) -> float:
     return math.pow(max_p, alpha)
+
+
+class DeviceBackend(Backend):
+    """The rank-local compute on the GPU: the shard's sum tree and ring in
+    HBM, descent/gather/learn/update/RMSprop through libdqn_b200 (the same
+    kernels and step plan as ``learn_step``)."""
+
+    def __init__(self, online, target, memory, optimizer, config):
+        from . import agent
+        from .replay import PrioritizedReplay
+        if not isinstance(memory, PrioritizedReplay):
+            raise ValueError("the data-parallel learner shards a PrioritizedReplay")
+        self.plan = agent._StepPlan(online, target, memory, optimizer, config)
+        self.mem, self.on, self.opt = memory, online, optimizer
+
+    def shard_total(self) -> float:
+        return self.mem.tree.total
+
+    def shard_size(self) -> int:
+        return self.mem.size
+
+    def max_priority(self) -> float:
+        return self.mem.max_priority
+
+    def descend(self, q_local):
+        tree = self.mem.tree
+        idx = tree.find(np.asarray(q_local, dtype=np.float64))
+        leaf = tree.nodes[tree._leaf_base + idx]
+        return idx.cpu().numpy(), leaf.cpu().numpy()
+
+    def pack(self, local_idx):
+        import torch
+        ring = self.mem.memory
+        n = len(local_idx)
+        idx = torch.as_tensor(np.asarray(local_idx, dtype=np.int64), device="cuda")
+        s = torch.empty((n,) + ring.state_shape, dtype=ring.states.dtype, device="cuda")
+        s2 = torch.empty_like(s)
+        a = torch.empty(n, dtype=torch.int64, device="cuda")
+        r = torch.empty(n, dtype=torch.float64, device="cuda")
+        t = torch.empty(n, dtype=torch.uint8, device="cuda")
+        if n:
+            ring.gather_into(idx, n, s, s2, a, r, t)
+        return {"s": s, "s2": s2, "a": a, "r": r, "t": t}
+
+    def learn(self, batch, weights):
+        import torch
+        p = self.plan
+        k = p.k
+        p.x[:k].copy_(batch["s"])
+        p.x[k:].copy_(batch["s2"])
+        p.a.copy_(batch["a"])
+        p.r.copy_(batch["r"])
+        p.t.copy_(batch["t"].to(torch.bool))
+        p.w.copy_(torch.as_tensor(np.asarray(weights, dtype=np.float64)))
+        p.enqueue_learn()
+        return p.d_out[k:2 * k].cpu().numpy()
+
+    def grads(self):
+        return self.on.flat_grads
+
+    def apply_update(self, local_idx, td, max_p):
+        self.mem.update_priorities(np.asarray(local_idx, dtype=np.int64), td)
+        self.mem.max_priority = max_p
+
+    def optimizer_step(self) -> None:
+        self.opt.step()
