@@ -126,7 +126,11 @@ class _StepPlan:
         on_rows = 2 * k if self.double else k
         self.on_bind = online.binding(on_rows)
         self.on_view = online.prefix_binding(self.on_bind, k) if self.double else self.on_bind
+        # wgrad runs on a side stream concurrently with the dgrad chain: it
+        # gets a view with its own scratch (split-K partials and counters)
+        self.on_wview = online.prefix_binding(self.on_bind, k, own_scratch=True)
         self.tg_bind = target.binding(k)
+        self.side = torch.cuda.Stream()
         self.graph = None
         self.calls = 0
         self.h2d_bytes = (k + 1) * 8 if self.per else k * 8
@@ -157,15 +161,30 @@ class _StepPlan:
 
     def enqueue_learn(self) -> None:
         """Targets, TD loss, backward and wgrad from the batch already in
-        self.x ([s; s']), self.a/r/t and IS weights self.w."""
+        self.x ([s; s']), self.a/r/t and IS weights self.w.
+
+        Two streams (both captured into the step's CUDA graph): the target
+        forward runs beside the online forward, and each layer's wgrad runs
+        beside the rest of the dgrad chain as soon as that layer's output
+        gradient exists (it has its own scratch / split-K counters)."""
+        torch = _lib.require_cuda()
         st = _lib.stream_ptr()
         k = self.k
         on, tg = self.online, self.target
+        s0, s1 = torch.cuda.current_stream(), self.side
+        ev = torch.cuda.Event
+        e_in = ev()
+        e_in.record(s0)
+        with torch.cuda.stream(s1):
+            s1.wait_event(e_in)
+            tg.forward_into(self.x[k:], self.tg_bind)
+            e_tg = ev()
+            e_tg.record(s1)
         if self.double:
             on.forward_into(self.x, self.on_bind)
         else:
             on.forward_into(self.x[:k], self.on_bind)
-        tg.forward_into(self.x[k:], self.tg_bind)
+        s0.wait_event(e_tg)
         nA = self.nA
         q_on = self.on_bind.act[-1]
         out = self.d_out
@@ -175,10 +194,23 @@ class _StepPlan:
                   self.t.data_ptr(), self.w.data_ptr(), k, nA, self.gamma, self.flags_td,
                   out[:k].data_ptr(), out[k:2 * k].data_ptr(), out[2 * k:3 * k].data_ptr(),
                   self.on_view.dact[-1].data_ptr(), out[3 * k:].data_ptr())
-        self.on_view.x = self.x[:k]
-        self.on_view.struct.x = self.x.data_ptr()
-        on.backward_from(self.on_view, need_input_grad=False)
-        on.wgrad_into(self.on_view)
+        for v in (self.on_view, self.on_wview):
+            v.x = self.x[:k]
+            v.struct.x = self.x.data_ptr()
+            v.struct.dx = None                     # conv1 dX is never needed
+        e = ev()
+        e.record(s0)
+        for layer in reversed(range(len(on._units))):
+            with torch.cuda.stream(s1):           # wgrad of `layer` once its grad exists
+                s1.wait_event(e)
+                on.layer_into(self.on_wview, layer, 2)
+            if layer > 0:                          # dgrad chain continues on s0
+                on.layer_into(self.on_view, layer, 1)
+                e = ev()
+                e.record(s0)
+        e_w = ev()
+        e_w.record(s1)
+        s0.wait_event(e_w)
         if self.grad_clip > 0.0:
             _lib.call("dqn_clip_gradients", st, on.flat_grads.data_ptr(), on.n_flat,
                       self.grad_clip, self.norm.data_ptr())

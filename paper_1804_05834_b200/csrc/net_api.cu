@@ -17,7 +17,7 @@ int simt_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *gra
                      const dqn_binding *b);
 int64_t simt_scratch_floats(const dqn_net_desc *net, int batch);
 int simt_validate(const dqn_net_desc *net);
-bool tc_layer_supported(const dqn_net_desc *net, int l);
+bool tc_layer_supported(const dqn_net_desc *net, int l, int phase);
 int64_t tc_scratch_floats(const dqn_net_desc *net, int batch);
 int tc_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
                      const dqn_binding *b);
@@ -27,28 +27,31 @@ int tc_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads
                    const dqn_binding *b);
 
 // tcgen05 trunk for supported geometries unless the descriptor asks for SIMT
-static bool use_tc(const dqn_net_desc *net, int l) {
-  return net->algo != 1 && tc_layer_supported(net, l);
+static bool use_tc(const dqn_net_desc *net, int l, int phase) {
+  return net->algo != 1 && tc_layer_supported(net, l, phase);
 }
 
+// SIMT and tcgen05 partial buffers share the front of the scratch; the
+// split-K tile-counter table (kTileCounters ints) always sits after both.
+constexpr int64_t kTileCounters = 4096;   // == tc::kMaxTiles
 static int64_t scratch_need(const dqn_net_desc *net, int batch) {
   const int64_t a = simt_scratch_floats(net, batch), b = tc_scratch_floats(net, batch);
-  return a > b ? a : b;
+  return (a > b ? a : b) + kTileCounters;
 }
 
 static int layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
                          const dqn_binding *b, int32_t *flags) {
-  if (use_tc(net, l)) return tc_layer_forward(st, net, l, params, b);
+  if (use_tc(net, l, 0)) return tc_layer_forward(st, net, l, params, b);
   return simt_layer_forward(st, net, l, params, b, flags);
 }
 static int layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
                           const dqn_binding *b) {
-  if (use_tc(net, l)) return tc_layer_backward(st, net, l, params, b);
+  if (use_tc(net, l, 1)) return tc_layer_backward(st, net, l, params, b);
   return simt_layer_backward(st, net, l, params, b);
 }
 static int layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
                        const dqn_binding *b) {
-  if (use_tc(net, l)) return tc_layer_wgrad(st, net, l, grads, b);
+  if (use_tc(net, l, 2)) return tc_layer_wgrad(st, net, l, grads, b);
   return simt_layer_wgrad(st, net, l, grads, b);
 }
 

@@ -48,13 +48,21 @@ constexpr int kGatherChunk = kGatherThreads * kGatherUnroll;  // int4 per CTA
 __global__ void __launch_bounds__(kGatherThreads)
 ring_gather_vec_kernel(const int4 *__restrict__ states, const int4 *__restrict__ next_states,
                        int64_t slot_vecs, const int64_t *__restrict__ idx,
-                       int4 *__restrict__ out_s, int4 *__restrict__ out_s2) {
+                       int4 *__restrict__ out_s, int4 *__restrict__ out_s2,
+                       const int64_t *__restrict__ actions, const double *__restrict__ rewards,
+                       const uint8_t *__restrict__ terminals, int64_t *out_a, double *out_r,
+                       uint8_t *out_t) {
   const int j = blockIdx.y;
   const int which = blockIdx.z;
+  const int64_t slot = __ldg(idx + j);
+  if (blockIdx.x == 0 && which == 0 && threadIdx.x == 0) {   // the sample's metadata
+    if (out_a) out_a[j] = actions[slot];
+    if (out_r) out_r[j] = rewards[slot];
+    if (out_t) out_t[j] = terminals[slot];
+  }
   const int4 *src = which ? next_states : states;
   int4 *dst = which ? out_s2 : out_s;
   if (dst == nullptr) return;
-  const int64_t slot = __ldg(idx + j);
   const int4 *s = src + slot * slot_vecs;
   int4 *d = dst + (int64_t)j * slot_vecs;
   const int64_t base = (int64_t)blockIdx.x * kGatherChunk + threadIdx.x;
@@ -409,6 +417,67 @@ tree_update_small_kernel(double *__restrict__ nodes, int depth, const int64_t *_
   }
 }
 
+// update_priorities for k <= 32 (the learner's batch): one warp, no shared
+// memory or barriers.  Lanes whose paths meet are found with
+// __match_any_sync; a node's untouched child comes from the up-front sibling
+// loads, a touched one from the lane that owns it (__shfl_sync).
+__global__ void __launch_bounds__(32)
+tree_update_warp_kernel(double *__restrict__ nodes, int depth, const int64_t *__restrict__ limit_p,
+                        const int64_t *__restrict__ idx, const double *__restrict__ td, int k,
+                        double alpha, double eps, double *__restrict__ max_p, int32_t *flags) {
+  constexpr unsigned FULL = 0xffffffffu;
+  if (flags && (*flags & (DQN_FLAG_ZERO_TOTAL | DQN_FLAG_NONFINITE_OUT))) return;
+  const int t = threadIdx.x;
+  const int64_t limit = *limit_p;
+  int64_t leaf = 0;
+  double v = 0.0, p = -INFINITY;
+  bool bad = false;
+  if (t < k) {
+    leaf = idx[t];
+    p = __dadd_rn(fabs(td[t]), eps);                     // |td| + eps
+    bad = leaf < 0 || leaf >= limit;
+    if (!bad) {
+      v = pow(p, alpha);                                  // raw ** alpha
+      bad = !(v >= 0.0) || isinf(v);
+    }
+  }
+  const unsigned badmask = __ballot_sync(FULL, bad);
+  const int kk = badmask ? __ffs(badmask) - 1 : k;       // first failing position
+  const bool valid = t < kk;
+  const int64_t node = (int64_t(1) << depth) + leaf;
+  const long long uniq = -1 - (long long)t;               // never equal to a node id
+  const unsigned same_leaf = __match_any_sync(FULL, valid ? (long long)node : uniq);
+  const bool act = valid && (31 - __clz(same_leaf)) == t;  // last write wins
+  double sib[kMaxDepth];
+#pragma unroll
+  for (int l = 0; l < kMaxDepth; ++l)
+    if (l < depth) sib[l] = act ? nodes[(node >> l) ^ 1] : 0.0;
+  if (act) nodes[node] = v;
+  double cur = v;
+#pragma unroll
+  for (int l = 0; l < kMaxDepth; ++l) {
+    if (l >= depth) break;
+    const int64_t me = node >> l;
+    const unsigned fam = __match_any_sync(FULL, act ? (long long)(me >> 1) : uniq);
+    const unsigned self = __match_any_sync(FULL, act ? (long long)me : uniq);
+    const unsigned other = fam & ~self;                   // lanes holding the sibling
+    const double shared = __shfl_sync(FULL, cur, other ? __ffs(other) - 1 : t);
+    const double sv = other ? shared : sib[l];
+    cur = (me & 1) ? __dadd_rn(sv, cur) : __dadd_rn(cur, sv);   // left + right
+    if (act) nodes[me >> 1] = cur;
+  }
+  if (kk < k) {
+    if (t == kk)
+      raise_flag(flags, (leaf < 0 || leaf >= limit) ? DQN_FLAG_INDEX : DQN_FLAG_BAD_PRIORITY);
+    return;
+  }
+  if (max_p != nullptr) {
+    double m = p;
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+    if (t == 0 && m > *max_p) *max_p = m;
+  }
+}
+
 // store (replay.py:207-210): n consecutive slots get max_p^alpha.
 __global__ void __launch_bounds__(kTreeThreads)
 tree_store_kernel(double *__restrict__ nodes, int depth, int64_t capacity, int64_t slot,
@@ -468,18 +537,21 @@ extern "C" int dqn_ring_gather(void *stream, const uint8_t *states, const uint8_
   DQN_CHECK_ARG(idx && k >= 0 && slot_bytes > 0, "ring_gather: bad args");
   if (k == 0) return DQN_OK;
   cudaStream_t st = as_stream(stream);
+  const bool vec = (out_states || out_next_states) && slot_bytes % 16 == 0 &&
+                   ((uintptr_t)states % 16 == 0) && ((uintptr_t)next_states % 16 == 0) &&
+                   ((uintptr_t)out_states % 16 == 0) && ((uintptr_t)out_next_states % 16 == 0);
+  if (vec) {   // frames + metadata in one launch
+    const int64_t vecs = slot_bytes / 16;
+    dim3 grid((unsigned)((vecs + kGatherChunk - 1) / kGatherChunk), (unsigned)k, 2);
+    ring_gather_vec_kernel<<<grid, kGatherThreads, 0, st>>>(
+        reinterpret_cast<const int4 *>(states), reinterpret_cast<const int4 *>(next_states), vecs,
+        idx, reinterpret_cast<int4 *>(out_states), reinterpret_cast<int4 *>(out_next_states),
+        actions, rewards, terminals, out_actions, out_rewards, out_terminals);
+    DQN_LAUNCH_CHECK("ring_gather");
+    return DQN_OK;
+  }
   if (out_states || out_next_states) {
-    const bool vec = slot_bytes % 16 == 0 && ((uintptr_t)states % 16 == 0) &&
-                     ((uintptr_t)next_states % 16 == 0) && ((uintptr_t)out_states % 16 == 0) &&
-                     ((uintptr_t)out_next_states % 16 == 0);
-    if (vec) {
-      const int64_t vecs = slot_bytes / 16;
-      dim3 grid((unsigned)((vecs + kGatherChunk - 1) / kGatherChunk), (unsigned)k, 2);
-      ring_gather_vec_kernel<<<grid, kGatherThreads, 0, st>>>(
-          reinterpret_cast<const int4 *>(states), reinterpret_cast<const int4 *>(next_states),
-          vecs, idx, reinterpret_cast<int4 *>(out_states),
-          reinterpret_cast<int4 *>(out_next_states));
-    } else {
+    {
       dim3 grid((unsigned)((slot_bytes + 255) / 256 < 64 ? (slot_bytes + 255) / 256 : 64),
                 (unsigned)k, 2);
       ring_gather_bytes_kernel<<<grid, 256, 0, st>>>(states, next_states, slot_bytes, idx,
@@ -548,6 +620,12 @@ extern "C" int dqn_tree_update(void *stream, double *nodes, int32_t depth, const
                                double eps, double *max_p, int32_t *flags) {
   DQN_CHECK_ARG(nodes && size && idx && td && k >= 0 && depth >= 1, "tree_update: bad args");
   if (k == 0) return DQN_OK;
+  if (k <= 32 && depth <= kMaxDepth) {
+    tree_update_warp_kernel<<<1, 32, 0, as_stream(stream)>>>(nodes, depth, size, idx, td, k, alpha,
+                                                             eps, max_p, flags);
+    DQN_LAUNCH_CHECK("tree_update_warp");
+    return DQN_OK;
+  }
   if (k <= kSmallK && depth <= kMaxDepth) {
     tree_update_small_kernel<<<1, ((k + 31) / 32) * 32, 0, as_stream(stream)>>>(
         nodes, depth, size, idx, td, k, alpha, eps, max_p, flags);

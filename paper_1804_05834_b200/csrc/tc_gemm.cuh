@@ -190,19 +190,140 @@ struct Smem {
 
 constexpr int tmem_cols(int bn) { return bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256; }
 
-// pipeline depth that fits ~200 KB of operand stages
+// pipeline depth: the register-staged prefetch already overlaps the next
+// gather with the MMAs, so two stages suffice; keeping a CTA under ~110 KB
+// of shared memory lets two CTAs share an SM (16 warps hiding gather latency)
 constexpr int auto_stages(int bn, bool split_a, bool split_b) {
   const int bytes = (split_a ? kPieces : 1) * BM * BK * 4 + (split_b ? kPieces : 1) * bn * BK * 4;
-  const int s = (200 * 1024) / bytes;
-  return s > 4 ? 4 : (s < 1 ? 1 : s);
+  const int s = (110 * 1024) / bytes;
+  return s > 2 ? 2 : (s < 1 ? 1 : s);
 }
 
+__device__ __forceinline__ float comp(const float4 &v, int j) {
+  return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
+}
+
+// Gathers one R x BK operand tile per k-block into registers and stores it
+// K-major.  Units are owned by thread u % 256 with the same rows in every
+// k-block, so row bases are computed once.
+//  * MNC == false (source contiguous along k): unit = chunk (row, 4 k), one
+//    16-byte load via f1(base, k, kend);
+//  * MNC == true (source contiguous along rows, e.g. W[k][n] or dY[pix][co]):
+//    unit = 4 rows x 4 k, four 16-byte loads along the rows via
+//    f4(base, k, kend, v[4]) (consecutive lanes = consecutive row quads =
+//    coalesced), transposed in registers into four K-major chunks.
+// Optionally accumulates the per-row sums of everything stored (bias grads).
+template <bool MNC, int R>
+struct Gather {
+  static constexpr int UNITS = MNC ? R * BK / 16 : R * BK / 4;
+  static constexpr int U = (UNITS + kThreads - 1) / kThreads;
+  static constexpr int V = MNC ? 4 : 1;
+  long long base[U];
+  float4 v[U][V];
+  float bsum[U][V];
+
+  __device__ static void coords(int u, int &row, int &k) {
+    if (!MNC) {
+      chunk_coords(u, row, k);
+    } else {
+      const int q = u % (R / 4), kc = u / (R / 4);
+      row = 4 * q;
+      k = 4 * kc;
+    }
+  }
+  template <class RowFn>
+  __device__ void init(RowFn rowfn) {
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const int u = threadIdx.x + i * kThreads;
+      int row, k;
+      coords(u, row, k);
+      base[i] = u < UNITS ? rowfn(row) : -1;
+#pragma unroll
+      for (int j = 0; j < V; ++j) bsum[i][j] = 0.f;
+    }
+  }
+  template <class F1, class F4>
+  __device__ void fetch(int k0, int kend, F1 &&f1, F4 &&f4) {
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const int u = threadIdx.x + i * kThreads;
+      int row, k;
+      coords(u, row, k);
+      if (base[i] < 0) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) v[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else if constexpr (!MNC) {
+        v[i][0] = f1(base[i], k0 + k, kend);
+      } else {
+        f4(base[i], k0 + k, kend, v[i]);
+      }
+    }
+  }
+  __device__ void store(uint32_t tile, uint32_t piece_stride, int pieces, bool bias) {
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const int u = threadIdx.x + i * kThreads;
+      if (u >= UNITS) continue;
+      int row, k;
+      coords(u, row, k);
+      if constexpr (!MNC) {
+        store_split(tile + chunk_off(R, row, k), piece_stride, v[i][0], pieces);
+        if (bias)
+          bsum[i][0] = __fadd_rn(bsum[i][0], __fadd_rn(__fadd_rn(v[i][0].x, v[i][0].y),
+                                                       __fadd_rn(v[i][0].z, v[i][0].w)));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 c = make_float4(comp(v[i][0], j), comp(v[i][1], j), comp(v[i][2], j),
+                                       comp(v[i][3], j));
+          store_split(tile + chunk_off(R, row + j, k), piece_stride, c, pieces);
+          if (bias)
+            bsum[i][j] =
+                __fadd_rn(bsum[i][j], __fadd_rn(__fadd_rn(c.x, c.y), __fadd_rn(c.z, c.w)));
+        }
+      }
+    }
+  }
+  template <int RR>
+  __device__ void dump_bias(float (&red)[RR][8]) const {
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const int u = threadIdx.x + i * kThreads;
+      if (u >= UNITS) continue;
+      int row, k;
+      coords(u, row, k);
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+        if (row + j < RR) red[row + j][k >> 2] = bsum[i][j];
+    }
+  }
+};
+
+// Policies derive from this; it supplies the gather form a policy does not
+// use (never called: the Gather of that operand uses the other form).
+struct PolBase {
+  __device__ float4 a(long long, int, int) const { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ float4 b(long long, int, int) const { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ void a4(long long, int, int, float4 (&)[4]) const {}
+  __device__ void b4(long long, int, int, float4 (&)[4]) const {}
+};
+
+// Split-K tiles count arrivals in a per-binding int table (the tail of the
+// binding scratch, zero-initialised); the last CTA resets its counter, so the
+// table is all-zero between launches (graph-replay safe) and two kernels on
+// different streams with different bindings never share counters.
+constexpr int kMaxTiles = 4096;
+
 // Policy interface (all __device__, const):
-//   static constexpr int BN, STAGES; static constexpr bool SPLIT_A, SPLIT_B;
-//   int M, N;  int kbeg(z), kend(z);
+//   static constexpr int BN, STAGES; static constexpr bool SPLIT_A, SPLIT_B, BIAS_FROM_B;
+//   int M, N, ksplits;  int kbeg(split), kend(split);
+//   float *partial ([problems][ksplits][M][N] when ksplits > 1)
+//   gridDim.z = problems * ksplits; a_row/b_row/final4 get the problem index
 //   long long a_row(m) / b_row(n)          -- per-row base (-1: row out of range)
 //   float4 a(base, k, kend) / b(base, k, kend) -- values at k..k+3 (0 beyond kend)
-//   void store4(m, n, float4 v, z)         -- epilogue for columns n..n+3 of row m
+//   void final4(m, n, float4 v)            -- epilogue for columns n..n+3 of row m
+//   BIAS_FROM_B: float *bias_out (+= column sums of B over k), *bias_partial
 // nacc: the K loop of a tile round-robins its k-blocks over nacc TMEM
 // accumulators that the epilogue sums in fixed order -- shorter tensor-core
 // accumulation chains (each chain rounds in the tensor pipe) for ~fp32-SIMT
@@ -217,11 +338,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   constexpr bool TWO = Pol::SPLIT_A || Pol::SPLIT_B;
   const int TCOLS = tmem_cols(BN * nacc * (TWO ? 2 : 1));
   constexpr uint32_t IDESC = make_idesc_tf32(BN, false, false);   // both K-major
-  constexpr int CA = BM * BK / 4 / kThreads;                      // A chunks per thread (8)
-  constexpr int CB = (BN * BK / 4 + kThreads - 1) / kThreads;     // B chunks per thread
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[STAGES];
   __shared__ uint32_t tmem_slot;
+  __shared__ float bias_red[Pol::BIAS_FROM_B ? BN : 1][8];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {
@@ -238,25 +358,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   }
 
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, z = blockIdx.z;
-  const int kbeg = p.kbeg(z), kend = p.kend(z);
+  // blockIdx.z = problem * ksplits + split: a split of K (partials +
+  // last-CTA fixup) and an independent problem index (e.g. a stride phase)
+  const int ks = p.ksplits, zs = z % ks, zp = z / ks;
+  const bool SPLITK = ks > 1;
+  const int kbeg = p.kbeg(zs), kend = p.kend(zs);
+  float *const part = p.partial + (SPLITK ? (int64_t)zp * ks * p.M * p.N : 0);
   const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
   const uint32_t sbase = smem_u32(smem);
 
-  // per-thread row bases (same rows in every k-block)
-  long long abase[CA], bbase[CB];
-#pragma unroll
-  for (int i = 0; i < CA; ++i) {
-    int row, k;
-    chunk_coords(threadIdx.x + i * kThreads, row, k);
-    abase[i] = p.a_row(m0 + row);
-  }
-#pragma unroll
-  for (int i = 0; i < CB; ++i) {
-    const int c = threadIdx.x + i * kThreads;
-    int row, k;
-    chunk_coords(c, row, k);
-    bbase[i] = (c < BN * BK / 4) ? p.b_row(n0 + row) : -1;
-  }
+  // operand gathers (rows fixed per thread across k-blocks; see Gather)
+  Gather<Pol::A_MNC, BM> ga;
+  Gather<Pol::B_MNC, BN> gb;
+  ga.init([&](int r) { return p.a_row(m0 + r, zp); });
+  gb.init([&](int r) { return p.b_row(n0 + r, zp); });
 
   tc_fence_before();
   __syncthreads();
@@ -265,43 +380,23 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
 
   // register-staged prefetch: tile kb+1 is in flight while tile kb is
   // committed to smem and multiplied
-  float4 ra[CA], rb[CB];
   auto fetch = [&](int k0) {
-#pragma unroll
-    for (int i = 0; i < CA; ++i) {
-      int row, k;
-      chunk_coords(threadIdx.x + i * kThreads, row, k);
-      ra[i] = abase[i] >= 0 ? p.a(abase[i], k0 + k, kend) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int i = 0; i < CB; ++i) {
-      int row, k;
-      chunk_coords(threadIdx.x + i * kThreads, row, k);
-      rb[i] = bbase[i] >= 0 ? p.b(bbase[i], k0 + k, kend) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    // generic lambdas: only the form matching the policy's layout is instantiated
+    ga.fetch(k0, kend, [&](auto b, int k, int ke) { return p.a(b, k, ke); },
+             [&](auto b, int k, int ke, auto &v) { p.a4(b, k, ke, v); });
+    gb.fetch(k0, kend, [&](auto b, int k, int ke) { return p.b(b, k, ke); },
+             [&](auto b, int k, int ke, auto &v) { p.b4(b, k, ke, v); });
   };
   if (nk > 0) fetch(kbeg);
+  const bool want_bias = Pol::BIAS_FROM_B && blockIdx.x == 0;
 
   for (int kb = 0; kb < nk; ++kb) {
     const int s = kb % STAGES;
     if (kb >= STAGES) mbar_wait(&bars[s], ((kb / STAGES) - 1) & 1);
     const uint32_t st = sbase + s * STAGE_BYTES;
     const uint32_t a_t = st, b_t = st + NA * A_BYTES;     // piece p at +p*A_BYTES / +p*B_BYTES
-#pragma unroll
-    for (int i = 0; i < CA; ++i) {
-      int row, k;
-      chunk_coords(threadIdx.x + i * kThreads, row, k);
-      store_split(a_t + chunk_off(BM, row, k), A_BYTES, ra[i], NA);
-    }
-#pragma unroll
-    for (int i = 0; i < CB; ++i) {
-      const int c = threadIdx.x + i * kThreads;
-      if (c < BN * BK / 4) {
-        int row, k;
-        chunk_coords(c, row, k);
-        store_split(b_t + chunk_off(BN, row, k), B_BYTES, rb[i], NB);
-      }
-    }
+    ga.store(a_t, A_BYTES, NA, false);
+    gb.store(b_t, B_BYTES, NB, want_bias);
     if (kb + 1 < nk) fetch(kbeg + (kb + 1) * BK);
     fence_proxy_async();
     __syncthreads();
@@ -368,8 +463,66 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   for (int idx = threadIdx.x; idx < BM * C4; idx += kThreads) {
     const int rr = idx / C4, c4 = idx - rr * C4;
     const int m = m0 + rr, n = n0 + c4 * 4;
-    if (m < p.M && n < p.N)
-      p.store4(m, n, *reinterpret_cast<const float4 *>(&stage[rr * ES + c4 * 4]), z);
+    if (m < p.M && n < p.N) {
+      const float4 v = *reinterpret_cast<const float4 *>(&stage[rr * ES + c4 * 4]);
+      if (!SPLITK)
+        p.final4(m, n, v, zp);
+      else
+        *reinterpret_cast<float4 *>(part + ((int64_t)zs * p.M + m) * p.N + n) = v;
+    }
+  }
+  // bias gradients folded into the B gather: column sums of this CTA's slice
+  if constexpr (Pol::BIAS_FROM_B) if (blockIdx.x == 0) {
+    gb.dump_bias(bias_red);
+    __syncthreads();
+    if (threadIdx.x < BN && n0 + (int)threadIdx.x < p.N) {
+      float s = bias_red[threadIdx.x][0];
+#pragma unroll
+      for (int kc = 1; kc < 8; ++kc) s = __fadd_rn(s, bias_red[threadIdx.x][kc]);
+      const int n = n0 + threadIdx.x;
+      if (!SPLITK)
+        p.bias_out[n] = __fadd_rn(p.bias_out[n], s);
+      else
+        p.bias_partial[(int64_t)zs * p.N + n] = s;
+    }
+  }
+  // split-K fixup: the last CTA of a tile sums every split's partial in split
+  // order (deterministic, whichever CTA arrives last) and runs the epilogue
+  if (SPLITK) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    const int tile = (zp * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0) s_last = (atomicAdd(&p.counters[tile], 1) == ks - 1);
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+#pragma unroll 2
+      for (int idx = threadIdx.x; idx < BM * C4; idx += kThreads) {
+        const int rr = idx / C4, c4 = idx - rr * C4;
+        const int m = m0 + rr, n = n0 + c4 * 4;
+        if (m < p.M && n < p.N) {
+          float4 v = __ldcg(reinterpret_cast<const float4 *>(part + (int64_t)m * p.N + n));
+          for (int zz = 1; zz < ks; ++zz) {
+            const float4 t = __ldcg(reinterpret_cast<const float4 *>(
+                part + ((int64_t)zz * p.M + m) * p.N + n));
+            v.x = __fadd_rn(v.x, t.x);
+            v.y = __fadd_rn(v.y, t.y);
+            v.z = __fadd_rn(v.z, t.z);
+            v.w = __fadd_rn(v.w, t.w);
+          }
+          p.final4(m, n, v, zp);
+        }
+      }
+      if (Pol::BIAS_FROM_B && blockIdx.x == 0 && threadIdx.x < BN && n0 + (int)threadIdx.x < p.N) {
+        const int n = n0 + threadIdx.x;
+        float s = __ldcg(p.bias_partial + n);
+        for (int zz = 1; zz < ks; ++zz)
+          s = __fadd_rn(s, __ldcg(p.bias_partial + (int64_t)zz * p.N + n));
+        p.bias_out[n] = __fadd_rn(p.bias_out[n], s);
+      }
+      if (threadIdx.x == 0) p.counters[tile] = 0;      // reusable by the next launch
+    }
   }
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS)
@@ -395,13 +548,17 @@ int launch(cudaStream_t st, const Pol &p, int splits, const char *what) {
     configured = true;
   }
   dim3 grid((p.M + BM - 1) / BM, (p.N + Pol::BN - 1) / Pol::BN, splits);
+  if (p.ksplits > 1 && (int64_t)grid.x * grid.y * (splits / p.ksplits) > kMaxTiles) {
+    set_error("%s: %u x %u tiles exceed the split-K counter table", what, grid.x, grid.y);
+    return DQN_ERR_UNSUPPORTED;
+  }
   static const int env_nacc = [] {
     const char *e = getenv("DQN_TC_NACC");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 2;      // 2 accumulator pairs: <= 256 TMEM columns at BN <= 64
   }();
   int nacc = env_nacc < 1 ? 1 : env_nacc;
   const int pair = (Pol::SPLIT_A || Pol::SPLIT_B) ? 2 : 1;
-  while (nacc > 1 && Pol::BN * nacc * pair > 512) --nacc;
+  while (nacc > 1 && Pol::BN * nacc * pair > 256) --nacc;   // 2 CTAs/SM can always allocate
   tc_gemm_kernel<Pol><<<grid, kThreads, bytes, st>>>(p, nacc);
   DQN_LAUNCH_CHECK(what);
   return DQN_OK;

@@ -1,32 +1,29 @@
 // Conv trunk on the 5th-gen tensor cores: every GEMM-shaped phase of the
 // convolution / linear layers runs through the tcgen05 engine (tc_gemm.cuh)
-// with implicit-GEMM operand gathers -- no im2col buffer in HBM.
+// with implicit-GEMM operand gathers -- no im2col / col2im buffers in HBM and
+// no separate reduction launches (split-K partials are reduced in-kernel by
+// the last CTA of each tile, bias gradients are folded into the wgrad GEMM).
 //
-//   forward  (layers.py:226-233, 148-150):  C[pix, co]  = im2col(x)[pix, k] * W[k, co]
-//            A gathered from NHWC x (uint8 frames: exact integers, the
-//            1/255 of envs.py:300-311 applied in the epilogue), B = W gathered
-//            along k, epilogue bias + ReLU (or split-K partials).
-//   dgrad    (layers.py:235-248, 152-155):  dpatch[pix, r] = dY[pix, co] * W[r, co]
-//            (then the deterministic col2im gather), linear layers write dX
-//            directly with the ReLU mask of the layer below.
-//   wgrad    (layers.py:250-255, 157-160):  dW[r, co] = sum_pix im2col(x)[pix, r] * dY[pix, co]
-//            reduction over pixels, split over pixels, fixed-order reduce;
-//            bias grads by a fixed-order column sum.
+//   forward  (layers.py:226-233, 148-150):  Y[pix, co] = im2col(X)[pix, k] * W[k, co]
+//            A gathered from NHWC X (uint8 frames: exact integers, the 1/255
+//            of envs.py:300-311 applied in the epilogue), B = W gathered along
+//            k; epilogue bias + ReLU.
+//   dgrad    (layers.py:235-248, 152-155):  per stride phase (py, px),
+//            dX[pix, c] = sum_{ti,tj,co} dY[y/s - ti, x/s - tj, co] * W[py+s*ti, px+s*tj, c, co]
+//            -- the gather form of col2im, only the taps that exist (no 4x
+//            zero work for the stride-2 layer), masked by the ReLU below.
+//            Linear layers: dX = dY * W^T with the mask.
+//   wgrad    (layers.py:250-255, 157-160):  dW[r, co] = sum_pix im2col(X)[pix, r] * dY[pix, co]
+//            split over pixels; db[co] = sum_pix dY[pix, co] from the same B
+//            gather.
 //
-// Returns DQN_ERR_UNSUPPORTED for geometries this engine does not tile
-// (channel counts not multiple of 4 / 16); the caller then uses the SIMT
-// kernels of net_simt.cu.
+// Geometries this engine does not tile fall back to the SIMT kernels of
+// net_simt.cu (tc_layer_supported).
 #include "tc_gemm.cuh"
 
 #include <algorithm>
 
 namespace dqn {
-
-int launch_splitk_reduce(cudaStream_t st, const float *partial, int splits, int64_t MN, int N,
-                         const float *bias, float *y, int relu, const float *mask);
-int launch_col2im(cudaStream_t st, const float *dpatch, const Geo &g, int batch,
-                  const float *mask, float *dx);
-
 namespace {
 
 __device__ __forceinline__ float4 ld4(const float *p) {
@@ -39,7 +36,6 @@ __device__ __forceinline__ float4 ld4(const uint8_t *p) {
                      (float)(u >> 24));
 }
 __device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
-
 
 // four scalar loads along k for sources that are contiguous along rows
 template <typename T>
@@ -66,37 +62,46 @@ __device__ __forceinline__ int patch_off(const Geo &g, int k) {
   return i * g.W * g.C + (k - i * rowlen);
 }
 
-__device__ __forceinline__ void store4(float *p, float4 v) { *reinterpret_cast<float4 *>(p) = v; }
-__device__ __forceinline__ float4 load4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+__device__ __forceinline__ void st4(float *p, float4 v) { *reinterpret_cast<float4 *>(p) = v; }
+__device__ __forceinline__ float4 ld4_rw(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+
+__device__ __forceinline__ float4 relu_mask(float4 v, const float *mask) {
+  const float4 mk = ld4_rw(mask);
+  v.x = mk.x > 0.f ? v.x : 0.f;
+  v.y = mk.y > 0.f ? v.y : 0.f;
+  v.z = mk.z > 0.f ? v.z : 0.f;
+  v.w = mk.w > 0.f ? v.w : 0.f;
+  return v;
+}
 
 // ---------------------------------------------------------------- forward
 template <typename InT, int BN_>
-struct FwdPol {
+struct FwdPol : tc::PolBase {
   static constexpr bool U8 = sizeof(InT) == 1;
-  static constexpr bool SPLIT_A = !U8, SPLIT_B = true;
+  static constexpr bool SPLIT_A = !U8, SPLIT_B = true, BIAS_FROM_B = false;
+  static constexpr bool A_MNC = false, B_MNC = true;
   static constexpr int BN = BN_, STAGES = tc::auto_stages(BN_, SPLIT_A, SPLIT_B);
   const InT *x;
   const float *w, *bias;
   float *y, *partial;
+  float *bias_out, *bias_partial;       // unused
+  int *counters;
   Geo g;
-  int M, N, K, klen, relu, split;
+  int M, N, K, klen, relu, ksplits;
   __device__ int kbeg(int z) const { return z * klen; }
   __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
-  __device__ long long a_row(int m) const { return m < M ? pixel_base(g, m) : -1; }
+  __device__ long long a_row(int m, int) const { return m < M ? pixel_base(g, m) : -1; }
   __device__ float4 a(long long base, int k, int ke) const {
     if (k >= ke) return zero4();
     return ld4(x + base + patch_off(g, k));
   }
-  __device__ long long b_row(int n) const { return n < N ? n : -1; }
-  __device__ float4 b(long long n, int k, int ke) const {     // W[k][n]: gather along k
-    if (k >= ke) return zero4();
-    return ld4_strided(w + (int64_t)k * N + n, N, min(4, ke - k));
+  __device__ long long b_row(int n, int) const { return n < N ? n : -1; }
+  // W[k][n..n+3] for k..k+3 (row-contiguous source, transposed by the engine)
+  __device__ void b4(long long n, int k, int ke, float4 (&v)[4]) const {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) v[t] = (k + t < ke) ? ld4(w + (int64_t)(k + t) * N + n) : zero4();
   }
-  __device__ void store4(int m, int n, float4 v, int z) const {
-    if (split) {
-      dqn::store4(partial + ((int64_t)z * M + m) * N + n, v);
-      return;
-    }
+  __device__ void final4(int m, int n, float4 v, int) const {
     float t[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -105,145 +110,166 @@ struct FwdPol {
       if (relu && u < 0.f) u = 0.f;
       t[j] = u;
     }
-    dqn::store4(y + (int64_t)m * N + n, make_float4(t[0], t[1], t[2], t[3]));
+    st4(y + (int64_t)m * N + n, make_float4(t[0], t[1], t[2], t[3]));
   }
 };
 
-// ------------------------------------------------------------------ dgrad
-// C[m, n] = sum_k dY[m, k] * W[n, k]  (W row-major [R][Cout])
+// --------------------------------------------------------- linear dgrad
+// dX[m, f] = sum_co dY[m, co] * W[f, co]  (W row-major [F][Cout])
 template <int BN_>
-struct DgradPol {
-  static constexpr bool SPLIT_A = true, SPLIT_B = true;
+struct LinDgradPol : tc::PolBase {
+  static constexpr bool SPLIT_A = true, SPLIT_B = true, BIAS_FROM_B = false;
+  static constexpr bool A_MNC = false, B_MNC = false;
   static constexpr int BN = BN_, STAGES = tc::auto_stages(BN_, SPLIT_A, SPLIT_B);
   const float *dy, *w, *mask;
   float *out, *partial;
-  int M, N, K, klen, split;
+  float *bias_out, *bias_partial;
+  int *counters;
+  int M, N, K, klen, ksplits;
   __device__ int kbeg(int z) const { return z * klen; }
   __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
-  __device__ long long a_row(int m) const { return m < M ? (long long)m * K : -1; }
+  __device__ long long a_row(int m, int) const { return m < M ? (long long)m * K : -1; }
   __device__ float4 a(long long base, int k, int ke) const {
     return k < ke ? ld4(dy + base + k) : zero4();
   }
-  __device__ long long b_row(int n) const { return n < N ? (long long)n * K : -1; }
+  __device__ long long b_row(int n, int) const { return n < N ? (long long)n * K : -1; }
   __device__ float4 b(long long base, int k, int ke) const {
     return k < ke ? ld4(w + base + k) : zero4();
   }
-  __device__ void store4(int m, int n, float4 v, int z) const {
-    if (split) {
-      dqn::store4(partial + ((int64_t)z * M + m) * N + n, v);
-      return;
-    }
+  __device__ void final4(int m, int n, float4 v, int) const {
     const int64_t o = (int64_t)m * N + n;
-    if (mask != nullptr) {
-      const float4 mk = load4(mask + o);
-      v.x = mk.x > 0.f ? v.x : 0.f;
-      v.y = mk.y > 0.f ? v.y : 0.f;
-      v.z = mk.z > 0.f ? v.z : 0.f;
-      v.w = mk.w > 0.f ? v.w : 0.f;
-    }
-    dqn::store4(out + o, v);
+    st4(out + o, mask ? relu_mask(v, mask + o) : v);
+  }
+};
+
+// ----------------------------------------------------------- conv dgrad
+// One stride phase (py, px) per blockIdx.z: rows are the input pixels
+// (img, yq, xq) with y = yq*sh + py, x = xq*sw + px; k = (ti, tj, co).
+template <int BN_>
+struct ConvDgradPol : tc::PolBase {
+  static constexpr bool SPLIT_A = true, SPLIT_B = true, BIAS_FROM_B = false;
+  static constexpr bool A_MNC = false, B_MNC = false;
+  static constexpr int BN = BN_, STAGES = tc::auto_stages(BN_, SPLIT_A, SPLIT_B);
+  const float *dy, *w, *mask;
+  float *out, *partial;
+  float *bias_out, *bias_partial;
+  int *counters;
+  Geo g;
+  int M, N, K;         // M = batch * max phase extent, N = C, K = (fh/sh)(fw/sw)Cout
+  int batch, klen, ksplits;
+  __device__ int kbeg(int z) const { return z * klen; }
+  __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
+  __device__ void phase(int z, int &py, int &px, int &hq, int &wq) const {
+    py = z / g.sw;
+    px = z - py * g.sw;
+    hq = (g.H - py + g.sh - 1) / g.sh;
+    wq = (g.W - px + g.sw - 1) / g.sw;
+  }
+  // row base packs (img, yq, xq) of the input pixel; -1 beyond this phase
+  __device__ long long a_row(int m, int z) const {
+    int py, px, hq, wq;
+    phase(z, py, px, hq, wq);
+    const int per = hq * wq;
+    if (m >= batch * per) return -1;
+    const int img = m / per, r = m - img * per, yq = r / wq, xq = r - yq * wq;
+    return ((long long)img << 32) | ((long long)yq << 16) | xq;
+  }
+  __device__ float4 a(long long rb, int k, int ke) const {
+    if (k >= ke) return zero4();
+    const int img = (int)(rb >> 32), yq = (int)((rb >> 16) & 0xFFFF), xq = (int)(rb & 0xFFFF);
+    const int tw = g.fw / g.sw;
+    const int tap = k / g.N, co = k - tap * g.N;
+    const int ti = tap / tw, tj = tap - ti * tw;
+    const int oy = yq - ti, ox = xq - tj;
+    if (oy < 0 || ox < 0 || oy >= g.OH || ox >= g.OW) return zero4();
+    return ld4(dy + (((int64_t)img * g.OH + oy) * g.OW + ox) * g.N + co);
+  }
+  __device__ long long b_row(int c, int z) const {
+    if (c >= N) return -1;
+    int py, px, hq, wq;
+    phase(z, py, px, hq, wq);
+    return ((long long)c << 16) | (py << 8) | px;
+  }
+  __device__ float4 b(long long rb, int k, int ke) const {
+    if (k >= ke) return zero4();
+    const int c = (int)(rb >> 16), py = (int)((rb >> 8) & 0xFF), px = (int)(rb & 0xFF);
+    const int tw = g.fw / g.sw;
+    const int tap = k / g.N, co = k - tap * g.N;
+    const int ti = tap / tw, tj = tap - ti * tw;
+    const int i = py + g.sh * ti, j = px + g.sw * tj;
+    return ld4(w + (((int64_t)i * g.fw + j) * g.C + c) * g.N + co);
+  }
+  __device__ void final4(int m, int c, float4 v, int z) const {
+    int py, px, hq, wq;
+    phase(z, py, px, hq, wq);
+    const int per = hq * wq;
+    if (m >= batch * per) return;
+    const int img = m / per, r = m - img * per, yq = r / wq, xq = r - yq * wq;
+    const int y = yq * g.sh + py, x = xq * g.sw + px;
+    const int64_t o = (((int64_t)img * g.H + y) * g.W + x) * g.C + c;
+    st4(out + o, mask ? relu_mask(v, mask + o) : v);
   }
 };
 
 // ------------------------------------------------------------------ wgrad
 // C[r, co] = sum_pix im2col(x)[pix, r] * dY[pix, co]; the reduction runs
-// over pixels, so both operands are gathered 4 pixels at a time.
+// over pixels, so both operands are gathered 4 pixels at a time; the bias
+// gradient is the column sum of the same dY gather.
 template <typename InT, int BN_>
-struct WgradPol {
+struct WgradPol : tc::PolBase {
   static constexpr bool U8 = sizeof(InT) == 1;
-  static constexpr bool SPLIT_A = !U8, SPLIT_B = true;
+  static constexpr bool SPLIT_A = !U8, SPLIT_B = true, BIAS_FROM_B = true;
+  static constexpr bool A_MNC = true, B_MNC = true;
   static constexpr int BN = BN_, STAGES = tc::auto_stages(BN_, SPLIT_A, SPLIT_B);
   const InT *x;
   const float *dy;
   float *grad, *partial;
+  float *bias_out, *bias_partial;
+  int *counters;
   Geo g;
-  int M, N, K, klen, split;     // M = R (patch length), N = Cout, K = pixels
+  int M, N, K, klen, ksplits;     // M = R (patch length), N = Cout, K = pixels
   __device__ int kbeg(int z) const { return z * klen; }
   __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
-  __device__ long long a_row(int r) const { return r < M ? patch_off(g, r) : -1; }
-  __device__ float4 a(long long roff, int pix, int ke) const {
-    if (pix >= ke) return zero4();
-    // window bases of 4 consecutive pixels: walk along the output row
+  __device__ long long a_row(int r, int) const { return r < M ? patch_off(g, r) : -1; }
+  // patch rows r..r+3 (contiguous in NHWC: fw*C % 4 == 0) at pixels
+  // pix..pix+3: the window bases walk along the output row
+  __device__ void a4(long long roff, int pix, int ke, float4 (&v)[4]) const {
     const int P = g.OH * g.OW;
     int img = pix / P, p = pix - img * P;
     int oy = p / g.OW, ox = p - oy * g.OW;
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (pix + i < ke) {
         const long long base =
             (((long long)img * g.H + (long long)oy * g.sh) * g.W + (long long)ox * g.sw) * g.C;
-        v[i] = (float)__ldg(x + base + roff);
+        v[i] = ld4(x + base + roff);
+      } else {
+        v[i] = zero4();
       }
       if (++ox == g.OW) {
         ox = 0;
         if (++oy == g.OH) { oy = 0; ++img; }
       }
     }
-    return make_float4(v[0], v[1], v[2], v[3]);
   }
-  __device__ long long b_row(int n) const { return n < N ? n : -1; }
-  __device__ float4 b(long long n, int pix, int ke) const {
-    if (pix >= ke) return zero4();
-    return ld4_strided(dy + (int64_t)pix * N + n, N, min(4, ke - pix));
+  __device__ long long b_row(int n, int) const { return n < N ? n : -1; }
+  // dY[pix..pix+3][n..n+3]
+  __device__ void b4(long long n, int pix, int ke, float4 (&v)[4]) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = (pix + i < ke) ? ld4(dy + (int64_t)(pix + i) * N + n) : zero4();
   }
-  __device__ void store4(int r, int n, float4 v, int z) const {
-    if (split) {
-      dqn::store4(partial + ((int64_t)z * M + r) * N + n, v);
-      return;
-    }
+  __device__ void final4(int r, int n, float4 v, int) const {
     float *gp = grad + (int64_t)r * N + n;
-    float4 o = load4(gp);
+    float4 o = ld4_rw(gp);
     if (U8) {
       v.x = __fdiv_rn(v.x, 255.0f); v.y = __fdiv_rn(v.y, 255.0f);
       v.z = __fdiv_rn(v.z, 255.0f); v.w = __fdiv_rn(v.w, 255.0f);
     }
     o.x = __fadd_rn(o.x, v.x); o.y = __fadd_rn(o.y, v.y);
     o.z = __fadd_rn(o.z, v.z); o.w = __fadd_rn(o.w, v.w);
-    dqn::store4(gp, o);
+    st4(gp, o);
   }
 };
-
-// grad += scale(sum_z partial[z])  (fixed split order)
-__global__ void tc_wgrad_reduce_kernel(const float *__restrict__ partial, int splits, int64_t RN,
-                                       int u8, float *__restrict__ grad) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < RN;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    float s = partial[e];
-    for (int z = 1; z < splits; ++z) s = __fadd_rn(s, partial[(int64_t)z * RN + e]);
-    if (u8) s = __fdiv_rn(s, 255.0f);
-    grad[e] = __fadd_rn(grad[e], s);
-  }
-}
-
-// Bias gradients: db[n] += sum_m dY[m, n].  Pass 1: 32 columns x row blocks.
-constexpr int kColRowBlocks = 32;
-__global__ void colsum_partial_kernel(const float *__restrict__ dy, int M, int N,
-                                      float *__restrict__ part) {
-  __shared__ float red[8][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int n = blockIdx.x * 32 + tx;
-  const int rows = (M + kColRowBlocks - 1) / kColRowBlocks;
-  const int r0 = blockIdx.y * rows, r1 = min(M, r0 + rows);
-  float s = 0.f;
-  if (n < N)
-    for (int m = r0 + ty; m < r1; m += 8) s = __fadd_rn(s, dy[(int64_t)m * N + n]);
-  red[ty][tx] = s;
-  __syncthreads();
-  if (ty == 0 && n < N) {
-    float t = red[0][tx];
-    for (int i = 1; i < 8; ++i) t = __fadd_rn(t, red[i][tx]);
-    part[(int64_t)blockIdx.y * N + n] = t;
-  }
-}
-
-__global__ void colsum_final_kernel(const float *__restrict__ part, int N, float *__restrict__ db) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
-  float s = part[n];
-  for (int b = 1; b < kColRowBlocks; ++b) s = __fadd_rn(s, part[(int64_t)b * N + n]);
-  db[n] = __fadd_rn(db[n], s);
-}
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
@@ -255,15 +281,24 @@ bool conv_ok(const dqn_layer_desc &L) {
 
 // forward split length: a function of K only (batch-independent rows)
 inline int fwd_klen(int K) {
-  if (K >= 2048) return 128;
+  if (K >= 2048) return ceil_div(ceil_div(K, 8), tc::BK) * tc::BK;   // 8 splits (fc1: 416)
   if (K >= 512) return 192;
   return K;
 }
 
+// split count for a grid of `tiles` tiles: about two CTAs per SM (2 waves
+// of 148), at least 64 k per split, at most `cap` partials per fixup
+inline void split_k(int tiles, int K, int cap, int &klen, int &splits) {
+  splits = std::max(1, std::min({ceil_div(2 * kNumSMs, tiles), K / 64, cap}));
+  klen = ceil_div(ceil_div(K, splits), tc::BK) * tc::BK;
+  splits = ceil_div(K, klen);
+}
+
 template <typename InT, int BN>
 int fwd_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *params,
-               float *y, float *scratch, int batch) {
-  FwdPol<InT, BN> p;
+               float *y, float *scratch, int *counters, int batch) {
+  FwdPol<InT, BN> p{};
+  p.counters = counters;
   p.x = x;
   p.w = params + L.w_off;
   p.bias = params + L.b_off;
@@ -274,33 +309,26 @@ int fwd_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const flo
   p.N = L.out_c;
   p.K = L.fh * L.fw * L.in_c;
   p.klen = fwd_klen(p.K);
-  const int splits = ceil_div(p.K, p.klen);
-  p.split = splits > 1;
   p.relu = L.relu;
-  int rc = tc::launch(st, p, splits, "tc_fwd");
-  if (rc || splits == 1) return rc;
-  if (FwdPol<InT, BN>::U8) {
-    set_error("tc_fwd: split-K with uint8 input is not supported");
-    return DQN_ERR_UNSUPPORTED;
-  }
-  return launch_splitk_reduce(st, scratch, splits, (int64_t)p.M * p.N, p.N, p.bias, y, L.relu,
-                              nullptr);
+  p.ksplits = ceil_div(p.K, p.klen);
+  return tc::launch(st, p, p.ksplits, "tc_fwd");
 }
 
 template <typename InT>
 int fwd_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *params,
-                 float *y, float *scratch, int batch) {
+                 float *y, float *scratch, int *counters, int batch) {
   const int N = L.out_c;
-  if (N == 32) return fwd_launch<InT, 32>(st, L, x, params, y, scratch, batch);
-  if (N == 64) return fwd_launch<InT, 64>(st, L, x, params, y, scratch, batch);
-  if (N % 128 == 0) return fwd_launch<InT, 128>(st, L, x, params, y, scratch, batch);
+  if (N == 32) return fwd_launch<InT, 32>(st, L, x, params, y, scratch, counters, batch);
+  if (N == 64) return fwd_launch<InT, 64>(st, L, x, params, y, scratch, counters, batch);
+  if (N % 64 == 0) return fwd_launch<InT, 64>(st, L, x, params, y, scratch, counters, batch);
   return DQN_ERR_UNSUPPORTED;
 }
 
 template <int BN>
-int dgrad_gemm(cudaStream_t st, const float *dy, const float *w, const float *mask, float *out,
-               float *partial, int M, int N, int K, int klen) {
-  DgradPol<BN> p;
+int lin_dgrad_launch(cudaStream_t st, const float *dy, const float *w, const float *mask,
+                     float *out, float *partial, int *counters, int M, int N, int K) {
+  LinDgradPol<BN> p{};
+  p.counters = counters;
   p.dy = dy;
   p.w = w;
   p.mask = mask;
@@ -309,94 +337,119 @@ int dgrad_gemm(cudaStream_t st, const float *dy, const float *w, const float *ma
   p.M = M;
   p.N = N;
   p.K = K;
-  p.klen = klen;
-  const int splits = ceil_div(K, klen);
-  p.split = splits > 1;
-  int rc = tc::launch(st, p, splits, "tc_dgrad");
-  if (rc || splits == 1) return rc;
-  return launch_splitk_reduce(st, partial, splits, (int64_t)M * N, N, nullptr, out, 0, mask);
+  p.klen = std::min(K, 128);
+  p.ksplits = ceil_div(K, p.klen);
+  return tc::launch(st, p, p.ksplits, "tc_lin_dgrad");
 }
 
-int dgrad_pick(cudaStream_t st, const float *dy, const float *w, const float *mask, float *out,
-               float *partial, int M, int N, int K, int klen) {
-  // widest tile <= 128 columns that divides N (N % 16 == 0 is guaranteed)
+int lin_dgrad(cudaStream_t st, const float *dy, const float *w, const float *mask, float *out,
+              float *partial, int *counters, int M, int N, int K) {
   for (int bn : {128, 112, 96, 64, 32, 16}) {
     if (N % bn) continue;
     switch (bn) {
-      case 112: return dgrad_gemm<112>(st, dy, w, mask, out, partial, M, N, K, klen);
-      case 128: return dgrad_gemm<128>(st, dy, w, mask, out, partial, M, N, K, klen);
-      case 96: return dgrad_gemm<96>(st, dy, w, mask, out, partial, M, N, K, klen);
-      case 64: return dgrad_gemm<64>(st, dy, w, mask, out, partial, M, N, K, klen);
-      case 32: return dgrad_gemm<32>(st, dy, w, mask, out, partial, M, N, K, klen);
-      default: return dgrad_gemm<16>(st, dy, w, mask, out, partial, M, N, K, klen);
+      case 128: return lin_dgrad_launch<128>(st, dy, w, mask, out, partial, counters, M, N, K);
+      case 112: return lin_dgrad_launch<112>(st, dy, w, mask, out, partial, counters, M, N, K);
+      case 96: return lin_dgrad_launch<96>(st, dy, w, mask, out, partial, counters, M, N, K);
+      case 64: return lin_dgrad_launch<64>(st, dy, w, mask, out, partial, counters, M, N, K);
+      case 32: return lin_dgrad_launch<32>(st, dy, w, mask, out, partial, counters, M, N, K);
+      default: return lin_dgrad_launch<16>(st, dy, w, mask, out, partial, counters, M, N, K);
     }
   }
   return DQN_ERR_UNSUPPORTED;
 }
 
+template <int BN>
+int conv_dgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
+                      const float *mask, float *out, float *scratch, int *counters, int batch) {
+  ConvDgradPol<BN> p{};
+  p.counters = counters;
+  p.partial = scratch;
+  p.dy = dy;
+  p.w = w;
+  p.mask = mask;
+  p.out = out;
+  p.g = geo_of(L);
+  p.batch = batch;
+  p.M = batch * ceil_div(L.in_h, L.sh) * ceil_div(L.in_w, L.sw);
+  p.N = L.in_c;
+  p.K = (L.fh / L.sh) * (L.fw / L.sw) * L.out_c;
+  // split K until phases x tiles x splits fill the machine
+  split_k(L.sh * L.sw * ceil_div(p.M, tc::BM) * ceil_div(p.N, BN), p.K, 16, p.klen, p.ksplits);
+  return tc::launch(st, p, L.sh * L.sw * p.ksplits, "tc_conv_dgrad");
+}
+
+bool dgrad_tile_ok(int C) { return C == 16 || C == 32 || C == 48 || C == 64 || C == 96 || C % 128 == 0; }
+
+int conv_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
+               const float *mask, float *out, float *scratch, int *counters, int batch) {
+  switch (L.in_c) {
+    case 16: return conv_dgrad_launch<16>(st, L, dy, w, mask, out, scratch, counters, batch);
+    case 32: return conv_dgrad_launch<32>(st, L, dy, w, mask, out, scratch, counters, batch);
+    case 48: return conv_dgrad_launch<48>(st, L, dy, w, mask, out, scratch, counters, batch);
+    case 64: return conv_dgrad_launch<64>(st, L, dy, w, mask, out, scratch, counters, batch);
+    case 96: return conv_dgrad_launch<96>(st, L, dy, w, mask, out, scratch, counters, batch);
+    default: break;
+  }
+  if (L.in_c % 128 == 0) return conv_dgrad_launch<128>(st, L, dy, w, mask, out, scratch, counters, batch);
+  set_error("tc_conv_dgrad: %d input channels not tiled", L.in_c);
+  return DQN_ERR_UNSUPPORTED;
+}
+
+inline void wgrad_split(int M, int N, int K, int bn, int &klen, int &splits) {
+  // ~2 CTA waves over the machine, split lengths a multiple of BK
+  split_k(ceil_div(M, tc::BM) * ceil_div(N, bn), K, 32, klen, splits);
+}
+
 template <typename InT, int BN>
 int wgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *dy,
-                 float *grads, float *scratch, int batch) {
-  WgradPol<InT, BN> p;
+                 float *grads, float *scratch, int *counters, int batch) {
+  WgradPol<InT, BN> p{};
+  p.counters = counters;
   p.x = x;
   p.dy = dy;
   p.grad = grads + L.w_off;
-  p.partial = scratch;
+  p.bias_out = grads + L.b_off;
   p.g = geo_of(L);
   p.M = L.fh * L.fw * L.in_c;
   p.N = L.out_c;
   p.K = batch * L.out_h * L.out_w;
-  // ~2 CTA waves over the machine, split lengths a multiple of BK
-  const int tiles = ceil_div(p.M, tc::BM) * ceil_div(p.N, BN);
-  int splits = std::max(1, std::min(ceil_div(2 * kNumSMs, tiles), ceil_div(p.K, 4 * tc::BK)));
-  p.klen = ceil_div(ceil_div(p.K, splits), tc::BK) * tc::BK;
-  splits = ceil_div(p.K, p.klen);
-  p.split = splits > 1;
-  int rc = tc::launch(st, p, splits, "tc_wgrad");
-  if (rc) return rc;
-  float *bpart = scratch + (p.split ? (int64_t)splits * p.M * p.N : 0);
-  if (p.split) {
-    const int64_t RN = (int64_t)p.M * p.N;
-    tc_wgrad_reduce_kernel<<<(int)std::min<int64_t>((RN + 255) / 256, 148 * 8), 256, 0, st>>>(
-        scratch, splits, RN, WgradPol<InT, BN>::U8 ? 1 : 0, p.grad);
-    DQN_LAUNCH_CHECK("tc_wgrad_reduce");
-  }
-  colsum_partial_kernel<<<dim3(ceil_div(p.N, 32), kColRowBlocks), 256, 0, st>>>(dy, p.K, p.N, bpart);
-  DQN_LAUNCH_CHECK("colsum_partial");
-  colsum_final_kernel<<<ceil_div(p.N, 128), 128, 0, st>>>(bpart, p.N, grads + L.b_off);
-  DQN_LAUNCH_CHECK("colsum_final");
-  return DQN_OK;
+  int splits;
+  wgrad_split(p.M, p.N, p.K, BN, p.klen, splits);
+  p.partial = scratch;
+  p.bias_partial = scratch + (int64_t)splits * p.M * p.N;
+  p.ksplits = splits;
+  return tc::launch(st, p, splits, "tc_wgrad");
 }
 
 template <typename InT>
 int wgrad_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *dy,
-                   float *grads, float *scratch, int batch) {
+                   float *grads, float *scratch, int *counters, int batch) {
   const int N = L.out_c;
-  if (N == 32) return wgrad_launch<InT, 32>(st, L, x, dy, grads, scratch, batch);
-  if (N == 64) return wgrad_launch<InT, 64>(st, L, x, dy, grads, scratch, batch);
-  if (N % 128 == 0) return wgrad_launch<InT, 128>(st, L, x, dy, grads, scratch, batch);
+  if (N == 32) return wgrad_launch<InT, 32>(st, L, x, dy, grads, scratch, counters, batch);
+  if (N == 64) return wgrad_launch<InT, 64>(st, L, x, dy, grads, scratch, counters, batch);
+  if (N % 128 == 0) return wgrad_launch<InT, 128>(st, L, x, dy, grads, scratch, counters, batch);
   return DQN_ERR_UNSUPPORTED;
 }
 
 int64_t wgrad_scratch_tc(const dqn_layer_desc &L, int batch) {
   const int M = L.fh * L.fw * L.in_c, N = L.out_c, K = batch * L.out_h * L.out_w;
   const int bn = N == 32 ? 32 : N == 64 ? 64 : 128;
-  const int tiles = ceil_div(M, tc::BM) * ceil_div(N, bn);
-  int splits = std::max(1, std::min(ceil_div(2 * kNumSMs, tiles), ceil_div(K, 4 * tc::BK)));
-  const int klen = ceil_div(ceil_div(K, splits), tc::BK) * tc::BK;
-  splits = ceil_div(K, klen);
-  return (splits > 1 ? (int64_t)splits * M * N : 0) + (int64_t)kColRowBlocks * N;
+  int klen, splits;
+  wgrad_split(M, N, K, bn, klen, splits);
+  return (int64_t)splits * M * N + (int64_t)splits * N;
 }
 
 }  // namespace
 
-bool tc_layer_supported(const dqn_net_desc *net, int l) {
+// phase: 0 forward, 1 dgrad, 2 wgrad
+bool tc_layer_supported(const dqn_net_desc *net, int l, int phase) {
   const dqn_layer_desc &L = net->layer[l];
   if (!conv_ok(L)) return false;
   if (L.kind == DQN_LAYER_LINEAR && l == net->n_layers - 1 && L.out_c <= 32) return false;  // head
   const int N = L.out_c;
   if (!(N == 32 || N == 64 || N % 128 == 0)) return false;
-  if (l == 0 && net->input_u8 && fwd_klen(L.fh * L.fw * L.in_c) < L.fh * L.fw * L.in_c)
+  if (phase == 1 && L.kind == DQN_LAYER_CONV &&
+      (L.fh % L.sh || L.fw % L.sw || !dgrad_tile_ok(L.in_c)))
     return false;
   return true;
 }
@@ -404,19 +457,26 @@ bool tc_layer_supported(const dqn_net_desc *net, int l) {
 int64_t tc_scratch_floats(const dqn_net_desc *net, int batch) {
   int64_t m = 0;
   for (int l = 0; l < net->n_layers; ++l) {
-    if (!tc_layer_supported(net, l)) continue;
+    if (!tc_layer_supported(net, l, 0)) continue;
     const dqn_layer_desc &L = net->layer[l];
     const int M = batch * L.out_h * L.out_w, R = L.fh * L.fw * L.in_c, K = R;
-    const int kl = fwd_klen(K);
-    const int fs = ceil_div(K, kl);
+    const int fs = ceil_div(K, fwd_klen(K));
     m = std::max(m, fs > 1 ? (int64_t)fs * M * L.out_c : 0);
-    // dgrad: dpatch (conv) or split partials (linear, klen 128 over Cout)
-    const int ds = ceil_div(L.out_c, 128);
-    int64_t d = (L.kind == DQN_LAYER_CONV ? (int64_t)M * R : 0) + (ds > 1 ? (int64_t)ds * M * R : 0);
-    m = std::max(m, d);
+    if (L.kind == DQN_LAYER_LINEAR) m = std::max(m, (int64_t)ceil_div(L.out_c, 128) * M * R);
+    if (L.kind == DQN_LAYER_CONV && tc_layer_supported(net, l, 1)) {
+      const int Kd = (L.fh / L.sh) * (L.fw / L.sw) * L.out_c;
+      const int ds = std::max(1, std::min(Kd / 64, 16));     // split_k upper bound
+      const int64_t Md = (int64_t)batch * ceil_div(L.in_h, L.sh) * ceil_div(L.in_w, L.sw);
+      if (ds > 1) m = std::max(m, (int64_t)L.sh * L.sw * ds * Md * L.in_c);
+    }
     m = std::max(m, wgrad_scratch_tc(L, batch));
   }
   return m;
+}
+
+// split-K tile counters live in the last kMaxTiles slots of the binding scratch
+static int *counters_of(const dqn_binding *b) {
+  return reinterpret_cast<int *>(b->scratch + b->scratch_floats - tc::kMaxTiles);
 }
 
 int tc_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
@@ -424,8 +484,10 @@ int tc_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const floa
   const dqn_layer_desc &L = net->layer[l];
   const void *in = (l == 0) ? b->x : b->act[l - 1];
   if (l == 0 && net->input_u8)
-    return fwd_dispatch<uint8_t>(st, L, (const uint8_t *)in, params, b->act[l], b->scratch, b->batch);
-  return fwd_dispatch<float>(st, L, (const float *)in, params, b->act[l], b->scratch, b->batch);
+    return fwd_dispatch<uint8_t>(st, L, (const uint8_t *)in, params, b->act[l], b->scratch,
+                                  counters_of(b), b->batch);
+  return fwd_dispatch<float>(st, L, (const float *)in, params, b->act[l], b->scratch,
+                              counters_of(b), b->batch);
 }
 
 int tc_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
@@ -434,15 +496,12 @@ int tc_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const flo
   float *out = (l == 0) ? b->dx : b->dact[l - 1];
   if (out == nullptr) return DQN_OK;
   const float *mask = (l > 0 && net->layer[l - 1].relu) ? b->act[l - 1] : nullptr;
-  const int M = b->batch * L.out_h * L.out_w, R = L.fh * L.fw * L.in_c, K = L.out_c;
   const float *w = params + L.w_off;
-  if (L.kind == DQN_LAYER_LINEAR)
-    return dgrad_pick(st, b->dact[l], w, mask, out, b->scratch, M, R, K, std::min(K, 128));
-  float *dpatch = b->scratch;
-  int rc = dgrad_pick(st, b->dact[l], w, nullptr, dpatch, b->scratch + (int64_t)M * R, M, R, K,
-                      std::min(K, 128));
-  if (rc) return rc;
-  return launch_col2im(st, dpatch, geo_of(L), b->batch, mask, out);
+  if (L.kind == DQN_LAYER_LINEAR) {
+    const int M = b->batch, F = L.in_h * L.in_w * L.in_c;
+    return lin_dgrad(st, b->dact[l], w, mask, out, b->scratch, counters_of(b), M, F, L.out_c);
+  }
+  return conv_dgrad(st, L, b->dact[l], w, mask, out, b->scratch, counters_of(b), b->batch);
 }
 
 int tc_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
@@ -450,9 +509,10 @@ int tc_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads
   const dqn_layer_desc &L = net->layer[l];
   const void *in = (l == 0) ? b->x : b->act[l - 1];
   if (l == 0 && net->input_u8)
-    return wgrad_dispatch<uint8_t>(st, L, (const uint8_t *)in, b->dact[l], grads, b->scratch, b->batch);
-  return wgrad_dispatch<float>(st, L, (const float *)in, b->dact[l], grads, b->scratch, b->batch);
+    return wgrad_dispatch<uint8_t>(st, L, (const uint8_t *)in, b->dact[l], grads, b->scratch,
+                                    counters_of(b), b->batch);
+  return wgrad_dispatch<float>(st, L, (const float *)in, b->dact[l], grads, b->scratch,
+                                counters_of(b), b->batch);
 }
 
 }  // namespace dqn
-

@@ -88,7 +88,8 @@ class LayerView:
 class _Bind:
     """Per-batch activation buffers + the C dqn_binding struct."""
 
-    def __init__(self, net: "Network", batch: int, parent: "_Bind | None" = None):
+    def __init__(self, net: "Network", batch: int, parent: "_Bind | None" = None,
+                 own_scratch: bool = False):
         torch = _lib.require_cuda()
         self.batch = batch
         self.struct = _lib.Binding()
@@ -103,14 +104,18 @@ class _Bind:
             sf = int(_lib.lib.dqn_net_scratch_floats(C.byref(net._desc), batch))
             if sf < 0:
                 raise GeometryError("network geometry rejected by libdqn_b200")
-            self.scratch = torch.empty(max(sf, 1), dtype=torch.float32, device="cuda")
+            # zeroed: its tail is the split-K tile-counter table (self-resetting)
+            self.scratch = torch.zeros(max(sf, 1), dtype=torch.float32, device="cuda")
             self.scratch_floats = sf
         else:                       # prefix view: first `batch` rows of a larger binding
             self.act, self.dact, self.dx = parent.act, parent.dact, parent.dx
             self.scratch, self.scratch_floats = parent.scratch, parent.scratch_floats
             sf = int(_lib.lib.dqn_net_scratch_floats(C.byref(net._desc), batch))
-            if sf > self.scratch_floats:
-                self.scratch = torch.empty(sf, dtype=torch.float32, device="cuda")
+            if sf > self.scratch_floats or own_scratch:
+                # own scratch: kernels of this view may run concurrently with
+                # the parent's on another stream
+                sf = max(sf, self.scratch_floats)
+                self.scratch = torch.zeros(sf, dtype=torch.float32, device="cuda")
                 self.scratch_floats = sf
         for i in range(len(net._units)):
             self.struct.act[i] = self.act[i].data_ptr()
@@ -277,13 +282,19 @@ class Network:
             self._binds[batch] = b
         return b
 
-    def prefix_binding(self, parent: _Bind, batch: int) -> _Bind:
-        key = (id(parent), batch)
+    def prefix_binding(self, parent: _Bind, batch: int, own_scratch: bool = False) -> _Bind:
+        key = (id(parent), batch, own_scratch)
         v = self._views.get(key)
         if v is None:
-            v = _Bind(self, batch, parent=parent)
+            v = _Bind(self, batch, parent=parent, own_scratch=own_scratch)
             self._views[key] = v
         return v
+
+    def layer_into(self, bind: _Bind, layer: int, phase: int) -> None:
+        """One phase (0 fwd, 1 bwd to the layer's input, 2 wgrad) of one layer."""
+        _lib.call("dqn_net_layer", _lib.stream_ptr(), C.byref(self.desc_for(bind.x)),
+                  self.flat_values.data_ptr(), self.flat_grads.data_ptr(), C.byref(bind.struct),
+                  layer, phase, self._flags.data_ptr())
 
     def desc_for(self, x):
         import torch
