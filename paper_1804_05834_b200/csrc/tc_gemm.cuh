@@ -207,7 +207,8 @@ __device__ __forceinline__ float comp(const float4 &v, int j) {
 // K-major.  Units are owned by thread u % 256 with the same rows in every
 // k-block, so row bases are computed once.
 //  * MNC == false (source contiguous along k): unit = chunk (row, 4 k), one
-//    16-byte load via f1(base, k, kend);
+//    16-byte load via ld(base, koff(k)); all units of a thread share k, so
+//    the k-dependent address part is computed once per k-block;
 //  * MNC == true (source contiguous along rows, e.g. W[k][n] or dY[pix][co]):
 //    unit = 4 rows x 4 k, four 16-byte loads along the rows via
 //    f4(base, k, kend, v[4]) (consecutive lanes = consecutive row quads =
@@ -218,7 +219,10 @@ struct Gather {
   static constexpr int UNITS = MNC ? R * BK / 16 : R * BK / 4;
   static constexpr int U = (UNITS + kThreads - 1) / kThreads;
   static constexpr int V = MNC ? 4 : 1;
+  static_assert(!MNC || U == 1, "MNC gathers assume one unit per thread");
   long long base[U];
+  uint32_t soff[U];            // byte offset of the unit's (first) chunk in a piece tile
+  int kk;                      // the thread's k offset inside a k-block (same for all units)
   float4 v[U][V];
   float bsum[U][V];
 
@@ -239,36 +243,41 @@ struct Gather {
       int row, k;
       coords(u, row, k);
       base[i] = u < UNITS ? rowfn(row) : -1;
+      soff[i] = chunk_off(R, row, k);
+      kk = k;
 #pragma unroll
       for (int j = 0; j < V; ++j) bsum[i][j] = 0.f;
     }
   }
-  template <class F1, class F4>
-  __device__ void fetch(int k0, int kend, F1 &&f1, F4 &&f4) {
+  // K-major: koff(k) once per k-block, ld(base, koff) per unit (k < kend
+  // checked once: every unit of a thread shares k).  MNC: f4 per unit.
+  template <class KF, class LD, class F4>
+  __device__ void fetch(int k0, int kend, KF &&koff, LD &&ld, F4 &&f4) {
+    const int k = k0 + kk;
+    if constexpr (!MNC) {
+      const bool in = k < kend;
+      const int ko = in ? koff(k) : 0;
 #pragma unroll
-    for (int i = 0; i < U; ++i) {
-      const int u = threadIdx.x + i * kThreads;
-      int row, k;
-      coords(u, row, k);
-      if (base[i] < 0) {
+      for (int i = 0; i < U; ++i)
+        v[i][0] = (in && base[i] >= 0) ? ld(base[i], ko) : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
 #pragma unroll
-        for (int j = 0; j < V; ++j) v[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      } else if constexpr (!MNC) {
-        v[i][0] = f1(base[i], k0 + k, kend);
-      } else {
-        f4(base[i], k0 + k, kend, v[i]);
+      for (int i = 0; i < U; ++i) {
+        if (base[i] < 0) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          f4(base[i], k, kend, v[i]);
+        }
       }
     }
   }
   __device__ void store(uint32_t tile, uint32_t piece_stride, int pieces, bool bias) {
 #pragma unroll
     for (int i = 0; i < U; ++i) {
-      const int u = threadIdx.x + i * kThreads;
-      if (u >= UNITS) continue;
-      int row, k;
-      coords(u, row, k);
+      if (threadIdx.x + i * kThreads >= UNITS) continue;
       if constexpr (!MNC) {
-        store_split(tile + chunk_off(R, row, k), piece_stride, v[i][0], pieces);
+        store_split(tile + soff[i], piece_stride, v[i][0], pieces);
         if (bias)
           bsum[i][0] = __fadd_rn(bsum[i][0], __fadd_rn(__fadd_rn(v[i][0].x, v[i][0].y),
                                                        __fadd_rn(v[i][0].z, v[i][0].w)));
@@ -277,7 +286,7 @@ struct Gather {
         for (int j = 0; j < 4; ++j) {
           const float4 c = make_float4(comp(v[i][0], j), comp(v[i][1], j), comp(v[i][2], j),
                                        comp(v[i][3], j));
-          store_split(tile + chunk_off(R, row + j, k), piece_stride, c, pieces);
+          store_split(tile + soff[i] + 16 * j, piece_stride, c, pieces);   // rows row..row+3
           if (bias)
             bsum[i][j] =
                 __fadd_rn(bsum[i][j], __fadd_rn(__fadd_rn(c.x, c.y), __fadd_rn(c.z, c.w)));
@@ -303,8 +312,10 @@ struct Gather {
 // Policies derive from this; it supplies the gather form a policy does not
 // use (never called: the Gather of that operand uses the other form).
 struct PolBase {
-  __device__ float4 a(long long, int, int) const { return make_float4(0.f, 0.f, 0.f, 0.f); }
-  __device__ float4 b(long long, int, int) const { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ int a_koff(int) const { return 0; }
+  __device__ int b_koff(int) const { return 0; }
+  __device__ float4 a_ld(long long, int) const { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ float4 b_ld(long long, int) const { return make_float4(0.f, 0.f, 0.f, 0.f); }
   __device__ void a4(long long, int, int, float4 (&)[4]) const {}
   __device__ void b4(long long, int, int, float4 (&)[4]) const {}
 };
@@ -321,7 +332,9 @@ constexpr int kMaxTiles = 4096;
 //   float *partial ([problems][ksplits][M][N] when ksplits > 1)
 //   gridDim.z = problems * ksplits; a_row/b_row/final4 get the problem index
 //   long long a_row(m) / b_row(n)          -- per-row base (-1: row out of range)
-//   float4 a(base, k, kend) / b(base, k, kend) -- values at k..k+3 (0 beyond kend)
+//   K-major operand: int a_koff(k) -- k-dependent offset (once per k-block),
+//     float4 a_ld(base, koff) -- values at k..k+3 (k < kend checked by the engine)
+//   MN-contiguous operand: a4(base, k, kend, v[4]) -- rows base..+3 at k..k+3
 //   void final4(m, n, float4 v)            -- epilogue for columns n..n+3 of row m
 //   BIAS_FROM_B: float *bias_out (+= column sums of B over k), *bias_partial
 // nacc: the K loop of a tile round-robins its k-blocks over nacc TMEM
@@ -382,10 +395,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   // committed to smem and multiplied
   auto fetch = [&](int k0) {
     // generic lambdas: only the form matching the policy's layout is instantiated
-    ga.fetch(k0, kend, [&](auto b, int k, int ke) { return p.a(b, k, ke); },
-             [&](auto b, int k, int ke, auto &v) { p.a4(b, k, ke, v); });
-    gb.fetch(k0, kend, [&](auto b, int k, int ke) { return p.b(b, k, ke); },
-             [&](auto b, int k, int ke, auto &v) { p.b4(b, k, ke, v); });
+    ga.fetch(k0, kend, [&](int k) { return p.a_koff(k); },
+             [&](long long b, int ko) { return p.a_ld(b, ko); },
+             [&](long long b, int k, int ke, float4 (&v)[4]) { p.a4(b, k, ke, v); });
+    gb.fetch(k0, kend, [&](int k) { return p.b_koff(k); },
+             [&](long long b, int ko) { return p.b_ld(b, ko); },
+             [&](long long b, int k, int ke, float4 (&v)[4]) { p.b4(b, k, ke, v); });
   };
   if (nk > 0) fetch(kbeg);
   const bool want_bias = Pol::BIAS_FROM_B && blockIdx.x == 0;

@@ -91,10 +91,8 @@ struct FwdPol : tc::PolBase {
   __device__ int kbeg(int z) const { return z * klen; }
   __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
   __device__ long long a_row(int m, int) const { return m < M ? pixel_base(g, m) : -1; }
-  __device__ float4 a(long long base, int k, int ke) const {
-    if (k >= ke) return zero4();
-    return ld4(x + base + patch_off(g, k));
-  }
+  __device__ int a_koff(int k) const { return patch_off(g, k); }
+  __device__ float4 a_ld(long long base, int ko) const { return ld4(x + base + ko); }
   __device__ long long b_row(int n, int) const { return n < N ? n : -1; }
   // W[k][n..n+3] for k..k+3 (row-contiguous source, transposed by the engine)
   __device__ void b4(long long n, int k, int ke, float4 (&v)[4]) const {
@@ -129,13 +127,11 @@ struct LinDgradPol : tc::PolBase {
   __device__ int kbeg(int z) const { return z * klen; }
   __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
   __device__ long long a_row(int m, int) const { return m < M ? (long long)m * K : -1; }
-  __device__ float4 a(long long base, int k, int ke) const {
-    return k < ke ? ld4(dy + base + k) : zero4();
-  }
+  __device__ int a_koff(int k) const { return k; }
+  __device__ float4 a_ld(long long base, int ko) const { return ld4(dy + base + ko); }
   __device__ long long b_row(int n, int) const { return n < N ? (long long)n * K : -1; }
-  __device__ float4 b(long long base, int k, int ke) const {
-    return k < ke ? ld4(w + base + k) : zero4();
-  }
+  __device__ int b_koff(int k) const { return k; }
+  __device__ float4 b_ld(long long base, int ko) const { return ld4(w + base + ko); }
   __device__ void final4(int m, int n, float4 v, int) const {
     const int64_t o = (int64_t)m * N + n;
     st4(out + o, mask ? relu_mask(v, mask + o) : v);
@@ -174,31 +170,33 @@ struct ConvDgradPol : tc::PolBase {
     const int img = m / per, r = m - img * per, yq = r / wq, xq = r - yq * wq;
     return ((long long)img << 32) | ((long long)yq << 16) | xq;
   }
-  __device__ float4 a(long long rb, int k, int ke) const {
-    if (k >= ke) return zero4();
-    const int img = (int)(rb >> 32), yq = (int)((rb >> 16) & 0xFFFF), xq = (int)(rb & 0xFFFF);
+  // k = (tap (ti, tj), co) packed once per k-block as ti << 24 | tj << 16 | co
+  __device__ int a_koff(int k) const {
     const int tw = g.fw / g.sw;
     const int tap = k / g.N, co = k - tap * g.N;
     const int ti = tap / tw, tj = tap - ti * tw;
-    const int oy = yq - ti, ox = xq - tj;
+    return (ti << 24) | (tj << 16) | co;
+  }
+  __device__ float4 a_ld(long long rb, int ko) const {
+    const int img = (int)(rb >> 32), yq = (int)((rb >> 16) & 0xFFFF), xq = (int)(rb & 0xFFFF);
+    const int oy = yq - (ko >> 24), ox = xq - ((ko >> 16) & 0xFF), co = ko & 0xFFFF;
     if (oy < 0 || ox < 0 || oy >= g.OH || ox >= g.OW) return zero4();
     return ld4(dy + (((int64_t)img * g.OH + oy) * g.OW + ox) * g.N + co);
   }
+  // W[py + sh*ti][px + sw*tj][c][co] = row part (py, px, c) + k part (ti, tj, co)
   __device__ long long b_row(int c, int z) const {
     if (c >= N) return -1;
     int py, px, hq, wq;
     phase(z, py, px, hq, wq);
-    return ((long long)c << 16) | (py << 8) | px;
+    return (((long long)py * g.fw + px) * g.C + c) * g.N;
   }
-  __device__ float4 b(long long rb, int k, int ke) const {
-    if (k >= ke) return zero4();
-    const int c = (int)(rb >> 16), py = (int)((rb >> 8) & 0xFF), px = (int)(rb & 0xFF);
+  __device__ int b_koff(int k) const {
     const int tw = g.fw / g.sw;
     const int tap = k / g.N, co = k - tap * g.N;
     const int ti = tap / tw, tj = tap - ti * tw;
-    const int i = py + g.sh * ti, j = px + g.sw * tj;
-    return ld4(w + (((int64_t)i * g.fw + j) * g.C + c) * g.N + co);
+    return ((g.sh * ti) * g.fw + g.sw * tj) * g.C * g.N + co;
   }
+  __device__ float4 b_ld(long long base, int ko) const { return ld4(w + base + ko); }
   __device__ void final4(int m, int c, float4 v, int z) const {
     int py, px, hq, wq;
     phase(z, py, px, hq, wq);
