@@ -35,7 +35,7 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 32;               // fp32 elements per stage (4 MMA k-steps of 8)
-constexpr int kThreads = 256;          // 8 warps: all gather; warps w, w+4 share TMEM lanes
+constexpr int kThreads = 512;          // 16 warps: all gather; warps w, w+4, ... share TMEM lanes
 
 #ifndef DQN_TC_PIECES
 #define DQN_TC_PIECES 2
@@ -221,6 +221,7 @@ struct Gather {
   static constexpr int V = MNC ? 4 : 1;
   static_assert(!MNC || U == 1, "MNC gathers assume one unit per thread");
   long long base[U];
+  int t0;                      // this thread's first unit (rotated, see init)
   uint32_t soff[U];            // byte offset of the unit's (first) chunk in a piece tile
   int kk;                      // the thread's k offset inside a k-block (same for all units)
   float4 v[U][V];
@@ -235,11 +236,14 @@ struct Gather {
       k = 4 * kc;
     }
   }
+  // rot: threads [rot, rot + UNITS) take the first units, so the A and B
+  // gathers of a CTA can be laid on disjoint threads when both are short
   template <class RowFn>
-  __device__ void init(RowFn rowfn) {
+  __device__ void init(RowFn rowfn, int rot) {
+    t0 = (threadIdx.x + kThreads - rot) % kThreads;
 #pragma unroll
     for (int i = 0; i < U; ++i) {
-      const int u = threadIdx.x + i * kThreads;
+      const int u = t0 + i * kThreads;
       int row, k;
       coords(u, row, k);
       base[i] = u < UNITS ? rowfn(row) : -1;
@@ -275,7 +279,7 @@ struct Gather {
   __device__ void store(uint32_t tile, uint32_t piece_stride, int pieces, bool bias) {
 #pragma unroll
     for (int i = 0; i < U; ++i) {
-      if (threadIdx.x + i * kThreads >= UNITS) continue;
+      if (t0 + i * kThreads >= UNITS) continue;
       if constexpr (!MNC) {
         store_split(tile + soff[i], piece_stride, v[i][0], pieces);
         if (bias)
@@ -298,7 +302,7 @@ struct Gather {
   __device__ void dump_bias(float (&red)[RR][8]) const {
 #pragma unroll
     for (int i = 0; i < U; ++i) {
-      const int u = threadIdx.x + i * kThreads;
+      const int u = t0 + i * kThreads;
       if (u >= UNITS) continue;
       int row, k;
       coords(u, row, k);
@@ -383,8 +387,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   // operand gathers (rows fixed per thread across k-blocks; see Gather)
   Gather<Pol::A_MNC, BM> ga;
   Gather<Pol::B_MNC, BN> gb;
-  ga.init([&](int r) { return p.a_row(m0 + r, zp); });
-  gb.init([&](int r) { return p.b_row(n0 + r, zp); });
+  ga.init([&](int r) { return p.a_row(m0 + r, zp); }, 0);
+  gb.init([&](int r) { return p.b_row(n0 + r, zp); }, Gather<Pol::A_MNC, BM>::UNITS % kThreads);
 
   tc_fence_before();
   __syncthreads();
@@ -447,13 +451,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   // epilogue: TMEM -> registers -> smem (row-major staging) -> coalesced stores
   float *stage = reinterpret_cast<float *>(smem);
   constexpr int ES = Smem<BN>::EPI_STRIDE;
-  // warps w and w+4 read the same TMEM lane quarter (w % 4) and split the
+  // warps w, w+4, ... read the same TMEM lane quarter (w % 4) and split the
   // 16-column chunks between them
+  constexpr int GROUPS = kThreads / 128;
   const int quarter = warp & 3, half = warp >> 2;
   const int r = quarter * 32 + lane;
   const int nused = nk < nacc ? nk : nacc;
 #pragma unroll 1
-  for (int c = 16 * half; c < BN; c += 32) {
+  for (int c = 16 * half; c < BN; c += 16 * GROUPS) {
     float v[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = 0.f;
@@ -512,19 +517,28 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
     __syncthreads();
     if (s_last) {
       __threadfence();
-#pragma unroll 2
+      // partials summed in split order; 8 loads in flight per thread
+      const int64_t zstride = (int64_t)p.M * p.N;
+#pragma unroll 1
       for (int idx = threadIdx.x; idx < BM * C4; idx += kThreads) {
         const int rr = idx / C4, c4 = idx - rr * C4;
         const int m = m0 + rr, n = n0 + c4 * 4;
         if (m < p.M && n < p.N) {
-          float4 v = __ldcg(reinterpret_cast<const float4 *>(part + (int64_t)m * p.N + n));
-          for (int zz = 1; zz < ks; ++zz) {
-            const float4 t = __ldcg(reinterpret_cast<const float4 *>(
-                part + ((int64_t)zz * p.M + m) * p.N + n));
-            v.x = __fadd_rn(v.x, t.x);
-            v.y = __fadd_rn(v.y, t.y);
-            v.z = __fadd_rn(v.z, t.z);
-            v.w = __fadd_rn(v.w, t.w);
+          const float *src = part + (int64_t)m * p.N + n;
+          float4 v = __ldcg(reinterpret_cast<const float4 *>(src));
+          for (int z0 = 1; z0 < ks; z0 += 8) {
+            float4 t[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (z0 + j < ks) t[j] = __ldcg(reinterpret_cast<const float4 *>(src + (z0 + j) * zstride));
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (z0 + j < ks) {
+                v.x = __fadd_rn(v.x, t[j].x);
+                v.y = __fadd_rn(v.y, t[j].y);
+                v.z = __fadd_rn(v.z, t[j].z);
+                v.w = __fadd_rn(v.w, t[j].w);
+              }
           }
           p.final4(m, n, v, zp);
         }
