@@ -1,29 +1,38 @@
 // tcgen05 (5th-gen tensor core) implicit-GEMM engine for sm_100a.
 //
-// One CTA = 8 warps computes a 128 x BN tile of C = A * B^T (A: M x K,
-// B: N x K in "math" orientation) with the accumulator in TMEM:
-//   * all 256 threads gather operand chunks (16 B = 4 fp32) from global
-//     memory through a Policy (im2col addressing, transposed weights, ...),
-//     one k-block ahead in registers, split each value exactly into tf32
-//     pieces (x = hi + lo; kPieces = 3 gives h + m + l) and store them into
-//     shared memory in the canonical no-swizzle K-major UMMA layout (core
-//     matrices of 8 rows x 16 B);
-//   * thread 0 issues tcgen05.mma.kind::tf32 (M=128, N=BN, K=8) for the
-//     significant piece products (hi*hi, hi*lo, lo*hi: "3xTF32") and
-//     tcgen05.commit's an mbarrier per pipeline stage, so the gather of stage
-//     s+1 overlaps the MMAs of stage s;
-//   * accuracy: SURVEY.md App. A -- one bf16/tf32 pass misses the 1e-3
-//     one-step parity bar.  Measured here, the residual error of 3xTF32 is
-//     dominated by the tensor pipe's accumulation rounding, not by the
-//     dropped lo*lo term, so hi*hi and the small products go to separate
-//     TMEM accumulators and the K loop round-robins k-blocks over `nacc`
-//     accumulator pairs; the epilogue sums them in fp32 (~3e-7 rel. vs fp32
-//     SIMT per GEMM);
-//   * the epilogue reads TMEM with tcgen05.ld (warps w and w+4 own lanes
-//     32(w%4)..+31 = tile rows and split the columns), stages the tile
-//     row-major in shared memory and hands coalesced float4s to the Policy
-//     (bias / ReLU / mask / split-K partial / gradient accumulate).
-// Operands that are exact in tf32 (uint8 pixels) use one piece.
+// One CTA computes a 128 x BN tile of C = A * B^T (A: M x K, B: N x K in
+// "math" orientation), fp32 in and out, with ~fp32 accuracy from 3xTF32:
+//   x = hi + lo, hi = the top 19 bits of x (what a kind::tf32 MMA reads of an
+//   fp32 operand -- measured: it truncates, so x itself serves as hi),
+//   lo = x - hi, and A*B ~ hi*hi + hi*lo + lo*hi.
+//
+// Data paths (measured on B200: the 128 B/clk L1/shared-memory datapath is
+// the limit of a register gather that stages both operands in shared memory,
+// and a kind::tf32 MMA costs ~51 cycles for any N <= 64, 64 at N = 128):
+//   * A lives in tensor memory (the "TS" MMA form): a producer thread owns one
+//     tile row and a 16-k half of each 32-k block, loads its 16 values, and
+//     writes hi and lo with tcgen05.st (lane = row, column = k) -- A never
+//     touches shared memory;
+//   * B is gathered through registers into shared memory in the canonical
+//     no-swizzle K-major layout with its pieces stacked along N
+//     ([B_hi ; B_lo], 2*BN rows), so one MMA A_hi * [B_hi ; B_lo] (N = 2*BN)
+//     yields hi*hi and hi*lo side by side in TMEM and a second, A_lo * B_hi
+//     (N = BN), adds lo*hi to the small-term half: 2 MMAs per 8-k step
+//     instead of 3;
+//   * accuracy: the residual error is dominated by the tensor pipe's
+//     accumulation rounding, so hi*hi and the small terms accumulate in
+//     separate TMEM columns and k-blocks round-robin over `nacc` accumulator
+//     pairs; the epilogue sums them in fp32 in a fixed order (~5e-7 relative
+//     vs fp32 SIMT per GEMM; a single bf16/tf32 pass misses
+//     the 1e-3 one-step parity bar).
+// Warp roles: kGroups producer groups of 8 warps gather alternating k-blocks
+// into a STAGES-deep ring (A columns in TMEM, B tiles in shared memory) and
+// arrive on full[s]; one warp waits full[s], issues the MMAs and commits to
+// empty[s].  No block-wide barrier inside the K loop.
+// The epilogue reads TMEM with tcgen05.ld, stages the tile row-major in shared
+// memory and hands coalesced float4s to the Policy (bias / ReLU / mask /
+// split-K partial / gradient accumulate).  Exact operands (uint8 pixels) use
+// one piece.
 #pragma once
 
 #include "common.cuh"
@@ -34,13 +43,12 @@ namespace dqn {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 32;               // fp32 elements per stage (4 MMA k-steps of 8)
-constexpr int kThreads = 512;          // 16 warps: all gather; warps w, w+4, ... share TMEM lanes
-
-#ifndef DQN_TC_PIECES
-#define DQN_TC_PIECES 2
-#endif
-constexpr int kPieces = DQN_TC_PIECES;  // tf32 pieces per fp32 operand (2: hi/lo, 3: h/m/l)
+constexpr int BK = 32;                  // k per pipeline stage (4 MMA k-steps of 8)
+constexpr int kGroupThreads = 256;      // 8 warps: lane quarter w % 4, k-half w / 4
+constexpr int kGroups = 2;
+constexpr int kProducers = kGroups * kGroupThreads;
+constexpr int kThreads = kProducers + 32;
+constexpr int kTmemCols = 512;          // accumulators + A stages (one CTA per SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -59,6 +67,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void fence_barrier_init() {
@@ -84,24 +96,24 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   return d;                         // base offset 0, lbo mode 0, layout SWIZZLE_NONE
 }
 
-// Instruction descriptor: kind::tf32, fp32 accumulate, M = 128.
-__host__ __device__ constexpr uint32_t make_idesc_tf32(int n, bool a_mn, bool b_mn) {
+// Instruction descriptor: kind::tf32, fp32 accumulate, M = 128, both K-major
+// (kind::tf32 has no transposed operands: an MN-major B reads as zero).
+__host__ __device__ constexpr uint32_t make_idesc_tf32(int n) {
   return (1u << 4)                      // c_format = F32
          | (2u << 7)                    // a_format = TF32
          | (2u << 10)                   // b_format = TF32
-         | ((a_mn ? 1u : 0u) << 15)     // a_major
-         | ((b_mn ? 1u : 0u) << 16)     // b_major
          | ((uint32_t)(n >> 3) << 17)   // N >> 3
          | ((uint32_t)(BM >> 4) << 24); // M >> 4
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accumulate) {
+// D[tmem] (+)= A[tmem] * B[smem]^T
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
+                                       uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
@@ -124,38 +136,38 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float v[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 16 consecutive columns of this thread's TMEM lane (warp-collective)
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float v[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
+      "f"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
+__device__ __forceinline__ float tf32_lo(float x) { return __fsub_rn(x, tf32_hi(x)); }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y),
                "f"(v.z), "f"(v.w));
 }
 
-// x = h + m + l exactly, each exactly representable in tf32 (h: top 11
-// significant bits, m: next 11, l: the last 2), so products of the pieces are
-// exact in fp32 and the dropped m*l / l*m / l*l terms are below 2^-33 |x y|.
-__device__ __forceinline__ void store_split(uint32_t base, uint32_t level_stride, float4 v,
-                                            int levels) {
-  if (levels == 1) {
-    st_shared_v4(base, v);
-    return;
-  }
-  const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-  const float4 r = make_float4(__fsub_rn(v.x, h.x), __fsub_rn(v.y, h.y), __fsub_rn(v.z, h.z),
-                               __fsub_rn(v.w, h.w));
-  if (kPieces == 2) {          // hi/lo: lo keeps up to 13 bits, the MMA reads its top 11
-    st_shared_v4(base, h);
-    st_shared_v4(base + level_stride, r);
-    return;
-  }
-  const float4 m = make_float4(tf32_hi(r.x), tf32_hi(r.y), tf32_hi(r.z), tf32_hi(r.w));
-  const float4 l = make_float4(__fsub_rn(r.x, m.x), __fsub_rn(r.y, m.y), __fsub_rn(r.z, m.z),
-                               __fsub_rn(r.w, m.w));
-  st_shared_v4(base, h);
-  st_shared_v4(base + level_stride, m);
-  st_shared_v4(base + 2 * level_stride, l);
+// hi piece (x itself: the MMA reads its top 19 bits) and lo = x - hi (the
+// MMA reads the top 11 significant bits of lo)
+__device__ __forceinline__ void store_split(uint32_t base, uint32_t piece_stride, float4 v,
+                                            int pieces) {
+  st_shared_v4(base, v);
+  if (pieces > 1)
+    st_shared_v4(base + piece_stride,
+                 make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w)));
 }
 
 // Byte offset of a 16-byte chunk (row, 4 consecutive k) inside a K-major
@@ -170,42 +182,24 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t base, int R, int kstep) {
   return make_sdesc(base + kstep * 2 * R * 16, R * 16, 128);
 }
 
-// Operand tiles are gathered cooperatively: chunk c (16 B = row, 4 k) of an
-// R x BK tile is owned by thread c % 128, so every thread owns the same rows
-// in every k-block (row bases are computed once per CTA).  A quarter-warp
-// writes one contiguous 128-byte smem line (8 rows of one k-chunk).
+// B chunks are gathered cooperatively: chunk c (16 B = row, 4 k) of an
+// R x BK tile is owned by thread c % 256 of a producer group, so every thread
+// owns the same rows in every k-block (row bases are computed once per CTA).
+// A quarter-warp writes one contiguous 128-byte smem line (8 rows of one k-chunk).
 __device__ __forceinline__ void chunk_coords(int c, int &row, int &k) {
   const int r8 = c & 7, kc = (c >> 3) & 7, rg = c >> 6;
   row = rg * 8 + r8;
   k = kc * 4;
 }
 
-template <int BN>
-struct Smem {
-  static constexpr int A_BYTES = BM * BK * 4;
-  static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int EPI_STRIDE = BN + 4;                // floats per staged row
-  static constexpr int EPI_BYTES = BM * EPI_STRIDE * 4;
-};
-
-constexpr int tmem_cols(int bn) { return bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256; }
-
-// pipeline depth: the register-staged prefetch already overlaps the next
-// gather with the MMAs, so two stages suffice; keeping a CTA under ~110 KB
-// of shared memory lets two CTAs share an SM (16 warps hiding gather latency)
-constexpr int auto_stages(int bn, bool split_a, bool split_b) {
-  const int bytes = (split_a ? kPieces : 1) * BM * BK * 4 + (split_b ? kPieces : 1) * bn * BK * 4;
-  const int s = (110 * 1024) / bytes;
-  return s > 2 ? 2 : (s < 1 ? 1 : s);
-}
-
 __device__ __forceinline__ float comp(const float4 &v, int j) {
   return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
 }
 
-// Gathers one R x BK operand tile per k-block into registers and stores it
-// K-major.  Units are owned by thread u % 256 with the same rows in every
-// k-block, so row bases are computed once.
+// Gathers the BN x BK B tile of a k-block into registers and stores it
+// K-major with its pieces stacked along N (layout rows RL = pieces * BN;
+// piece p of row n is layout row p * BN + n).  Units are owned by thread
+// (u + rot) % 256 of a producer group with the same rows in every k-block.
 //  * MNC == false (source contiguous along k): unit = chunk (row, 4 k), one
 //    16-byte load via ld(base, koff(k)); all units of a thread share k, so
 //    the k-dependent address part is computed once per k-block;
@@ -214,15 +208,15 @@ __device__ __forceinline__ float comp(const float4 &v, int j) {
 //    f4(base, k, kend, v[4]) (consecutive lanes = consecutive row quads =
 //    coalesced), transposed in registers into four K-major chunks.
 // Optionally accumulates the per-row sums of everything stored (bias grads).
-template <bool MNC, int R>
+template <bool MNC, int R, int RL>
 struct Gather {
   static constexpr int UNITS = MNC ? R * BK / 16 : R * BK / 4;
-  static constexpr int U = (UNITS + kThreads - 1) / kThreads;
+  static constexpr int U = (UNITS + kGroupThreads - 1) / kGroupThreads;
   static constexpr int V = MNC ? 4 : 1;
   static_assert(!MNC || U == 1, "MNC gathers assume one unit per thread");
   long long base[U];
   int t0;                      // this thread's first unit (rotated, see init)
-  uint32_t soff[U];            // byte offset of the unit's (first) chunk in a piece tile
+  uint32_t soff[U];            // byte offset of the unit's (first) chunk in the tile
   int kk;                      // the thread's k offset inside a k-block (same for all units)
   float4 v[U][V];
   float bsum[U][V];
@@ -236,25 +230,21 @@ struct Gather {
       k = 4 * kc;
     }
   }
-  // rot: threads [rot, rot + UNITS) take the first units, so the A and B
-  // gathers of a CTA can be laid on disjoint threads when both are short
   template <class RowFn>
   __device__ void init(RowFn rowfn, int rot) {
-    t0 = (threadIdx.x + kThreads - rot) % kThreads;
+    t0 = (threadIdx.x % kGroupThreads + kGroupThreads - rot) % kGroupThreads;
 #pragma unroll
     for (int i = 0; i < U; ++i) {
-      const int u = t0 + i * kThreads;
+      const int u = t0 + i * kGroupThreads;
       int row, k;
       coords(u, row, k);
       base[i] = u < UNITS ? rowfn(row) : -1;
-      soff[i] = chunk_off(R, row, k);
+      soff[i] = chunk_off(RL, row, k);
       kk = k;
 #pragma unroll
       for (int j = 0; j < V; ++j) bsum[i][j] = 0.f;
     }
   }
-  // K-major: koff(k) once per k-block, ld(base, koff) per unit (k < kend
-  // checked once: every unit of a thread shares k).  MNC: f4 per unit.
   template <class KF, class LD, class F4>
   __device__ void fetch(int k0, int kend, KF &&koff, LD &&ld, F4 &&f4) {
     const int k = k0 + kk;
@@ -279,7 +269,7 @@ struct Gather {
   __device__ void store(uint32_t tile, uint32_t piece_stride, int pieces, bool bias) {
 #pragma unroll
     for (int i = 0; i < U; ++i) {
-      if (t0 + i * kThreads >= UNITS) continue;
+      if (t0 + i * kGroupThreads >= UNITS) continue;
       if constexpr (!MNC) {
         store_split(tile + soff[i], piece_stride, v[i][0], pieces);
         if (bias)
@@ -302,7 +292,7 @@ struct Gather {
   __device__ void dump_bias(float (&red)[RR][8]) const {
 #pragma unroll
     for (int i = 0; i < U; ++i) {
-      const int u = t0 + i * kThreads;
+      const int u = t0 + i * kGroupThreads;
       if (u >= UNITS) continue;
       int row, k;
       coords(u, row, k);
@@ -313,14 +303,11 @@ struct Gather {
   }
 };
 
-// Policies derive from this; it supplies the gather form a policy does not
-// use (never called: the Gather of that operand uses the other form).
+// Policies derive from this; it supplies the B gather form a policy does not
+// use (never called: the Gather uses the form of its layout).
 struct PolBase {
-  __device__ int a_koff(int) const { return 0; }
   __device__ int b_koff(int) const { return 0; }
-  __device__ float4 a_ld(long long, int) const { return make_float4(0.f, 0.f, 0.f, 0.f); }
   __device__ float4 b_ld(long long, int) const { return make_float4(0.f, 0.f, 0.f, 0.f); }
-  __device__ void a4(long long, int, int, float4 (&)[4]) const {}
   __device__ void b4(long long, int, int, float4 (&)[4]) const {}
 };
 
@@ -330,47 +317,95 @@ struct PolBase {
 // different streams with different bindings never share counters.
 constexpr int kMaxTiles = 4096;
 
+// Shared/tensor memory plan of a policy.
+template <class Pol>
+struct Plan {
+  static constexpr int BN = Pol::BN;
+  static constexpr int NA = Pol::SPLIT_A ? 2 : 1, NB = Pol::SPLIT_B ? 2 : 1;
+  static constexpr int RB = NB * BN;                   // stacked B rows (<= 256)
+  static constexpr int B_BYTES = RB * BK * 4;
+  static constexpr int A_COLS = NA * BK;               // TMEM columns per A stage
+  static constexpr int STAGES_SMEM = (200 * 1024) / B_BYTES;
+  static constexpr int STAGES_TMEM = (kTmemCols - 2 * BN) / A_COLS;   // nacc >= 1
+  static constexpr int S0 = STAGES_SMEM < STAGES_TMEM ? STAGES_SMEM : STAGES_TMEM;
+  static constexpr int STAGES = S0 > 4 ? 4 : S0;
+  static_assert(STAGES >= kGroups, "one ring slot per producer group at least");
+  static_assert(RB <= 256 && RB % 16 == 0 && BN % 16 == 0, "MMA N limits");
+  static constexpr int ACC_MAX = kTmemCols - STAGES * A_COLS;   // columns for accumulators
+  static constexpr int EPI_STRIDE = BN + 4;                      // floats per staged row
+  static constexpr int EPI_BYTES = BM * EPI_STRIDE * 4;
+  static constexpr int PIPE = STAGES * B_BYTES;
+  static constexpr int BYTES = PIPE > EPI_BYTES ? PIPE : EPI_BYTES;
+};
+
 // Policy interface (all __device__, const):
-//   static constexpr int BN, STAGES; static constexpr bool SPLIT_A, SPLIT_B, BIAS_FROM_B;
+//   static constexpr int BN; static constexpr bool SPLIT_A, SPLIT_B, BIAS_FROM_B, B_MNC;
 //   int M, N, ksplits;  int kbeg(split), kend(split);
 //   float *partial ([problems][ksplits][M][N] when ksplits > 1)
 //   gridDim.z = problems * ksplits; a_row/b_row/final4 get the problem index
 //   long long a_row(m) / b_row(n)          -- per-row base (-1: row out of range)
-//   K-major operand: int a_koff(k) -- k-dependent offset (once per k-block),
-//     float4 a_ld(base, koff) -- values at k..k+3 (k < kend checked by the engine)
-//   MN-contiguous operand: a4(base, k, kend, v[4]) -- rows base..+3 at k..k+3
+//   void a16(base, k, kend, float v[16])   -- A[row][k..k+15] (zero beyond kend;
+//                                             k is a multiple of 16)
+//   B K-major: int b_koff(k), float4 b_ld(base, koff) -- B[row][k..k+3];
+//   B MN-contiguous: b4(base, k, kend, v[4]) -- rows base..+3 at k..k+3
 //   void final4(m, n, float4 v)            -- epilogue for columns n..n+3 of row m
 //   BIAS_FROM_B: float *bias_out (+= column sums of B over k), *bias_partial
 // nacc: the K loop of a tile round-robins its k-blocks over nacc TMEM
-// accumulators that the epilogue sums in fixed order -- shorter tensor-core
-// accumulation chains (each chain rounds in the tensor pipe) for ~fp32-SIMT
-// accuracy on long reductions.
+// accumulator pairs that the epilogue sums in fixed order -- shorter
+// tensor-core accumulation chains for ~fp32-SIMT accuracy on long reductions.
+#ifdef DQN_TC_TRACE
+// per-CTA record: {ctaid, smid, t_entry, t_setup, t_kloop, t_epilogue, t_exit, nk,
+//                  t_first_store (producer 0), t_first_full (MMA warp), t_last_mma, 0}
+constexpr int kTraceCtas = 8192;
+__device__ unsigned long long g_trace[kTraceCtas * 12];
+__device__ unsigned int g_trace_n;
+__device__ int g_skip;        // diagnostic: 1 = no MMAs, 2 = no global loads, 4 = no operand stores
+#define TC_SKIP(bit) (g_skip & (bit))
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TC_MARK(i) \
+  if (threadIdx.x == 0) tr_[i] = gtimer();
+#else
+#define TC_SKIP(bit) false
+#define TC_MARK(i)
+#endif
+
 template <class Pol>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const int nacc) {
-  constexpr int BN = Pol::BN, STAGES = Pol::STAGES;
-  constexpr int A_BYTES = Smem<BN>::A_BYTES, B_BYTES = Smem<BN>::B_BYTES;
-  constexpr int NA = Pol::SPLIT_A ? kPieces : 1, NB = Pol::SPLIT_B ? kPieces : 1;
-  constexpr int STAGE_BYTES = NA * A_BYTES + NB * B_BYTES;
-  // accumulator pairs: [a] holds the h*h chain, [nacc + a] the small pieces
-  constexpr bool TWO = Pol::SPLIT_A || Pol::SPLIT_B;
-  const int TCOLS = tmem_cols(BN * nacc * (TWO ? 2 : 1));
-  constexpr uint32_t IDESC = make_idesc_tf32(BN, false, false);   // both K-major
+  using PL = Plan<Pol>;
+  constexpr int BN = Pol::BN, STAGES = PL::STAGES, NA = PL::NA, NB = PL::NB, RB = PL::RB;
+  constexpr int B_BYTES = PL::B_BYTES;
+  constexpr uint32_t IDESC_FULL = make_idesc_tf32(RB), IDESC_HALF = make_idesc_tf32(BN);
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bars[STAGES];
+  // full[s]: the producer group that filled slot s is done (256 arrivals);
+  // empty[s]: the MMAs reading slot s completed (tcgen05.commit); done: all MMAs
+  __shared__ uint64_t full[STAGES], empty[STAGES], done;
   __shared__ uint32_t tmem_slot;
-  __shared__ float bias_red[Pol::BIAS_FROM_B ? BN : 1][8];
+  __shared__ float bias_red[Pol::BIAS_FROM_B ? kGroups : 1][Pol::BIAS_FROM_B ? BN : 1][8];
 
+#ifdef DQN_TC_TRACE
+  unsigned long long tr_[6] = {0, 0, 0, 0, 0, 0};
+  __shared__ unsigned long long tr_mma[2];
+#endif
+  TC_MARK(0)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_slot)),
-                 "r"(TCOLS)
+                 "r"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (threadIdx.x == 32) {
 #pragma unroll
-    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], kGroupThreads);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&done, 1);
     fence_barrier_init();
   }
 
@@ -383,98 +418,136 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   float *const part = p.partial + (SPLITK ? (int64_t)zp * ks * p.M * p.N : 0);
   const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
   const uint32_t sbase = smem_u32(smem);
+  const bool producer = threadIdx.x < kProducers;
+  const int group = threadIdx.x / kGroupThreads;
+  // A ownership: TMEM lane quarter = warp % 4 (the warp's accessible lanes),
+  // k-half = (warp / 4) % 2 of each 32-k block
+  const int quarter = warp & 3, khalf = (warp >> 2) & 1;
+  const int arow = quarter * 32 + lane;
 
-  // operand gathers (rows fixed per thread across k-blocks; see Gather)
-  Gather<Pol::A_MNC, BM> ga;
-  Gather<Pol::B_MNC, BN> gb;
-  ga.init([&](int r) { return p.a_row(m0 + r, zp); }, 0);
-  gb.init([&](int r) { return p.b_row(n0 + r, zp); }, Gather<Pol::A_MNC, BM>::UNITS % kThreads);
+  long long abase = -1;
+  Gather<Pol::B_MNC, BN, RB> gb;
+  if (producer) {
+    abase = p.a_row(m0 + arow, zp);
+    gb.init([&](int r) { return p.b_row(n0 + r, zp); }, 0);
+  }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
-
-  // register-staged prefetch: tile kb+1 is in flight while tile kb is
-  // committed to smem and multiplied
-  auto fetch = [&](int k0) {
-    // generic lambdas: only the form matching the policy's layout is instantiated
-    ga.fetch(k0, kend, [&](int k) { return p.a_koff(k); },
-             [&](long long b, int ko) { return p.a_ld(b, ko); },
-             [&](long long b, int k, int ke, float4 (&v)[4]) { p.a4(b, k, ke, v); });
-    gb.fetch(k0, kend, [&](int k) { return p.b_koff(k); },
-             [&](long long b, int ko) { return p.b_ld(b, ko); },
-             [&](long long b, int k, int ke, float4 (&v)[4]) { p.b4(b, k, ke, v); });
-  };
-  if (nk > 0) fetch(kbeg);
+  // accumulator pairs [big | small] at columns a * 2BN, A stages after them
+  const uint32_t acol0 = (uint32_t)PL::ACC_MAX;
   const bool want_bias = Pol::BIAS_FROM_B && blockIdx.x == 0;
+  TC_MARK(1)
 
-  for (int kb = 0; kb < nk; ++kb) {
-    const int s = kb % STAGES;
-    if (kb >= STAGES) mbar_wait(&bars[s], ((kb / STAGES) - 1) & 1);
-    const uint32_t st = sbase + s * STAGE_BYTES;
-    const uint32_t a_t = st, b_t = st + NA * A_BYTES;     // piece p at +p*A_BYTES / +p*B_BYTES
-    ga.store(a_t, A_BYTES, NA, false);
-    gb.store(b_t, B_BYTES, NB, want_bias);
-    if (kb + 1 < nk) fetch(kbeg + (kb + 1) * BK);
-    fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tc_fence_after();
-      const uint32_t dbig = tmem + (uint32_t)((kb % nacc) * BN);
-      const uint32_t dsmall = dbig + (uint32_t)(nacc * BN);
+  if (producer) {
+    // group g gathers k-blocks g, g + kGroups, ... into ring slot kb % STAGES;
+    // a slot is refilled once the MMAs of k-block kb - STAGES completed
+    float av[16];
+    auto fetch = [&](int k0) {
+      if (TC_SKIP(2)) return;
+      if (abase >= 0) {
+        p.a16(abase, k0 + 16 * khalf, kend, av);
+      } else {
 #pragma unroll
-      for (int ks = 0; ks < BK / 8; ++ks) {
-        bool first_big = (kb < nacc && ks == 0), first_small = first_big;
-        // piece products with significance 2^0, 2^-11, 2^-22: (ia, ib), ia + ib < kPieces
-#pragma unroll
-        for (int sum = 0; sum < kPieces; ++sum)
-#pragma unroll
-          for (int ia = 0; ia <= sum; ++ia) {
-            const int ib = sum - ia;
-            if (ia >= NA || ib >= NB) continue;
-            bool &first = sum == 0 ? first_big : first_small;
-            mma_tf32(sum == 0 ? dbig : dsmall, op_desc(a_t + ia * A_BYTES, BM, ks),
-                     op_desc(b_t + ib * B_BYTES, BN, ks), IDESC, first ? 0u : 1u);
-            first = false;
-          }
+        for (int j = 0; j < 16; ++j) av[j] = 0.f;
       }
-      mma_commit(&bars[s]);
+      gb.fetch(k0, kend, [&](int k) { return p.b_koff(k); },
+               [&](long long b, int ko) { return p.b_ld(b, ko); },
+               [&](long long b, int k, int ke, float4 (&v)[4]) { p.b4(b, k, ke, v); });
+    };
+    if (group < nk) fetch(kbeg + group * BK);
+    for (int kb = group; kb < nk; kb += kGroups) {
+      const int s = kb % STAGES, use = kb / STAGES;
+      if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);    // MMAs of kb - STAGES done
+      tc_fence_after();
+#ifdef DQN_TC_TRACE
+      if (kb == 0 && threadIdx.x == 0) tr_[5] = gtimer();
+#endif
+      if (!TC_SKIP(4)) {
+        // A: hi (= the values) and lo pieces into this stage's TMEM columns
+        const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + acol0 +
+                            (uint32_t)(s * PL::A_COLS + 16 * khalf);
+        tmem_st16(ta, av);
+        if (NA > 1) {
+          float lo[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) lo[j] = tf32_lo(av[j]);
+          tmem_st16(ta + BK, lo);
+        }
+        gb.store(sbase + s * B_BYTES, BN * 16, NB, want_bias);
+        tmem_wait_st();
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(&full[s]);
+      // register-staged prefetch of this group's next k-block
+      if (kb + kGroups < nk) fetch(kbeg + (kb + kGroups) * BK);
     }
+  } else if (lane == 0) {
+    // MMA issuer: k-blocks in order, each slot released by tcgen05.commit
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(&full[s], (kb / STAGES) & 1);
+#ifdef DQN_TC_TRACE
+      if (kb == 0) tr_mma[0] = gtimer();
+#endif
+      tc_fence_after();
+      if (!TC_SKIP(1)) {
+        const uint32_t dbig = tmem + (uint32_t)((kb % nacc) * 2 * BN);
+        const uint32_t dsmall = dbig + (uint32_t)BN;
+        const uint32_t ta = tmem + acol0 + (uint32_t)(s * PL::A_COLS);
+        const uint32_t tb = sbase + s * B_BYTES;
+#pragma unroll
+        for (int kq = 0; kq < BK / 8; ++kq) {
+          const uint64_t db = op_desc(tb, RB, kq);
+          const uint32_t first = (kb < nacc && kq == 0) ? 0u : 1u;
+          // hi * [B_hi ; B_lo] -> [big | small]; the first touch of a pair overwrites
+          mma_ts(dbig, ta + 8 * kq, db, NB > 1 ? IDESC_FULL : IDESC_HALF, first);
+          // lo * B_hi -> small (initialised by the first MMA when B is split)
+          if (NA > 1) mma_ts(dsmall, ta + BK + 8 * kq, db, IDESC_HALF, NB > 1 ? 1u : first);
+        }
+      }
+      mma_commit(&empty[s]);
+    }
+#ifdef DQN_TC_TRACE
+    tr_mma[1] = gtimer();
+#endif
+    mma_commit(&done);
   }
-  if (nk > 0) {
-    const int s = (nk - 1) % STAGES;
-    mbar_wait(&bars[s], ((nk - 1) / STAGES) & 1);
-  }
+  mbar_wait(&done, 0);
+  TC_MARK(2)
   tc_fence_after();
 
   // epilogue: TMEM -> registers -> smem (row-major staging) -> coalesced stores
   float *stage = reinterpret_cast<float *>(smem);
-  constexpr int ES = Smem<BN>::EPI_STRIDE;
-  // warps w, w+4, ... read the same TMEM lane quarter (w % 4) and split the
-  // 16-column chunks between them
-  constexpr int GROUPS = kThreads / 128;
-  const int quarter = warp & 3, half = warp >> 2;
-  const int r = quarter * 32 + lane;
+  constexpr int ES = PL::EPI_STRIDE;
+  // producer warps w, w+4, ... read the same TMEM lane quarter (w % 4) and
+  // split the 16-column chunks between them
+  constexpr int CGROUPS = kProducers / 128;
+  const int cgrp = warp >> 2;
   const int nused = nk < nacc ? nk : nacc;
+  constexpr bool TWO = NA > 1 || NB > 1;
+  if (producer) {
 #pragma unroll 1
-  for (int c = 16 * half; c < BN; c += 16 * GROUPS) {
-    float v[16];
+    for (int c = 16 * cgrp; c < BN; c += 16 * CGROUPS) {
+      float v[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = 0.f;
-    // small-piece sums first (fixed order), then the h*h chains
-    const int na = TWO ? 2 * nacc : nacc;
-    for (int q = 0; q < na; ++q) {
-      const int a = TWO ? (q < nacc ? nacc + q : q - nacc) : q;   // smalls, then bigs
-      if ((a % nacc) >= nused) continue;
-      float t[16];
-      tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(a * BN + c), t);
+      for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      // small-term sums first (fixed order), then the h*h chains
+      for (int q = 0; q < 2 * nacc; ++q) {
+        const int a = q % nacc, small = q < nacc;
+        if (a >= nused || (small && !TWO)) continue;
+        float t[16];
+        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(a * 2 * BN + small * BN + c), t);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], t[j]);
+        for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], t[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j += 4)
+        *reinterpret_cast<float4 *>(&stage[arow * ES + c + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
     }
-#pragma unroll
-    for (int j = 0; j < 16; j += 4)
-      *reinterpret_cast<float4 *>(&stage[r * ES + c + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
   }
   tc_fence_before();
   __syncthreads();
@@ -493,12 +566,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   }
   // bias gradients folded into the B gather: column sums of this CTA's slice
   if constexpr (Pol::BIAS_FROM_B) if (blockIdx.x == 0) {
-    gb.dump_bias(bias_red);
+    if (producer) gb.dump_bias(bias_red[group]);
     __syncthreads();
     if (threadIdx.x < BN && n0 + (int)threadIdx.x < p.N) {
-      float s = bias_red[threadIdx.x][0];
+      float s = bias_red[0][threadIdx.x][0];
 #pragma unroll
-      for (int kc = 1; kc < 8; ++kc) s = __fadd_rn(s, bias_red[threadIdx.x][kc]);
+      for (int g = 0; g < kGroups; ++g)
+#pragma unroll
+        for (int kc = 0; kc < 8; ++kc)
+          if (g + kc > 0) s = __fadd_rn(s, bias_red[g][threadIdx.x][kc]);
       const int n = n0 + threadIdx.x;
       if (!SPLITK)
         p.bias_out[n] = __fadd_rn(p.bias_out[n], s);
@@ -506,6 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
         p.bias_partial[(int64_t)zs * p.N + n] = s;
     }
   }
+  TC_MARK(3)
   // split-K fixup: the last CTA of a tile sums every split's partial in split
   // order (deterministic, whichever CTA arrives last) and runs the epilogue
   if (SPLITK) {
@@ -553,17 +630,35 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
       if (threadIdx.x == 0) p.counters[tile] = 0;      // reusable by the next launch
     }
   }
+  __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols)
                  : "memory");
+#ifdef DQN_TC_TRACE
+  TC_MARK(4)
+  if (threadIdx.x == 0) {
+    const unsigned int i = atomicAdd(&g_trace_n, 1u);
+    if (i < kTraceCtas) {
+      unsigned int smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      unsigned long long *r = g_trace + 12ull * i;
+      r[0] = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      r[1] = smid;
+      for (int j = 0; j < 5; ++j) r[2 + j] = tr_[j];
+      r[7] = nk;
+      r[8] = tr_[5];
+      r[9] = tr_mma[0];
+      r[10] = tr_mma[1];
+      r[11] = 0;
+    }
+  }
+#endif
 }
 
 template <class Pol>
 inline int smem_bytes() {
-  constexpr int NA = Pol::SPLIT_A ? kPieces : 1, NB = Pol::SPLIT_B ? kPieces : 1;
-  constexpr int pipe = Pol::STAGES * (NA * Smem<Pol::BN>::A_BYTES + NB * Smem<Pol::BN>::B_BYTES);
-  constexpr int epi = Smem<Pol::BN>::EPI_BYTES;
-  return pipe > epi ? pipe : epi;
+  return Plan<Pol>::BYTES;
 }
 
 template <class Pol>
@@ -583,11 +678,11 @@ int launch(cudaStream_t st, const Pol &p, int splits, const char *what) {
   }
   static const int env_nacc = [] {
     const char *e = getenv("DQN_TC_NACC");
-    return e ? atoi(e) : 2;      // 2 accumulator pairs: <= 256 TMEM columns at BN <= 64
+    return e ? atoi(e) : 2;
   }();
+  // accumulator pairs [big | small] (2 * BN columns each) share TMEM with the A stages
   int nacc = env_nacc < 1 ? 1 : env_nacc;
-  const int pair = (Pol::SPLIT_A || Pol::SPLIT_B) ? 2 : 1;
-  while (nacc > 1 && Pol::BN * nacc * pair > 256) --nacc;   // 2 CTAs/SM can always allocate
+  while (nacc > 1 && 2 * Pol::BN * nacc > Plan<Pol>::ACC_MAX) --nacc;
   tc_gemm_kernel<Pol><<<grid, kThreads, bytes, st>>>(p, nacc);
   DQN_LAUNCH_CHECK(what);
   return DQN_OK;

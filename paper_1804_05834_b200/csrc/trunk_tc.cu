@@ -63,6 +63,23 @@ __device__ __forceinline__ int patch_off(const Geo &g, int k) {
 }
 
 __device__ __forceinline__ void st4(float *p, float4 v) { *reinterpret_cast<float4 *>(p) = v; }
+
+// 16 consecutive values (4-aligned run) into v, or zeros
+template <typename T>
+__device__ __forceinline__ void ld16(const T *p, float (&v)[16]) {
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const float4 q = ld4(p + 4 * t);
+    v[4 * t] = q.x;
+    v[4 * t + 1] = q.y;
+    v[4 * t + 2] = q.z;
+    v[4 * t + 3] = q.w;
+  }
+}
+__device__ __forceinline__ void zero16(float (&v)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = 0.f;
+}
 __device__ __forceinline__ float4 ld4_rw(const float *p) { return *reinterpret_cast<const float4 *>(p); }
 
 __device__ __forceinline__ float4 relu_mask(float4 v, const float *mask) {
@@ -79,8 +96,8 @@ template <typename InT, int BN_>
 struct FwdPol : tc::PolBase {
   static constexpr bool U8 = sizeof(InT) == 1;
   static constexpr bool SPLIT_A = !U8, SPLIT_B = true, BIAS_FROM_B = false;
-  static constexpr bool A_MNC = false, B_MNC = true;
-  static constexpr int BN = BN_, STAGES = tc::auto_stages(BN_, SPLIT_A, SPLIT_B);
+  static constexpr bool B_MNC = true;
+  static constexpr int BN = BN_;
   const InT *x;
   const float *w, *bias;
   float *y, *partial;
@@ -91,8 +108,11 @@ struct FwdPol : tc::PolBase {
   __device__ int kbeg(int z) const { return z * klen; }
   __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
   __device__ long long a_row(int m, int) const { return m < M ? pixel_base(g, m) : -1; }
-  __device__ int a_koff(int k) const { return patch_off(g, k); }
-  __device__ float4 a_ld(long long base, int ko) const { return ld4(x + base + ko); }
+  // 16 | fw * C: a 16-run of k stays inside one patch row
+  __device__ void a16(long long base, int k, int ke, float (&v)[16]) const {
+    if (k >= ke) return zero16(v);
+    ld16(x + base + patch_off(g, k), v);
+  }
   __device__ long long b_row(int n, int) const { return n < N ? n : -1; }
   // W[k][n..n+3] for k..k+3 (row-contiguous source, transposed by the engine)
   __device__ void b4(long long n, int k, int ke, float4 (&v)[4]) const {
@@ -117,8 +137,8 @@ struct FwdPol : tc::PolBase {
 template <int BN_>
 struct LinDgradPol : tc::PolBase {
   static constexpr bool SPLIT_A = true, SPLIT_B = true, BIAS_FROM_B = false;
-  static constexpr bool A_MNC = false, B_MNC = false;
-  static constexpr int BN = BN_, STAGES = tc::auto_stages(BN_, SPLIT_A, SPLIT_B);
+  static constexpr bool B_MNC = false;
+  static constexpr int BN = BN_;
   const float *dy, *w, *mask;
   float *out, *partial;
   float *bias_out, *bias_partial;
@@ -127,8 +147,10 @@ struct LinDgradPol : tc::PolBase {
   __device__ int kbeg(int z) const { return z * klen; }
   __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
   __device__ long long a_row(int m, int) const { return m < M ? (long long)m * K : -1; }
-  __device__ int a_koff(int k) const { return k; }
-  __device__ float4 a_ld(long long base, int ko) const { return ld4(dy + base + ko); }
+  __device__ void a16(long long base, int k, int ke, float (&v)[16]) const {
+    if (k >= ke) return zero16(v);
+    ld16(dy + base + k, v);
+  }
   __device__ long long b_row(int n, int) const { return n < N ? (long long)n * K : -1; }
   __device__ int b_koff(int k) const { return k; }
   __device__ float4 b_ld(long long base, int ko) const { return ld4(w + base + ko); }
@@ -144,8 +166,8 @@ struct LinDgradPol : tc::PolBase {
 template <int BN_>
 struct ConvDgradPol : tc::PolBase {
   static constexpr bool SPLIT_A = true, SPLIT_B = true, BIAS_FROM_B = false;
-  static constexpr bool A_MNC = false, B_MNC = false;
-  static constexpr int BN = BN_, STAGES = tc::auto_stages(BN_, SPLIT_A, SPLIT_B);
+  static constexpr bool B_MNC = false;
+  static constexpr int BN = BN_;
   const float *dy, *w, *mask;
   float *out, *partial;
   float *bias_out, *bias_partial;
@@ -170,18 +192,16 @@ struct ConvDgradPol : tc::PolBase {
     const int img = m / per, r = m - img * per, yq = r / wq, xq = r - yq * wq;
     return ((long long)img << 32) | ((long long)yq << 16) | xq;
   }
-  // k = (tap (ti, tj), co) packed once per k-block as ti << 24 | tj << 16 | co
-  __device__ int a_koff(int k) const {
+  // k = (tap (ti, tj), co); Cout % 16 == 0 keeps a 16-run inside one tap
+  __device__ void a16(long long rb, int k, int ke, float (&v)[16]) const {
+    if (k >= ke) return zero16(v);
+    const int img = (int)(rb >> 32), yq = (int)((rb >> 16) & 0xFFFF), xq = (int)(rb & 0xFFFF);
     const int tw = g.fw / g.sw;
     const int tap = k / g.N, co = k - tap * g.N;
     const int ti = tap / tw, tj = tap - ti * tw;
-    return (ti << 24) | (tj << 16) | co;
-  }
-  __device__ float4 a_ld(long long rb, int ko) const {
-    const int img = (int)(rb >> 32), yq = (int)((rb >> 16) & 0xFFFF), xq = (int)(rb & 0xFFFF);
-    const int oy = yq - (ko >> 24), ox = xq - ((ko >> 16) & 0xFF), co = ko & 0xFFFF;
-    if (oy < 0 || ox < 0 || oy >= g.OH || ox >= g.OW) return zero4();
-    return ld4(dy + (((int64_t)img * g.OH + oy) * g.OW + ox) * g.N + co);
+    const int oy = yq - ti, ox = xq - tj;
+    if (oy < 0 || ox < 0 || oy >= g.OH || ox >= g.OW) return zero16(v);
+    ld16(dy + (((int64_t)img * g.OH + oy) * g.OW + ox) * g.N + co, v);
   }
   // W[py + sh*ti][px + sw*tj][c][co] = row part (py, px, c) + k part (ti, tj, co)
   __device__ long long b_row(int c, int z) const {
@@ -217,8 +237,8 @@ template <typename InT, int BN_>
 struct WgradPol : tc::PolBase {
   static constexpr bool U8 = sizeof(InT) == 1;
   static constexpr bool SPLIT_A = !U8, SPLIT_B = true, BIAS_FROM_B = true;
-  static constexpr bool A_MNC = true, B_MNC = true;
-  static constexpr int BN = BN_, STAGES = tc::auto_stages(BN_, SPLIT_A, SPLIT_B);
+  static constexpr bool B_MNC = true;
+  static constexpr int BN = BN_;
   const InT *x;
   const float *dy;
   float *grad, *partial;
@@ -229,21 +249,18 @@ struct WgradPol : tc::PolBase {
   __device__ int kbeg(int z) const { return z * klen; }
   __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
   __device__ long long a_row(int r, int) const { return r < M ? patch_off(g, r) : -1; }
-  // patch rows r..r+3 (contiguous in NHWC: fw*C % 4 == 0) at pixels
-  // pix..pix+3: the window bases walk along the output row
-  __device__ void a4(long long roff, int pix, int ke, float4 (&v)[4]) const {
+  // patch element r at pixels pix..pix+15: the window bases walk along the
+  // output rows (a warp's 32 lanes = 32 consecutive patch elements: coalesced)
+  __device__ void a16(long long roff, int pix, int ke, float (&v)[16]) const {
     const int P = g.OH * g.OW;
     int img = pix / P, p = pix - img * P;
     int oy = p / g.OW, ox = p - oy * g.OW;
+    const InT *src = x + roff;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (pix + i < ke) {
-        const long long base =
-            (((long long)img * g.H + (long long)oy * g.sh) * g.W + (long long)ox * g.sw) * g.C;
-        v[i] = ld4(x + base + roff);
-      } else {
-        v[i] = zero4();
-      }
+    for (int i = 0; i < 16; ++i) {
+      const long long base =
+          (((long long)img * g.H + (long long)oy * g.sh) * g.W + (long long)ox * g.sw) * g.C;
+      v[i] = pix + i < ke ? (float)__ldg(src + base) : 0.f;
       if (++ox == g.OW) {
         ox = 0;
         if (++oy == g.OH) { oy = 0; ++img; }
@@ -446,6 +463,7 @@ bool tc_layer_supported(const dqn_net_desc *net, int l, int phase) {
   if (L.kind == DQN_LAYER_LINEAR && l == net->n_layers - 1 && L.out_c <= 32) return false;  // head
   const int N = L.out_c;
   if (!(N == 32 || N == 64 || N % 128 == 0)) return false;
+  if (phase == 0 && (L.fw * L.in_c) % 16) return false;      // A rows gathered in 16-runs
   if (phase == 1 && L.kind == DQN_LAYER_CONV &&
       (L.fh % L.sh || L.fw % L.sw || !dgrad_tile_ok(L.in_c)))
     return false;
@@ -514,3 +532,18 @@ int tc_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads
 }
 
 }  // namespace dqn
+
+#ifdef DQN_TC_TRACE
+// copies (and resets) the per-CTA trace records of tc_gemm_kernel launches
+extern "C" int dqn_tc_trace(unsigned long long *host, int max_ctas) {
+  unsigned int n = 0;
+  cudaMemcpyFromSymbol(&n, dqn::tc::g_trace_n, sizeof(n));
+  if (n > (unsigned)dqn::tc::kTraceCtas) n = dqn::tc::kTraceCtas;
+  if ((int)n > max_ctas) n = max_ctas;
+  if (n) cudaMemcpyFromSymbol(host, dqn::tc::g_trace, 12ull * n * sizeof(unsigned long long));
+  const unsigned int zero = 0;
+  cudaMemcpyToSymbol(dqn::tc::g_trace_n, &zero, sizeof(zero));
+  return (int)n;
+}
+extern "C" void dqn_tc_skip(int mask) { cudaMemcpyToSymbol(dqn::tc::g_skip, &mask, sizeof(mask)); }
+#endif
