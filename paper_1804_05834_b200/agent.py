@@ -166,7 +166,8 @@ class _StepPlan:
         Two streams (both captured into the step's CUDA graph): the target
         forward runs beside the online forward, and each layer's wgrad runs
         beside the rest of the dgrad chain as soon as that layer's output
-        gradient exists (it has its own scratch / split-K counters)."""
+        gradient exists (it has its own scratch / split-K counters); the first
+        layer's wgrad, which has no dgrad beside it, stays on the main stream."""
         torch = _lib.require_cuda()
         st = _lib.stream_ptr()
         k = self.k
@@ -201,13 +202,17 @@ class _StepPlan:
         e = ev()
         e.record(s0)
         for layer in reversed(range(len(on._units))):
+            if layer == 0:
+                # conv1 has no dgrad: its wgrad takes the main stream (and the
+                # dgrad binding's scratch) instead of queueing behind conv2's
+                on.layer_into(self.on_view, 0, 2)
+                break
             with torch.cuda.stream(s1):           # wgrad of `layer` once its grad exists
                 s1.wait_event(e)
                 on.layer_into(self.on_wview, layer, 2)
-            if layer > 0:                          # dgrad chain continues on s0
-                on.layer_into(self.on_view, layer, 1)
-                e = ev()
-                e.record(s0)
+            on.layer_into(self.on_view, layer, 1)  # dgrad chain continues on s0
+            e = ev()
+            e.record(s0)
         e_w = ev()
         e_w.record(s1)
         s0.wait_event(e_w)

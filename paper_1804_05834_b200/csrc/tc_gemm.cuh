@@ -311,10 +311,11 @@ struct PolBase {
   __device__ void b4(long long, int, int, float4 (&)[4]) const {}
 };
 
-// Split-K tiles count arrivals in a per-binding int table (the tail of the
-// binding scratch, zero-initialised); the last CTA resets its counter, so the
-// table is all-zero between launches (graph-replay safe) and two kernels on
-// different streams with different bindings never share counters.
+// Split-K tiles count arrivals (and finished reducers) in a per-binding int
+// table (the tail of the binding scratch, zero-initialised, two ints per
+// tile); the last reducer resets them, so the table is all-zero between
+// launches (graph-replay safe) and two kernels on different streams with
+// different bindings never share counters.
 constexpr int kMaxTiles = 4096;
 
 // Shared/tensor memory plan of a policy.
@@ -355,7 +356,7 @@ struct Plan {
 // tensor-core accumulation chains for ~fp32-SIMT accuracy on long reductions.
 #ifdef DQN_TC_TRACE
 // per-CTA record: {ctaid, smid, t_entry, t_setup, t_kloop, t_epilogue, t_exit, nk,
-//                  t_first_store (producer 0), t_first_full (MMA warp), t_last_mma, 0}
+//                  t_first_store (producer 0), t_first_full (MMA warp), t_last_mma, launch id}
 constexpr int kTraceCtas = 8192;
 __device__ unsigned long long g_trace[kTraceCtas * 12];
 __device__ unsigned int g_trace_n;
@@ -374,8 +375,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 template <class Pol>
-__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const int nacc) {
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const int nacc_arg) {
   using PL = Plan<Pol>;
+  const int nacc = nacc_arg & 0xFF;     // trace builds carry a launch id in the upper bits
   constexpr int BN = Pol::BN, STAGES = PL::STAGES, NA = PL::NA, NB = PL::NB, RB = PL::RB;
   constexpr int B_BYTES = PL::B_BYTES;
   constexpr uint32_t IDESC_FULL = make_idesc_tf32(RB), IDESC_HALF = make_idesc_tf32(BN);
@@ -583,51 +585,101 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
     }
   }
   TC_MARK(3)
-  // split-K fixup: the last CTA of a tile sums every split's partial in split
-  // order (deterministic, whichever CTA arrives last) and runs the epilogue
+  // split-K fixup: the last R CTAs to arrive at a tile each sum a slice of its
+  // rows over every split's partial in split order (deterministic whichever
+  // CTAs arrive last) and run the epilogue on it.  Reducers other than the
+  // very last wait for the remaining arrivals; they are deadlock-free because
+  // at most tiles * (R - 1) <= 60 CTAs of a launch ever wait, so two such
+  // launches side by side leave SMs for every pending CTA.
   if (SPLITK) {
-    __shared__ int s_last;
+    __shared__ int s_ticket;
     __threadfence();
     __syncthreads();
     const int tile = (zp * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    if (threadIdx.x == 0) s_last = (atomicAdd(&p.counters[tile], 1) == ks - 1);
+    const int tiles = gridDim.x * gridDim.y * (gridDim.z / ks);
+    int R = 60 / tiles + 1;
+    R = R > 8 ? 8 : R;
+    R = R > ks ? ks : R;
+    int *arrive = p.counters + 2 * tile, *finished = arrive + 1;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(arrive, 1);
     __syncthreads();
-    if (s_last) {
+    const int ticket = s_ticket;
+    if (ticket >= ks - R) {
+      const int red = ticket - (ks - R);
+      if (ticket < ks - 1) {
+        if (threadIdx.x == 0) {
+          int seen;
+          do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(arrive) : "memory");
+          } while (seen < ks);
+        }
+        __syncthreads();
+      }
       __threadfence();
-      // partials summed in split order; 8 loads in flight per thread
+      // rows [r0, r1) of the tile; partials summed in split order, two float4
+      // columns per pass and up to 4 splits per round (8 loads in flight per
+      // thread: a round trip costs ~1 us)
+      const int rows = (BM + R - 1) / R, r0 = red * rows, r1 = min(BM, r0 + rows);
       const int64_t zstride = (int64_t)p.M * p.N;
 #pragma unroll 1
-      for (int idx = threadIdx.x; idx < BM * C4; idx += kThreads) {
-        const int rr = idx / C4, c4 = idx - rr * C4;
-        const int m = m0 + rr, n = n0 + c4 * 4;
-        if (m < p.M && n < p.N) {
-          const float *src = part + (int64_t)m * p.N + n;
-          float4 v = __ldcg(reinterpret_cast<const float4 *>(src));
-          for (int z0 = 1; z0 < ks; z0 += 8) {
-            float4 t[8];
+      for (int idx0 = r0 * C4 + threadIdx.x; idx0 < r1 * C4; idx0 += 2 * kThreads) {
+        float4 acc[2];
+        const float *src[2];
+        bool ok[2];
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (z0 + j < ks) t[j] = __ldcg(reinterpret_cast<const float4 *>(src + (z0 + j) * zstride));
+        for (int f = 0; f < 2; ++f) {
+          const int idx = idx0 + f * kThreads;
+          const int rr = idx / C4, c4 = idx - rr * C4;
+          const int m = m0 + rr, n = n0 + c4 * 4;
+          ok[f] = idx < r1 * C4 && m < p.M && n < p.N;
+          src[f] = part + (int64_t)(ok[f] ? m : 0) * p.N + (ok[f] ? n : 0);
+        }
+#pragma unroll 1
+        for (int z0 = 0; z0 < ks; z0 += 4) {
+          float4 t[2][4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (z0 + j < ks) {
-                v.x = __fadd_rn(v.x, t[j].x);
-                v.y = __fadd_rn(v.y, t[j].y);
-                v.z = __fadd_rn(v.z, t[j].z);
-                v.w = __fadd_rn(v.w, t[j].w);
+          for (int f = 0; f < 2; ++f)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (ok[f] && z0 + j < ks)
+                t[f][j] = __ldcg(reinterpret_cast<const float4 *>(src[f] + (z0 + j) * zstride));
+#pragma unroll
+          for (int f = 0; f < 2; ++f)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (ok[f] && z0 + j < ks) {
+                if (z0 + j == 0) {
+                  acc[f] = t[f][j];
+                } else {
+                  acc[f].x = __fadd_rn(acc[f].x, t[f][j].x);
+                  acc[f].y = __fadd_rn(acc[f].y, t[f][j].y);
+                  acc[f].z = __fadd_rn(acc[f].z, t[f][j].z);
+                  acc[f].w = __fadd_rn(acc[f].w, t[f][j].w);
+                }
               }
-          }
-          p.final4(m, n, v, zp);
+        }
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+          if (!ok[f]) continue;
+          const int idx = idx0 + f * kThreads;
+          const int rr = idx / C4, c4 = idx - rr * C4;
+          p.final4(m0 + rr, n0 + c4 * 4, acc[f], zp);
         }
       }
-      if (Pol::BIAS_FROM_B && blockIdx.x == 0 && threadIdx.x < BN && n0 + (int)threadIdx.x < p.N) {
+      if (Pol::BIAS_FROM_B && red == 0 && blockIdx.x == 0 && threadIdx.x < BN &&
+          n0 + (int)threadIdx.x < p.N) {
         const int n = n0 + threadIdx.x;
         float s = __ldcg(p.bias_partial + n);
         for (int zz = 1; zz < ks; ++zz)
           s = __fadd_rn(s, __ldcg(p.bias_partial + (int64_t)zz * p.N + n));
         p.bias_out[n] = __fadd_rn(p.bias_out[n], s);
       }
-      if (threadIdx.x == 0) p.counters[tile] = 0;      // reusable by the next launch
+      // the last reducer to finish resets the tile's counters for the next launch
+      __syncthreads();
+      if (threadIdx.x == 0 && atomicAdd(finished, 1) == R - 1) {
+        *arrive = 0;
+        *finished = 0;
+      }
     }
   }
   __syncthreads();
@@ -650,11 +702,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
       r[8] = tr_[5];
       r[9] = tr_mma[0];
       r[10] = tr_mma[1];
-      r[11] = 0;
+      r[11] = (unsigned)nacc_arg >> 8;
     }
   }
 #endif
 }
+
+#ifdef DQN_TC_TRACE
+inline int next_launch_seq() {
+  static int seq = 0;
+  return ++seq;
+}
+#endif
 
 template <class Pol>
 inline int smem_bytes() {
@@ -672,7 +731,7 @@ int launch(cudaStream_t st, const Pol &p, int splits, const char *what) {
     configured = true;
   }
   dim3 grid((p.M + BM - 1) / BM, (p.N + Pol::BN - 1) / Pol::BN, splits);
-  if (p.ksplits > 1 && (int64_t)grid.x * grid.y * (splits / p.ksplits) > kMaxTiles) {
+  if (p.ksplits > 1 && 2 * (int64_t)grid.x * grid.y * (splits / p.ksplits) > kMaxTiles) {
     set_error("%s: %u x %u tiles exceed the split-K counter table", what, grid.x, grid.y);
     return DQN_ERR_UNSUPPORTED;
   }
@@ -683,6 +742,9 @@ int launch(cudaStream_t st, const Pol &p, int splits, const char *what) {
   // accumulator pairs [big | small] (2 * BN columns each) share TMEM with the A stages
   int nacc = env_nacc < 1 ? 1 : env_nacc;
   while (nacc > 1 && 2 * Pol::BN * nacc > Plan<Pol>::ACC_MAX) --nacc;
+#ifdef DQN_TC_TRACE
+  nacc |= (next_launch_seq() & 0xFFFFFF) << 8;
+#endif
   tc_gemm_kernel<Pol><<<grid, kThreads, bytes, st>>>(p, nacc);
   DQN_LAUNCH_CHECK(what);
   return DQN_OK;

@@ -301,11 +301,28 @@ inline int fwd_klen(int K) {
   return K;
 }
 
-// split count for a grid of `tiles` tiles: about two CTAs per SM (2 waves
-// of 148), at least 64 k per split, at most `cap` partials per fixup
-inline void split_k(int tiles, int K, int cap, int &klen, int &splits) {
-  splits = std::max(1, std::min({ceil_div(2 * kNumSMs, tiles), K / 64, cap}));
-  klen = ceil_div(ceil_div(K, splits), tc::BK) * tc::BK;
+// Split count for a grid of `tiles` output tiles of width bn, from a latency
+// model of the engine measured with the trace build (tools/tc_trace.py): one
+// CTA per SM, ~3 us per CTA for setup + first k-block + epilogue, ~0.8 us per
+// further 32-k block, and a split-K fixup of ~1.5 us plus the tile's partials
+// read by R reducer CTAs at ~70 KB/us each (R as in tc_gemm_kernel).
+inline void split_k(int tiles, int K, int bn, int cap, int &klen, int &splits) {
+  const int nkb = ceil_div(K, tc::BK);
+  double best = 1e30;
+  int bs = 1;
+  for (int s = 1; s <= std::min(cap, nkb); ++s) {
+    const int kl = ceil_div(ceil_div(K, s), tc::BK) * tc::BK;
+    if (ceil_div(K, kl) != s) continue;              // same split as a smaller s
+    const int waves = ceil_div(tiles * s, kNumSMs);
+    const int R = std::min({60 / tiles + 1, 8, s});
+    double t = waves * (3.0 + (kl / tc::BK - 1) * 0.8);
+    if (s > 1) t += 1.5 + (double)s * tc::BM * bn * 4 / (70e3 * R);
+    if (t < best - 1e-9) {
+      best = t;
+      bs = s;
+    }
+  }
+  klen = ceil_div(ceil_div(K, bs), tc::BK) * tc::BK;
   splits = ceil_div(K, klen);
 }
 
@@ -389,7 +406,7 @@ int conv_dgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const float *dy,
   p.N = L.in_c;
   p.K = (L.fh / L.sh) * (L.fw / L.sw) * L.out_c;
   // split K until phases x tiles x splits fill the machine
-  split_k(L.sh * L.sw * ceil_div(p.M, tc::BM) * ceil_div(p.N, BN), p.K, 16, p.klen, p.ksplits);
+  split_k(L.sh * L.sw * ceil_div(p.M, tc::BM) * ceil_div(p.N, BN), p.K, BN, 16, p.klen, p.ksplits);
   return tc::launch(st, p, L.sh * L.sw * p.ksplits, "tc_conv_dgrad");
 }
 
@@ -412,7 +429,7 @@ int conv_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const 
 
 inline void wgrad_split(int M, int N, int K, int bn, int &klen, int &splits) {
   // ~2 CTA waves over the machine, split lengths a multiple of BK
-  split_k(ceil_div(M, tc::BM) * ceil_div(N, bn), K, 32, klen, splits);
+  split_k(ceil_div(M, tc::BM) * ceil_div(N, bn), K, bn, 32, klen, splits);
 }
 
 template <typename InT, int BN>
@@ -481,7 +498,7 @@ int64_t tc_scratch_floats(const dqn_net_desc *net, int batch) {
     if (L.kind == DQN_LAYER_LINEAR) m = std::max(m, (int64_t)ceil_div(L.out_c, 128) * M * R);
     if (L.kind == DQN_LAYER_CONV && tc_layer_supported(net, l, 1)) {
       const int Kd = (L.fh / L.sh) * (L.fw / L.sw) * L.out_c;
-      const int ds = std::max(1, std::min(Kd / 64, 16));     // split_k upper bound
+      const int ds = std::max(1, std::min(ceil_div(Kd, tc::BK), 16));   // split_k upper bound
       const int64_t Md = (int64_t)batch * ceil_div(L.in_h, L.sh) * ceil_div(L.in_w, L.sw);
       if (ds > 1) m = std::max(m, (int64_t)L.sh * L.sw * ds * Md * L.in_c);
     }
