@@ -50,7 +50,7 @@ typedef enum {
 #define DQN_FLAG_BAD_PRIORITY   0x10 /* SumTree.set with negative / non-finite value */
 
 const char *dqn_last_error(void);
-int dqn_abi_version(void);
+int dqn_abi_version(void);             /* 2 */
 /* 1 if this library was built with the tcgen05 (sm_100a UMMA) conv trunk */
 int dqn_has_tcgen05(void);
 /* kernels launched (or captured) through this library so far, all threads */
@@ -145,9 +145,23 @@ typedef struct {
   float *dx;               /* input gradient (NULL = skip, as the learner does) */
   float *scratch;
   int64_t scratch_floats;
+  /* optional: layer 0's transposed im2col of x (uint8 input only), filled by
+   * dqn_net_im2col_t; when set, layer 0's wgrad reads its patch operand from
+   * it as contiguous rows instead of gathering bytes (NULL = gather) */
+  uint8_t *xt;
 } dqn_binding;
 
 int64_t dqn_net_scratch_floats(const dqn_net_desc *net, int32_t batch);
+
+/* Bytes of layer 0's transposed im2col for `batch` (0 when the network's
+ * input is not uint8 or layer 0 is not a tcgen05 convolution). */
+int64_t dqn_net_im2col_t_bytes(const dqn_net_desc *net, int32_t batch);
+
+/* bind->xt[r][pix] = x patch element r of output pixel pix for layer 0
+ * (r < fh*fw*C, pix < batch*OH*OW): the wgrad operand of layers.py:250-255
+ * laid out along the reduction.  Run it anywhere between the batch gather
+ * and the wgrad (the learner puts it beside the forward pass). */
+int dqn_net_im2col_t(void *stream, const dqn_net_desc *net, const dqn_binding *bind);
 
 /* Network.forward (network.py:90-104): all layers front to back. */
 int dqn_net_forward(void *stream, const dqn_net_desc *net, const float *params,

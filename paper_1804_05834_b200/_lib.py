@@ -49,7 +49,7 @@ class NetDesc(C.Structure):
 class Binding(C.Structure):
     _fields_ = [("batch", i32), ("pad_", i32), ("x", vp), ("act", vp * MAX_LAYERS),
                 ("dact", vp * MAX_LAYERS), ("dx", vp), ("scratch", vp),
-                ("scratch_floats", i64)]
+                ("scratch_floats", i64), ("xt", vp)]
 
 
 _SIGS = {
@@ -66,6 +66,8 @@ _SIGS = {
     "dqn_tree_set": ([vp, vp, i32, i64, vp, vp, i32, vp], C.c_int),
     "dqn_tree_rebuild": ([vp, vp, i32], C.c_int),
     "dqn_net_scratch_floats": ([C.POINTER(NetDesc), i32], i64),
+    "dqn_net_im2col_t_bytes": ([C.POINTER(NetDesc), i32], i64),
+    "dqn_net_im2col_t": ([vp, C.POINTER(NetDesc), C.POINTER(Binding)], C.c_int),
     "dqn_net_forward": ([vp, C.POINTER(NetDesc), vp, C.POINTER(Binding), vp], C.c_int),
     "dqn_net_backward": ([vp, C.POINTER(NetDesc), vp, C.POINTER(Binding), vp], C.c_int),
     "dqn_net_wgrad": ([vp, C.POINTER(NetDesc), vp, C.POINTER(Binding)], C.c_int),

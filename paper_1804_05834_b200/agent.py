@@ -20,6 +20,7 @@ Device pipeline of one update:
 
 from __future__ import annotations
 
+import ctypes as C
 import os
 from dataclasses import dataclass
 
@@ -130,6 +131,13 @@ class _StepPlan:
         # gets a view with its own scratch (split-K partials and counters)
         self.on_wview = online.prefix_binding(self.on_bind, k, own_scratch=True)
         self.tg_bind = target.binding(k)
+        # conv1's wgrad reads its uint8 patch operand from a transposed im2col
+        # built beside the forward pass (dqn_net_im2col_t), not byte gathers
+        self.on_desc = online.desc_for(self.x)
+        nb = int(_lib.lib.dqn_net_im2col_t_bytes(C.byref(self.on_desc), k))
+        self.xt = torch.empty(nb, dtype=torch.uint8, device=dev) if nb > 0 else None
+        if self.xt is not None:
+            self.on_view.struct.xt = self.xt.data_ptr()
         self.side = torch.cuda.Stream()
         self.graph = None
         self.calls = 0
@@ -178,6 +186,13 @@ class _StepPlan:
         e_in.record(s0)
         with torch.cuda.stream(s1):
             s1.wait_event(e_in)
+            e_xt = None
+            if self.xt is not None:              # read by the last wgrad only
+                self.on_view.struct.x = self.x.data_ptr()
+                _lib.call("dqn_net_im2col_t", _lib.stream_ptr(), C.byref(self.on_desc),
+                          C.byref(self.on_view.struct))
+                e_xt = ev()
+                e_xt.record(s1)
             tg.forward_into(self.x[k:], self.tg_bind)
             e_tg = ev()
             e_tg.record(s1)
@@ -205,6 +220,8 @@ class _StepPlan:
             if layer == 0:
                 # conv1 has no dgrad: its wgrad takes the main stream (and the
                 # dgrad binding's scratch) instead of queueing behind conv2's
+                if e_xt is not None:
+                    s0.wait_event(e_xt)
                 on.layer_into(self.on_view, 0, 2)
                 break
             with torch.cuda.stream(s1):           # wgrad of `layer` once its grad exists

@@ -26,9 +26,11 @@
 //     vs fp32 SIMT per GEMM; a single bf16/tf32 pass misses
 //     the 1e-3 one-step parity bar).
 // Warp roles: kGroups producer groups of 8 warps gather alternating k-blocks
-// into a STAGES-deep ring (A columns in TMEM, B tiles in shared memory) and
-// arrive on full[s]; one warp waits full[s], issues the MMAs and commits to
-// empty[s].  No block-wide barrier inside the K loop.
+// (two k-blocks of loads in flight per thread) into a STAGES-deep ring (A
+// columns in TMEM, B tiles in shared memory) and arrive on full[s]; the
+// group's first thread waits full[s], issues the MMAs into the group's own
+// accumulator pair and commits to empty[s].  No block-wide barrier inside the
+// K loop.
 // The epilogue reads TMEM with tcgen05.ld, stages the tile row-major in shared
 // memory and hands coalesced float4s to the Policy (bias / ReLU / mask /
 // split-K partial / gradient accumulate).  Exact operands (uint8 pixels) use
@@ -47,7 +49,11 @@ constexpr int BK = 32;                  // k per pipeline stage (4 MMA k-steps o
 constexpr int kGroupThreads = 256;      // 8 warps: lane quarter w % 4, k-half w / 4
 constexpr int kGroups = 2;
 constexpr int kProducers = kGroups * kGroupThreads;
-constexpr int kThreads = kProducers + 32;
+// no separate MMA warp: thread 0 of group g issues the MMAs of its own
+// k-blocks into accumulator pair g (16 warps = 4 per SMSP keep the 128
+// register/thread budget; a 17th warp would cut it to 96)
+constexpr int kThreads = kProducers;
+constexpr int kNacc = kGroups;          // accumulator pairs, one per group
 constexpr int kTmemCols = 512;          // accumulators + A stages (one CTA per SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -218,8 +224,8 @@ struct Gather {
   int t0;                      // this thread's first unit (rotated, see init)
   uint32_t soff[U];            // byte offset of the unit's (first) chunk in the tile
   int kk;                      // the thread's k offset inside a k-block (same for all units)
-  float4 v[U][V];
   float bsum[U][V];
+  using Regs = float4[U][V];   // one k-block's values (the caller double-buffers them)
 
   __device__ static void coords(int u, int &row, int &k) {
     if (!MNC) {
@@ -246,7 +252,7 @@ struct Gather {
     }
   }
   template <class KF, class LD, class F4>
-  __device__ void fetch(int k0, int kend, KF &&koff, LD &&ld, F4 &&f4) {
+  __device__ void fetch(Regs &v, int k0, int kend, KF &&koff, LD &&ld, F4 &&f4) {
     const int k = k0 + kk;
     if constexpr (!MNC) {
       const bool in = k < kend;
@@ -266,7 +272,8 @@ struct Gather {
       }
     }
   }
-  __device__ void store(uint32_t tile, uint32_t piece_stride, int pieces, bool bias) {
+  __device__ void store(const Regs &v, uint32_t tile, uint32_t piece_stride, int pieces,
+                        bool bias) {
 #pragma unroll
     for (int i = 0; i < U; ++i) {
       if (t0 + i * kGroupThreads >= UNITS) continue;
@@ -327,12 +334,13 @@ struct Plan {
   static constexpr int B_BYTES = RB * BK * 4;
   static constexpr int A_COLS = NA * BK;               // TMEM columns per A stage
   static constexpr int STAGES_SMEM = (200 * 1024) / B_BYTES;
-  static constexpr int STAGES_TMEM = (kTmemCols - 2 * BN) / A_COLS;   // nacc >= 1
+  static constexpr int STAGES_TMEM = (kTmemCols - 2 * kNacc * BN) / A_COLS;
   static constexpr int S0 = STAGES_SMEM < STAGES_TMEM ? STAGES_SMEM : STAGES_TMEM;
   static constexpr int STAGES = S0 > 4 ? 4 : S0;
   static_assert(STAGES >= kGroups, "one ring slot per producer group at least");
   static_assert(RB <= 256 && RB % 16 == 0 && BN % 16 == 0, "MMA N limits");
   static constexpr int ACC_MAX = kTmemCols - STAGES * A_COLS;   // columns for accumulators
+  static_assert(2 * kNacc * BN <= ACC_MAX, "accumulator pairs do not fit in TMEM");
   static constexpr int EPI_STRIDE = BN + 4;                      // floats per staged row
   static constexpr int EPI_BYTES = BM * EPI_STRIDE * 4;
   static constexpr int PIPE = STAGES * B_BYTES;
@@ -358,7 +366,7 @@ struct Plan {
 // per-CTA record: {ctaid, smid, t_entry, t_setup, t_kloop, t_epilogue, t_exit, nk,
 //                  t_first_store (producer 0), t_first_full (MMA warp), t_last_mma, launch id}
 constexpr int kTraceCtas = 8192;
-__device__ unsigned long long g_trace[kTraceCtas * 12];
+__device__ unsigned long long g_trace[kTraceCtas * 28];
 __device__ unsigned int g_trace_n;
 __device__ int g_skip;        // diagnostic: 1 = no MMAs, 2 = no global loads, 4 = no operand stores
 #define TC_SKIP(bit) (g_skip & (bit))
@@ -375,21 +383,25 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 template <class Pol>
-__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const int nacc_arg) {
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const int launch_id) {
   using PL = Plan<Pol>;
-  const int nacc = nacc_arg & 0xFF;     // trace builds carry a launch id in the upper bits
+  constexpr int nacc = kNacc;
   constexpr int BN = Pol::BN, STAGES = PL::STAGES, NA = PL::NA, NB = PL::NB, RB = PL::RB;
   constexpr int B_BYTES = PL::B_BYTES;
   constexpr uint32_t IDESC_FULL = make_idesc_tf32(RB), IDESC_HALF = make_idesc_tf32(BN);
   extern __shared__ __align__(1024) uint8_t smem[];
   // full[s]: the producer group that filled slot s is done (256 arrivals);
-  // empty[s]: the MMAs reading slot s completed (tcgen05.commit); done: all MMAs
+  // empty[s]: the MMAs reading slot s completed (tcgen05.commit); done: all
+  // MMAs of every group
   __shared__ uint64_t full[STAGES], empty[STAGES], done;
   __shared__ uint32_t tmem_slot;
   __shared__ float bias_red[Pol::BIAS_FROM_B ? kGroups : 1][Pol::BIAS_FROM_B ? BN : 1][8];
 
 #ifdef DQN_TC_TRACE
   unsigned long long tr_[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long tk_[16];             // group 0, k-blocks 0, 2, 4, 6: enter, empty ok, arrived, mma issued
+#pragma unroll
+  for (int j = 0; j < 16; ++j) tk_[j] = 0;
   __shared__ unsigned long long tr_mma[2];
 #endif
   TC_MARK(0)
@@ -407,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
       mbar_init(&full[s], kGroupThreads);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(&done, 1);
+    mbar_init(&done, kGroups);
     fence_barrier_init();
   }
 
@@ -420,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   float *const part = p.partial + (SPLITK ? (int64_t)zp * ks * p.M * p.N : 0);
   const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
   const uint32_t sbase = smem_u32(smem);
-  const bool producer = threadIdx.x < kProducers;
+  constexpr bool producer = true;        // every warp gathers
   const int group = threadIdx.x / kGroupThreads;
   // A ownership: TMEM lane quarter = warp % 4 (the warp's accessible lanes),
   // k-half = (warp / 4) % 2 of each 32-k block
@@ -445,24 +457,35 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
 
   if (producer) {
     // group g gathers k-blocks g, g + kGroups, ... into ring slot kb % STAGES;
-    // a slot is refilled once the MMAs of k-block kb - STAGES completed
-    float av[16];
-    auto fetch = [&](int k0) {
+    // a slot is refilled once the MMAs of k-block kb - STAGES completed.
+    // Two register buffers per thread: a group has two k-blocks of loads in
+    // flight (a global round trip is ~1 us, a k-block's MMAs ~0.1 us).
+    using GB = Gather<Pol::B_MNC, BN, RB>;
+    float av0[16], av1[16];
+    typename GB::Regs bv0, bv1;
+    auto fetch = [&](float (&av)[16], typename GB::Regs &bv, int kb) {
       if (TC_SKIP(2)) return;
+      const int k0 = kbeg + kb * BK;
       if (abase >= 0) {
         p.a16(abase, k0 + 16 * khalf, kend, av);
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) av[j] = 0.f;
       }
-      gb.fetch(k0, kend, [&](int k) { return p.b_koff(k); },
+      gb.fetch(bv, k0, kend, [&](int k) { return p.b_koff(k); },
                [&](long long b, int ko) { return p.b_ld(b, ko); },
                [&](long long b, int k, int ke, float4 (&v)[4]) { p.b4(b, k, ke, v); });
     };
-    if (group < nk) fetch(kbeg + group * BK);
-    for (int kb = group; kb < nk; kb += kGroups) {
+    auto put = [&](const float (&av)[16], const typename GB::Regs &bv, int kb) {
       const int s = kb % STAGES, use = kb / STAGES;
+#ifdef DQN_TC_TRACE
+      const bool tk = threadIdx.x == 0 && kb < 8;
+      if (tk) tk_[(kb >> 1) * 4 + 0] = gtimer();
+#endif
       if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);    // MMAs of kb - STAGES done
+#ifdef DQN_TC_TRACE
+      if (tk) tk_[(kb >> 1) * 4 + 1] = gtimer();
+#endif
       tc_fence_after();
 #ifdef DQN_TC_TRACE
       if (kb == 0 && threadIdx.x == 0) tr_[5] = gtimer();
@@ -478,45 +501,61 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
           for (int j = 0; j < 16; ++j) lo[j] = tf32_lo(av[j]);
           tmem_st16(ta + BK, lo);
         }
-        gb.store(sbase + s * B_BYTES, BN * 16, NB, want_bias);
+        gb.store(bv, sbase + s * B_BYTES, BN * 16, NB, want_bias);
         tmem_wait_st();
       }
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(&full[s]);
-      // register-staged prefetch of this group's next k-block
-      if (kb + kGroups < nk) fetch(kbeg + (kb + kGroups) * BK);
-    }
-  } else if (lane == 0) {
-    // MMA issuer: k-blocks in order, each slot released by tcgen05.commit
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      mbar_wait(&full[s], (kb / STAGES) & 1);
 #ifdef DQN_TC_TRACE
-      if (kb == 0) tr_mma[0] = gtimer();
+      if (tk) tk_[(kb >> 1) * 4 + 2] = gtimer();
 #endif
-      tc_fence_after();
-      if (!TC_SKIP(1)) {
-        const uint32_t dbig = tmem + (uint32_t)((kb % nacc) * 2 * BN);
-        const uint32_t dsmall = dbig + (uint32_t)BN;
-        const uint32_t ta = tmem + acol0 + (uint32_t)(s * PL::A_COLS);
-        const uint32_t tb = sbase + s * B_BYTES;
+      // the group's first thread issues its k-block's MMAs into pair `group`
+      // (one issuing thread per accumulator chain: fixed order)
+      if (threadIdx.x % kGroupThreads == 0) {
+        mbar_wait(&full[s], use & 1);
+#ifdef DQN_TC_TRACE
+        if (kb == 0) tr_mma[0] = gtimer();
+#endif
+        tc_fence_after();
+        if (!TC_SKIP(1)) {
+          const uint32_t dbig = tmem + (uint32_t)(group * 2 * BN);
+          const uint32_t dsmall = dbig + (uint32_t)BN;
+          const uint32_t ta = tmem + acol0 + (uint32_t)(s * PL::A_COLS);
+          const uint32_t tb = sbase + s * B_BYTES;
 #pragma unroll
-        for (int kq = 0; kq < BK / 8; ++kq) {
-          const uint64_t db = op_desc(tb, RB, kq);
-          const uint32_t first = (kb < nacc && kq == 0) ? 0u : 1u;
-          // hi * [B_hi ; B_lo] -> [big | small]; the first touch of a pair overwrites
-          mma_ts(dbig, ta + 8 * kq, db, NB > 1 ? IDESC_FULL : IDESC_HALF, first);
-          // lo * B_hi -> small (initialised by the first MMA when B is split)
-          if (NA > 1) mma_ts(dsmall, ta + BK + 8 * kq, db, IDESC_HALF, NB > 1 ? 1u : first);
+          for (int kq = 0; kq < BK / 8; ++kq) {
+            const uint64_t db = op_desc(tb, RB, kq);
+            const uint32_t first = (kb < kGroups && kq == 0) ? 0u : 1u;
+            // hi * [B_hi ; B_lo] -> [big | small]; the first touch of a pair overwrites
+            mma_ts(dbig, ta + 8 * kq, db, NB > 1 ? IDESC_FULL : IDESC_HALF, first);
+            // lo * B_hi -> small (initialised by the first MMA when B is split)
+            if (NA > 1) mma_ts(dsmall, ta + BK + 8 * kq, db, IDESC_HALF, NB > 1 ? 1u : first);
+          }
         }
-      }
-      mma_commit(&empty[s]);
-    }
+        mma_commit(&empty[s]);
 #ifdef DQN_TC_TRACE
-    tr_mma[1] = gtimer();
+        if (tk) tk_[(kb >> 1) * 4 + 3] = gtimer();
 #endif
-    mma_commit(&done);
+      }
+    };
+    constexpr int G = kGroups;
+    if (group < nk) fetch(av0, bv0, group);
+    if (group + G < nk) fetch(av1, bv1, group + G);
+    for (int kb = group; kb < nk; kb += 2 * G) {
+      put(av0, bv0, kb);
+      if (kb + 2 * G < nk) fetch(av0, bv0, kb + 2 * G);
+      if (kb + G < nk) {
+        put(av1, bv1, kb + G);
+        if (kb + 3 * G < nk) fetch(av1, bv1, kb + 3 * G);
+      }
+    }
+    if (threadIdx.x % kGroupThreads == 0) {
+#ifdef DQN_TC_TRACE
+      if (group == 0) tr_mma[1] = gtimer();
+#endif
+      mma_commit(&done);       // arrives once this group's MMAs completed
+    }
   }
   mbar_wait(&done, 0);
   TC_MARK(2)
@@ -529,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   // split the 16-column chunks between them
   constexpr int CGROUPS = kProducers / 128;
   const int cgrp = warp >> 2;
-  const int nused = nk < nacc ? nk : nacc;
+  const int nused = nk < nacc ? nk : nacc;   // pair g holds k-blocks g, g + kGroups, ...
   constexpr bool TWO = NA > 1 || NB > 1;
   if (producer) {
 #pragma unroll 1
@@ -694,7 +733,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
     if (i < kTraceCtas) {
       unsigned int smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      unsigned long long *r = g_trace + 12ull * i;
+      unsigned long long *r = g_trace + 28ull * i;
+      for (int j = 0; j < 16; ++j) r[12 + j] = tk_[j];
       r[0] = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
       r[1] = smid;
       for (int j = 0; j < 5; ++j) r[2 + j] = tr_[j];
@@ -702,7 +742,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
       r[8] = tr_[5];
       r[9] = tr_mma[0];
       r[10] = tr_mma[1];
-      r[11] = (unsigned)nacc_arg >> 8;
+      r[11] = (unsigned)launch_id;
     }
   }
 #endif
@@ -735,17 +775,11 @@ int launch(cudaStream_t st, const Pol &p, int splits, const char *what) {
     set_error("%s: %u x %u tiles exceed the split-K counter table", what, grid.x, grid.y);
     return DQN_ERR_UNSUPPORTED;
   }
-  static const int env_nacc = [] {
-    const char *e = getenv("DQN_TC_NACC");
-    return e ? atoi(e) : 2;
-  }();
-  // accumulator pairs [big | small] (2 * BN columns each) share TMEM with the A stages
-  int nacc = env_nacc < 1 ? 1 : env_nacc;
-  while (nacc > 1 && 2 * Pol::BN * nacc > Plan<Pol>::ACC_MAX) --nacc;
+  int launch_id = 0;
 #ifdef DQN_TC_TRACE
-  nacc |= (next_launch_seq() & 0xFFFFFF) << 8;
+  launch_id = next_launch_seq();
 #endif
-  tc_gemm_kernel<Pol><<<grid, kThreads, bytes, st>>>(p, nacc);
+  tc_gemm_kernel<Pol><<<grid, kThreads, bytes, st>>>(p, launch_id);
   DQN_LAUNCH_CHECK(what);
   return DQN_OK;
 }

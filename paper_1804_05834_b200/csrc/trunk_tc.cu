@@ -240,6 +240,7 @@ struct WgradPol : tc::PolBase {
   static constexpr bool B_MNC = true;
   static constexpr int BN = BN_;
   const InT *x;
+  const uint8_t *xt;              // optional transposed im2col [M][K] (uint8 input)
   const float *dy;
   float *grad, *partial;
   float *bias_out, *bias_partial;
@@ -248,10 +249,22 @@ struct WgradPol : tc::PolBase {
   int M, N, K, klen, ksplits;     // M = R (patch length), N = Cout, K = pixels
   __device__ int kbeg(int z) const { return z * klen; }
   __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
-  __device__ long long a_row(int r, int) const { return r < M ? patch_off(g, r) : -1; }
-  // patch element r at pixels pix..pix+15: the window bases walk along the
-  // output rows (a warp's 32 lanes = 32 consecutive patch elements: coalesced)
+  __device__ long long a_row(int r, int) const {
+    if (r >= M) return -1;
+    return xt ? (long long)r * K : patch_off(g, r);
+  }
+  // patch element r at pixels pix..pix+15: one 16-byte row segment of xt, or
+  // a walk of the window bases along the output rows (a warp's 32 lanes = 32
+  // consecutive patch elements: coalesced)
   __device__ void a16(long long roff, int pix, int ke, float (&v)[16]) const {
+    if (xt) {
+      if (pix >= ke) return zero16(v);        // K % 16 == 0: whole runs
+      const uint4 q = __ldg(reinterpret_cast<const uint4 *>(xt + roff + pix));
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = (float)((w[j >> 2] >> (8 * (j & 3))) & 0xFF);
+      return;
+    }
     const int P = g.OH * g.OW;
     int img = pix / P, p = pix - img * P;
     int oy = p / g.OW, ox = p - oy * g.OW;
@@ -376,11 +389,11 @@ int lin_dgrad_launch(cudaStream_t st, const float *dy, const float *w, const flo
 
 int lin_dgrad(cudaStream_t st, const float *dy, const float *w, const float *mask, float *out,
               float *partial, int *counters, int M, int N, int K) {
-  for (int bn : {128, 112, 96, 64, 32, 16}) {
+  // tiles of at most 96 columns: two [big | small] accumulator pairs + the A
+  // stages fit in TMEM
+  for (int bn : {64, 96, 32, 16}) {
     if (N % bn) continue;
     switch (bn) {
-      case 128: return lin_dgrad_launch<128>(st, dy, w, mask, out, partial, counters, M, N, K);
-      case 112: return lin_dgrad_launch<112>(st, dy, w, mask, out, partial, counters, M, N, K);
       case 96: return lin_dgrad_launch<96>(st, dy, w, mask, out, partial, counters, M, N, K);
       case 64: return lin_dgrad_launch<64>(st, dy, w, mask, out, partial, counters, M, N, K);
       case 32: return lin_dgrad_launch<32>(st, dy, w, mask, out, partial, counters, M, N, K);
@@ -410,7 +423,7 @@ int conv_dgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const float *dy,
   return tc::launch(st, p, L.sh * L.sw * p.ksplits, "tc_conv_dgrad");
 }
 
-bool dgrad_tile_ok(int C) { return C == 16 || C == 32 || C == 48 || C == 64 || C == 96 || C % 128 == 0; }
+bool dgrad_tile_ok(int C) { return C == 16 || C == 32 || C == 48 || C == 64 || C == 96 || C % 64 == 0; }
 
 int conv_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
                const float *mask, float *out, float *scratch, int *counters, int batch) {
@@ -422,19 +435,19 @@ int conv_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const 
     case 96: return conv_dgrad_launch<96>(st, L, dy, w, mask, out, scratch, counters, batch);
     default: break;
   }
-  if (L.in_c % 128 == 0) return conv_dgrad_launch<128>(st, L, dy, w, mask, out, scratch, counters, batch);
+  if (L.in_c % 64 == 0) return conv_dgrad_launch<64>(st, L, dy, w, mask, out, scratch, counters, batch);
   set_error("tc_conv_dgrad: %d input channels not tiled", L.in_c);
   return DQN_ERR_UNSUPPORTED;
 }
 
 inline void wgrad_split(int M, int N, int K, int bn, int &klen, int &splits) {
   // ~2 CTA waves over the machine, split lengths a multiple of BK
-  split_k(ceil_div(M, tc::BM) * ceil_div(N, bn), K, bn, 32, klen, splits);
+  split_k(ceil_div(M, tc::BM) * ceil_div(N, bn), K, bn, 128, klen, splits);
 }
 
 template <typename InT, int BN>
-int wgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *dy,
-                 float *grads, float *scratch, int *counters, int batch) {
+int wgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const uint8_t *xt,
+                 const float *dy, float *grads, float *scratch, int *counters, int batch) {
   WgradPol<InT, BN> p{};
   p.counters = counters;
   p.x = x;
@@ -445,6 +458,7 @@ int wgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const f
   p.M = L.fh * L.fw * L.in_c;
   p.N = L.out_c;
   p.K = batch * L.out_h * L.out_w;
+  p.xt = (xt && p.K % 16 == 0) ? xt : nullptr;      // whole 16-pixel runs only
   int splits;
   wgrad_split(p.M, p.N, p.K, BN, p.klen, splits);
   p.partial = scratch;
@@ -454,18 +468,17 @@ int wgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const f
 }
 
 template <typename InT>
-int wgrad_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *dy,
-                   float *grads, float *scratch, int *counters, int batch) {
+int wgrad_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const uint8_t *xt,
+                   const float *dy, float *grads, float *scratch, int *counters, int batch) {
   const int N = L.out_c;
-  if (N == 32) return wgrad_launch<InT, 32>(st, L, x, dy, grads, scratch, counters, batch);
-  if (N == 64) return wgrad_launch<InT, 64>(st, L, x, dy, grads, scratch, counters, batch);
-  if (N % 128 == 0) return wgrad_launch<InT, 128>(st, L, x, dy, grads, scratch, counters, batch);
+  if (N == 32) return wgrad_launch<InT, 32>(st, L, x, xt, dy, grads, scratch, counters, batch);
+  if (N % 64 == 0) return wgrad_launch<InT, 64>(st, L, x, xt, dy, grads, scratch, counters, batch);
   return DQN_ERR_UNSUPPORTED;
 }
 
 int64_t wgrad_scratch_tc(const dqn_layer_desc &L, int batch) {
   const int M = L.fh * L.fw * L.in_c, N = L.out_c, K = batch * L.out_h * L.out_w;
-  const int bn = N == 32 ? 32 : N == 64 ? 64 : 128;
+  const int bn = N == 32 ? 32 : 64;
   int klen, splits;
   wgrad_split(M, N, K, bn, klen, splits);
   return (int64_t)splits * M * N + (int64_t)splits * N;
@@ -542,11 +555,49 @@ int tc_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads
   const dqn_layer_desc &L = net->layer[l];
   const void *in = (l == 0) ? b->x : b->act[l - 1];
   if (l == 0 && net->input_u8)
-    return wgrad_dispatch<uint8_t>(st, L, (const uint8_t *)in, b->dact[l], grads, b->scratch,
-                                    counters_of(b), b->batch);
-  return wgrad_dispatch<float>(st, L, (const float *)in, b->dact[l], grads, b->scratch,
+    return wgrad_dispatch<uint8_t>(st, L, (const uint8_t *)in, b->xt, b->dact[l], grads,
+                                    b->scratch, counters_of(b), b->batch);
+  return wgrad_dispatch<float>(st, L, (const float *)in, nullptr, b->dact[l], grads, b->scratch,
                                 counters_of(b), b->batch);
 }
+
+
+namespace {
+// xt[r][pix] for 16 consecutive pixels per thread (one 16-byte store); the
+// warp's 32 lanes take 32 consecutive patch elements of one pixel group, so
+// each byte load of the warp reads one contiguous segment of a window row
+__global__ void im2col_t_u8_kernel(const uint8_t *__restrict__ x, Geo g, int R, int K,
+                                   uint8_t *__restrict__ xt) {
+  const int nq = K / 16;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)R * nq) return;
+  const int q = (int)(idx / R), r = (int)(idx - (int64_t)q * R);
+  const int roff = patch_off(g, r);
+  const int P = g.OH * g.OW;
+  int pix = q * 16;
+  int img = pix / P, p = pix - img * P;
+  int oy = p / g.OW, ox = p - oy * g.OW;
+  uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const long long base =
+        (((long long)img * g.H + (long long)oy * g.sh) * g.W + (long long)ox * g.sw) * g.C;
+    w[j >> 2] |= (uint32_t)__ldg(x + base + roff) << (8 * (j & 3));
+    if (++ox == g.OW) {
+      ox = 0;
+      if (++oy == g.OH) { oy = 0; ++img; }
+    }
+  }
+  *reinterpret_cast<uint4 *>(xt + (int64_t)r * K + q * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+bool im2col_t_ok(const dqn_net_desc *net, int batch) {
+  if (!net->input_u8 || net->n_layers < 1 || net->algo == 1) return false;
+  const dqn_layer_desc &L = net->layer[0];
+  if (L.kind != DQN_LAYER_CONV || !tc_layer_supported(net, 0, 2)) return false;
+  return ((int64_t)batch * L.out_h * L.out_w) % 16 == 0;
+}
+}  // namespace
 
 }  // namespace dqn
 
@@ -557,10 +608,36 @@ extern "C" int dqn_tc_trace(unsigned long long *host, int max_ctas) {
   cudaMemcpyFromSymbol(&n, dqn::tc::g_trace_n, sizeof(n));
   if (n > (unsigned)dqn::tc::kTraceCtas) n = dqn::tc::kTraceCtas;
   if ((int)n > max_ctas) n = max_ctas;
-  if (n) cudaMemcpyFromSymbol(host, dqn::tc::g_trace, 12ull * n * sizeof(unsigned long long));
+  if (n) cudaMemcpyFromSymbol(host, dqn::tc::g_trace, 28ull * n * sizeof(unsigned long long));
   const unsigned int zero = 0;
   cudaMemcpyToSymbol(dqn::tc::g_trace_n, &zero, sizeof(zero));
   return (int)n;
 }
 extern "C" void dqn_tc_skip(int mask) { cudaMemcpyToSymbol(dqn::tc::g_skip, &mask, sizeof(mask)); }
 #endif
+
+extern "C" int64_t dqn_net_im2col_t_bytes(const dqn_net_desc *net, int32_t batch) {
+  if (!net || batch < 1 || !dqn::im2col_t_ok(net, batch)) return 0;
+  const dqn_layer_desc &L = net->layer[0];
+  return (int64_t)L.fh * L.fw * L.in_c * batch * L.out_h * L.out_w;
+}
+
+extern "C" int dqn_net_im2col_t(void *stream, const dqn_net_desc *net, const dqn_binding *bind) {
+  using namespace dqn;
+  if (!net || !bind || !bind->x || !bind->xt || bind->batch < 1) {
+    set_error("net_im2col_t: network / binding / x / xt missing");
+    return DQN_ERR_INVALID_ARG;
+  }
+  if (!im2col_t_ok(net, bind->batch)) {
+    set_error("net_im2col_t: layer 0 has no transposed-im2col wgrad (uint8 tcgen05 conv, 16 | pixels)");
+    return DQN_ERR_UNSUPPORTED;
+  }
+  const dqn_layer_desc &L = net->layer[0];
+  const int R = L.fh * L.fw * L.in_c, K = bind->batch * L.out_h * L.out_w;
+  const int64_t n = (int64_t)R * (K / 16);
+  im2col_t_u8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+      (const uint8_t *)bind->x, geo_of(L), R, K, bind->xt);
+  DQN_LAUNCH_CHECK("net_im2col_t");
+  return DQN_OK;
+}
+

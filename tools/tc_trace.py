@@ -24,9 +24,9 @@ from paper_1804_05834_b200 import _lib, synth  # noqa: E402
 
 
 def read_trace():
-    buf = (C.c_ulonglong * (8192 * 12))()
+    buf = (C.c_ulonglong * (8192 * 28))()
     n = _lib.lib.dqn_tc_trace(buf, 8192)
-    return np.frombuffer(buf, dtype=np.uint64, count=12 * n).reshape(n, 12).astype(np.int64)
+    return np.frombuffer(buf, dtype=np.uint64, count=28 * n).reshape(n, 28).astype(np.int64)
 
 
 def main(skip=0):
@@ -82,6 +82,16 @@ def main(skip=0):
                 rel = lambda c: (t[:, c] - t[:, 3]) / 1e3          # noqa: E731  (from setup end)
                 print(f"{'':18s} from setup end: first store {rel(8).mean():5.2f}  first full {rel(9).mean():5.2f}"
                       f"  last mma issued {rel(10).mean():5.2f}  done {rel(4).mean():5.2f}")
+                # group 0 thread 0, k-blocks 0/2/4/6: enter put, empty ok, arrived, MMAs issued
+                tk = t[:, 12:28].reshape(-1, 4, 4)
+                parts = []
+                for j in range(4):
+                    ok = tk[:, j, 0] > 0
+                    if not ok.any():
+                        break
+                    e = (tk[ok, j, :] - t[ok, 3][:, None]) / 1e3
+                    parts.append(f"kb{2 * j}: " + "/".join(f"{e[:, c].mean():.2f}" for c in range(4)))
+                print(f"{'':18s} " + "  ".join(parts))
     net.flat_grads.zero_()
 
 
