@@ -7,6 +7,9 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdarg.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #include "../../include/dqn_b200.h"
 
@@ -33,6 +36,50 @@ __device__ __forceinline__ void raise_flag(int32_t *flags, int32_t bit) {
 }
 
 constexpr int kNumSMs = 148;
+
+// Programmatic dependent launch: every kernel of the library is launched with
+// programmatic stream serialization (launch_k), so it may be scheduled while
+// the previous kernel of its stream drains.  Each kernel therefore
+//   * calls pdl_trigger() first -- its own dependent may be scheduled once all
+//     of this grid's CTAs are resident (a waiting dependent never holds SMs
+//     this grid still needs);
+//   * calls pdl_wait() before its first global access that depends on (or
+//     overwrites data of) earlier kernels: it returns once every prerequisite
+//     grid has completed and its memory is visible.
+// Prologue work before pdl_wait (TMEM allocation, barrier setup, index math
+// on kernel parameters) overlaps the previous kernel's tail.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_begin() {
+  pdl_trigger();
+  pdl_wait();
+}
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("DQN_B200_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Layer geometry in NHWC terms (linear layers: H = W = OH = OW = 1).
 struct Geo {

@@ -58,6 +58,7 @@ conv_fwd_kernel(const InT *__restrict__ x, const float *__restrict__ w,
                 const float *__restrict__ bias, float *__restrict__ y,
                 float *__restrict__ partial, Geo g, int M, int K, int klen, int relu,
                 const float *__restrict__ mask) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   constexpr int THREADS = BM * BN / 16;
   __shared__ __align__(16) float As[BK][BM + APAD];
   __shared__ __align__(16) float Bs[BK][BN + APAD];
@@ -137,6 +138,7 @@ conv_fwd_kernel(const InT *__restrict__ x, const float *__restrict__ w,
 __global__ void splitk_bias_kernel(const float *__restrict__ partial, int splits, int64_t MN,
                                    int N, const float *__restrict__ bias, float *__restrict__ y,
                                    int relu, const float *__restrict__ mask) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < MN;
        e += (int64_t)gridDim.x * blockDim.x) {
     float s = partial[e];
@@ -155,6 +157,7 @@ __global__ void splitk_bias_kernel(const float *__restrict__ partial, int splits
 // atomics.  Optional ReLU mask of the layer below.
 __global__ void col2im_kernel(const float *__restrict__ dpatch, Geo g, int64_t total,
                               const float *__restrict__ mask, float *__restrict__ dx) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   const int R = g.fh * g.fw * g.C;
   // element index fits 32 bits for any learner batch (checked by the caller)
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (int)total;
@@ -188,6 +191,7 @@ template <typename InT, int BN>
 __global__ void __launch_bounds__(BM *BN / 16)
 wgrad_kernel(const InT *__restrict__ x, const float *__restrict__ dy, float *__restrict__ partial,
              float *__restrict__ bpartial, Geo g, int M, int R, int mlen) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   constexpr int THREADS = BM * BN / 16;
   __shared__ __align__(16) float As[BK][BM + APAD];
   __shared__ __align__(16) float Bs[BK][BN + APAD];
@@ -268,6 +272,7 @@ wgrad_kernel(const InT *__restrict__ x, const float *__restrict__ dy, float *__r
 __global__ void wgrad_reduce_kernel(const float *__restrict__ partial,
                                     const float *__restrict__ bpartial, int splits, int64_t RN,
                                     int N, float *__restrict__ gw, float *__restrict__ gb) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   const int64_t total = RN + N;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -295,6 +300,7 @@ head_fwd_kernel(const float *__restrict__ x, int F, const float *__restrict__ wv
                 const float *__restrict__ bv, const float *__restrict__ wa,
                 const float *__restrict__ ba, int nA, int dueling, float *__restrict__ q,
                 int32_t *flags) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   __shared__ float red[kMaxHeadOut][kHeadThreads];
   const int row = blockIdx.x, t = threadIdx.x;
   const float *xr = x + (int64_t)row * F;
@@ -351,6 +357,7 @@ head_fwd_kernel(const float *__restrict__ x, int F, const float *__restrict__ wv
 __global__ void head_bwd_kernel(const float *__restrict__ dq, int B, int nA, int dueling,
                                 const float *__restrict__ wv, const float *__restrict__ wa, int F,
                                 const float *__restrict__ mask_act, float *__restrict__ dx) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   const int64_t total = (int64_t)B * F;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -383,6 +390,7 @@ __global__ void __launch_bounds__(128)
 head_wgrad_kernel(const float *__restrict__ x, const float *__restrict__ dq, int B, int F, int nA,
                   int dueling, float *__restrict__ gwv, float *__restrict__ gbv,
                   float *__restrict__ gwa, float *__restrict__ gba) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   __shared__ float xs[kHeadRows][128];
   __shared__ float gs[kHeadRows][kMaxHeadOut];
   const int nout = dueling ? nA + 1 : nA;
@@ -500,15 +508,15 @@ int launch_gemm(cudaStream_t st, const InT *x, const Geo &g, const float *w, con
   const int splits = (K + klen - 1) / klen;
   dim3 grid((M + BM - 1) / BM, (g.N + bn - 1) / bn, splits);
   if (bn == 32)
-    conv_fwd_kernel<InT, 32, TB><<<grid, BM * 32 / 16, 0, st>>>(x, w, bias, y, scratch, g, M, K,
+    launch_k(conv_fwd_kernel<InT, 32, TB>, grid, BM * 32 / 16, 0, st, x, w, bias, y, scratch, g, M, K,
                                                                 klen, relu, mask);
   else
-    conv_fwd_kernel<InT, 64, TB><<<grid, BM * 64 / 16, 0, st>>>(x, w, bias, y, scratch, g, M, K,
+    launch_k(conv_fwd_kernel<InT, 64, TB>, grid, BM * 64 / 16, 0, st, x, w, bias, y, scratch, g, M, K,
                                                                 klen, relu, mask);
   DQN_LAUNCH_CHECK("gemm");
   if (splits > 1) {
     const int64_t MN = (int64_t)M * g.N;
-    splitk_bias_kernel<<<(int)std::min<int64_t>((MN + 255) / 256, 148 * 8), 256, 0, st>>>(
+    launch_k(splitk_bias_kernel, (int)std::min<int64_t>((MN + 255) / 256, 148 * 8), 256, 0, st, 
         scratch, splits, MN, g.N, bias, y, relu, mask);
     DQN_LAUNCH_CHECK("splitk_bias");
   }
@@ -538,12 +546,12 @@ int launch_wgrad(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const f
   float *bpartial = scratch + (int64_t)splits * R * g.N;
   dim3 grid((R + BM - 1) / BM, (g.N + bn - 1) / bn, splits);
   if (bn == 32)
-    wgrad_kernel<InT, 32><<<grid, BM * 32 / 16, 0, st>>>(x, dy, partial, bpartial, g, M, R, mlen);
+    launch_k(wgrad_kernel<InT, 32>, grid, BM * 32 / 16, 0, st, x, dy, partial, bpartial, g, M, R, mlen);
   else
-    wgrad_kernel<InT, 64><<<grid, BM * 64 / 16, 0, st>>>(x, dy, partial, bpartial, g, M, R, mlen);
+    launch_k(wgrad_kernel<InT, 64>, grid, BM * 64 / 16, 0, st, x, dy, partial, bpartial, g, M, R, mlen);
   DQN_LAUNCH_CHECK("wgrad");
   const int64_t RN = (int64_t)R * g.N;
-  wgrad_reduce_kernel<<<(int)std::min<int64_t>((RN + g.N + 255) / 256, 148 * 8), 256, 0, st>>>(
+  launch_k(wgrad_reduce_kernel, (int)std::min<int64_t>((RN + g.N + 255) / 256, 148 * 8), 256, 0, st, 
       partial, bpartial, splits, RN, g.N, grads + L.w_off, grads + L.b_off);
   DQN_LAUNCH_CHECK("wgrad_reduce");
   return DQN_OK;
@@ -569,7 +577,7 @@ int launch_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, cons
                                     scratch + (int64_t)M * R, M, g.N);
   if (rc) return rc;
   const int64_t total = (int64_t)batch * g.H * g.W * g.C;
-  col2im_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+  launch_k(col2im_kernel, (int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st, 
       dpatch, g, total, mask_act, dx);
   DQN_LAUNCH_CHECK("col2im");
   return DQN_OK;
@@ -598,7 +606,7 @@ int validate(const dqn_net_desc *net) {
 
 int launch_splitk_reduce(cudaStream_t st, const float *partial, int splits, int64_t MN, int N,
                          const float *bias, float *y, int relu, const float *mask) {
-  splitk_bias_kernel<<<(int)std::min<int64_t>((MN + 255) / 256, 148 * 8), 256, 0, st>>>(
+  launch_k(splitk_bias_kernel, (int)std::min<int64_t>((MN + 255) / 256, 148 * 8), 256, 0, st, 
       partial, splits, MN, N, bias, y, relu, mask);
   DQN_LAUNCH_CHECK("splitk_reduce");
   return DQN_OK;
@@ -607,7 +615,7 @@ int launch_splitk_reduce(cudaStream_t st, const float *partial, int splits, int6
 int launch_col2im(cudaStream_t st, const float *dpatch, const Geo &g, int batch,
                   const float *mask, float *dx) {
   const int64_t total = (int64_t)batch * g.H * g.W * g.C;
-  col2im_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+  launch_k(col2im_kernel, (int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st, 
       dpatch, g, total, mask, dx);
   DQN_LAUNCH_CHECK("col2im");
   return DQN_OK;
@@ -625,7 +633,7 @@ int simt_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const fl
       set_error("head cannot read u8 input");
       return DQN_ERR_UNSUPPORTED;
     }
-    head_fwd_kernel<<<b->batch, kHeadThreads, 0, st>>>(
+    launch_k(head_fwd_kernel, b->batch, kHeadThreads, 0, st, 
         (const float *)in, F, duel ? params + L.w_off : nullptr, duel ? params + L.b_off : nullptr,
         duel ? params + L.w2_off : params + L.w_off, duel ? params + L.b2_off : params + L.b_off,
         L.out_c, duel, b->act[l], flags);
@@ -649,7 +657,7 @@ int simt_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const f
     const int F = L.in_h * L.in_w * L.in_c;
     const bool duel = L.kind == DQN_LAYER_DUELING;
     const int64_t total = (int64_t)b->batch * F;
-    head_bwd_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, st>>>(
+    launch_k(head_bwd_kernel, (int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, st, 
         b->dact[l], b->batch, L.out_c, duel, duel ? params + L.w_off : nullptr,
         duel ? params + L.w2_off : params + L.w_off, F, mask, out);
     DQN_LAUNCH_CHECK("head_bwd");
@@ -665,7 +673,7 @@ int simt_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *gra
   if (is_head(net, l)) {
     const int F = L.in_h * L.in_w * L.in_c;
     const bool duel = L.kind == DQN_LAYER_DUELING;
-    head_wgrad_kernel<<<(F + 1 + 127) / 128, 128, 0, st>>>(
+    launch_k(head_wgrad_kernel, (F + 1 + 127) / 128, 128, 0, st, 
         (const float *)in, b->dact[l], b->batch, F, L.out_c, duel,
         duel ? grads + L.w_off : nullptr, duel ? grads + L.b_off : nullptr,
         duel ? grads + L.w2_off : grads + L.w_off, duel ? grads + L.b2_off : grads + L.b_off);

@@ -33,6 +33,7 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 
 __global__ void ring_fill_hash_kernel(uint64_t *__restrict__ out, int64_t total_words,
                                       int64_t first_word, uint64_t base) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (; i < total_words; i += stride) out[i] = splitmix64(base | (uint64_t)(first_word + i));
@@ -52,6 +53,7 @@ ring_gather_vec_kernel(const int4 *__restrict__ states, const int4 *__restrict__
                        const int64_t *__restrict__ actions, const double *__restrict__ rewards,
                        const uint8_t *__restrict__ terminals, int64_t *out_a, double *out_r,
                        uint8_t *out_t) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   const int j = blockIdx.y;
   const int which = blockIdx.z;
   const int64_t slot = __ldg(idx + j);
@@ -83,6 +85,7 @@ __global__ void ring_gather_bytes_kernel(const uint8_t *__restrict__ states,
                                          const uint8_t *__restrict__ next_states,
                                          int64_t slot_bytes, const int64_t *__restrict__ idx,
                                          uint8_t *__restrict__ out_s, uint8_t *__restrict__ out_s2) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   const int j = blockIdx.y;
   const int which = blockIdx.z;
   const uint8_t *src = which ? next_states : states;
@@ -99,6 +102,7 @@ __global__ void ring_gather_meta_kernel(const int64_t *__restrict__ actions,
                                         const uint8_t *__restrict__ terminals,
                                         const int64_t *__restrict__ idx, int k,
                                         int64_t *out_a, double *out_r, uint8_t *out_t) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= k) return;
   int64_t s = idx[j];
@@ -148,6 +152,7 @@ __global__ void tree_sample_kernel(const double *__restrict__ nodes, int depth,
                                    const double *__restrict__ beta_p, int64_t *__restrict__ idx,
                                    double *__restrict__ prob, double *__restrict__ weight,
                                    int32_t *flags) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   __shared__ double red[32];
   const int j = threadIdx.x;
   const double total = nodes[1];
@@ -190,6 +195,7 @@ __global__ void tree_sample_raw_kernel(const double *__restrict__ nodes, int dep
                                        const double *__restrict__ beta_p, int64_t *__restrict__ idx,
                                        double *__restrict__ prob, double *__restrict__ weight,
                                        double *__restrict__ block_max, int32_t *flags) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   __shared__ double red[32];
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const double total = nodes[1];
@@ -225,6 +231,7 @@ __global__ void tree_sample_raw_kernel(const double *__restrict__ nodes, int dep
 
 __global__ void tree_sample_norm_kernel(double *__restrict__ weight, int k,
                                         const double *__restrict__ block_max, int nblocks) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   __shared__ double mx;
   if (threadIdx.x == 0) {
     double v = block_max[0];
@@ -239,6 +246,7 @@ __global__ void tree_sample_norm_kernel(double *__restrict__ weight, int k,
 __global__ void tree_find_kernel(const double *__restrict__ nodes, int depth,
                                  const double *__restrict__ q, int64_t n, int64_t *__restrict__ idx,
                                  int32_t *flags) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   const double total = nodes[1];
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (!(total > 0.0)) {
@@ -275,6 +283,7 @@ tree_update_kernel(double *__restrict__ nodes, int depth, const int64_t *__restr
                    const int64_t *__restrict__ idx, const double *__restrict__ td, int k,
                    double alpha, double eps, double *__restrict__ max_p, int32_t *flags,
                    int mode) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   __shared__ int64_t s_node[kTreeThreads];
   __shared__ int s_first_bad;
   __shared__ double s_red[32];
@@ -348,6 +357,7 @@ __global__ void __launch_bounds__(kSmallK)
 tree_update_small_kernel(double *__restrict__ nodes, int depth, const int64_t *__restrict__ limit_p,
                          const int64_t *__restrict__ idx, const double *__restrict__ td, int k,
                          double alpha, double eps, double *__restrict__ max_p, int32_t *flags) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   __shared__ int64_t s_node[kSmallK];
   __shared__ double s_val[kSmallK];
   __shared__ int s_first_bad;
@@ -425,6 +435,7 @@ __global__ void __launch_bounds__(32)
 tree_update_warp_kernel(double *__restrict__ nodes, int depth, const int64_t *__restrict__ limit_p,
                         const int64_t *__restrict__ idx, const double *__restrict__ td, int k,
                         double alpha, double eps, double *__restrict__ max_p, int32_t *flags) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   constexpr unsigned FULL = 0xffffffffu;
   if (flags && (*flags & (DQN_FLAG_ZERO_TOTAL | DQN_FLAG_NONFINITE_OUT))) return;
   const int t = threadIdx.x;
@@ -482,6 +493,7 @@ tree_update_warp_kernel(double *__restrict__ nodes, int depth, const int64_t *__
 __global__ void __launch_bounds__(kTreeThreads)
 tree_store_kernel(double *__restrict__ nodes, int depth, int64_t capacity, int64_t slot,
                   int64_t n, const double *__restrict__ max_p, double alpha) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   __shared__ int64_t s_node[kTreeThreads];
   const int t = threadIdx.x;
   const double v = pow(*max_p, alpha);
@@ -498,6 +510,7 @@ tree_store_kernel(double *__restrict__ nodes, int depth, int64_t capacity, int64
 }
 
 __global__ void tree_level_kernel(double *__restrict__ nodes, int64_t lo, int64_t hi) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   for (int64_t a = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < hi;
        a += (int64_t)gridDim.x * blockDim.x)
     nodes[a] = __dadd_rn(nodes[2 * a], nodes[2 * a + 1]);
@@ -521,7 +534,7 @@ extern "C" int dqn_ring_fill_hash(void *stream, uint8_t *frames, int64_t slot0, 
   const int64_t words = slot_bytes / 8;
   const int64_t total = nslots * words;
   if (total == 0) return DQN_OK;
-  ring_fill_hash_kernel<<<grid_for(total, 256, 148 * 64), 256, 0, as_stream(stream)>>>(
+  launch_k(ring_fill_hash_kernel, grid_for(total, 256, 148 * 64), 256, 0, as_stream(stream), 
       reinterpret_cast<uint64_t *>(frames + slot0 * slot_bytes), total, slot0 * words,
       counter_base);
   DQN_LAUNCH_CHECK("ring_fill_hash");
@@ -543,7 +556,7 @@ extern "C" int dqn_ring_gather(void *stream, const uint8_t *states, const uint8_
   if (vec) {   // frames + metadata in one launch
     const int64_t vecs = slot_bytes / 16;
     dim3 grid((unsigned)((vecs + kGatherChunk - 1) / kGatherChunk), (unsigned)k, 2);
-    ring_gather_vec_kernel<<<grid, kGatherThreads, 0, st>>>(
+    launch_k(ring_gather_vec_kernel, grid, kGatherThreads, 0, st, 
         reinterpret_cast<const int4 *>(states), reinterpret_cast<const int4 *>(next_states), vecs,
         idx, reinterpret_cast<int4 *>(out_states), reinterpret_cast<int4 *>(out_next_states),
         actions, rewards, terminals, out_actions, out_rewards, out_terminals);
@@ -554,13 +567,13 @@ extern "C" int dqn_ring_gather(void *stream, const uint8_t *states, const uint8_
     {
       dim3 grid((unsigned)((slot_bytes + 255) / 256 < 64 ? (slot_bytes + 255) / 256 : 64),
                 (unsigned)k, 2);
-      ring_gather_bytes_kernel<<<grid, 256, 0, st>>>(states, next_states, slot_bytes, idx,
+      launch_k(ring_gather_bytes_kernel, grid, 256, 0, st, states, next_states, slot_bytes, idx,
                                                      out_states, out_next_states);
     }
     DQN_LAUNCH_CHECK("ring_gather");
   }
   if (out_actions || out_rewards || out_terminals) {
-    ring_gather_meta_kernel<<<(k + 255) / 256, 256, 0, st>>>(actions, rewards, terminals, idx, k,
+    launch_k(ring_gather_meta_kernel, (k + 255) / 256, 256, 0, st, actions, rewards, terminals, idx, k,
                                                             out_actions, out_rewards,
                                                             out_terminals);
     DQN_LAUNCH_CHECK("ring_gather_meta");
@@ -577,7 +590,7 @@ extern "C" int dqn_tree_sample(void *stream, const double *nodes, int32_t depth,
   cudaStream_t st = as_stream(stream);
   if (k <= 1024) {
     int threads = ((k + 31) / 32) * 32;
-    tree_sample_kernel<<<1, threads, 0, st>>>(nodes, depth, size, u, k, beta, idx, prob, weight,
+    launch_k(tree_sample_kernel, 1, threads, 0, st, nodes, depth, size, u, k, beta, idx, prob, weight,
                                               flags);
     DQN_LAUNCH_CHECK("tree_sample");
     return DQN_OK;
@@ -597,10 +610,10 @@ extern "C" int dqn_tree_sample(void *stream, const double *nodes, int32_t depth,
     if (st_) return st_;
     scratch_n = blocks;
   }
-  tree_sample_raw_kernel<<<blocks, threads, 0, st>>>(nodes, depth, size, u, k, beta, idx, prob,
+  launch_k(tree_sample_raw_kernel, blocks, threads, 0, st, nodes, depth, size, u, k, beta, idx, prob,
                                                      weight, scratch, flags);
   DQN_LAUNCH_CHECK("tree_sample_raw");
-  tree_sample_norm_kernel<<<grid_for(k, 256), 256, 0, st>>>(weight, k, scratch, blocks);
+  launch_k(tree_sample_norm_kernel, grid_for(k, 256), 256, 0, st, weight, k, scratch, blocks);
   DQN_LAUNCH_CHECK("tree_sample_norm");
   return DQN_OK;
 }
@@ -609,7 +622,7 @@ extern "C" int dqn_tree_find(void *stream, const double *nodes, int32_t depth,
                              const double *queries, int64_t n, int64_t *idx, int32_t *flags) {
   DQN_CHECK_ARG(nodes && queries && idx && n >= 0 && depth >= 1, "tree_find: bad args");
   if (n == 0) return DQN_OK;
-  tree_find_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(nodes, depth, queries, n, idx,
+  launch_k(tree_find_kernel, grid_for(n, 256), 256, 0, as_stream(stream), nodes, depth, queries, n, idx,
                                                                      flags);
   DQN_LAUNCH_CHECK("tree_find");
   return DQN_OK;
@@ -621,18 +634,18 @@ extern "C" int dqn_tree_update(void *stream, double *nodes, int32_t depth, const
   DQN_CHECK_ARG(nodes && size && idx && td && k >= 0 && depth >= 1, "tree_update: bad args");
   if (k == 0) return DQN_OK;
   if (k <= 32 && depth <= kMaxDepth) {
-    tree_update_warp_kernel<<<1, 32, 0, as_stream(stream)>>>(nodes, depth, size, idx, td, k, alpha,
+    launch_k(tree_update_warp_kernel, 1, 32, 0, as_stream(stream), nodes, depth, size, idx, td, k, alpha,
                                                              eps, max_p, flags);
     DQN_LAUNCH_CHECK("tree_update_warp");
     return DQN_OK;
   }
   if (k <= kSmallK && depth <= kMaxDepth) {
-    tree_update_small_kernel<<<1, ((k + 31) / 32) * 32, 0, as_stream(stream)>>>(
+    launch_k(tree_update_small_kernel, 1, ((k + 31) / 32) * 32, 0, as_stream(stream), 
         nodes, depth, size, idx, td, k, alpha, eps, max_p, flags);
     DQN_LAUNCH_CHECK("tree_update_small");
     return DQN_OK;
   }
-  tree_update_kernel<<<1, kTreeThreads, 0, as_stream(stream)>>>(nodes, depth, size, 0, idx, td, k,
+  launch_k(tree_update_kernel, 1, kTreeThreads, 0, as_stream(stream), nodes, depth, size, 0, idx, td, k,
                                                                 alpha, eps, max_p, flags, 0);
   DQN_LAUNCH_CHECK("tree_update");
   return DQN_OK;
@@ -642,7 +655,7 @@ extern "C" int dqn_tree_set(void *stream, double *nodes, int32_t depth, int64_t 
                             const int64_t *idx, const double *values, int32_t k, int32_t *flags) {
   DQN_CHECK_ARG(nodes && idx && values && k >= 0 && depth >= 1, "tree_set: bad args");
   if (k == 0) return DQN_OK;
-  tree_update_kernel<<<1, kTreeThreads, 0, as_stream(stream)>>>(nodes, depth, nullptr, capacity, idx,
+  launch_k(tree_update_kernel, 1, kTreeThreads, 0, as_stream(stream), nodes, depth, nullptr, capacity, idx,
                                                                 values, k, 0.0, 0.0, nullptr,
                                                                 flags, 1);
   DQN_LAUNCH_CHECK("tree_set");
@@ -654,7 +667,7 @@ extern "C" int dqn_tree_store(void *stream, double *nodes, int32_t depth, int64_
   DQN_CHECK_ARG(nodes && max_p && capacity >= 1 && slot >= 0 && slot < capacity && n >= 0,
                 "tree_store: bad args");
   if (n == 0) return DQN_OK;
-  tree_store_kernel<<<1, kTreeThreads, 0, as_stream(stream)>>>(nodes, depth, capacity, slot, n,
+  launch_k(tree_store_kernel, 1, kTreeThreads, 0, as_stream(stream), nodes, depth, capacity, slot, n,
                                                                max_p, alpha);
   DQN_LAUNCH_CHECK("tree_store");
   return DQN_OK;
@@ -664,7 +677,7 @@ extern "C" int dqn_tree_rebuild(void *stream, double *nodes, int32_t depth) {
   DQN_CHECK_ARG(nodes && depth >= 1 && depth < 40, "tree_rebuild: bad args");
   for (int l = depth - 1; l >= 0; --l) {
     const int64_t lo = int64_t(1) << l, hi = int64_t(1) << (l + 1);
-    tree_level_kernel<<<grid_for(hi - lo, 256), 256, 0, as_stream(stream)>>>(nodes, lo, hi);
+    launch_k(tree_level_kernel, grid_for(hi - lo, 256), 256, 0, as_stream(stream), nodes, lo, hi);
     DQN_LAUNCH_CHECK("tree_rebuild");
   }
   return DQN_OK;

@@ -449,6 +449,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // everything above (TMEM allocation, barriers, row bases from kernel
+  // parameters) overlapped the previous kernel; operands are read only now
+  pdl_wait();
   const uint32_t tmem = tmem_slot;
   // accumulator pairs [big | small] at columns a * 2BN, A stages after them
   const uint32_t acol0 = (uint32_t)PL::ACC_MAX;
@@ -558,6 +561,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
     }
   }
   mbar_wait(&done, 0);
+  // the next kernel may be scheduled now (common.cuh): its prologue overlaps
+  // this tile's epilogue and split-K fixup, not the K loop
+  pdl_trigger();
   TC_MARK(2)
   tc_fence_after();
 
@@ -779,7 +785,7 @@ int launch(cudaStream_t st, const Pol &p, int splits, const char *what) {
 #ifdef DQN_TC_TRACE
   launch_id = next_launch_seq();
 #endif
-  tc_gemm_kernel<Pol><<<grid, kThreads, bytes, st>>>(p, launch_id);
+  launch_k(tc_gemm_kernel<Pol>, grid, kThreads, bytes, st, p, launch_id);
   DQN_LAUNCH_CHECK(what);
   return DQN_OK;
 }

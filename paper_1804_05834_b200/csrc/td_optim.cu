@@ -26,6 +26,7 @@ td_loss_kernel(const float *__restrict__ q_on, const float *__restrict__ q_next_
                const double *__restrict__ weights, int B, int nA, double gamma, int flags,
                double *__restrict__ targets, double *__restrict__ td,
                double *__restrict__ losses, float *__restrict__ dq, double *__restrict__ stats) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   __shared__ double s_abs[kTdThreads], s_loss[kTdThreads];
   const int t = threadIdx.x;
   double acc_abs = 0.0, acc_loss = 0.0;
@@ -89,6 +90,7 @@ td_loss_kernel(const float *__restrict__ q_on, const float *__restrict__ q_next_
 // -------------------------------------------------------------- RMSprop
 
 __global__ void rms_scan_kernel(const float *__restrict__ g, int64_t n, int32_t *flags) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -107,6 +109,7 @@ __device__ __forceinline__ void rms_one(float &w, float &g, float &a, float lr, 
 __global__ void rms_apply_kernel(float *__restrict__ w, float *__restrict__ g,
                                  float *__restrict__ acc, int64_t n, float lr, float rho,
                                  float omr, float eps, const int32_t *__restrict__ flags) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   // optim.py:38-40: a non-finite gradient aborts the step before any update;
   // any earlier failure of this step (the reference would have raised before
   // reaching the optimizer) does too.  Flags are sticky until the host reads.
@@ -138,6 +141,7 @@ constexpr int kNormBlocks = 148;
 
 __global__ void sqnorm_partial_kernel(const float *__restrict__ g, int64_t n,
                                       double *__restrict__ partial) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   __shared__ double red[256];
   double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -156,6 +160,7 @@ __global__ void sqnorm_partial_kernel(const float *__restrict__ g, int64_t n,
 
 __global__ void sqnorm_final_kernel(double *__restrict__ partial, int nb, double max_norm,
                                     double *__restrict__ norm_out) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   if (threadIdx.x != 0) return;
   double s = 0.0;
   for (int i = 0; i < nb; ++i) s = __dadd_rn(s, partial[i]);
@@ -167,6 +172,7 @@ __global__ void sqnorm_final_kernel(double *__restrict__ partial, int nb, double
 
 __global__ void grad_scale_kernel(float *__restrict__ g, int64_t n,
                                   const double *__restrict__ scale_p) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   const double sd = *scale_p;
   if (sd == 0.0) return;
   const float s = (float)sd;
@@ -190,7 +196,7 @@ extern "C" int dqn_td_loss(void *stream, const float *q_online, const float *q_n
                     td && losses && dq && batch >= 1 && n_actions >= 1,
                 "td_loss: bad args");
   DQN_CHECK_ARG(!(flags & DQN_TD_DOUBLE) || q_next_online, "td_loss: double needs q_next_online");
-  td_loss_kernel<<<1, kTdThreads, 0, as_stream(stream)>>>(
+  launch_k(td_loss_kernel, 1, kTdThreads, 0, as_stream(stream), 
       q_online, q_next_online, q_next_target, actions, rewards, terminals, weights, batch,
       n_actions, gamma, flags, targets, td, losses, dq, stats);
   DQN_LAUNCH_CHECK("td_loss");
@@ -205,10 +211,10 @@ extern "C" int dqn_rmsprop_step(void *stream, float *w, float *g, float *acc, in
   if (n == 0) return DQN_OK;
   cudaStream_t st = as_stream(stream);
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
-  rms_scan_kernel<<<blocks, 256, 0, st>>>(g, n, flags);
+  launch_k(rms_scan_kernel, blocks, 256, 0, st, g, n, flags);
   DQN_LAUNCH_CHECK("rms_scan");
   const int blocks4 = (int)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, 148 * 4));
-  rms_apply_kernel<<<blocks4, 256, 0, st>>>(w, g, acc, n, lr, rho, one_minus_rho, eps, flags);
+  launch_k(rms_apply_kernel, blocks4, 256, 0, st, w, g, acc, n, lr, rho, one_minus_rho, eps, flags);
   DQN_LAUNCH_CHECK("rms_apply");
   return DQN_OK;
 }
@@ -223,11 +229,11 @@ extern "C" int dqn_clip_gradients(void *stream, float *g, int64_t n, double max_
     if (st) return st;
   }
   cudaStream_t st = as_stream(stream);
-  sqnorm_partial_kernel<<<kNormBlocks, 256, 0, st>>>(g, n, partial);
+  launch_k(sqnorm_partial_kernel, kNormBlocks, 256, 0, st, g, n, partial);
   DQN_LAUNCH_CHECK("sqnorm_partial");
-  sqnorm_final_kernel<<<1, 32, 0, st>>>(partial, kNormBlocks, max_norm, norm_out);
+  launch_k(sqnorm_final_kernel, 1, 32, 0, st, partial, kNormBlocks, max_norm, norm_out);
   DQN_LAUNCH_CHECK("sqnorm_final");
-  grad_scale_kernel<<<kNormBlocks, 256, 0, st>>>(g, n, partial + kNormBlocks);
+  launch_k(grad_scale_kernel, kNormBlocks, 256, 0, st, g, n, partial + kNormBlocks);
   DQN_LAUNCH_CHECK("grad_scale");
   return DQN_OK;
 }

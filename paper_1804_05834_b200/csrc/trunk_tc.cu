@@ -382,8 +382,7 @@ int lin_dgrad_launch(cudaStream_t st, const float *dy, const float *w, const flo
   p.M = M;
   p.N = N;
   p.K = K;
-  p.klen = std::min(K, 128);
-  p.ksplits = ceil_div(K, p.klen);
+  split_k(ceil_div(M, tc::BM) * ceil_div(N, BN), K, BN, 16, p.klen, p.ksplits);
   return tc::launch(st, p, p.ksplits, "tc_lin_dgrad");
 }
 
@@ -508,7 +507,8 @@ int64_t tc_scratch_floats(const dqn_net_desc *net, int batch) {
     const int M = batch * L.out_h * L.out_w, R = L.fh * L.fw * L.in_c, K = R;
     const int fs = ceil_div(K, fwd_klen(K));
     m = std::max(m, fs > 1 ? (int64_t)fs * M * L.out_c : 0);
-    if (L.kind == DQN_LAYER_LINEAR) m = std::max(m, (int64_t)ceil_div(L.out_c, 128) * M * R);
+    if (L.kind == DQN_LAYER_LINEAR)     // lin dgrad partials: split_k caps at 16 splits
+      m = std::max(m, (int64_t)std::min(16, ceil_div(L.out_c, tc::BK)) * M * R);
     if (L.kind == DQN_LAYER_CONV && tc_layer_supported(net, l, 1)) {
       const int Kd = (L.fh / L.sh) * (L.fw / L.sw) * L.out_c;
       const int ds = std::max(1, std::min(ceil_div(Kd, tc::BK), 16));   // split_k upper bound
@@ -568,6 +568,7 @@ namespace {
 // each byte load of the warp reads one contiguous segment of a window row
 __global__ void im2col_t_u8_kernel(const uint8_t *__restrict__ x, Geo g, int R, int K,
                                    uint8_t *__restrict__ xt) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
   const int nq = K / 16;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)R * nq) return;
@@ -635,7 +636,7 @@ extern "C" int dqn_net_im2col_t(void *stream, const dqn_net_desc *net, const dqn
   const dqn_layer_desc &L = net->layer[0];
   const int R = L.fh * L.fw * L.in_c, K = bind->batch * L.out_h * L.out_w;
   const int64_t n = (int64_t)R * (K / 16);
-  im2col_t_u8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+  launch_k(im2col_t_u8_kernel, (unsigned)((n + 255) / 256), 256, 0, as_stream(stream), 
       (const uint8_t *)bind->x, geo_of(L), R, K, bind->xt);
   DQN_LAUNCH_CHECK("net_im2col_t");
   return DQN_OK;
