@@ -279,9 +279,18 @@ def layer_roofline(P, on, plan, peaks, peak_kind, reps=50):
     ms, name, phase, fl, batch = best
     achieved = fl / (ms * 1e-3) / 1e12
     peak = float(peaks["bf16_tflops"])
-    return {"kernel": f"{name}.{['fwd', 'dgrad', 'wgrad'][phase]} (batch {batch})",
+    label = f"{name}.{['fwd', 'dgrad', 'wgrad'][phase]} (batch {batch})"
+    traffic, traffic_src = None, None
+    try:      # dram__bytes_read + dram__bytes_write per launch from a committed ncu capture
+        t = json.load(open(REPO / "profiles" / "roofline_traffic.json"))
+        if label in t.get("kernels", {}):
+            traffic, traffic_src = t["kernels"][label]["dram_bytes"], t.get("source")
+    except (OSError, ValueError):
+        pass
+    return {"kernel": label,
             "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": None, "peak_source": f"{peak_kind} bf16 dense burst",
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+            "peak_source": f"{peak_kind} bf16 dense burst",
             "algorithmic_flop_per_launch": fl, "avg_launch_us": ms * 1e3}, rows
 
 
