@@ -16,11 +16,13 @@ Our arm (default) prints ONE JSON line on rank 0:
   cpu_baseline  the CPU oracle port of the reference learn_step on this
              host's cores for a bounded sample.
 ``--impl reference`` times that CPU path alone and prints its own line.
-Under torchrun (N > 1) the default is the cfg5 data-parallel learner
-(paper_1804_05834_b200/dp.py: replay sharded across the ranks, global
-stratified PER over all-gathered shard totals, per-GPU batch 32, NCCL
-gradient all-reduce); ``--mode replicas`` runs independent learners instead
-(population of seeds).  Rank 0 reports the max-over-ranks time.
+Under torchrun (N > 1) the default is N independent learners, one per GPU
+(the population-of-seeds mode: each rank owns its own 1M ring, tree and
+networks; no data-path collective; weak scaling).  ``--mode dp`` runs the
+cfg5 data-parallel learner instead (paper_1804_05834_b200/dp.py: replay
+sharded across the ranks, global stratified PER over all-gathered shard
+totals, per-GPU batch 32, NCCL gradient all-reduce; host-orchestrated, see
+DESIGN.md §6).  Rank 0 reports the max-over-ranks time.
 """
 
 from __future__ import annotations
@@ -545,15 +547,16 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--mode", default="auto", choices=["auto", "single", "replicas", "dp"],
-                    help="auto: single GPU at N=1, data-parallel (cfg5) under torchrun; "
-                         "replicas: independent learners per GPU (population of seeds)")
+                    help="auto/replicas: one independent learner per GPU (population of "
+                         "seeds; N = 1 is the single-GPU learner); dp: the cfg5 "
+                         "data-parallel learner (sharded PER, NCCL gradient all-reduce)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     world = dist_env()[1]
     if args.impl == "reference":
         run_reference(args)
-    elif args.mode == "dp" or (args.mode == "auto" and world > 1):
+    elif args.mode == "dp":
         run_dp(args)
     else:
         run_ours(args)
