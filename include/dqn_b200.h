@@ -184,6 +184,25 @@ int dqn_net_layer(void *stream, const dqn_net_desc *net, const float *params, fl
 
 /* ---------------------------------------------------------- loss / optim */
 
+/* Work bytes dqn_head_td needs for `batch` rows and `n_actions` actions
+ * (zero-initialised once by the caller; left zeroed between calls). */
+int64_t dqn_head_td_work_bytes(int32_t batch, int32_t n_actions);
+
+/* The learner's head block in two launches (replaces head forward x2,
+ * dqn_td_loss, the head's dgrad and wgrad of learn_step, agent.py:91-132):
+ * Q heads of the online net (on_bind: [s; s'] rows for Double DQN) and the
+ * target net (tg_bind: s' rows) from their hidden features, then the TD block
+ * exactly as dqn_td_loss (targets/td/losses/stats, dq into on_view->dact[L-1]),
+ * the head backward into on_view->dact[L-2] (masked by the hidden ReLU) and
+ * the head weight gradient added to on_grads.  Linear or dueling heads with
+ * at most 18 actions and batch <= 1024; DQN_ERR_UNSUPPORTED otherwise. */
+int dqn_head_td(void *stream, const dqn_net_desc *on_net, const float *on_params,
+                float *on_grads, const dqn_binding *on_bind, const dqn_binding *on_view,
+                const dqn_net_desc *tg_net, const float *tg_params, const dqn_binding *tg_bind,
+                const int64_t *actions, const double *rewards, const uint8_t *terminals,
+                const double *weights, double gamma, int32_t td_flags, double *targets,
+                double *td, double *losses, double *stats, void *work, int32_t *flags);
+
 #define DQN_TD_DOUBLE 0x1
 #define DQN_TD_HUBER 0x2
 #define DQN_TD_REWARD_CLIP 0x4

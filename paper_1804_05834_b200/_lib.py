@@ -67,6 +67,10 @@ _SIGS = {
     "dqn_tree_rebuild": ([vp, vp, i32], C.c_int),
     "dqn_net_scratch_floats": ([C.POINTER(NetDesc), i32], i64),
     "dqn_net_im2col_t_bytes": ([C.POINTER(NetDesc), i32], i64),
+    "dqn_head_td_work_bytes": ([i32, i32], i64),
+    "dqn_head_td": ([vp, C.POINTER(NetDesc), vp, vp, C.POINTER(Binding), C.POINTER(Binding),
+                     C.POINTER(NetDesc), vp, C.POINTER(Binding), vp, vp, vp, vp, f64, i32,
+                     vp, vp, vp, vp, vp, vp], C.c_int),
     "dqn_net_im2col_t": ([vp, C.POINTER(NetDesc), C.POINTER(Binding)], C.c_int),
     "dqn_net_forward": ([vp, C.POINTER(NetDesc), vp, C.POINTER(Binding), vp], C.c_int),
     "dqn_net_backward": ([vp, C.POINTER(NetDesc), vp, C.POINTER(Binding), vp], C.c_int),

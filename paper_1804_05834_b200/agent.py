@@ -131,6 +131,16 @@ class _StepPlan:
         # gets a view with its own scratch (split-K partials and counters)
         self.on_wview = online.prefix_binding(self.on_bind, k, own_scratch=True)
         self.tg_bind = target.binding(k)
+        # the Q heads, TD block, head backward and head wgrad run as one fused
+        # launch (dqn_head_td) when the head fits it (nA <= 18, batch <= 1024)
+        units = online._units
+        self.head_layer = len(units) - 1
+        self.fused_head = (len(units) >= 2 and units[-1]["kind"] in (_lib.LAYER_LINEAR,
+                                                                     _lib.LAYER_DUELING)
+                           and self.nA <= 18 and k <= 1024
+                           and os.environ.get("DQN_B200_FUSED_HEAD", "1") != "0")
+        self.head_work = torch.zeros(int(_lib.lib.dqn_head_td_work_bytes(k, self.nA)),
+                                     dtype=torch.uint8, device=dev)
         # conv1's wgrad reads its uint8 patch operand from a transposed im2col
         # built beside the forward pass (dqn_net_im2col_t), not byte gathers
         self.on_desc = online.desc_for(self.x)
@@ -193,30 +203,44 @@ class _StepPlan:
                           C.byref(self.on_view.struct))
                 e_xt = ev()
                 e_xt.record(s1)
-            tg.forward_into(self.x[k:], self.tg_bind)
+            tg.forward_into(self.x[k:], self.tg_bind, upto=self.head_layer if self.fused_head else None)
             e_tg = ev()
             e_tg.record(s1)
+        upto = self.head_layer if self.fused_head else None
         if self.double:
-            on.forward_into(self.x, self.on_bind)
+            on.forward_into(self.x, self.on_bind, upto=upto)
         else:
-            on.forward_into(self.x[:k], self.on_bind)
+            on.forward_into(self.x[:k], self.on_bind, upto=upto)
         s0.wait_event(e_tg)
         nA = self.nA
-        q_on = self.on_bind.act[-1]
         out = self.d_out
-        _lib.call("dqn_td_loss", st, q_on.data_ptr(),
-                  q_on[k * nA:].data_ptr() if self.double else None,
-                  self.tg_bind.act[-1].data_ptr(), self.a.data_ptr(), self.r.data_ptr(),
-                  self.t.data_ptr(), self.w.data_ptr(), k, nA, self.gamma, self.flags_td,
-                  out[:k].data_ptr(), out[k:2 * k].data_ptr(), out[2 * k:3 * k].data_ptr(),
-                  self.on_view.dact[-1].data_ptr(), out[3 * k:].data_ptr())
         for v in (self.on_view, self.on_wview):
             v.x = self.x[:k]
             v.struct.x = self.x.data_ptr()
             v.struct.dx = None                     # conv1 dX is never needed
+        if self.fused_head:
+            # both Q heads + targets/TD/loss + head dX + head wgrad in one launch
+            _lib.call("dqn_head_td", st, C.byref(on.desc_for(self.x)), on.flat_values.data_ptr(),
+                      on.flat_grads.data_ptr(), C.byref(self.on_bind.struct),
+                      C.byref(self.on_view.struct), C.byref(tg.desc_for(self.x)),
+                      tg.flat_values.data_ptr(), C.byref(self.tg_bind.struct),
+                      self.a.data_ptr(), self.r.data_ptr(), self.t.data_ptr(), self.w.data_ptr(),
+                      self.gamma, self.flags_td, out[:k].data_ptr(), out[k:2 * k].data_ptr(),
+                      out[2 * k:3 * k].data_ptr(), out[3 * k:].data_ptr(),
+                      self.head_work.data_ptr(), self.flags.data_ptr())
+            first = self.head_layer - 1
+        else:
+            q_on = self.on_bind.act[-1]
+            _lib.call("dqn_td_loss", st, q_on.data_ptr(),
+                      q_on[k * nA:].data_ptr() if self.double else None,
+                      self.tg_bind.act[-1].data_ptr(), self.a.data_ptr(), self.r.data_ptr(),
+                      self.t.data_ptr(), self.w.data_ptr(), k, nA, self.gamma, self.flags_td,
+                      out[:k].data_ptr(), out[k:2 * k].data_ptr(), out[2 * k:3 * k].data_ptr(),
+                      self.on_view.dact[-1].data_ptr(), out[3 * k:].data_ptr())
+            first = len(on._units) - 1
         e = ev()
         e.record(s0)
-        for layer in reversed(range(len(on._units))):
+        for layer in reversed(range(first + 1)):
             if layer == 0:
                 # conv1 has no dgrad: its wgrad takes the main stream (and the
                 # dgrad binding's scratch) instead of queueing behind conv2's

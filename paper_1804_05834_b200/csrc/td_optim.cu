@@ -11,6 +11,7 @@
 // optim.py:44-46 under NEP-50 weak-scalar promotion, so it is bit-exact given
 // identical gradients.
 #include "common.cuh"
+#include "td_row.cuh"
 
 #include <algorithm>
 
@@ -31,44 +32,11 @@ td_loss_kernel(const float *__restrict__ q_on, const float *__restrict__ q_next_
   const int t = threadIdx.x;
   double acc_abs = 0.0, acc_loss = 0.0;
   for (int j = t; j < B; j += blockDim.x) {
-    const float *qt = q_next_tg + (int64_t)j * nA;
-    double boot;
-    if (flags & DQN_TD_DOUBLE) {
-      // a* = argmax_a Q_online(s', a), first maximum (agent.py:70)
-      const float *qo = q_next_on + (int64_t)j * nA;
-      int best = 0;
-      float bv = qo[0];
-      for (int a = 1; a < nA; ++a)
-        if (qo[a] > bv) { bv = qo[a]; best = a; }
-      boot = __dmul_rn(gamma, (double)qt[best]);
-    } else {
-      float mx = qt[0];
-      for (int a = 1; a < nA; ++a) mx = fmaxf(mx, qt[a]);
-      boot = __dmul_rn(gamma, (double)mx);   // gamma * q_next.max(axis=1)
-    }
-    double r = rewards[j];
-    if (flags & DQN_TD_REWARD_CLIP) r = fmin(fmax(r, -1.0), 1.0);   // agent.py:102-103
-    const double y = __dadd_rn(r, terminals[j] ? 0.0 : boot);       // r + where(t, 0, boot)
-    const int64_t a = actions[j];
-    const double qsa = (double)q_on[(int64_t)j * nA + a];
-    const double d = __dsub_rn(y, qsa);
-    const double w = weights[j];
-    double loss, g;
-    if (flags & DQN_TD_HUBER) {
-      const double ad = fabs(d);
-      loss = __dmul_rn(w, ad <= 1.0 ? __dmul_rn(__dmul_rn(0.5, d), d) : __dsub_rn(ad, 0.5));
-      g = __dmul_rn(-w, fmin(fmax(d, -1.0), 1.0));
-    } else {
-      loss = __dmul_rn(__dmul_rn(__dmul_rn(0.5, w), d), d);   // ((0.5*w)*d)*d
-      g = __dmul_rn(-w, d);                                   // (-w)*d
-    }
-    targets[j] = y;
-    td[j] = d;
-    losses[j] = loss;
-    const float gf = __double2float_rn(g);
-    for (int c = 0; c < nA; ++c) dq[(int64_t)j * nA + c] = (c == a) ? gf : 0.f;
-    acc_abs = __dadd_rn(acc_abs, fabs(d));
-    acc_loss = __dadd_rn(acc_loss, loss);
+    double ad, l;
+    td_row(j, q_on, q_next_on, q_next_tg, actions, rewards, terminals, weights, nA, gamma, flags,
+           targets, td, losses, dq, ad, l);
+    acc_abs = __dadd_rn(acc_abs, ad);
+    acc_loss = __dadd_rn(acc_loss, l);
   }
   if (stats == nullptr) return;
   s_abs[t] = acc_abs;

@@ -317,12 +317,17 @@ class Network:
             raise GeometryError(f"input shape {tuple(x.shape[1:])} != network input {self.input_shape}")
         return x.contiguous()
 
-    def forward_into(self, x, bind: _Bind) -> None:
-        """Enqueue the forward phase for a prepared device input (no sync)."""
+    def forward_into(self, x, bind: _Bind, upto: int | None = None) -> None:
+        """Enqueue the forward phase for a prepared device input (no sync);
+        ``upto`` stops before that layer (the learner's fused head takes over)."""
         bind.x = x
         bind.struct.x = x.data_ptr()
-        _lib.call("dqn_net_forward", _lib.stream_ptr(), C.byref(self.desc_for(x)),
-                  self.flat_values.data_ptr(), C.byref(bind.struct), self._flags.data_ptr())
+        if upto is None:
+            _lib.call("dqn_net_forward", _lib.stream_ptr(), C.byref(self.desc_for(x)),
+                      self.flat_values.data_ptr(), C.byref(bind.struct), self._flags.data_ptr())
+            return
+        for layer in range(upto):
+            self.layer_into(bind, layer, 0)
 
     def check_output(self) -> None:
         f = int(self._flags.item())
