@@ -45,7 +45,8 @@ namespace dqn {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 32;                  // k per pipeline stage (4 MMA k-steps of 8)
+constexpr int BK = 64;                  // k per pipeline stage (8 MMA k-steps of 8)
+constexpr int kKc = BK / 4;             // 16-byte k-chunks per row of a stage
 constexpr int kGroupThreads = 256;      // 8 warps: lane quarter w % 4, k-half w / 4
 constexpr int kGroups = 2;
 constexpr int kProducers = kGroups * kGroupThreads;
@@ -193,7 +194,7 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t base, int R, int kstep) {
 // owns the same rows in every k-block (row bases are computed once per CTA).
 // A quarter-warp writes one contiguous 128-byte smem line (8 rows of one k-chunk).
 __device__ __forceinline__ void chunk_coords(int c, int &row, int &k) {
-  const int r8 = c & 7, kc = (c >> 3) & 7, rg = c >> 6;
+  const int r8 = c & 7, kc = (c >> 3) % kKc, rg = c / (8 * kKc);
   row = rg * 8 + r8;
   k = kc * 4;
 }
@@ -296,7 +297,7 @@ struct Gather {
     }
   }
   template <int RR>
-  __device__ void dump_bias(float (&red)[RR][8]) const {
+  __device__ void dump_bias(float (&red)[RR][kKc]) const {
 #pragma unroll
     for (int i = 0; i < U; ++i) {
       const int u = t0 + i * kGroupThreads;
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   // MMAs of every group
   __shared__ uint64_t full[STAGES], empty[STAGES], done;
   __shared__ uint32_t tmem_slot;
-  __shared__ float bias_red[Pol::BIAS_FROM_B ? kGroups : 1][Pol::BIAS_FROM_B ? BN : 1][8];
+  __shared__ float bias_red[Pol::BIAS_FROM_B ? kGroups : 1][Pol::BIAS_FROM_B ? BN : 1][kKc];
 
 #ifdef DQN_TC_TRACE
   unsigned long long tr_[6] = {0, 0, 0, 0, 0, 0};
@@ -461,25 +462,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   if (producer) {
     // group g gathers k-blocks g, g + kGroups, ... into ring slot kb % STAGES;
     // a slot is refilled once the MMAs of k-block kb - STAGES completed.
-    // Two register buffers per thread: a group has two k-blocks of loads in
-    // flight (a global round trip is ~1 us, a k-block's MMAs ~0.1 us).
+    // One register buffer per thread: a 64-k block's loads are in flight
+    // while the previous block is stored and multiplied.
     using GB = Gather<Pol::B_MNC, BN, RB>;
-    float av0[16], av1[16];
-    typename GB::Regs bv0, bv1;
-    auto fetch = [&](float (&av)[16], typename GB::Regs &bv, int kb) {
+    constexpr int AR = BK / 32;                  // 16-runs of A per thread
+    float av[AR][16];
+    typename GB::Regs bv;
+    auto fetch = [&](int kb) {
       if (TC_SKIP(2)) return;
       const int k0 = kbeg + kb * BK;
-      if (abase >= 0) {
-        p.a16(abase, k0 + 16 * khalf, kend, av);
-      } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) av[j] = 0.f;
+      for (int h = 0; h < AR; ++h) {
+        if (abase >= 0) {
+          p.a16(abase, k0 + (BK / 2) * khalf + 16 * h, kend, av[h]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) av[h][j] = 0.f;
+        }
       }
       gb.fetch(bv, k0, kend, [&](int k) { return p.b_koff(k); },
                [&](long long b, int ko) { return p.b_ld(b, ko); },
                [&](long long b, int k, int ke, float4 (&v)[4]) { p.b4(b, k, ke, v); });
     };
-    auto put = [&](const float (&av)[16], const typename GB::Regs &bv, int kb) {
+    auto put = [&](int kb) {
       const int s = kb % STAGES, use = kb / STAGES;
 #ifdef DQN_TC_TRACE
       const bool tk = threadIdx.x == 0 && kb < 8;
@@ -496,13 +501,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
       if (!TC_SKIP(4)) {
         // A: hi (= the values) and lo pieces into this stage's TMEM columns
         const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + acol0 +
-                            (uint32_t)(s * PL::A_COLS + 16 * khalf);
-        tmem_st16(ta, av);
-        if (NA > 1) {
-          float lo[16];
+                            (uint32_t)(s * PL::A_COLS + (BK / 2) * khalf);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) lo[j] = tf32_lo(av[j]);
-          tmem_st16(ta + BK, lo);
+        for (int h = 0; h < AR; ++h) {
+          tmem_st16(ta + 16 * h, av[h]);
+          if (NA > 1) {
+            float lo[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) lo[j] = tf32_lo(av[h][j]);
+            tmem_st16(ta + BK + 16 * h, lo);
+          }
         }
         gb.store(bv, sbase + s * B_BYTES, BN * 16, NB, want_bias);
         tmem_wait_st();
@@ -542,16 +550,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
 #endif
       }
     };
-    constexpr int G = kGroups;
-    if (group < nk) fetch(av0, bv0, group);
-    if (group + G < nk) fetch(av1, bv1, group + G);
-    for (int kb = group; kb < nk; kb += 2 * G) {
-      put(av0, bv0, kb);
-      if (kb + 2 * G < nk) fetch(av0, bv0, kb + 2 * G);
-      if (kb + G < nk) {
-        put(av1, bv1, kb + G);
-        if (kb + 3 * G < nk) fetch(av1, bv1, kb + 3 * G);
-      }
+    if (group < nk) fetch(group);
+    for (int kb = group; kb < nk; kb += kGroups) {
+      put(kb);
+      if (kb + kGroups < nk) fetch(kb + kGroups);
     }
     if (threadIdx.x % kGroupThreads == 0) {
 #ifdef DQN_TC_TRACE
@@ -620,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
 #pragma unroll
       for (int g = 0; g < kGroups; ++g)
 #pragma unroll
-        for (int kc = 0; kc < 8; ++kc)
+        for (int kc = 0; kc < kKc; ++kc)
           if (g + kc > 0) s = __fadd_rn(s, bias_red[g][threadIdx.x][kc]);
       const int n = n0 + threadIdx.x;
       if (!SPLITK)

@@ -388,12 +388,11 @@ int lin_dgrad_launch(cudaStream_t st, const float *dy, const float *w, const flo
 
 int lin_dgrad(cudaStream_t st, const float *dy, const float *w, const float *mask, float *out,
               float *partial, int *counters, int M, int N, int K) {
-  // tiles of at most 96 columns: two [big | small] accumulator pairs + the A
+  // tiles of at most 64 columns: two [big | small] accumulator pairs + the A
   // stages fit in TMEM
-  for (int bn : {64, 96, 32, 16}) {
+  for (int bn : {64, 32, 16}) {
     if (N % bn) continue;
     switch (bn) {
-      case 96: return lin_dgrad_launch<96>(st, dy, w, mask, out, partial, counters, M, N, K);
       case 64: return lin_dgrad_launch<64>(st, dy, w, mask, out, partial, counters, M, N, K);
       case 32: return lin_dgrad_launch<32>(st, dy, w, mask, out, partial, counters, M, N, K);
       default: return lin_dgrad_launch<16>(st, dy, w, mask, out, partial, counters, M, N, K);
@@ -422,7 +421,7 @@ int conv_dgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const float *dy,
   return tc::launch(st, p, L.sh * L.sw * p.ksplits, "tc_conv_dgrad");
 }
 
-bool dgrad_tile_ok(int C) { return C == 16 || C == 32 || C == 48 || C == 64 || C == 96 || C % 64 == 0; }
+bool dgrad_tile_ok(int C) { return C == 16 || C == 32 || C == 48 || C % 64 == 0; }
 
 int conv_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
                const float *mask, float *out, float *scratch, int *counters, int batch) {
@@ -431,7 +430,6 @@ int conv_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const 
     case 32: return conv_dgrad_launch<32>(st, L, dy, w, mask, out, scratch, counters, batch);
     case 48: return conv_dgrad_launch<48>(st, L, dy, w, mask, out, scratch, counters, batch);
     case 64: return conv_dgrad_launch<64>(st, L, dy, w, mask, out, scratch, counters, batch);
-    case 96: return conv_dgrad_launch<96>(st, L, dy, w, mask, out, scratch, counters, batch);
     default: break;
   }
   if (L.in_c % 64 == 0) return conv_dgrad_launch<64>(st, L, dy, w, mask, out, scratch, counters, batch);
