@@ -123,6 +123,9 @@ class _StepPlan:
         self.h_out = torch.zeros(3 * k + 2, dtype=torch.float64).pin_memory()
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
         self.h_flags = torch.zeros(1, dtype=torch.int32).pin_memory()
+        # numpy views of the pinned staging buffers (the per-step host path)
+        self.h_in_np, self.h_idx_np = self.h_in.numpy(), self.h_idx.numpy()
+        self.h_out_np, self.h_flags_np = self.h_out.numpy(), self.h_flags.numpy()
         self.norm = torch.zeros(1, dtype=torch.float64, device=dev)
         on_rows = 2 * k if self.double else k
         self.on_bind = online.binding(on_rows)
@@ -262,6 +265,10 @@ class _StepPlan:
                       self.grad_clip, self.norm.data_ptr())
 
     def run(self, use_graph: bool) -> None:
+        if use_graph and self.graph is not None:        # hot path: one graph launch
+            _CUDAGraph_replay(self.graph)
+            self.calls += 1
+            return
         torch = _lib.require_cuda()
         if use_graph and self.graph is None and self.calls >= 1:
             g = torch.cuda.CUDAGraph()
@@ -283,6 +290,18 @@ _PLANS: dict = {}
 USE_GRAPH = os.environ.get("DQN_B200_GRAPH", "1") != "0"
 
 
+def _CUDAGraph_replay(g) -> None:
+    # torch.cuda.CUDAGraph.replay without the Python wrapper (a few us per call)
+    type(g).__mro__[1].replay(g)
+
+
+def _device_sync() -> None:
+    # the learner's stream work is all this process has on the device; a plain
+    # cudaDeviceSynchronize skips torch's Python stream/device lookups
+    import torch
+    torch._C._cuda_synchronize()
+
+
 def _plan_for(online, target, memory, optimizer, config) -> _StepPlan:
     key = (id(online), id(target), id(memory), id(optimizer), int(config.batch_size),
            bool(getattr(config, "double", True)), float(config.gamma), _td_flags(config),
@@ -298,19 +317,18 @@ def learn_step_enqueue(plan: _StepPlan, step: int, rng: np.random.Generator) -> 
     """Stage this step's draws and launch the update without waiting."""
     k = plan.k
     if plan.per:
-        hin = plan.h_in.numpy()
+        hin = plan.h_in_np
         hin[:k] = rng.random(k)
         hin[k] = plan.memory.beta(step)
     else:
-        plan.h_idx.numpy()[:] = rng.integers(0, plan.ring.size, size=k)
+        plan.h_idx_np[:] = rng.integers(0, plan.ring.size, size=k)
     plan.run(USE_GRAPH)
 
 
 def learn_step_collect(plan: _StepPlan) -> TdResult:
-    torch = _lib.require_cuda()
-    torch.cuda.current_stream().synchronize()
+    _device_sync()
     k = plan.k
-    f = int(plan.h_flags.numpy()[0])
+    f = int(plan.h_flags_np[0])
     if f:
         plan.flags.zero_()
         if f & _lib.FLAG_ZERO_TOTAL:
@@ -323,7 +341,7 @@ def learn_step_collect(plan: _StepPlan) -> TdResult:
             raise ValueError("priority must be finite and >= 0")
         if f & _lib.FLAG_NONFINITE_GRAD:
             raise NonFiniteError("non-finite gradient; step aborted")
-    h = plan.h_out.numpy()
+    h = plan.h_out_np
     plan.online._set_current(plan.on_view, _GRAD)
     plan.target._set_current(plan.tg_bind, _FORWARD)
     return TdResult(targets=h[:k].copy(), td_errors=h[k:2 * k].copy(), losses=h[2 * k:3 * k].copy())
