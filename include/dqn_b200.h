@@ -225,6 +225,13 @@ int dqn_td_loss(void *stream, const float *q_online, const float *q_next_online,
 int dqn_rmsprop_step(void *stream, float *w, float *g, float *acc, int64_t n,
                      float lr, float rho, float one_minus_rho, float eps, int32_t *flags);
 
+/* The update of dqn_rmsprop_step without the finiteness scan, for gradients
+ * whose producers raised DQN_FLAG_NONFINITE_GRAD as they wrote them
+ * (dqn_net_layer phase 2 with a flag word, dqn_head_td): skipped on any error
+ * flag, exactly as dqn_rmsprop_step. */
+int dqn_rmsprop_apply(void *stream, float *w, float *g, float *acc, int64_t n, float lr,
+                      float rho, float one_minus_rho, float eps, int32_t *flags);
+
 /* clip_gradients (optim.py:61-75): fp64 global L2 norm into *norm_out; if
  * norm > max_norm, g *= f32(max_norm / norm). */
 int dqn_clip_gradients(void *stream, float *g, int64_t n, double max_norm, double *norm_out);

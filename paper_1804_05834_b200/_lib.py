@@ -79,6 +79,7 @@ _SIGS = {
     "dqn_td_loss": ([vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, f64, i32, vp, vp, vp, vp, vp],
                     C.c_int),
     "dqn_rmsprop_step": ([vp, vp, vp, vp, i64, f32, f32, f32, f32, vp], C.c_int),
+    "dqn_rmsprop_apply": ([vp, vp, vp, vp, i64, f32, f32, f32, f32, vp], C.c_int),
     "dqn_clip_gradients": ([vp, vp, i64, f64, vp], C.c_int),
     "dqn_sync_target": ([vp, vp, vp, i64], C.c_int),
 }

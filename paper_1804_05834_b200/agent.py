@@ -152,6 +152,7 @@ class _StepPlan:
         if self.xt is not None:
             self.on_view.struct.xt = self.xt.data_ptr()
         self.side = torch.cuda.Stream()
+        self.tree_stream = torch.cuda.Stream()
         self.graph = None
         self.calls = 0
         self.h2d_bytes = (k + 1) * 8 if self.per else k * 8
@@ -171,16 +172,20 @@ class _StepPlan:
         else:
             self.idx.copy_(self.h_idx, non_blocking=True)
         ring.gather_into(self.idx, k, self.x[:k], self.x[k:], self.a, self.r, self.t)
-        self.enqueue_learn()
-        if self.per:
-            self.memory.update_priorities_dev(self.idx, self.d_out[k:2 * k], k, self.flags)
-        self.opt.enqueue_step(self.flags)
+        # priorities are updated inside enqueue_learn, beside the backward pass
+        self.enqueue_learn(priorities=self.per)
+        if self.grad_clip > 0.0:
+            self.opt.enqueue_step(self.flags)      # clipping rescales: rescan
+        else:
+            # every gradient of the update came from launches that flagged
+            # non-finite values into self.flags as they wrote them
+            self.opt.enqueue_apply(self.flags)
         if io:
             self.h_out.copy_(self.d_out, non_blocking=True)
             self.h_flags.copy_(self.flags, non_blocking=True)
         del torch
 
-    def enqueue_learn(self) -> None:
+    def enqueue_learn(self, priorities: bool = False) -> None:
         """Targets, TD loss, backward and wgrad from the batch already in
         self.x ([s; s']), self.a/r/t and IS weights self.w.
 
@@ -188,7 +193,10 @@ class _StepPlan:
         forward runs beside the online forward, and each layer's wgrad runs
         beside the rest of the dgrad chain as soon as that layer's output
         gradient exists (it has its own scratch / split-K counters); the first
-        layer's wgrad, which has no dgrad beside it, stays on the main stream."""
+        layer's wgrad, which has no dgrad beside it, stays on the main stream.
+        With ``priorities`` the sum-tree update (replay.py:232-241) runs on a
+        third stream as soon as the TD errors exist and joins before the
+        optimizer, which still sees its error flags first."""
         torch = _lib.require_cuda()
         st = _lib.stream_ptr()
         k = self.k
@@ -243,23 +251,32 @@ class _StepPlan:
             first = len(on._units) - 1
         e = ev()
         e.record(s0)
+        e_tree = None
+        if priorities:
+            with torch.cuda.stream(self.tree_stream):
+                self.tree_stream.wait_event(e)
+                self.memory.update_priorities_dev(self.idx, out[k:2 * k], k, self.flags)
+                e_tree = ev()
+                e_tree.record(self.tree_stream)
         for layer in reversed(range(first + 1)):
             if layer == 0:
                 # conv1 has no dgrad: its wgrad takes the main stream (and the
                 # dgrad binding's scratch) instead of queueing behind conv2's
                 if e_xt is not None:
                     s0.wait_event(e_xt)
-                on.layer_into(self.on_view, 0, 2)
+                on.layer_into(self.on_view, 0, 2, self.flags)
                 break
             with torch.cuda.stream(s1):           # wgrad of `layer` once its grad exists
                 s1.wait_event(e)
-                on.layer_into(self.on_wview, layer, 2)
+                on.layer_into(self.on_wview, layer, 2, self.flags)
             on.layer_into(self.on_view, layer, 1)  # dgrad chain continues on s0
             e = ev()
             e.record(s0)
         e_w = ev()
         e_w.record(s1)
         s0.wait_event(e_w)
+        if e_tree is not None:
+            s0.wait_event(e_tree)
         if self.grad_clip > 0.0:
             _lib.call("dqn_clip_gradients", st, on.flat_grads.data_ptr(), on.n_flat,
                       self.grad_clip, self.norm.data_ptr())

@@ -35,6 +35,22 @@ __device__ __forceinline__ void raise_flag(int32_t *flags, int32_t bit) {
   if (flags) atomicOr(flags, bit);
 }
 
+// Gradient producers flag non-finite values as they write them, so an
+// optimizer step that follows only them need not rescan the gradients
+// (dqn_rmsprop_apply; optim.py:38-40 semantics).
+__device__ __forceinline__ void note_grad(int32_t *flags, float v) {
+  if (flags && !isfinite(v)) atomicOr(flags, DQN_FLAG_NONFINITE_GRAD);
+}
+__device__ __forceinline__ void acc_grad(float *g, float s, int32_t *flags) {
+  const float v = __fadd_rn(*g, s);
+  *g = v;
+  note_grad(flags, v);
+}
+__device__ __forceinline__ void note_grad4(int32_t *flags, float4 v) {
+  if (flags && !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w)))
+    atomicOr(flags, DQN_FLAG_NONFINITE_GRAD);
+}
+
 constexpr int kNumSMs = 148;
 
 // Programmatic dependent launch: every kernel of the library is launched with

@@ -208,14 +208,14 @@ __global__ void __launch_bounds__(kHeadCta) head_bwd_wgrad_kernel(const HeadTdAr
     const float s = acc[o];
     if (p.dueling) {
       if (o == 0) {
-        if (f < F) p.gwv[f] = __fadd_rn(p.gwv[f], s); else p.gbv[0] = __fadd_rn(p.gbv[0], s);
+        if (f < F) acc_grad(&p.gwv[f], s, p.flags); else acc_grad(&p.gbv[0], s, p.flags);
       } else {
-        if (f < F) p.gwa[(int64_t)f * NA + o - 1] = __fadd_rn(p.gwa[(int64_t)f * NA + o - 1], s);
-        else p.gba[o - 1] = __fadd_rn(p.gba[o - 1], s);
+        if (f < F) acc_grad(&p.gwa[(int64_t)f * NA + o - 1], s, p.flags);
+        else acc_grad(&p.gba[o - 1], s, p.flags);
       }
     } else {
-      if (f < F) p.gwa[(int64_t)f * NA + o] = __fadd_rn(p.gwa[(int64_t)f * NA + o], s);
-      else p.gba[o] = __fadd_rn(p.gba[o], s);
+      if (f < F) acc_grad(&p.gwa[(int64_t)f * NA + o], s, p.flags);
+      else acc_grad(&p.gba[o], s, p.flags);
     }
   }
 }

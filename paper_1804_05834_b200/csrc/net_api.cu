@@ -14,7 +14,7 @@ int simt_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const fl
 int simt_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
                         const dqn_binding *b);
 int simt_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
-                     const dqn_binding *b);
+                     const dqn_binding *b, int32_t *flags);
 int64_t simt_scratch_floats(const dqn_net_desc *net, int batch);
 int simt_validate(const dqn_net_desc *net);
 bool tc_layer_supported(const dqn_net_desc *net, int l, int phase);
@@ -24,7 +24,7 @@ int tc_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const floa
 int tc_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
                       const dqn_binding *b);
 int tc_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
-                   const dqn_binding *b);
+                   const dqn_binding *b, int32_t *flags);
 
 // tcgen05 trunk for supported geometries unless the descriptor asks for SIMT
 static bool use_tc(const dqn_net_desc *net, int l, int phase) {
@@ -49,10 +49,11 @@ static int layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const
   if (use_tc(net, l, 1)) return tc_layer_backward(st, net, l, params, b);
   return simt_layer_backward(st, net, l, params, b);
 }
+// flags (optional): every written gradient is checked for non-finite values
 static int layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
-                       const dqn_binding *b) {
-  if (use_tc(net, l, 2)) return tc_layer_wgrad(st, net, l, grads, b);
-  return simt_layer_wgrad(st, net, l, grads, b);
+                       const dqn_binding *b, int32_t *flags) {
+  if (use_tc(net, l, 2)) return tc_layer_wgrad(st, net, l, grads, b, flags);
+  return simt_layer_wgrad(st, net, l, grads, b, flags);
 }
 
 namespace {
@@ -145,7 +146,7 @@ extern "C" int dqn_net_wgrad(void *stream, const dqn_net_desc *net, float *grads
   int st = check_binding(net, bind);
   if (st) return st;
   for (int l = net->n_layers - 1; l >= 0; --l) {
-    st = layer_wgrad(as_stream(stream), net, l, grads, bind);
+    st = layer_wgrad(as_stream(stream), net, l, grads, bind, nullptr);
     if (st) return st;
   }
   return DQN_OK;
@@ -163,7 +164,7 @@ extern "C" int dqn_net_layer(void *stream, const dqn_net_desc *net, const float 
   switch (phase) {
     case 0: return layer_forward(as_stream(stream), net, layer, params, bind, flags);
     case 1: return layer_backward(as_stream(stream), net, layer, params, bind);
-    case 2: return layer_wgrad(as_stream(stream), net, layer, grads, bind);
+    case 2: return layer_wgrad(as_stream(stream), net, layer, grads, bind, flags);
     default: set_error("net_layer: bad phase %d", phase); return DQN_ERR_INVALID_ARG;
   }
 }

@@ -271,7 +271,8 @@ wgrad_kernel(const InT *__restrict__ x, const float *__restrict__ dy, float *__r
 // grad += sum_z partial[z]  (fixed order); bias likewise.
 __global__ void wgrad_reduce_kernel(const float *__restrict__ partial,
                                     const float *__restrict__ bpartial, int splits, int64_t RN,
-                                    int N, float *__restrict__ gw, float *__restrict__ gb) {
+                                    int N, float *__restrict__ gw, float *__restrict__ gb,
+                                    int32_t *flags) {
   pdl_begin();   // programmatic dependent launch (common.cuh)
   const int64_t total = RN + N;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -279,12 +280,12 @@ __global__ void wgrad_reduce_kernel(const float *__restrict__ partial,
     if (e < RN) {
       float s = partial[e];
       for (int z = 1; z < splits; ++z) s = __fadd_rn(s, partial[(int64_t)z * RN + e]);
-      gw[e] = __fadd_rn(gw[e], s);
+      acc_grad(&gw[e], s, flags);
     } else {
       const int n = (int)(e - RN);
       float s = bpartial[n];
       for (int z = 1; z < splits; ++z) s = __fadd_rn(s, bpartial[(int64_t)z * N + n]);
-      gb[n] = __fadd_rn(gb[n], s);
+      acc_grad(&gb[n], s, flags);
     }
   }
 }
@@ -389,7 +390,7 @@ constexpr int kHeadRows = 64;
 __global__ void __launch_bounds__(128)
 head_wgrad_kernel(const float *__restrict__ x, const float *__restrict__ dq, int B, int F, int nA,
                   int dueling, float *__restrict__ gwv, float *__restrict__ gbv,
-                  float *__restrict__ gwa, float *__restrict__ gba) {
+                  float *__restrict__ gwa, float *__restrict__ gba, int32_t *flags) {
   pdl_begin();   // programmatic dependent launch (common.cuh)
   __shared__ float xs[kHeadRows][128];
   __shared__ float gs[kHeadRows][kMaxHeadOut];
@@ -431,14 +432,14 @@ head_wgrad_kernel(const float *__restrict__ x, const float *__restrict__ dq, int
     const float s = acc[o];
     if (dueling) {
       if (o == 0) {
-        if (f < F) gwv[f] = __fadd_rn(gwv[f], s); else gbv[0] = __fadd_rn(gbv[0], s);
+        if (f < F) acc_grad(&gwv[f], s, flags); else acc_grad(&gbv[0], s, flags);
       } else {
-        if (f < F) gwa[(int64_t)f * nA + o - 1] = __fadd_rn(gwa[(int64_t)f * nA + o - 1], s);
-        else gba[o - 1] = __fadd_rn(gba[o - 1], s);
+        if (f < F) acc_grad(&gwa[(int64_t)f * nA + o - 1], s, flags);
+        else acc_grad(&gba[o - 1], s, flags);
       }
     } else {
-      if (f < F) gwa[(int64_t)f * nA + o] = __fadd_rn(gwa[(int64_t)f * nA + o], s);
-      else gba[o] = __fadd_rn(gba[o], s);
+      if (f < F) acc_grad(&gwa[(int64_t)f * nA + o], s, flags);
+      else acc_grad(&gba[o], s, flags);
     }
   }
 }
@@ -534,7 +535,7 @@ int launch_fwd(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const flo
 
 template <typename InT>
 int launch_wgrad(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *dy,
-                 float *grads, float *scratch, int batch) {
+                 float *grads, float *scratch, int batch, int32_t *flags) {
   Geo g = geo_of(L);
   const int M = batch * g.OH * g.OW, R = g.fh * g.fw * g.C;
   const int bn = pick_bn(g.N);
@@ -552,7 +553,7 @@ int launch_wgrad(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const f
   DQN_LAUNCH_CHECK("wgrad");
   const int64_t RN = (int64_t)R * g.N;
   launch_k(wgrad_reduce_kernel, (int)std::min<int64_t>((RN + g.N + 255) / 256, 148 * 8), 256, 0, st, 
-      partial, bpartial, splits, RN, g.N, grads + L.w_off, grads + L.b_off);
+      partial, bpartial, splits, RN, g.N, grads + L.w_off, grads + L.b_off, flags);
   DQN_LAUNCH_CHECK("wgrad_reduce");
   return DQN_OK;
 }
@@ -667,7 +668,7 @@ int simt_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const f
 }
 
 int simt_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
-                     const dqn_binding *b) {
+                     const dqn_binding *b, int32_t *flags) {
   const dqn_layer_desc &L = net->layer[l];
   const void *in = (l == 0) ? b->x : b->act[l - 1];
   if (is_head(net, l)) {
@@ -676,13 +677,16 @@ int simt_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *gra
     launch_k(head_wgrad_kernel, (F + 1 + 127) / 128, 128, 0, st, 
         (const float *)in, b->dact[l], b->batch, F, L.out_c, duel,
         duel ? grads + L.w_off : nullptr, duel ? grads + L.b_off : nullptr,
-        duel ? grads + L.w2_off : grads + L.w_off, duel ? grads + L.b2_off : grads + L.b_off);
+        duel ? grads + L.w2_off : grads + L.w_off, duel ? grads + L.b2_off : grads + L.b_off,
+        flags);
     DQN_LAUNCH_CHECK("head_wgrad");
     return DQN_OK;
   }
   if (l == 0 && net->input_u8)
-    return launch_wgrad<uint8_t>(st, L, (const uint8_t *)in, b->dact[l], grads, b->scratch, b->batch);
-  return launch_wgrad<float>(st, L, (const float *)in, b->dact[l], grads, b->scratch, b->batch);
+    return launch_wgrad<uint8_t>(st, L, (const uint8_t *)in, b->dact[l], grads, b->scratch,
+                                 b->batch, flags);
+  return launch_wgrad<float>(st, L, (const float *)in, b->dact[l], grads, b->scratch, b->batch,
+                             flags);
 }
 
 int64_t simt_scratch_floats(const dqn_net_desc *net, int batch) {

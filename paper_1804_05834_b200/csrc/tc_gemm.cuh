@@ -314,6 +314,7 @@ struct Gather {
 // Policies derive from this; it supplies the B gather form a policy does not
 // use (never called: the Gather uses the form of its layout).
 struct PolBase {
+  __device__ void note_bias(float) const {}      // BIAS_FROM_B: the written bias gradient
   __device__ int b_koff(int) const { return 0; }
   __device__ float4 b_ld(long long, int) const { return make_float4(0.f, 0.f, 0.f, 0.f); }
   __device__ void b4(long long, int, int, float4 (&)[4]) const {}
@@ -625,9 +626,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
         for (int kc = 0; kc < kKc; ++kc)
           if (g + kc > 0) s = __fadd_rn(s, bias_red[g][threadIdx.x][kc]);
       const int n = n0 + threadIdx.x;
-      if (!SPLITK)
+      if (!SPLITK) {
         p.bias_out[n] = __fadd_rn(p.bias_out[n], s);
-      else
+        p.note_bias(p.bias_out[n]);
+      } else
         p.bias_partial[(int64_t)zs * p.N + n] = s;
     }
   }
@@ -720,6 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
         for (int zz = 1; zz < ks; ++zz)
           s = __fadd_rn(s, __ldcg(p.bias_partial + (int64_t)zz * p.N + n));
         p.bias_out[n] = __fadd_rn(p.bias_out[n], s);
+        p.note_bias(p.bias_out[n]);
       }
       // the last reducer to finish resets the tile's counters for the next launch
       __syncthreads();

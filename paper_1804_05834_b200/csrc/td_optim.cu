@@ -187,6 +187,23 @@ extern "C" int dqn_rmsprop_step(void *stream, float *w, float *g, float *acc, in
   return DQN_OK;
 }
 
+// The apply kernel alone: for gradients whose producers flagged non-finite
+// values as they wrote them (dqn_net_layer phase 2 with flags, dqn_head_td);
+// the step is skipped on any error flag exactly as in dqn_rmsprop_step.
+extern "C" int dqn_rmsprop_apply(void *stream, float *w, float *g, float *acc, int64_t n,
+                                 float lr, float rho, float one_minus_rho, float eps,
+                                 int32_t *flags) {
+  DQN_CHECK_ARG(w && g && acc && flags && n >= 0, "rmsprop: bad args");
+  DQN_CHECK_ARG(((uintptr_t)w | (uintptr_t)g | (uintptr_t)acc) % 16 == 0,
+                "rmsprop: buffers must be 16-byte aligned");
+  if (n == 0) return DQN_OK;
+  const int blocks4 = (int)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, 148 * 4));
+  launch_k(rms_apply_kernel, blocks4, 256, 0, as_stream(stream), w, g, acc, n, lr, rho,
+           one_minus_rho, eps, flags);
+  DQN_LAUNCH_CHECK("rms_apply");
+  return DQN_OK;
+}
+
 extern "C" int dqn_clip_gradients(void *stream, float *g, int64_t n, double max_norm,
                                   double *norm_out) {
   DQN_CHECK_ARG(g && norm_out && n >= 0, "clip: bad args");

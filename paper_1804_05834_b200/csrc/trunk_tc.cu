@@ -241,6 +241,7 @@ struct WgradPol : tc::PolBase {
   static constexpr int BN = BN_;
   const InT *x;
   const uint8_t *xt;              // optional transposed im2col [M][K] (uint8 input)
+  int32_t *flags;                 // non-finite gradients are flagged as written (or nullptr)
   const float *dy;
   float *grad, *partial;
   float *bias_out, *bias_partial;
@@ -296,7 +297,9 @@ struct WgradPol : tc::PolBase {
     o.x = __fadd_rn(o.x, v.x); o.y = __fadd_rn(o.y, v.y);
     o.z = __fadd_rn(o.z, v.z); o.w = __fadd_rn(o.w, v.w);
     st4(gp, o);
+    note_grad4(flags, o);
   }
+  __device__ void note_bias(float b) const { note_grad(flags, b); }
 };
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -444,8 +447,10 @@ inline void wgrad_split(int M, int N, int K, int bn, int &klen, int &splits) {
 
 template <typename InT, int BN>
 int wgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const uint8_t *xt,
-                 const float *dy, float *grads, float *scratch, int *counters, int batch) {
+                 const float *dy, float *grads, float *scratch, int *counters, int batch,
+                 int32_t *flags) {
   WgradPol<InT, BN> p{};
+  p.flags = flags;
   p.counters = counters;
   p.x = x;
   p.dy = dy;
@@ -466,10 +471,13 @@ int wgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const u
 
 template <typename InT>
 int wgrad_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const uint8_t *xt,
-                   const float *dy, float *grads, float *scratch, int *counters, int batch) {
+                   const float *dy, float *grads, float *scratch, int *counters, int batch,
+                   int32_t *flags) {
   const int N = L.out_c;
-  if (N == 32) return wgrad_launch<InT, 32>(st, L, x, xt, dy, grads, scratch, counters, batch);
-  if (N % 64 == 0) return wgrad_launch<InT, 64>(st, L, x, xt, dy, grads, scratch, counters, batch);
+  if (N == 32)
+    return wgrad_launch<InT, 32>(st, L, x, xt, dy, grads, scratch, counters, batch, flags);
+  if (N % 64 == 0)
+    return wgrad_launch<InT, 64>(st, L, x, xt, dy, grads, scratch, counters, batch, flags);
   return DQN_ERR_UNSUPPORTED;
 }
 
@@ -549,14 +557,14 @@ int tc_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const flo
 }
 
 int tc_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
-                   const dqn_binding *b) {
+                   const dqn_binding *b, int32_t *flags) {
   const dqn_layer_desc &L = net->layer[l];
   const void *in = (l == 0) ? b->x : b->act[l - 1];
   if (l == 0 && net->input_u8)
     return wgrad_dispatch<uint8_t>(st, L, (const uint8_t *)in, b->xt, b->dact[l], grads,
-                                    b->scratch, counters_of(b), b->batch);
+                                    b->scratch, counters_of(b), b->batch, flags);
   return wgrad_dispatch<float>(st, L, (const float *)in, nullptr, b->dact[l], grads, b->scratch,
-                                counters_of(b), b->batch);
+                                counters_of(b), b->batch, flags);
 }
 
 

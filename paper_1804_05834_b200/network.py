@@ -290,11 +290,13 @@ class Network:
             self._views[key] = v
         return v
 
-    def layer_into(self, bind: _Bind, layer: int, phase: int) -> None:
-        """One phase (0 fwd, 1 bwd to the layer's input, 2 wgrad) of one layer."""
+    def layer_into(self, bind: _Bind, layer: int, phase: int, flags=None) -> None:
+        """One phase (0 fwd, 1 bwd to the layer's input, 2 wgrad) of one layer;
+        ``flags`` (default: the network's) receives non-finite outputs and,
+        for wgrad, non-finite gradients as they are written."""
         _lib.call("dqn_net_layer", _lib.stream_ptr(), C.byref(self.desc_for(bind.x)),
                   self.flat_values.data_ptr(), self.flat_grads.data_ptr(), C.byref(bind.struct),
-                  layer, phase, self._flags.data_ptr())
+                  layer, phase, (self._flags if flags is None else flags).data_ptr())
 
     def desc_for(self, x):
         import torch
