@@ -284,14 +284,24 @@ struct Gather {
           bsum[i][0] = __fadd_rn(bsum[i][0], __fadd_rn(__fadd_rn(v[i][0].x, v[i][0].y),
                                                        __fadd_rn(v[i][0].z, v[i][0].w)));
       } else {
+        float4 c[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float4 c = make_float4(comp(v[i][0], j), comp(v[i][1], j), comp(v[i][2], j),
-                                       comp(v[i][3], j));
-          store_split(tile + soff[i] + 16 * j, piece_stride, c, pieces);   // rows row..row+3
+          c[j] = make_float4(comp(v[i][0], j), comp(v[i][1], j), comp(v[i][2], j),
+                             comp(v[i][3], j));                     // row row + j
           if (bias)
-            bsum[i][j] =
-                __fadd_rn(bsum[i][j], __fadd_rn(__fadd_rn(c.x, c.y), __fadd_rn(c.z, c.w)));
+            bsum[i][j] = __fadd_rn(bsum[i][j], __fadd_rn(__fadd_rn(c[j].x, c[j].y),
+                                                         __fadd_rn(c[j].z, c[j].w)));
+        }
+        // Store the four chunks in a lane-rotated order: at each store the
+        // warp's rows then cover all 8 rows of a core matrix (row % 8), so the
+        // 16-byte stores hit all 32 banks (4 wavefronts instead of 16).
+        const int rot = (int)(soff[i] >> 7) & 3;          // (row / 8) % 4
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int j = (t + rot) & 3;
+          const float4 cj = (j & 2) ? ((j & 1) ? c[3] : c[2]) : ((j & 1) ? c[1] : c[0]);
+          store_split(tile + soff[i] + 16 * j, piece_stride, cj, pieces);
         }
       }
     }
@@ -370,7 +380,8 @@ struct Plan {
 constexpr int kTraceCtas = 8192;
 __device__ unsigned long long g_trace[kTraceCtas * 28];
 __device__ unsigned int g_trace_n;
-__device__ int g_skip;        // diagnostic: 1 = no MMAs, 2 = no global loads, 4 = no operand stores
+__device__ int g_skip;        // diagnostic: 1 = no MMAs, 2 = no global loads, 4 = no operand stores,
+                              // 8 = no A stores to TMEM, 16 = no B stores to smem
 #define TC_SKIP(bit) (g_skip & (bit))
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -503,17 +514,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
         // A: hi (= the values) and lo pieces into this stage's TMEM columns
         const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + acol0 +
                             (uint32_t)(s * PL::A_COLS + (BK / 2) * khalf);
+        if (!TC_SKIP(8)) {
 #pragma unroll
-        for (int h = 0; h < AR; ++h) {
-          tmem_st16(ta + 16 * h, av[h]);
-          if (NA > 1) {
-            float lo[16];
+          for (int h = 0; h < AR; ++h) {
+            tmem_st16(ta + 16 * h, av[h]);
+            if (NA > 1) {
+              float lo[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) lo[j] = tf32_lo(av[h][j]);
-            tmem_st16(ta + BK + 16 * h, lo);
+              for (int j = 0; j < 16; ++j) lo[j] = tf32_lo(av[h][j]);
+              tmem_st16(ta + BK + 16 * h, lo);
+            }
           }
         }
-        gb.store(bv, sbase + s * B_BYTES, BN * 16, NB, want_bias);
+        if (!TC_SKIP(16)) gb.store(bv, sbase + s * B_BYTES, BN * 16, NB, want_bias);
         tmem_wait_st();
       }
       fence_proxy_async();
