@@ -333,6 +333,7 @@ def _plan_for(online, target, memory, optimizer, config) -> _StepPlan:
 def learn_step_enqueue(plan: _StepPlan, step: int, rng: np.random.Generator) -> None:
     """Stage this step's draws and launch the update without waiting."""
     k = plan.k
+    plan.h_flags_np[0] = _SENTINEL      # overwritten by the update's last copy
     if plan.per:
         hin = plan.h_in_np
         hin[:k] = rng.random(k)
@@ -342,8 +343,28 @@ def learn_step_enqueue(plan: _StepPlan, step: int, rng: np.random.Generator) -> 
     plan.run(USE_GRAPH)
 
 
-def learn_step_collect(plan: _StepPlan) -> TdResult:
+_POLL_SPINS = 200_000          # ~20-50 ms of polling, then a blocking synchronize
+
+
+def _wait_result(plan: _StepPlan) -> None:
+    """The graph's last node copies the flag word to pinned host memory; the
+    host set it to a sentinel before the launch, so polling it observes the
+    end of the update (the TdResult copy precedes it on the same stream)
+    a few microseconds sooner than cudaDeviceSynchronize wakes up.  Errors
+    and slow steps fall through to the synchronize, which raises."""
+    hf = plan.h_flags_np
+    if plan.graph is not None and USE_GRAPH:
+        for _ in range(_POLL_SPINS):
+            if hf[0] != _SENTINEL:
+                return
     _device_sync()
+
+
+_SENTINEL = -(1 << 30)
+
+
+def learn_step_collect(plan: _StepPlan) -> TdResult:
+    _wait_result(plan)
     k = plan.k
     f = int(plan.h_flags_np[0])
     if f:
