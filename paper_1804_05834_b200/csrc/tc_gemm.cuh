@@ -199,6 +199,30 @@ __device__ __forceinline__ void chunk_coords(int c, int &row, int &k) {
   k = kc * 4;
 }
 
+// thread-block cluster helpers (split-K reduced through distributed smem)
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_addr(uint32_t local, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float ld_dsmem(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ float comp(const float4 &v, int j) {
   return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
 }
@@ -396,7 +420,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 template <class Pol>
-__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const int launch_id) {
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const int launch_id,
+                                                               const int cluster_ks) {
   using PL = Plan<Pol>;
   constexpr int nacc = kNacc;
   constexpr int BN = Pol::BN, STAGES = PL::STAGES, NA = PL::NA, NB = PL::NB, RB = PL::RB;
@@ -623,10 +648,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
       const float4 v = *reinterpret_cast<const float4 *>(&stage[rr * ES + c4 * 4]);
       if (!SPLITK)
         p.final4(m, n, v, zp);
-      else
+      else if (!cluster_ks)
         *reinterpret_cast<float4 *>(part + ((int64_t)zs * p.M + m) * p.N + n) = v;
     }
   }
+  __shared__ float bias_cl[Pol::BIAS_FROM_B ? BN : 1];     // cluster split-K: this CTA's bias sums
   // bias gradients folded into the B gather: column sums of this CTA's slice
   if constexpr (Pol::BIAS_FROM_B) if (blockIdx.x == 0) {
     if (producer) gb.dump_bias(bias_red[group]);
@@ -642,11 +668,53 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
       if (!SPLITK) {
         p.bias_out[n] = __fadd_rn(p.bias_out[n], s);
         p.note_bias(p.bias_out[n]);
-      } else
+      } else if (cluster_ks) {
+        bias_cl[threadIdx.x] = s;
+      } else {
         p.bias_partial[(int64_t)zs * p.N + n] = s;
+      }
     }
   }
   TC_MARK(3)
+  // split-K across a thread-block cluster (cluster_ks = splits <= 8 along z):
+  // every rank holds its partial tile in its staging smem; rank r sums rows
+  // [r*BM/ks, ...) over ranks 0..ks-1 in order through distributed shared
+  // memory (the global path's order: identical results) and runs the epilogue
+  if (SPLITK && cluster_ks) {
+    cluster_sync();                              // all ranks' partials staged
+    const int rows = (BM + ks - 1) / ks, r0 = zs * rows, r1 = min(BM, r0 + rows);
+    for (int idx = r0 * C4 + threadIdx.x; idx < r1 * C4; idx += kThreads) {
+      const int rr = idx / C4, c4 = idx - rr * C4;
+      const int m = m0 + rr, n = n0 + c4 * 4;
+      if (m < p.M && n < p.N) {
+        const uint32_t la = smem_u32(&stage[rr * ES + c4 * 4]);
+        float4 t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < ks) t[q] = ld_dsmem4(dsmem_addr(la, q));
+        float4 acc = t[0];
+#pragma unroll
+        for (int q = 1; q < 8; ++q)
+          if (q < ks) {
+            acc.x = __fadd_rn(acc.x, t[q].x);
+            acc.y = __fadd_rn(acc.y, t[q].y);
+            acc.z = __fadd_rn(acc.z, t[q].z);
+            acc.w = __fadd_rn(acc.w, t[q].w);
+          }
+        p.final4(m, n, acc, zp);
+      }
+    }
+    if constexpr (Pol::BIAS_FROM_B)
+      if (blockIdx.x == 0 && zs == 0 && threadIdx.x < BN && n0 + (int)threadIdx.x < p.N) {
+        const uint32_t la = smem_u32(&bias_cl[threadIdx.x]);
+        float s = ld_dsmem(dsmem_addr(la, 0));
+        for (int q = 1; q < ks; ++q) s = __fadd_rn(s, ld_dsmem(dsmem_addr(la, q)));
+        const int n = n0 + threadIdx.x;
+        p.bias_out[n] = __fadd_rn(p.bias_out[n], s);
+        p.note_bias(p.bias_out[n]);
+      }
+    cluster_sync();                              // peers' smem read by everyone
+  } else
   // split-K fixup: the last R CTAs to arrive at a tile each sum a slice of its
   // rows over every split's partial in split order (deterministic whichever
   // CTAs arrive last) and run the epilogue on it.  Reducers other than the
@@ -784,6 +852,17 @@ inline int smem_bytes() {
   return Plan<Pol>::BYTES;
 }
 
+// Opt-in (DQN_B200_CLUSTER_SPLITK=1): each kernel alone is faster, but in the
+// learner's two-stream graph the GPC-level placement of clusters costs more
+// than it saves (measured: ~5360 vs ~5430 updates/s).
+inline bool cluster_splitk_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("DQN_B200_CLUSTER_SPLITK");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <class Pol>
 int launch(cudaStream_t st, const Pol &p, int splits, const char *what) {
   const int bytes = smem_bytes<Pol>();
@@ -803,7 +882,29 @@ int launch(cudaStream_t st, const Pol &p, int splits, const char *what) {
 #ifdef DQN_TC_TRACE
   launch_id = next_launch_seq();
 #endif
-  launch_k(tc_gemm_kernel<Pol>, grid, kThreads, bytes, st, p, launch_id);
+  // splits of one tile form a thread-block cluster (<= 8, portable) and are
+  // reduced through distributed shared memory; more splits use the global
+  // partials and the last-arrivals fixup
+  // (only with slack in the grid: clusters are placed within a GPC, so a
+  // near-full grid of clusters fragments into a second wave)
+  const int64_t ctas = (int64_t)grid.x * grid.y * grid.z;
+  const int cks = (p.ksplits > 1 && p.ksplits <= 8 && ctas <= 128 && cluster_splitk_enabled())
+                      ? p.ksplits : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = cks ? cks : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = cks ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, tc_gemm_kernel<Pol>, p, launch_id, cks);
   DQN_LAUNCH_CHECK(what);
   return DQN_OK;
 }
