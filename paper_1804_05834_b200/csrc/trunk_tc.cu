@@ -267,17 +267,28 @@ struct WgradPol : tc::PolBase {
       return;
     }
     const int P = g.OH * g.OW;
-    int img = pix / P, p = pix - img * P;
+    const int img = pix / P, p = pix - img * P;
     int oy = p / g.OW, ox = p - oy * g.OW;
-    const InT *src = x + roff;
+    // incremental walk over the window bases (one add per pixel)
+    const InT *src = x + roff +
+                     (((long long)img * g.H + (long long)oy * g.sh) * g.W + (long long)ox * g.sw) * g.C;
+    const long long step = (long long)g.sw * g.C;
+    const long long row_jump = ((long long)g.sh * g.W - (long long)(g.OW - 1) * g.sw) * g.C;
+    const long long img_jump = ((long long)g.H * g.W - (long long)(g.OH - 1) * g.sh * g.W -
+                                (long long)(g.OW - 1) * g.sw) * g.C;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const long long base =
-          (((long long)img * g.H + (long long)oy * g.sh) * g.W + (long long)ox * g.sw) * g.C;
-      v[i] = pix + i < ke ? (float)__ldg(src + base) : 0.f;
+      v[i] = pix + i < ke ? (float)__ldg(src) : 0.f;
       if (++ox == g.OW) {
         ox = 0;
-        if (++oy == g.OH) { oy = 0; ++img; }
+        if (++oy == g.OH) {
+          oy = 0;
+          src += img_jump;
+        } else {
+          src += row_jump;
+        }
+      } else {
+        src += step;
       }
     }
   }
