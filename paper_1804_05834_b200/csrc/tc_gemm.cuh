@@ -402,7 +402,7 @@ struct Plan {
 // per-CTA record: {ctaid, smid, t_entry, t_setup, t_kloop, t_epilogue, t_exit, nk,
 //                  t_first_store (producer 0), t_first_full (MMA warp), t_last_mma, launch id}
 constexpr int kTraceCtas = 8192;
-__device__ unsigned long long g_trace[kTraceCtas * 28];
+__device__ unsigned long long g_trace[kTraceCtas * 30];
 __device__ unsigned int g_trace_n;
 __device__ int g_skip;        // diagnostic: 1 = no MMAs, 2 = no global loads, 4 = no operand stores,
                               // 8 = no A stores to TMEM, 16 = no B stores to smem
@@ -451,6 +451,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+#ifdef DQN_TC_TRACE
+  unsigned long long t_alloc = 0, t_presync = 0;
+  if (threadIdx.x == 0) t_alloc = gtimer();
+#endif
   if (threadIdx.x == 32) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
@@ -484,6 +488,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
     gb.init([&](int r) { return p.b_row(n0 + r, zp); }, 0);
   }
 
+#ifdef DQN_TC_TRACE
+  if (threadIdx.x == 0) t_presync = gtimer();
+#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -825,8 +832,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
     if (i < kTraceCtas) {
       unsigned int smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      unsigned long long *r = g_trace + 28ull * i;
+      unsigned long long *r = g_trace + 30ull * i;
       for (int j = 0; j < 16; ++j) r[12 + j] = tk_[j];
+      r[28] = t_alloc;
+      r[29] = t_presync;
       r[0] = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
       r[1] = smid;
       for (int j = 0; j < 5; ++j) r[2 + j] = tr_[j];

@@ -626,7 +626,7 @@ extern "C" int dqn_tc_trace(unsigned long long *host, int max_ctas) {
   cudaMemcpyFromSymbol(&n, dqn::tc::g_trace_n, sizeof(n));
   if (n > (unsigned)dqn::tc::kTraceCtas) n = dqn::tc::kTraceCtas;
   if ((int)n > max_ctas) n = max_ctas;
-  if (n) cudaMemcpyFromSymbol(host, dqn::tc::g_trace, 28ull * n * sizeof(unsigned long long));
+  if (n) cudaMemcpyFromSymbol(host, dqn::tc::g_trace, 30ull * n * sizeof(unsigned long long));
   const unsigned int zero = 0;
   cudaMemcpyToSymbol(dqn::tc::g_trace_n, &zero, sizeof(zero));
   return (int)n;

@@ -26,9 +26,9 @@ from paper_1804_05834_b200 import _lib  # noqa: E402
 
 
 def read_trace():
-    buf = (C.c_ulonglong * (8192 * 28))()
+    buf = (C.c_ulonglong * (8192 * 30))()
     n = _lib.lib.dqn_tc_trace(buf, 8192)
-    return np.frombuffer(buf, dtype=np.uint64, count=28 * n).reshape(n, 28).astype(np.int64)
+    return np.frombuffer(buf, dtype=np.uint64, count=30 * n).reshape(n, 30).astype(np.int64)
 
 
 def main():

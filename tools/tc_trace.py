@@ -24,9 +24,9 @@ from paper_1804_05834_b200 import _lib, synth  # noqa: E402
 
 
 def read_trace():
-    buf = (C.c_ulonglong * (8192 * 28))()
+    buf = (C.c_ulonglong * (8192 * 30))()
     n = _lib.lib.dqn_tc_trace(buf, 8192)
-    return np.frombuffer(buf, dtype=np.uint64, count=28 * n).reshape(n, 28).astype(np.int64)
+    return np.frombuffer(buf, dtype=np.uint64, count=30 * n).reshape(n, 30).astype(np.int64)
 
 
 def main(skip=0):
@@ -92,6 +92,10 @@ def main(skip=0):
                     e = (tk[ok, j, :] - t[ok, 3][:, None]) / 1e3
                     parts.append(f"kb{2 * j}: " + "/".join(f"{e[:, c].mean():.2f}" for c in range(4)))
                 print(f"{'':18s} " + "  ".join(parts))
+                al = (t[:, 28] - t[:, 2]) / 1e3
+                ps = (t[:, 29] - t[:, 2]) / 1e3
+                print(f"{'':18s} setup split: tmem alloc done {al.mean():.2f}  pre-sync {ps.mean():.2f}  "
+                      f"after pdl_wait {((t[:, 3] - t[:, 2]) / 1e3).mean():.2f} (us from entry)")
     net.flat_grads.zero_()
 
 
