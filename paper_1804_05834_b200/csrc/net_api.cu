@@ -33,7 +33,7 @@ static bool use_tc(const dqn_net_desc *net, int l, int phase) {
 
 // SIMT and tcgen05 partial buffers share the front of the scratch; the
 // split-K tile-counter table (kTileCounters ints) always sits after both.
-constexpr int64_t kTileCounters = 4096;   // == tc::kMaxTiles
+constexpr int64_t kTileCounters = 16384;   // == tc::kMaxTiles
 static int64_t scratch_need(const dqn_net_desc *net, int batch) {
   const int64_t a = simt_scratch_floats(net, batch), b = tc_scratch_floats(net, batch);
   return (a > b ? a : b) + kTileCounters;

@@ -567,6 +567,99 @@ __global__ void tree_level_kernel(double *__restrict__ nodes, int64_t lo, int64_
     nodes[a] = __dadd_rn(nodes[2 * a], nodes[2 * a + 1]);
 }
 
+// ---- bulk priority update (k >= kBulkK): many CTAs, bit-exact with the
+// sequential reference.  The reference recomputes every ancestor as the sum
+// of its current children, so the final tree equals: final leaf values (last
+// write in batch order wins) + every internal level rebuilt bottom-up.
+constexpr int kBulkK = 4096;
+
+__device__ __forceinline__ bool bulk_value(const int64_t *idx, const double *td, int j,
+                                           int64_t limit, double alpha, double eps, double &v) {
+  const int64_t i = idx[j];
+  if (i < 0 || i >= limit) return false;
+  v = pow(__dadd_rn(fabs(td[j]), eps), alpha);
+  return v >= 0.0 && !isinf(v);
+}
+
+// first invalid position in batch order (index range, then value)
+__global__ void tree_bulk_check_kernel(const int64_t *__restrict__ idx, const double *__restrict__ td,
+                                       int k, const int64_t *__restrict__ limit_p, double alpha,
+                                       double eps, int *__restrict__ first_bad,
+                                       const int32_t *__restrict__ flags) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
+  const int64_t limit = *limit_p;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    double v;
+    if (!bulk_value(idx, td, j, limit, alpha, eps, v)) atomicMin(first_bad, j);
+  }
+}
+
+// winner[leaf] = last batch position writing it (positions before first_bad)
+__global__ void tree_bulk_winner_kernel(const int64_t *__restrict__ idx, int k,
+                                        const int *__restrict__ first_bad, int *__restrict__ winner,
+                                        const int32_t *__restrict__ flags) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
+  if (flags && (*flags & (DQN_FLAG_ZERO_TOTAL | DQN_FLAG_NONFINITE_OUT))) return;
+  const int kk = min(*first_bad, k);           // INT_MAX at rest: no invalid position
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < kk; j += gridDim.x * blockDim.x)
+    atomicMax(winner + idx[j], j);
+}
+
+// the winning position writes its leaf and clears the winner slot
+__global__ void tree_bulk_scatter_kernel(double *__restrict__ nodes, int depth,
+                                         const int64_t *__restrict__ idx,
+                                         const double *__restrict__ td, int k, double alpha,
+                                         double eps, const int *__restrict__ first_bad,
+                                         int *__restrict__ winner,
+                                         const int32_t *__restrict__ flags) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
+  if (flags && (*flags & (DQN_FLAG_ZERO_TOTAL | DQN_FLAG_NONFINITE_OUT))) return;
+  const int kk = min(*first_bad, k);
+  const int64_t base = int64_t(1) << depth;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < kk; j += gridDim.x * blockDim.x) {
+    const int64_t i = idx[j];
+    if (winner[i] == j) {
+      nodes[base + i] = pow(__dadd_rn(fabs(td[j]), eps), alpha);
+      winner[i] = -1;
+    }
+  }
+}
+
+// flags (first invalid position) or max_priority = max(max_priority, max |td| + eps)
+__global__ void tree_bulk_finish_kernel(const int64_t *__restrict__ idx,
+                                        const double *__restrict__ td, int k,
+                                        const int64_t *__restrict__ limit_p, double eps,
+                                        int *__restrict__ first_bad, double *__restrict__ max_p,
+                                        int32_t *flags) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
+  __shared__ double red[32];
+  if (flags && (*flags & (DQN_FLAG_ZERO_TOTAL | DQN_FLAG_NONFINITE_OUT))) {
+    if (threadIdx.x == 0) *first_bad = 0x7fffffff;
+    return;
+  }
+  const int kk = *first_bad;
+  const int t = threadIdx.x;
+  if (kk < k) {
+    if (t == 0) {
+      const int64_t i = idx[kk];
+      raise_flag(flags, (i < 0 || i >= *limit_p) ? DQN_FLAG_INDEX : DQN_FLAG_BAD_PRIORITY);
+      *first_bad = 0x7fffffff;               // reset for the next call
+    }
+    return;                                   // reference raises: max_p untouched
+  }
+  double m = -INFINITY;
+  for (int j = t; j < k; j += blockDim.x) m = fmax(m, __dadd_rn(fabs(td[j]), eps));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((t & 31) == 0) red[t >> 5] = m;
+  __syncthreads();
+  if (t == 0) {
+    double v = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+    if (max_p && v > *max_p) *max_p = v;       // max(self.max_priority, p.max())
+    *first_bad = 0x7fffffff;
+  }
+}
+
 inline int grid_for(int64_t n, int threads, int cap = 148 * 16) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -694,6 +787,47 @@ extern "C" int dqn_tree_update(void *stream, double *nodes, int32_t depth, const
     launch_k(tree_update_small_kernel, 1, ((k + 31) / 32) * 32, 0, as_stream(stream), 
         nodes, depth, size, idx, td, k, alpha, eps, max_p, flags);
     DQN_LAUNCH_CHECK("tree_update_small");
+    return DQN_OK;
+  }
+  // bulk path: process-wide scratch (first_bad + a winner slot per leaf,
+  // allocated outside graph capture and kept at rest: first_bad = INT_MAX,
+  // winner = -1)
+  static int *bulk = nullptr;
+  static int64_t bulk_leaves = 0;
+  cudaStream_t st = as_stream(stream);
+  const int64_t leaves = int64_t(1) << depth;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  if (k >= kBulkK && (bulk_leaves >= leaves || cap == cudaStreamCaptureStatusNone)) {
+    if (bulk_leaves < leaves) {
+      if (bulk) cudaFree(bulk);
+      int stc = cuda_status(cudaMalloc(&bulk, sizeof(int) * (leaves + 1)), "tree_update scratch");
+      if (stc) { bulk = nullptr; bulk_leaves = 0; return stc; }
+      cudaMemsetAsync(bulk + 1, 0xFF, sizeof(int) * leaves, st);       // winner = -1
+      const int big = 0x7fffffff;
+      cudaMemcpyAsync(bulk, &big, sizeof(int), cudaMemcpyHostToDevice, st);
+      cudaStreamSynchronize(st);
+      bulk_leaves = leaves;
+    }
+    int *first_bad = bulk, *winner = bulk + 1;
+    const int g = grid_for(k, 256);
+    launch_k(tree_bulk_check_kernel, g, 256, 0, st, idx, td, k, size, alpha, eps, first_bad,
+             (const int32_t *)flags);
+    DQN_LAUNCH_CHECK("tree_update_bulk_check");
+    launch_k(tree_bulk_winner_kernel, g, 256, 0, st, idx, k, first_bad, winner,
+             (const int32_t *)flags);
+    DQN_LAUNCH_CHECK("tree_update_bulk_winner");
+    launch_k(tree_bulk_scatter_kernel, g, 256, 0, st, nodes, depth, idx, td, k, alpha, eps,
+             first_bad, winner, (const int32_t *)flags);
+    DQN_LAUNCH_CHECK("tree_update_bulk_scatter");
+    for (int l = depth - 1; l >= 0; --l) {
+      const int64_t lo = int64_t(1) << l, hi = int64_t(1) << (l + 1);
+      launch_k(tree_level_kernel, grid_for(hi - lo, 256), 256, 0, st, nodes, lo, hi);
+      DQN_LAUNCH_CHECK("tree_update_bulk_level");
+    }
+    launch_k(tree_bulk_finish_kernel, 1, 1024, 0, st, idx, td, k, size, eps, first_bad, max_p,
+             flags);
+    DQN_LAUNCH_CHECK("tree_update_bulk_finish");
     return DQN_OK;
   }
   launch_k(tree_update_kernel, 1, kTreeThreads, 0, as_stream(stream), nodes, depth, size, 0, idx, td, k,

@@ -359,7 +359,7 @@ struct PolBase {
 // tile); the last reducer resets them, so the table is all-zero between
 // launches (graph-replay safe) and two kernels on different streams with
 // different bindings never share counters.
-constexpr int kMaxTiles = 4096;
+constexpr int kMaxTiles = 16384;
 
 // Shared/tensor memory plan of a policy.
 template <class Pol>

@@ -193,3 +193,50 @@ def test_update_duplicates_last_wins_large_batch(P):
     chk.rebuild()
     assert np.array_equal(chk.nodes, got)
     assert mem.max_priority == ref.max_priority
+
+
+def _bulk_case(P, n, k, seed):
+    mem = _per(P, cap=n)
+    mem.memory._set_size(n)
+    mem.tree.load_leaves(np.ones(n))
+    ref = O.PerReplay(n, (1, 1, 1), 0.6, 0.01)
+    ref.ring.size = n
+    ref.tree.nodes[ref.tree.base:ref.tree.base + n] = 1.0
+    ref.tree.rebuild()
+    rng = np.random.default_rng(seed)
+    idx = rng.integers(0, n, size=k)             # >= 4096: the multi-CTA bulk path
+    td = rng.random(k) * 4
+    return mem, ref, idx, td
+
+
+def test_update_bulk_path_bit_exact_with_duplicates(P):
+    mem, ref, idx, td = _bulk_case(P, n=50_000, k=40_000, seed=8)
+    mem.update_priorities(idx, td)
+    ref.update_priorities(idx, td)
+    got = mem.tree.nodes.cpu().numpy()
+    assert ulp_diff(got[ref.tree.base:], ref.tree.nodes[ref.tree.base:]).max() <= 1
+    chk = O.HeapTree(50_000)
+    chk.nodes[:] = got
+    chk.rebuild()
+    assert np.array_equal(chk.nodes, got)            # every ancestor = sum of children
+    assert mem.max_priority == ref.max_priority
+    # a second bulk call reuses the scratch (winner table back at rest)
+    idx2 = np.random.default_rng(9).integers(0, 50_000, size=8192)
+    td2 = np.random.default_rng(10).random(8192)
+    mem.update_priorities(idx2, td2)
+    ref.update_priorities(idx2, td2)
+    got = mem.tree.nodes.cpu().numpy()
+    assert ulp_diff(got[ref.tree.base:], ref.tree.nodes[ref.tree.base:]).max() <= 1
+
+
+def test_update_bulk_path_partial_update_then_index_error(P):
+    mem, ref, idx, td = _bulk_case(P, n=20_000, k=12_000, seed=11)
+    idx[9000] = 20_000                                # out of range mid-batch
+    max_before = mem.max_priority
+    with pytest.raises(IndexError):
+        mem.update_priorities(idx, td)
+    with pytest.raises(IndexError):
+        ref.update_priorities(idx, td)                # the reference writes [0, 9000) first
+    got = mem.tree.nodes.cpu().numpy()
+    assert ulp_diff(got[ref.tree.base:], ref.tree.nodes[ref.tree.base:]).max() <= 1
+    assert mem.max_priority == max_before             # untouched on the raising call

@@ -1,0 +1,158 @@
+"""Large-batch per-kernel microbenchmarks ("per-kernel
+evidence"): achieved GB/s of the frame gather, the 1M-leaf sum-tree sample
+and update and the RMSprop apply against the measured HBM copy peak, and
+TFLOP/s of every conv-trunk GEMM phase at B = 4096 against the measured
+dense bf16 peak (MEASURED_PEAKS.json).  Device time from CUDA events around
+CUDA-graph replays (no host launch overhead in the number).
+
+usage: python tools/kernel_bench.py [out.json]
+"""
+import json
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1804_05834_b200 as P  # noqa: E402
+from paper_1804_05834_b200 import _lib  # noqa: E402
+
+
+def peaks():
+    try:
+        d = json.load(open(ROOT / "MEASURED_PEAKS.json"))
+        return float(d.get("hbm_gbs", 6562.6)), float(d.get("bf16_tflops", 1652.6))
+    except (OSError, ValueError):
+        return 6562.6, 1652.6
+
+
+def dev_time_us(fn, reps=10, replays=20):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(replays):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / (reps * replays)
+
+
+def main():
+    hbm, bf16 = peaks()
+    out = {"hbm_peak_gbps": hbm, "bf16_peak_tflops": bf16, "kernels": []}
+
+    def add(name, us, bytes_=None, flop=None, note=""):
+        r = {"kernel": name, "us": us, "note": note}
+        if bytes_ is not None:
+            r["algorithmic_bytes"] = bytes_
+            r["gbps"] = bytes_ / (us * 1e-6) / 1e9
+            r["frac_hbm"] = r["gbps"] / hbm
+        if flop is not None:
+            r["algorithmic_flop"] = flop
+            r["tflops"] = flop / (us * 1e-6) / 1e12
+            r["frac_bf16"] = r["tflops"] / bf16
+        out["kernels"].append(r)
+        print(json.dumps(r), flush=True)
+
+    # --- replay ring gather, k = 4096 (1M-slot ring: rows are HBM-resident)
+    cap = int(os.environ.get("CAP", "1000000"))
+    mem = P.PrioritizedReplay(cap, (84, 84, 4), P.PriorityConfig(0.6, 0.01, P.RunConfig().beta_schedule()))
+    mem.fill_synthetic(1, cap)
+    ring = mem.memory
+    k = 4096
+    idx = torch.as_tensor(np.random.default_rng(0).integers(0, cap, k), device="cuda")
+    s = torch.empty((k, 84, 84, 4), dtype=torch.uint8, device="cuda")
+    s2 = torch.empty_like(s)
+    a = torch.empty(k, dtype=torch.int64, device="cuda")
+    r = torch.empty(k, dtype=torch.float64, device="cuda")
+    t = torch.empty(k, dtype=torch.bool, device="cuda")
+    us = dev_time_us(lambda: ring.gather_into(idx, k, s, s2, a, r, t))
+    add("ring_gather k=4096", us, bytes_=2 * 2 * k * 28224 + k * (8 + 8 + 8 + 8 + 1),
+        note="frames read+write, metadata")
+
+    # --- sum-tree sample / update, 1M leaves
+    kq = 1 << 20
+    u = torch.rand(kq, dtype=torch.float64, device="cuda")
+    beta = torch.full((1,), 0.4, dtype=torch.float64, device="cuda")
+    qi = torch.empty(kq, dtype=torch.int64, device="cuda")
+    qp = torch.empty(kq, dtype=torch.float64, device="cuda")
+    qw = torch.empty(kq, dtype=torch.float64, device="cuda")
+    fl = torch.zeros(1, dtype=torch.int32, device="cuda")
+    us = dev_time_us(lambda: mem.sample_indices(u, kq, beta, qi, qp, qw, fl), reps=3, replays=5)
+    add("tree_sample k=1M", us, bytes_=kq * 200,
+        note=f"{kq / (us * 1e-6) / 1e6:.0f} M samples/s; 200 B/query algorithmic (20 nodes + leaf + u, idx/P/w out)")
+    for kk in (32, 4096, 1 << 20):
+        ui = torch.as_tensor(np.random.default_rng(1).permutation(cap)[:kk], device="cuda")
+        td = torch.rand(kk, dtype=torch.float64, device="cuda")
+        us = dev_time_us(lambda: mem.update_priorities_dev(ui, td, kk, fl), reps=3, replays=5)
+        add(f"tree_update k={kk}", us, bytes_=kk * (20 * 24 + 24),
+            note="leaf write + 20 ancestor read-modify-writes per index (upper bound, shared ancestors)")
+
+    # --- RMSprop apply over the Atari dueling net
+    net = P.build_network("atari", (84, 84, 4), 4, True)
+    P.init_params(net, 1)
+    opt = P.RmsProp(net)
+    net.flat_grads.normal_(0, 1e-3)
+    n = net.n_flat
+    fl.zero_()
+    us = dev_time_us(lambda: opt.enqueue_apply(fl))
+    assert int(fl.item()) == 0, "optimizer skipped (flag set)"
+    add("rms_apply (1,686,693 params)", us, bytes_=5 * 4 * 1686693 + 4 * 1686693,
+        note="w,g,acc read + w,acc write (+ g zeroed)")
+
+    # --- conv-trunk GEMM phases at B = 4096
+    B = 4096
+    x = torch.as_tensor(np.random.default_rng(2).integers(0, 256, (B, 84, 84, 4), dtype=np.uint8),
+                        device="cuda")
+    bind = net.binding(B)
+    bind.x = x
+    bind.struct.x = x.data_ptr()
+    for i in range(len(net._units)):
+        bind.dact[i].normal_(0, 1e-2)
+    desc = net.desc_for(x)
+    net.forward_into(x, bind)
+    torch.cuda.synchronize()
+    import ctypes as C
+    for li, unit in enumerate(net._units):
+        if unit["kind"] == 2:
+            continue
+        for phase in (0, 1, 2):
+            if phase == 1 and li == 0:
+                continue
+            args = (C.byref(desc), net.flat_values.data_ptr(), net.flat_grads.data_ptr(),
+                    C.byref(bind.struct), li, phase, fl.data_ptr())
+            # the stream is resolved inside the call: it must be the capture stream
+            us = dev_time_us(lambda: _lib.call("dqn_net_layer", _lib.stream_ptr(), *args),
+                             reps=3, replays=5)
+            os_ = unit["out_shape"]
+            oh, ow, nn = os_ if len(os_) == 3 else (1, 1, os_[0])
+            h, w, c = unit["in_shape"]
+            fh, fw, sh, sw = unit["geo"]
+            if phase == 1 and (sh > 1 or sw > 1):
+                flop = 2.0 * B * h * w * c * nn * (fh // sh) * (fw // sw)
+            else:
+                flop = 2.0 * B * oh * ow * nn * fh * fw * c
+            add(f"{unit['name']}.{['fwd', 'dgrad', 'wgrad'][phase]} B=4096", us, flop=flop,
+                note="3xTF32 on tcgen05 (implementation FLOPs are 2-3x the algorithmic)")
+    net.flat_grads.zero_()
+    path = sys.argv[1] if len(sys.argv) > 1 else str(ROOT / "gpurun_out" / "kernel_bench.json")
+    json.dump(out, open(path, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
