@@ -319,17 +319,19 @@ class Network:
             raise GeometryError(f"input shape {tuple(x.shape[1:])} != network input {self.input_shape}")
         return x.contiguous()
 
-    def forward_into(self, x, bind: _Bind, upto: int | None = None) -> None:
+    def forward_into(self, x, bind: _Bind, upto: int | None = None, flags=None) -> None:
         """Enqueue the forward phase for a prepared device input (no sync);
-        ``upto`` stops before that layer (the learner's fused head takes over)."""
+        ``upto`` stops before that layer (the learner's fused head takes over);
+        ``flags`` (default: the network's) receives non-finite outputs."""
         bind.x = x
         bind.struct.x = x.data_ptr()
+        fl = self._flags if flags is None else flags
         if upto is None:
             _lib.call("dqn_net_forward", _lib.stream_ptr(), C.byref(self.desc_for(x)),
-                      self.flat_values.data_ptr(), C.byref(bind.struct), self._flags.data_ptr())
+                      self.flat_values.data_ptr(), C.byref(bind.struct), fl.data_ptr())
             return
         for layer in range(upto):
-            self.layer_into(bind, layer, 0)
+            self.layer_into(bind, layer, 0, fl)
 
     def check_output(self) -> None:
         f = int(self._flags.item())
