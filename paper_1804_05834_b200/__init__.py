@@ -11,12 +11,15 @@ device (there is no CPU fallback).
 from . import _lib  # noqa: F401  (loads libdqn_b200.so or raises ImportError)
 from .agent import (TdResult, compute_target_double, compute_target_dqn,  # noqa: F401
                     learn_step)
+from .checkpoint import (Checkpoint, load_checkpoint, load_params_into,  # noqa: F401
+                         save_checkpoint)
 from .config import PRESETS, RunConfig, resolve_config  # noqa: F401
 from .envs import (Catch, Environment, EnvSpec, EnvStep, GridWorld, Preprocessor,  # noqa: F401
                    TabularChain, bilinear_resize, make_env, preprocess_frame)
 from .metrics import MetricRecord, MetricsWriter, RecordCollector  # noqa: F401
-from .errors import (ConfigError, DeepQError, GeometryError, NonFiniteError,  # noqa: F401
-                     PhaseOrderError)
+from .errors import (ArchitectureMismatchError, CheckpointCRCError,  # noqa: F401
+                     CheckpointError, CheckpointMagicError, CheckpointVersionError,
+                     ConfigError, DeepQError, GeometryError, NonFiniteError, PhaseOrderError)
 from .network import (ARCHITECTURES, LayerSpec, Network, build_network,  # noqa: F401
                       init_params, load_params, trunk_layers)
 from .optim import RmsProp, clip_gradients, sync_target  # noqa: F401
@@ -29,7 +32,9 @@ from .trainer import Trainer, evaluate, run_training, select_action  # noqa: F40
 __version__ = "0.1.0"
 
 __all__ = [
-    "ARCHITECTURES", "Catch", "ConfigError", "EnvSpec", "EnvStep", "Environment", "GridWorld",
+    "ARCHITECTURES", "ArchitectureMismatchError", "Catch", "Checkpoint", "CheckpointCRCError",
+    "CheckpointError", "CheckpointMagicError", "CheckpointVersionError", "load_checkpoint",
+    "load_params_into", "save_checkpoint", "ConfigError", "EnvSpec", "EnvStep", "Environment", "GridWorld",
     "MetricRecord", "MetricsWriter", "PRESETS", "Preprocessor", "RecordCollector", "TabularChain",
     "Trainer", "bilinear_resize", "evaluate", "make_env", "preprocess_frame", "resolve_config",
     "run_training", "select_action", "DeepQError", "GeometryError", "LayerSpec",
