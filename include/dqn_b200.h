@@ -239,6 +239,16 @@ int dqn_clip_gradients(void *stream, float *g, int64_t n, double max_norm, doubl
 /* sync_target (optim.py:78-89): bitwise copy of the flat parameter buffer. */
 int dqn_sync_target(void *stream, float *dst, const float *src, int64_t n);
 
+/* preprocess_frame (envs.py:289-311) for n raw uint8 frames [n][h][w][c]
+ * (c = 1 gray or 3 RGB): /255, BT.601 luma, half-pixel bilinear resize to
+ * out_h x out_w, all in fp64 in the reference's operation order, then f32 --
+ * bit-exact.  Output pixel (i, j) of frame f goes to
+ * out[f * frame_stride + (i * out_w + j) * pix_stride] (pix_stride = stack
+ * depth writes one channel of an HWC frame stack). */
+int dqn_preprocess_frames(void *stream, const uint8_t *frames, int64_t n, int h, int w, int c,
+                          int out_h, int out_w, float *out, int64_t frame_stride,
+                          int64_t pix_stride);
+
 #ifdef __cplusplus
 }
 #endif

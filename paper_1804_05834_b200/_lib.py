@@ -82,6 +82,8 @@ _SIGS = {
     "dqn_rmsprop_apply": ([vp, vp, vp, vp, i64, f32, f32, f32, f32, vp], C.c_int),
     "dqn_clip_gradients": ([vp, vp, i64, f64, vp], C.c_int),
     "dqn_sync_target": ([vp, vp, vp, i64], C.c_int),
+    "dqn_preprocess_frames": ([vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, i64,
+                               i64], C.c_int),
 }
 
 for _name, (_args, _res) in _SIGS.items():

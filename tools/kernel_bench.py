@@ -85,6 +85,16 @@ def main():
     add("ring_gather k=4096", us, bytes_=2 * 2 * k * 28224 + k * (8 + 8 + 8 + 8 + 1),
         note="frames read+write, metadata")
 
+    # --- frame preprocessing: 1024 raw 210x160 RGB frames -> 84x84 f32
+    from paper_1804_05834_b200 import frames as FR
+    nf = 1024
+    raw = torch.as_tensor(np.random.default_rng(3).integers(0, 256, (nf, 210, 160, 3), dtype=np.uint8),
+                          device="cuda")
+    pout = torch.empty((nf, 84, 84), dtype=torch.float32, device="cuda")
+    us = dev_time_us(lambda: FR.preprocess_into(raw, (84, 84), pout, 84 * 84, 1))
+    add("preprocess_frames 1024x210x160x3 -> 84x84", us, bytes_=nf * (210 * 160 * 3 + 84 * 84 * 4),
+        note="u8 RGB read once + f32 frame written; fp64 luma + bilinear, bit-exact")
+
     # --- sum-tree sample / update, 1M leaves
     kq = 1 << 20
     u = torch.rand(kq, dtype=torch.float64, device="cuda")
