@@ -355,20 +355,16 @@ def run_ours(args):
     d_draws = torch.as_tensor(draws, device="cuda")
     # a copy of the graph without the host copies: capture enqueue() with
     # device-side inputs
-    g = torch.cuda.CUDAGraph()
-    cs = torch.cuda.Stream()
-    cs.wait_stream(torch.cuda.current_stream())
     saved_in = (plan.h_in, plan.h_idx)
-    with torch.cuda.stream(cs):
-        slot = torch.zeros_like(d_draws[0])
-        if plan.per:
-            plan.h_in = slot
-        else:
-            plan.h_idx = slot
-        with torch.cuda.graph(g, stream=cs):
-            plan.enqueue(io=False)
-    torch.cuda.current_stream().wait_stream(cs)
+    slot = torch.zeros_like(d_draws[0])
+    if plan.per:
+        plan.h_in = slot
+    else:
+        plan.h_idx = slot
+    # same capture stream / node priorities as learn_step's own graph
+    g_keep, g = agent.capture_graph(lambda: plan.enqueue(io=False), plan.capture_stream)
     plan.h_in, plan.h_idx = saved_in
+    sp = torch.cuda.current_stream().cuda_stream
     stream = torch.cuda.current_stream()
     peaks, peak_kind = load_peaks()
     if world > 1:
@@ -380,7 +376,7 @@ def run_ours(args):
         e0.record(stream)
         for s in range(K):
             slot.copy_(d_draws[s], non_blocking=True)
-            g.replay()
+            g.launch(sp)
             if (s + 1) % TARGET_SYNC_UPDATES == 0:
                 P.sync_target(on, tg)
         e1.record(stream)

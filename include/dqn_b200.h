@@ -239,6 +239,14 @@ int dqn_clip_gradients(void *stream, float *g, int64_t n, double max_norm, doubl
 /* sync_target (optim.py:78-89): bitwise copy of the flat parameter buffer. */
 int dqn_sync_target(void *stream, float *dst, const float *src, int64_t n);
 
+/* CUDA-graph plumbing for the learner (no reference counterpart: the
+ * reference runs eagerly).  Instantiate a captured cudaGraph_t, optionally
+ * honouring per-kernel-node priorities (every launch of this library carries
+ * its stream's priority), launch it, destroy it. */
+int dqn_graph_instantiate(void *graph, int use_node_priority, void **exec_out);
+int dqn_graph_launch(void *exec, void *stream);
+int dqn_graph_destroy(void *exec);
+
 /* preprocess_frame (envs.py:289-311) for n raw uint8 frames [n][h][w][c]
  * (c = 1 gray or 3 RGB): /255, BT.601 luma, half-pixel bilinear resize to
  * out_h x out_w, all in fp64 in the reference's operation order, then f32 --

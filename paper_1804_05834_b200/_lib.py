@@ -82,6 +82,9 @@ _SIGS = {
     "dqn_rmsprop_apply": ([vp, vp, vp, vp, i64, f32, f32, f32, f32, vp], C.c_int),
     "dqn_clip_gradients": ([vp, vp, i64, f64, vp], C.c_int),
     "dqn_sync_target": ([vp, vp, vp, i64], C.c_int),
+    "dqn_graph_instantiate": ([vp, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+    "dqn_graph_launch": ([vp, vp], C.c_int),
+    "dqn_graph_destroy": ([vp], C.c_int),
     "dqn_preprocess_frames": ([vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, i64,
                                i64], C.c_int),
 }
@@ -110,8 +113,12 @@ def call(name: str, *args) -> None:
     reference's exception type."""
     st = getattr(lib, name)(*args)
     if st != OK:
-        msg = lib.dqn_last_error().decode(errors="replace")
-        raise _STATUS_EXC.get(st, DeepQError)(f"{name}: {msg}")
+        raise_status(st, name)
+
+
+def raise_status(st: int, name: str) -> None:
+    msg = lib.dqn_last_error().decode(errors="replace")
+    raise _STATUS_EXC.get(st, DeepQError)(f"{name}: {msg}")
 
 
 def require_cuda():

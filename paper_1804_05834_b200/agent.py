@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -151,9 +152,18 @@ class _StepPlan:
         self.xt = torch.empty(nb, dtype=torch.uint8, device=dev) if nb > 0 else None
         if self.xt is not None:
             self.on_view.struct.xt = self.xt.data_ptr()
-        self.side = torch.cuda.Stream()
-        self.tree_stream = torch.cuda.Stream()
+        # DQN_B200_PRIO=1: the capture stream (dgrad chain) and the priority-
+        # update stream run at the highest priority, the side stream (target
+        # forward, wgrads) at the lowest, node priorities honoured by the
+        # graph.  Off by default: measured 1-2 % slower (the update is mostly
+        # SM-time bound and the target forward on the side stream is critical)
+        hi = -8 if USE_PRIORITY else 0
+        self.side = torch.cuda.Stream(priority=0)
+        self.tree_stream = torch.cuda.Stream(priority=hi)
+        self.capture_stream = torch.cuda.Stream(priority=hi)
         self.graph = None
+        self.graph_exec = None
+        self.dev = torch.cuda.current_device()
         self.calls = 0
         self.h2d_bytes = (k + 1) * 8 if self.per else k * 8
         self.d2h_bytes = (3 * k + 2) * 8 + 4
@@ -194,6 +204,8 @@ class _StepPlan:
         beside the rest of the dgrad chain as soon as that layer's output
         gradient exists (it has its own scratch / split-K counters); the first
         layer's wgrad, which has no dgrad beside it, stays on the main stream.
+        conv1's transposed patch operand (im2col_t) is built after the target
+        forward: it is read only by the last wgrad.
         With ``priorities`` the sum-tree update (replay.py:232-241) runs on a
         third stream as soon as the TD errors exist and joins before the
         optimizer, which still sees its error flags first."""
@@ -207,6 +219,9 @@ class _StepPlan:
         e_in.record(s0)
         with torch.cuda.stream(s1):
             s1.wait_event(e_in)
+            tg.forward_into(self.x[k:], self.tg_bind, upto=self.head_layer if self.fused_head else None)
+            e_tg = ev()
+            e_tg.record(s1)
             e_xt = None
             if self.xt is not None:              # read by the last wgrad only
                 self.on_view.struct.x = self.x.data_ptr()
@@ -214,9 +229,6 @@ class _StepPlan:
                           C.byref(self.on_view.struct))
                 e_xt = ev()
                 e_xt.record(s1)
-            tg.forward_into(self.x[k:], self.tg_bind, upto=self.head_layer if self.fused_head else None)
-            e_tg = ev()
-            e_tg.record(s1)
         upto = self.head_layer if self.fused_head else None
         if self.double:
             on.forward_into(self.x, self.on_bind, upto=upto)
@@ -282,22 +294,17 @@ class _StepPlan:
                       self.grad_clip, self.norm.data_ptr())
 
     def run(self, use_graph: bool) -> None:
-        if use_graph and self.graph is not None:        # hot path: one graph launch
-            _CUDAGraph_replay(self.graph)
+        if use_graph and self.graph_exec is not None:   # hot path: one graph launch
+            rc = _GRAPH_LAUNCH(self.graph_exec.ptr, _RAW_STREAM(self.dev))
+            if rc:
+                _lib.raise_status(rc, "dqn_graph_launch")
             self.calls += 1
             return
         torch = _lib.require_cuda()
         if use_graph and self.graph is None and self.calls >= 1:
-            g = torch.cuda.CUDAGraph()
-            s = torch.cuda.Stream()
-            s.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s):
-                with torch.cuda.graph(g, stream=s):
-                    self.enqueue()
-            torch.cuda.current_stream().wait_stream(s)
-            self.graph = g
-        if use_graph and self.graph is not None:
-            self.graph.replay()
+            self.graph, self.graph_exec = capture_graph(self.enqueue, self.capture_stream)
+        if use_graph and self.graph_exec is not None:
+            self.graph_exec.launch(_lib.stream_ptr())
         else:
             self.enqueue()
         self.calls += 1
@@ -305,6 +312,50 @@ class _StepPlan:
 
 _PLANS: dict = {}
 USE_GRAPH = os.environ.get("DQN_B200_GRAPH", "1") != "0"
+USE_PRIORITY = os.environ.get("DQN_B200_PRIO", "0") == "1"
+_GRAPH_LAUNCH = _lib.lib.dqn_graph_launch
+
+
+def _RAW_STREAM(dev: int) -> int:
+    # the caller's current stream (raw pointer) without building a Stream object
+    import torch
+    global _RAW_STREAM
+    _RAW_STREAM = torch._C._cuda_getCurrentRawStream
+    return _RAW_STREAM(dev)
+
+
+class _Exec:
+    """An instantiated graph (cudaGraphExec_t), destroyed with its owner."""
+
+    def __init__(self, graph):
+        self.ptr = C.c_void_p()
+        _lib.call("dqn_graph_instantiate", C.c_void_p(graph.raw_cuda_graph()),
+                  1 if USE_PRIORITY else 0, C.byref(self.ptr))
+        self._fin = weakref.finalize(self, _lib.lib.dqn_graph_destroy, self.ptr)
+
+    @property
+    def _as_parameter_(self):
+        return self.ptr
+
+    def launch(self, stream_ptr: int) -> None:
+        rc = _GRAPH_LAUNCH(self.ptr, stream_ptr)
+        if rc:
+            _lib.raise_status(rc, "dqn_graph_launch")
+
+
+def capture_graph(fn, stream):
+    """Capture ``fn()`` on ``stream`` (its priority becomes the priority of
+    the kernel nodes launched on it) and instantiate the graph honouring
+    node priorities.  Returns (torch CUDAGraph owning the graph and its
+    memory pool, _Exec)."""
+    torch = _lib.require_cuda()
+    g = torch.cuda.CUDAGraph(keep_graph=True)
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+    torch.cuda.current_stream().wait_stream(stream)
+    return g, _Exec(g)
 
 
 def _CUDAGraph_replay(g) -> None:

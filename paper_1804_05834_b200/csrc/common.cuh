@@ -81,6 +81,22 @@ inline bool pdl_enabled() {
   return on;
 }
 
+// Kernel-node priority = the launching stream's priority, so a CUDA graph
+// instantiated with cudaGraphInstantiateFlagUseNodePriority (dqn_graph_
+// instantiate) schedules the learner's critical dgrad chain ahead of the
+// side-stream wgrads when both have CTAs waiting for an SM.
+inline cudaLaunchAttribute priority_attr(cudaStream_t st) {
+  int prio = 0;
+  if (cudaStreamGetPriority(st, &prio) != cudaSuccess) {
+    (void)cudaGetLastError();
+    prio = 0;
+  }
+  cudaLaunchAttribute a;
+  a.id = cudaLaunchAttributePriority;
+  a.val.priority = prio;
+  return a;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                             cudaStream_t st, Args &&...args) {
@@ -89,11 +105,12 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1] = priority_attr(st);
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

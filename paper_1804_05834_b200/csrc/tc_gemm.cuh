@@ -904,15 +904,16 @@ int launch(cudaStream_t st, const Pol &p, int splits, const char *what) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = bytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = 1;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = cks ? cks : 1;
+  attr[1] = priority_attr(st);
+  attr[2].id = cudaLaunchAttributeClusterDimension;
+  attr[2].val.clusterDim.x = 1;
+  attr[2].val.clusterDim.y = 1;
+  attr[2].val.clusterDim.z = cks ? cks : 1;
   cfg.attrs = attr;
-  cfg.numAttrs = cks ? 2 : 1;
+  cfg.numAttrs = cks ? 3 : 2;
   cudaLaunchKernelEx(&cfg, tc_gemm_kernel<Pol>, p, launch_id, cks);
   DQN_LAUNCH_CHECK(what);
   return DQN_OK;

@@ -229,3 +229,28 @@ extern "C" int dqn_sync_target(void *stream, float *dst, const float *src, int64
                                      as_stream(stream)),
                      "sync_target");
 }
+
+// --- CUDA graphs with per-node priorities ---------------------------------
+// torch.cuda.CUDAGraph(keep_graph=True) captures the learner update; the
+// graph is instantiated here with cudaGraphInstantiateFlagUseNodePriority so
+// the kernel-node priorities set by launch_k (= the capturing stream's
+// priority) order CTA dispatch between the critical chain and side streams.
+extern "C" int dqn_graph_instantiate(void *graph, int use_node_priority, void **exec_out) {
+  DQN_CHECK_ARG(graph && exec_out, "graph_instantiate: null pointer");
+  cudaGraphExec_t ex = nullptr;
+  const unsigned long long fl = use_node_priority ? cudaGraphInstantiateFlagUseNodePriority : 0;
+  const int rc = cuda_status(cudaGraphInstantiateWithFlags(&ex, (cudaGraph_t)graph, fl),
+                             "graph_instantiate");
+  if (rc != DQN_OK) return rc;
+  *exec_out = (void *)ex;
+  return DQN_OK;
+}
+
+extern "C" int dqn_graph_launch(void *exec, void *stream) {
+  return cuda_status(cudaGraphLaunch((cudaGraphExec_t)exec, as_stream(stream)), "graph_launch");
+}
+
+extern "C" int dqn_graph_destroy(void *exec) {
+  if (!exec) return DQN_OK;
+  return cuda_status(cudaGraphExecDestroy((cudaGraphExec_t)exec), "graph_destroy");
+}

@@ -36,13 +36,13 @@ print(f"learn_step e2e: {(t1 - t0) / N * 1e6:.1f} us/update")
 st = torch.cuda.current_stream()
 t0 = time.perf_counter()
 for s in range(N):
-    plan.graph.replay()
+    plan.graph_exec.launch(torch.cuda.current_stream().cuda_stream)
     st.synchronize()
 t1 = time.perf_counter()
 print(f"graph.replay + sync: {(t1 - t0) / N * 1e6:.1f} us/update")
 t0 = time.perf_counter()
 for s in range(N):
-    plan.graph.replay()
+    plan.graph_exec.launch(torch.cuda.current_stream().cuda_stream)
 torch.cuda.synchronize()
 t1 = time.perf_counter()
 print(f"graph.replay back-to-back: {(t1 - t0) / N * 1e6:.1f} us/update")
