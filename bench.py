@@ -459,57 +459,103 @@ def run_ours(args):
 
 
 def run_dp(args):
-    """cfg5: data-parallel learner, replay sharded over the ranks (capacity /
-    N each), global stratified PER over shard totals, per-rank batch 32,
-    NCCL gradient all-reduce (paper_1804_05834_b200/dp.py).  value = batch-32
-    learner updates/s summed over the GPUs (= transitions/s / 32)."""
+    """cfg5: the data-parallel learner (dp.DeviceDataParallelLearner): replay
+    sharded over the ranks (capacity / N each, CUDA-IPC shareable), global
+    stratified PER over the shard totals, per-rank batch 32 (global 32 N),
+    frames read from the owners' rings over NVLink, NCCL gradient all-reduce,
+    the whole global update one CUDA graph per rank.  value = batch-32
+    learner updates/s summed over the GPUs (= global updates/s x N =
+    transitions/s / 32), device-timed over graph launches with the uniforms
+    pre-drawn in HBM; e2e = DeviceDataParallelLearner.step with host draws
+    and host results every step."""
     import torch
     import torch.distributed as dist
     import paper_1804_05834_b200 as P
-    from paper_1804_05834_b200 import _lib, dp
+    from paper_1804_05834_b200 import _lib, agent, dp
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if not dist.is_initialized():
+        if "MASTER_ADDR" not in os.environ:             # plain `python bench.py --mode dp`
+            import socket
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                os.environ["MASTER_PORT"] = str(so.getsockname()[1])
+            os.environ["MASTER_ADDR"] = "127.0.0.1"
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl")
     c = CONFIGS["cfg4"]
     cap = (args.capacity or c["capacity"]) // world
     k = args.batch
+    K = k * world
     cfg = P.RunConfig(batch_size=k, double=True, dueling=True, beta_end_step=50_000_000)
     on = P.build_network("atari", (84, 84, 4), 4, True)
     tg = P.build_network("atari", (84, 84, 4), 4, True)
     P.init_params(on, np.random.SeedSequence([1, 3]))          # identical on every rank
     P.sync_target(on, tg)
     opt = P.RmsProp(on, cfg.learning_rate, cfg.rms_decay, cfg.rms_epsilon)
-    mem = P.PrioritizedReplay(cap, (84, 84, 4), P.PriorityConfig(0.6, 0.01, cfg.beta_schedule()))
+    mem = P.PrioritizedReplay(cap, (84, 84, 4), P.PriorityConfig(0.6, 0.01, cfg.beta_schedule()),
+                              shareable=True)
     mem.fill_synthetic(100 + rank, cap)
-    learner = dp.DataParallelLearner(dp.DeviceBackend(on, tg, mem, opt, cfg), k, 0.6, 0.01, "cuda")
+    learner = dp.DeviceDataParallelLearner(on, tg, mem, opt, cfg)
     rng = np.random.default_rng(np.random.SeedSequence([1, 2]))  # common draws on all ranks
     step0 = 50_000
     for s in range(args.warmup):
-        learner.step(rng.random(k * world), mem.beta(step0 + s))
+        learner.step(rng.random(K), mem.beta(step0 + s))
+    assert learner.graph_exec is not None, "data-parallel graph was not captured"
     n0 = _lib.lib.dqn_launch_count()
-    learner.step(rng.random(k * world), mem.beta(step0 + args.warmup))
+    agent.USE_GRAPH = False
+    g_saved = learner.graph_exec
+    learner.graph_exec = None
+    learner.step(rng.random(K), mem.beta(step0 + args.warmup))        # one eager step: count
     launches = int(_lib.lib.dqn_launch_count() - n0)
+    learner.graph_exec = g_saved
+    agent.USE_GRAPH = True
+
+    # --- device-resident loop: pre-drawn inputs in HBM, one graph per update
+    draws = np.empty((args.steps, K + 1))
+    for s in range(args.steps):
+        draws[s, :K] = rng.random(K)
+        draws[s, K] = mem.beta(step0 + 200 + s)
+    d_draws = torch.as_tensor(draws, device="cuda")
+    slot = torch.zeros_like(d_draws[0])
+    saved = learner.h_in
+    learner.h_in = slot
+    g_keep, g = agent.capture_graph(learner.enqueue, learner.plan.capture_stream)
+    learner.h_in = saved
+    sp = torch.cuda.current_stream().cuda_stream
     stream = torch.cuda.current_stream()
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
         e0.record(stream)
-        t0 = time.perf_counter()
         for s in range(args.steps):
-            learner.step(rng.random(k * world), mem.beta(step0 + 100 + s))
+            slot.copy_(d_draws[s], non_blocking=True)
+            g.launch(sp)
             if (s + 1) % TARGET_SYNC_UPDATES == 0:
                 P.sync_target(on, tg)
         e1.record(stream)
         torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-    ms = max(e0.elapsed_time(e1), wall * 1e3)
+    ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = world * args.steps / (ms / 1e3)
+
+    # --- e2e: the public step() with host draws and host results
+    dist.barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for s in range(args.steps):
+        learner.step(rng.random(K), mem.beta(step0 + 400 + s))
+    e3.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e2.elapsed_time(e3)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e = world * args.steps / (float(t.item()) / 1e3)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT + " (batch-32 updates, all GPUs)",
@@ -518,16 +564,18 @@ def run_dp(args):
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (hash-generated u8 frames per shard, random-init nets)",
             "config": {"workload": "cfg5 Dueling+Double+PER data-parallel, replay sharded",
-                       "capacity": cap * world, "global_batch": k * world, "per_gpu_batch": k,
-                       "parallelism": f"dp{world} (sharded PER, NCCL allreduce)"},
+                       "capacity": cap * world, "global_batch": K, "per_gpu_batch": k,
+                       "parallelism": f"dp{world} (sharded PER, peer-ring gather, NCCL allreduce)",
+                       "l2": "1M-slot ring (56 GB) >> L2: sampled rows come from HBM"},
             "transitions_per_sec": value * k,
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 8 * (k * world + 1),
-                    "d2h_bytes_per_step": 8 * 3 * k * world,
-                    "path": "dp.DataParallelLearner.step (host-orchestrated, every step)"},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * (K + 1),
+                    "d2h_bytes_per_step": 8 * 4 * K + 4,
+                    "path": "dp.DeviceDataParallelLearner.step (one graph launch per update)"},
             "gpu_launches": launches * args.steps, "launches_per_step": launches,
             "clocks": clk.summary(), "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
+    learner.close()
     dist.destroy_process_group()
 
 

@@ -239,6 +239,66 @@ int dqn_clip_gradients(void *stream, float *g, int64_t n, double max_norm, doubl
 /* sync_target (optim.py:78-89): bitwise copy of the flat parameter buffer. */
 int dqn_sync_target(void *stream, float *dst, const float *src, int64_t n);
 
+/* ---- data-parallel learner (algorithm in dp.py) --------
+ * N ranks (one per GPU), rank r owns replay shard r (global transition g at
+ * rank g % N, slot g / N) with its own sum tree; K = k * N strata per global
+ * update.  The reference has no distributed mode: each entry restates one
+ * step of a global learn_step (agent.py:91-132, replay.py:215-241) over the
+ * union of the shards. */
+typedef struct dqn_peer_ring {    /* a rank's ring, mapped into this process */
+  const uint8_t *states;
+  const uint8_t *next_states;
+  const int64_t *actions;
+  const double *rewards;
+  const uint8_t *terminals;
+} dqn_peer_ring;
+
+/* out3 = [tree total, ring size, max_priority] of this shard (all_gathered). */
+int dqn_dp_shard_info(void *stream, const double *nodes, const int64_t *size,
+                      const double *max_p, double *out3);
+/* info = N x 3 gathered shard infos; u = K uniforms (same on every rank).
+ * T = totals summed in rank order; q_j = clip((j + u_j) * T / K) as
+ * SumTree.find clips; owner_j = first shard whose prefix mass reaches q_j;
+ * q_local = q_j - prefix[owner_j]; sums = [T, total size, max of max_p].
+ * With table != NULL the owner descent of dqn_dp_descend is fused in (this
+ * rank's tree = nodes/depth). */
+int dqn_dp_route(void *stream, const double *info, int32_t world, const double *u, int32_t K,
+                 int64_t *owner, double *q_local, double *sums, int32_t *flags,
+                 const double *nodes, int32_t depth, int32_t rank, double *table);
+/* table[j] = (leaf index, leaf value) for the strata this rank owns, zeros
+ * elsewhere (all_reduce SUM gives every rank the full table). */
+int dqn_dp_descend(void *stream, const double *nodes, int32_t depth, const int64_t *owner,
+                   const double *q_local, int32_t K, int32_t rank, double *table);
+/* P_j = leaf_j / T, w_j = (size_total * P_j)^-beta / max_j w_j (replay.py:227-229
+ * over the global batch); local_idx[j] = table index; w_mine = this rank's k. */
+int dqn_dp_weights(void *stream, const double *table, const double *sums, const double *beta,
+                   int32_t K, int32_t k, int32_t rank, int64_t *local_idx, double *w_all,
+                   double *w_mine);
+/* This rank's strata [rank k, (rank+1) k) read from the owners' rings
+ * (rings[N], peer mappings; slot = table[j].index): states to x[0..k), next
+ * states to x[k..2k).  With sums != NULL one extra CTA computes the IS
+ * weights of dqn_dp_weights in the same launch. */
+int dqn_dp_gather(void *stream, const dqn_peer_ring *rings, const int64_t *owner,
+                  const double *table, int32_t k, int32_t rank, int64_t slot_bytes, uint8_t *x,
+                  int64_t *actions, double *rewards, uint8_t *terminals, const double *sums,
+                  const double *beta, int32_t K, int64_t *local_idx, double *w_all,
+                  double *w_mine);
+/* The owned strata in global batch order -> idx_c/td_c/*n_c (for
+ * dqn_tree_update_n); max_p = max(max_p, max_j |td_j| + eps) over all K. */
+int dqn_dp_owned(void *stream, const int64_t *owner, const int64_t *local_idx,
+                 const double *td_all, int32_t K, int32_t rank, double eps, int64_t *idx_c,
+                 double *td_c, int32_t *n_c, double *max_p, const int32_t *flags);
+/* dqn_tree_update with the batch length read from device memory (*k_dev <= k_max <= 256). */
+int dqn_tree_update_n(void *stream, double *nodes, int32_t depth, const int64_t *size,
+                      const int64_t *idx, const double *td, int32_t k_max, const int32_t *k_dev,
+                      double alpha, double eps, double *max_p, int32_t *flags);
+/* Process-shareable device memory for replay shards (CUDA IPC). */
+int dqn_dev_alloc(int64_t bytes, void **ptr);
+int dqn_dev_free(void *ptr);
+int dqn_ipc_handle(void *ptr, uint8_t *handle64);
+int dqn_ipc_open(const uint8_t *handle64, void **ptr);
+int dqn_ipc_close(void *ptr);
+
 /* CUDA-graph plumbing for the learner (no reference counterpart: the
  * reference runs eagerly).  Instantiate a captured cudaGraph_t, optionally
  * honouring per-kernel-node priorities (every launch of this library carries

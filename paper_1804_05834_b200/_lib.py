@@ -82,6 +82,21 @@ _SIGS = {
     "dqn_rmsprop_apply": ([vp, vp, vp, vp, i64, f32, f32, f32, f32, vp], C.c_int),
     "dqn_clip_gradients": ([vp, vp, i64, f64, vp], C.c_int),
     "dqn_sync_target": ([vp, vp, vp, i64], C.c_int),
+    "dqn_dp_shard_info": ([vp, vp, vp, vp, vp], C.c_int),
+    "dqn_dp_route": ([vp, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_int, C.c_int, vp],
+                     C.c_int),
+    "dqn_dp_descend": ([vp, vp, C.c_int, vp, vp, C.c_int, C.c_int, vp], C.c_int),
+    "dqn_dp_weights": ([vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, vp], C.c_int),
+    "dqn_dp_gather": ([vp, vp, vp, vp, C.c_int, C.c_int, i64, vp, vp, vp, vp, vp, vp, C.c_int, vp,
+                       vp, vp], C.c_int),
+    "dqn_dp_owned": ([vp, vp, vp, vp, C.c_int, C.c_int, C.c_double, vp, vp, vp, vp, vp], C.c_int),
+    "dqn_tree_update_n": ([vp, vp, C.c_int, vp, vp, vp, C.c_int, vp, C.c_double, C.c_double, vp,
+                           vp], C.c_int),
+    "dqn_dev_alloc": ([i64, C.POINTER(C.c_void_p)], C.c_int),
+    "dqn_dev_free": ([vp], C.c_int),
+    "dqn_ipc_handle": ([vp, vp], C.c_int),
+    "dqn_ipc_open": ([vp, C.POINTER(C.c_void_p)], C.c_int),
+    "dqn_ipc_close": ([vp], C.c_int),
     "dqn_graph_instantiate": ([vp, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
     "dqn_graph_launch": ([vp, vp], C.c_int),
     "dqn_graph_destroy": ([vp], C.c_int),

@@ -195,7 +195,7 @@ class _StepPlan:
             self.h_flags.copy_(self.flags, non_blocking=True)
         del torch
 
-    def enqueue_learn(self, priorities: bool = False) -> None:
+    def enqueue_learn(self, priorities: bool = False, td_hook=None) -> None:
         """Targets, TD loss, backward and wgrad from the batch already in
         self.x ([s; s']), self.a/r/t and IS weights self.w.
 
@@ -264,10 +264,15 @@ class _StepPlan:
         e = ev()
         e.record(s0)
         e_tree = None
-        if priorities:
+        if priorities or td_hook is not None:
+            # ``td_hook`` (the data-parallel learner) replaces the local
+            # priority update with its own work on the TD errors
             with torch.cuda.stream(self.tree_stream):
                 self.tree_stream.wait_event(e)
-                self.memory.update_priorities_dev(self.idx, out[k:2 * k], k, self.flags)
+                if td_hook is not None:
+                    td_hook()
+                else:
+                    self.memory.update_priorities_dev(self.idx, out[k:2 * k], k, self.flags)
                 e_tree = ev()
                 e_tree.record(self.tree_stream)
         for layer in reversed(range(first + 1)):

@@ -1,0 +1,88 @@
+// SumTree.find descent shared by the replay and data-parallel kernels.
+#pragma once
+#include "common.cuh"
+
+namespace dqn {
+
+static __device__ __forceinline__ double sel2(double a, double b, int i) { return i ? b : a; }
+static __device__ __forceinline__ double sel4(const double (&v)[4], int i) {
+  return (i & 2) ? sel2(v[2], v[3], i & 1) : sel2(v[0], v[1], i & 1);
+}
+static __device__ __forceinline__ double sel8(const double (&v)[8], int i) {
+  return (i & 4) ? ((i & 2) ? sel2(v[6], v[7], i & 1) : sel2(v[4], v[5], i & 1))
+                 : ((i & 2) ? sel2(v[2], v[3], i & 1) : sel2(v[0], v[1], i & 1));
+}
+
+// SumTree.find descent for one query mass (replay.py:172-181).  Returns the
+// leaf index; *leaf_value (optional) receives nodes[leaf].
+//
+// Four levels per dependent round trip: the left-child sums of the next four
+// levels below node n are nodes[2n], nodes[4n + {0,2}], nodes[8n + {0,2,4,6}]
+// and nodes[16n + {0,2,..,14}] -- four short contiguous runs -- so all 15 are
+// loaded together and the four compare/subtract steps then run exactly as the
+// reference's per-level loop (same operations, same order).  The last group
+// also loads the right children, which yields the leaf value for free.
+static __device__ __forceinline__ int64_t tree_descend(const double *__restrict__ nodes, int depth,
+                                                double q, double hi,
+                                                double *leaf_value = nullptr) {
+  q = fmin(fmax(q, 1e-300), hi);            // np.clip(q, 1e-300, nextafter(total, 0))
+  int64_t n = 1;
+  int l = 0;
+  double leaf = -1.0;
+  for (; l + 4 <= depth; l += 4) {
+    const bool last = l + 4 == depth;
+    const double c1 = __ldg(nodes + 2 * n);
+    double c2[2], c3[4], c4[8], c4r[8];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) c2[i] = __ldg(nodes + 4 * n + 2 * i);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c3[i] = __ldg(nodes + 8 * n + 2 * i);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c4[i] = __ldg(nodes + 16 * n + 2 * i);
+    if (last && leaf_value) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c4r[i] = __ldg(nodes + 16 * n + 2 * i + 1);
+    }
+    const bool r1 = q > c1;
+    if (r1) q = __dsub_rn(q, c1);                 // q -= left_sum * go_right
+    const int i1 = r1 ? 1 : 0;
+    const double l2 = sel2(c2[0], c2[1], i1);
+    const bool r2 = q > l2;
+    if (r2) q = __dsub_rn(q, l2);
+    const int i2 = 2 * i1 + (r2 ? 1 : 0);
+    const double l3 = sel4(c3, i2);
+    const bool r3 = q > l3;
+    if (r3) q = __dsub_rn(q, l3);
+    const int i3 = 2 * i2 + (r3 ? 1 : 0);
+    const double l4 = sel8(c4, i3);
+    const bool r4 = q > l4;
+    if (r4) q = __dsub_rn(q, l4);
+    n = 16 * n + 2 * i3 + (r4 ? 1 : 0);
+    if (last && leaf_value) leaf = r4 ? sel8(c4r, i3) : l4;
+  }
+  // remaining levels: two per round trip, then one
+  for (; l + 2 <= depth; l += 2) {
+    const double ls = __ldg(nodes + 2 * n);               // nodes[2n]
+    const double lls = __ldg(nodes + 4 * n);              // nodes[4n]   (left-left)
+    const double rls = __ldg(nodes + 4 * n + 2);          // nodes[4n+2] (right-left)
+    const bool r1 = q > ls;
+    if (r1) q = __dsub_rn(q, ls);
+    const int64_t c = 2 * n + (r1 ? 1 : 0);
+    const double ls2 = r1 ? rls : lls;
+    const bool r2 = q > ls2;
+    if (r2) q = __dsub_rn(q, ls2);
+    n = 2 * c + (r2 ? 1 : 0);
+  }
+  for (; l < depth; ++l) {
+    const int64_t left = n << 1;
+    const double ls = __ldg(nodes + left);
+    const bool right = q > ls;
+    if (right) q = __dsub_rn(q, ls);          // q -= left_sum * go_right
+    n = left + (right ? 1 : 0);
+  }
+  if (leaf_value) *leaf_value = leaf >= 0.0 ? leaf : __ldg(nodes + n);
+  return n - (int64_t(1) << depth);
+}
+
+
+}  // namespace dqn

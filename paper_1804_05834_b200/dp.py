@@ -300,3 +300,218 @@ class DeviceBackend(Backend):
 
     def optimizer_step(self) -> None:
         self.opt.step()
+
+
+# ---------------------------------------------------------------------------
+# the device pipeline: one CUDA graph per rank, collectives inside
+# ---------------------------------------------------------------------------
+
+class _PeerRing:
+    """ctypes mirror of dqn_peer_ring (include/dqn_b200.h)."""
+
+    @staticmethod
+    def struct():
+        import ctypes as C
+
+        class S(C.Structure):
+            _fields_ = [("states", C.c_void_p), ("next_states", C.c_void_p),
+                        ("actions", C.c_void_p), ("rewards", C.c_void_p),
+                        ("terminals", C.c_void_p)]
+        return S
+
+
+_RING_FIELDS = ("states", "next_states", "actions", "rewards", "terminals")
+
+
+class DeviceDataParallelLearner:
+    """The sharded learner of this module as a device pipeline (csrc/dp.cu):
+    every step of ``DataParallelLearner.step`` is a fixed-size kernel or NCCL
+    collective, captured once into a CUDA graph per rank and replayed.
+
+    * shard infos: ``all_gather`` of [total, size, max_p] (N x 24 B);
+    * routing, owner descent, the (index, leaf) table ``all_reduce`` (K x 16 B)
+      and the IS weights on the device, identical on every rank;
+    * frames: each rank reads its K/N strata straight from the owners' rings
+      through CUDA IPC mappings (NVLink peer loads in ``dqn_dp_gather``), so
+      no frame bytes go through a collective;
+    * the local update (the single-GPU learner's forward/backward/wgrad
+      graph), gradient ``all_reduce`` (6.7 MB, NCCL), TD ``all_gather``,
+      owner-side priority update in global batch order, flag ``all_reduce``
+      (max) so every rank skips a failed step together, RMSprop.
+
+    ``memory`` must be a ``PrioritizedReplay(..., shareable=True)`` when the
+    world size is above one.  ``step(u, beta)`` takes the K = k * N uniforms
+    from a generator common to all ranks and returns a ``DpStepResult``.
+    """
+
+    def __init__(self, online, target, memory, optimizer, config, group=None):
+        import ctypes as C
+        import torch
+        import torch.distributed as dist
+        from . import _lib, agent, nccl
+        from .replay import PrioritizedReplay
+        if not isinstance(memory, PrioritizedReplay):
+            raise ValueError("the data-parallel learner shards a PrioritizedReplay")
+        self.rank = dist.get_rank(group)
+        self.world = N = dist.get_world_size(group)
+        self.mem, self.on, self.opt = memory, online, optimizer
+        self.k = k = int(config.batch_size)
+        self.K = K = k * N
+        if K > 1024:
+            raise ValueError("global batch above 1024 strata")
+        self.alpha, self.eps = float(memory.config.alpha), float(memory.config.epsilon)
+        self.grad_clip = float(getattr(config, "grad_clip", 0.0))
+        self.plan = agent._StepPlan(online, target, memory, optimizer, config)
+        self.plan.grad_clip = 0.0          # clipping applies to the reduced gradient (below)
+        self.comm = nccl.Communicator(group)
+        # the TD all_gather runs on the priority stream beside the backward
+        # pass: a second communicator keeps its order independent of the
+        # gradient all_reduce on the main stream
+        self.comm_td = nccl.Communicator(group)
+        ring = memory.memory
+        # peer rings: own arrays locally, the others' through IPC mappings
+        own = [getattr(ring, f).data_ptr() for f in _RING_FIELDS]
+        if N > 1:
+            if not ring.shared:
+                raise ValueError("world size > 1 needs PrioritizedReplay(..., shareable=True)")
+            mine = [ring.shared[f].handle() for f in _RING_FIELDS]
+            allh = [None] * N
+            dist.all_gather_object(allh, mine, group=group)
+        S = _PeerRing.struct()
+        table = (S * N)()
+        self._opened = []
+        for r in range(N):
+            if r == self.rank:
+                ptrs = own
+            else:
+                ptrs = []
+                for h in allh[r]:
+                    p = C.c_void_p()
+                    _lib.call("dqn_ipc_open", (C.c_uint8 * 64).from_buffer_copy(h), C.byref(p))
+                    self._opened.append(p)
+                    ptrs.append(p.value)
+            table[r] = S(*ptrs)
+        raw = bytes(table)
+        self.rings = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to("cuda")
+        dev = "cuda"
+        f64 = torch.float64
+        self.h_in = torch.zeros(K + 1, dtype=f64).pin_memory()          # u | beta
+        self.d_in = torch.zeros(K + 1, dtype=f64, device=dev)
+        self.info = torch.zeros(3, dtype=f64, device=dev)
+        self.info_all = torch.zeros(3 * N, dtype=f64, device=dev)
+        self.owner = torch.zeros(K, dtype=torch.int64, device=dev)
+        self.q_local = torch.zeros(K, dtype=f64, device=dev)
+        self.sums = torch.zeros(3, dtype=f64, device=dev)
+        self.table = torch.zeros(2 * K, dtype=f64, device=dev)
+        self.local_idx = torch.zeros(K, dtype=torch.int64, device=dev)
+        self.w_all = torch.zeros(K, dtype=f64, device=dev)
+        self.td_all = torch.zeros(K, dtype=f64, device=dev)
+        self.idx_c = torch.zeros(K, dtype=torch.int64, device=dev)
+        self.td_c = torch.zeros(K, dtype=f64, device=dev)
+        self.n_c = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.norm = torch.zeros(1, dtype=f64, device=dev)
+        # results: td | w | owner | local idx (as f64) + flags
+        self.d_res = torch.zeros(4 * K, dtype=f64, device=dev)
+        self.h_res = torch.zeros(4 * K, dtype=f64).pin_memory()
+        self.h_flags = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.h_in_np, self.h_res_np = self.h_in.numpy(), self.h_res.numpy()
+        self.h_flags_np = self.h_flags.numpy()
+        self.graph = self.graph_exec = None
+        self.calls = 0
+
+    def close(self) -> None:
+        from . import _lib
+        for p in self._opened:
+            _lib.lib.dqn_ipc_close(p)
+        self._opened = []
+        self.comm.close()
+        self.comm_td.close()
+
+    def enqueue(self) -> None:
+        """One global update on the current stream (capturable)."""
+        from . import _lib, nccl
+        p, k, K, N = self.plan, self.k, self.K, self.world
+        st = _lib.stream_ptr()
+        tree, ring = self.mem.tree, self.mem.memory
+        flags = p.flags
+        self.d_in.copy_(self.h_in, non_blocking=True)
+        _lib.call("dqn_dp_shard_info", st, tree.nodes.data_ptr(), ring._size_dev.data_ptr(),
+                  self.mem._max_p.data_ptr(), self.info.data_ptr())
+        self.comm.all_gather(self.info, self.info_all, st)
+        # routing with the owner descent fused in -> (index, leaf) table
+        _lib.call("dqn_dp_route", st, self.info_all.data_ptr(), N, self.d_in.data_ptr(), K,
+                  self.owner.data_ptr(), self.q_local.data_ptr(), self.sums.data_ptr(),
+                  flags.data_ptr(), tree.nodes.data_ptr(), tree.depth, self.rank,
+                  self.table.data_ptr())
+        self.comm.all_reduce(self.table, nccl.NCCL_SUM, st)
+        # peer-ring gather of this rank's strata, IS weights in the same launch
+        _lib.call("dqn_dp_gather", st, self.rings.data_ptr(), self.owner.data_ptr(),
+                  self.table.data_ptr(), k, self.rank, ring.slot_bytes, p.x.data_ptr(),
+                  p.a.data_ptr(), p.r.data_ptr(), p.t.data_ptr(), self.sums.data_ptr(),
+                  self.d_in[K:].data_ptr(), K, self.local_idx.data_ptr(), self.w_all.data_ptr(),
+                  p.w.data_ptr())
+
+        def td_branch():
+            # beside the backward pass (priority stream): TD errors of all
+            # ranks, the owned strata in global order, this shard's update
+            s2 = _lib.stream_ptr()
+            self.comm_td.all_gather(p.d_out[k:2 * k], self.td_all, s2)
+            _lib.call("dqn_dp_owned", s2, self.owner.data_ptr(), self.local_idx.data_ptr(),
+                      self.td_all.data_ptr(), K, self.rank, self.eps, self.idx_c.data_ptr(),
+                      self.td_c.data_ptr(), self.n_c.data_ptr(), self.mem._max_p.data_ptr(),
+                      flags.data_ptr())
+            _lib.call("dqn_tree_update_n", s2, tree.nodes.data_ptr(), tree.depth,
+                      ring._size_dev.data_ptr(), self.idx_c.data_ptr(), self.td_c.data_ptr(), K,
+                      self.n_c.data_ptr(), self.alpha, self.eps, None, flags.data_ptr())
+
+        p.enqueue_learn(td_hook=td_branch)
+        g = self.on.flat_grads
+        self.comm.all_reduce(g, nccl.NCCL_SUM, st)
+        self.comm.all_reduce(flags, nccl.NCCL_MAX, st)
+        if self.grad_clip > 0.0:
+            _lib.call("dqn_clip_gradients", st, g.data_ptr(), self.on.n_flat, self.grad_clip,
+                      self.norm.data_ptr())
+            self.opt.enqueue_step(flags)
+        else:
+            self.opt.enqueue_apply(flags)
+        r = self.d_res
+        r[:K].copy_(self.td_all)
+        r[K:2 * K].copy_(self.w_all)
+        r[2 * K:3 * K].copy_(self.owner)
+        r[3 * K:].copy_(self.local_idx)
+        self.h_res.copy_(r, non_blocking=True)
+        self.h_flags.copy_(flags, non_blocking=True)
+
+    def step(self, u: np.ndarray, beta: float) -> DpStepResult:
+        from . import _lib, agent
+        from .errors import NonFiniteError
+        K = self.K
+        self.h_in_np[:K] = np.asarray(u, dtype=np.float64)
+        self.h_in_np[K] = float(beta)
+        self.h_flags_np[0] = agent._SENTINEL
+        if self.graph_exec is None and self.calls >= 1 and agent.USE_GRAPH:
+            self.graph, self.graph_exec = agent.capture_graph(self.enqueue,
+                                                              self.plan.capture_stream)
+        if self.graph_exec is not None:
+            self.graph_exec.launch(_lib.stream_ptr())
+        else:
+            self.enqueue()
+        self.calls += 1
+        agent._device_sync()
+        f = int(self.h_flags_np[0])
+        if f:
+            self.plan.flags.zero_()
+            if f & _lib.FLAG_ZERO_TOTAL:
+                raise ValueError("zero total priority; nothing can be sampled")
+            if f & _lib.FLAG_NONFINITE_OUT:
+                raise NonFiniteError("non-finite network output")
+            if f & _lib.FLAG_INDEX:
+                raise IndexError("transition index out of range")
+            if f & _lib.FLAG_BAD_PRIORITY:
+                raise ValueError("priority must be finite and >= 0")
+            raise NonFiniteError("non-finite gradient; step aborted")
+        h = self.h_res_np
+        owner = h[2 * K:3 * K].astype(np.int64)
+        local = h[3 * K:].astype(np.int64)
+        return DpStepResult(indices=global_slot(owner, local, self.world), weights=h[K:2 * K].copy(),
+                            td_errors=h[:K].copy(), owner=owner)

@@ -99,10 +99,51 @@ def _frames(x, dtype):
     return t.to(device="cuda", dtype=dtype)
 
 
-class ReplayMemory:
-    """FIFO ring with uniform with-replacement sampling (replay.py:74-124)."""
+_TYPESTR = {"uint8": "|u1", "bool": "|b1", "int64": "<i8", "float64": "<f8", "float32": "<f4"}
 
-    def __init__(self, capacity: int, state_shape: tuple[int, ...], dtype=np.uint8):
+
+class _SharedAlloc:
+    """A plain cudaMalloc allocation (dqn_dev_alloc) so that its CUDA IPC
+    handle covers exactly this buffer; viewed as a torch tensor through
+    ``__cuda_array_interface__`` (zero copy; the tensor keeps it alive)."""
+
+    def __init__(self, shape, dtype):
+        import ctypes as C
+        import weakref
+        torch = _torch()
+        self.dtype = dtype
+        nbytes = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+        self.ptr = C.c_void_p()
+        _lib.call("dqn_dev_alloc", max(nbytes, 16), C.byref(self.ptr))
+        self._fin = weakref.finalize(self, _lib.lib.dqn_dev_free, C.c_void_p(self.ptr.value))
+        self.__cuda_array_interface__ = {
+            "shape": tuple(int(s) for s in shape), "typestr": _TYPESTR[str(dtype).split(".")[-1]],
+            "data": (self.ptr.value, False), "version": 3, "strides": None}
+
+    def handle(self) -> bytes:
+        import ctypes as C
+        buf = (C.c_uint8 * 64)()
+        _lib.call("dqn_ipc_handle", self.ptr, buf)
+        return bytes(buf)
+
+
+def _shared_tensor(shape, dtype):
+    torch = _torch()
+    a = _SharedAlloc(shape, dtype)
+    t = torch.as_tensor(a, device="cuda")
+    t.zero_()
+    return t, a
+
+
+class ReplayMemory:
+    """FIFO ring with uniform with-replacement sampling (replay.py:74-124).
+
+    ``shareable=True`` allocates the five arrays as plain device allocations
+    whose CUDA IPC handles other processes can map (the data-parallel
+    learner's peer gather, dp.py)."""
+
+    def __init__(self, capacity: int, state_shape: tuple[int, ...], dtype=np.uint8,
+                 shareable: bool = False):
         if capacity < 1:
             raise ValueError(f"capacity must be >= 1, got {capacity}")
         torch = _torch()
@@ -115,11 +156,18 @@ class ReplayMemory:
             tdt = torch.float32
         else:
             raise ValueError(f"ring dtype must be uint8 or float32, got {self.np_dtype}")
-        self.states = torch.zeros((self.capacity,) + self.state_shape, dtype=tdt, device="cuda")
-        self.next_states = torch.zeros_like(self.states)
-        self.actions = torch.zeros(self.capacity, dtype=torch.int64, device="cuda")
-        self.rewards = torch.zeros(self.capacity, dtype=torch.float64, device="cuda")
-        self.terminals = torch.zeros(self.capacity, dtype=torch.bool, device="cuda")
+        shapes = {"states": ((self.capacity,) + self.state_shape, tdt),
+                  "next_states": ((self.capacity,) + self.state_shape, tdt),
+                  "actions": ((self.capacity,), torch.int64),
+                  "rewards": ((self.capacity,), torch.float64),
+                  "terminals": ((self.capacity,), torch.bool)}
+        self.shared = {}
+        for name, (shp, dt) in shapes.items():
+            if shareable:
+                t, self.shared[name] = _shared_tensor(shp, dt)
+            else:
+                t = torch.zeros(shp, dtype=dt, device="cuda")
+            setattr(self, name, t)
         self.slot_bytes = int(self.states[0].numel() * self.states.element_size())
         self.cursor = 0
         self.size = 0
@@ -297,9 +345,9 @@ class PrioritizedReplay:
     """Ring + sum tree over p^alpha (replay.py:184-241)."""
 
     def __init__(self, capacity: int, state_shape: tuple[int, ...],
-                 config: PriorityConfig | None = None, dtype=np.uint8):
+                 config: PriorityConfig | None = None, dtype=np.uint8, shareable: bool = False):
         torch = _torch()
-        self.memory = ReplayMemory(capacity, state_shape, dtype=dtype)
+        self.memory = ReplayMemory(capacity, state_shape, dtype=dtype, shareable=shareable)
         self.config = config or PriorityConfig()
         self.tree = SumTree(capacity)
         self._max_p = torch.ones(1, dtype=torch.float64, device="cuda")   # raw p-space
