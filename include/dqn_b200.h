@@ -284,10 +284,13 @@ int dqn_dp_gather(void *stream, const dqn_peer_ring *rings, const int64_t *owner
                   const double *beta, int32_t K, int64_t *local_idx, double *w_all,
                   double *w_mine);
 /* The owned strata in global batch order -> idx_c/td_c/*n_c (for
- * dqn_tree_update_n); max_p = max(max_p, max_j |td_j| + eps) over all K. */
+ * dqn_tree_update_n); max_p = max(max_p, sums[2], max_j |td_j| + eps) over
+ * all K, so every shard keeps the global running max priority (sums from
+ * dqn_dp_route; NULL = this shard's only). */
 int dqn_dp_owned(void *stream, const int64_t *owner, const int64_t *local_idx,
                  const double *td_all, int32_t K, int32_t rank, double eps, int64_t *idx_c,
-                 double *td_c, int32_t *n_c, double *max_p, const int32_t *flags);
+                 double *td_c, int32_t *n_c, double *max_p, const int32_t *flags,
+                 const double *sums);
 /* dqn_tree_update with the batch length read from device memory (*k_dev <= k_max <= 256). */
 int dqn_tree_update_n(void *stream, double *nodes, int32_t depth, const int64_t *size,
                       const int64_t *idx, const double *td, int32_t k_max, const int32_t *k_dev,

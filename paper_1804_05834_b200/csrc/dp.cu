@@ -222,7 +222,7 @@ __global__ void dp_owned_kernel(const int64_t *__restrict__ owner,
                                 const double *__restrict__ td_all, int K, int rank, double eps,
                                 int64_t *__restrict__ idx_c, double *__restrict__ td_c,
                                 int32_t *__restrict__ n_c, double *__restrict__ max_p,
-                                const int32_t *flags) {
+                                const int32_t *flags, const double *__restrict__ sums) {
   pdl_begin();
   __shared__ int s_pos[1025];
   __shared__ double red[32];
@@ -254,6 +254,7 @@ __global__ void dp_owned_kernel(const int64_t *__restrict__ owner,
   if (j == 0 && !bad && !(flags && (*flags & (DQN_FLAG_ZERO_TOTAL | DQN_FLAG_NONFINITE_OUT)))) {
     double v = red[0];
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+    if (sums) v = fmax(v, sums[2]);      // the global running max over the shards
     if (v > *max_p) *max_p = v;
   }
 }
@@ -328,12 +329,12 @@ extern "C" int dqn_dp_gather(void *stream, const dqn_peer_ring *rings, const int
 extern "C" int dqn_dp_owned(void *stream, const int64_t *owner, const int64_t *local_idx,
                             const double *td_all, int32_t K, int32_t rank, double eps,
                             int64_t *idx_c, double *td_c, int32_t *n_c, double *max_p,
-                            const int32_t *flags) {
+                            const int32_t *flags, const double *sums) {
   DQN_CHECK_ARG(owner && local_idx && td_all && idx_c && td_c && n_c && max_p && K >= 1 &&
                     K <= 1024,
                 "dp_owned: bad args");
   launch_k(dp_owned_kernel, 1, threads_for(K), 0, as_stream(stream), owner, local_idx, td_all, K,
-           rank, eps, idx_c, td_c, n_c, max_p, flags);
+           rank, eps, idx_c, td_c, n_c, max_p, flags, sums);
   DQN_LAUNCH_CHECK("dp_owned");
   return DQN_OK;
 }

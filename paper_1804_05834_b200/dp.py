@@ -344,16 +344,26 @@ class DeviceDataParallelLearner:
     from a generator common to all ranks and returns a ``DpStepResult``.
     """
 
-    def __init__(self, online, target, memory, optimizer, config, group=None):
+    def __init__(self, online, target, memory, optimizer, config, group=None, *,
+                 _emulated=None):
+        """``_emulated`` (tests only): ``(rank, world, comm_factory, rings)``
+        -- ranks as threads of one process on one GPU, collectives emulated
+        on the host by ``comm_factory()``, ``rings`` the N shard memories
+        (local pointers instead of IPC mappings)."""
         import ctypes as C
         import torch
-        import torch.distributed as dist
         from . import _lib, agent, nccl
         from .replay import PrioritizedReplay
         if not isinstance(memory, PrioritizedReplay):
             raise ValueError("the data-parallel learner shards a PrioritizedReplay")
-        self.rank = dist.get_rank(group)
-        self.world = N = dist.get_world_size(group)
+        if _emulated is None:
+            import torch.distributed as dist
+            self.rank = dist.get_rank(group)
+            self.world = N = dist.get_world_size(group)
+            make_comm = lambda: nccl.Communicator(group)  # noqa: E731
+        else:
+            self.rank, N, make_comm, emu_rings = _emulated
+            self.world = N
         self.mem, self.on, self.opt = memory, online, optimizer
         self.k = k = int(config.batch_size)
         self.K = K = k * N
@@ -363,15 +373,15 @@ class DeviceDataParallelLearner:
         self.grad_clip = float(getattr(config, "grad_clip", 0.0))
         self.plan = agent._StepPlan(online, target, memory, optimizer, config)
         self.plan.grad_clip = 0.0          # clipping applies to the reduced gradient (below)
-        self.comm = nccl.Communicator(group)
+        self.comm = make_comm()
         # the TD all_gather runs on the priority stream beside the backward
         # pass: a second communicator keeps its order independent of the
         # gradient all_reduce on the main stream
-        self.comm_td = nccl.Communicator(group)
+        self.comm_td = make_comm()
         ring = memory.memory
         # peer rings: own arrays locally, the others' through IPC mappings
         own = [getattr(ring, f).data_ptr() for f in _RING_FIELDS]
-        if N > 1:
+        if N > 1 and _emulated is None:
             if not ring.shared:
                 raise ValueError("world size > 1 needs PrioritizedReplay(..., shareable=True)")
             mine = [ring.shared[f].handle() for f in _RING_FIELDS]
@@ -381,7 +391,9 @@ class DeviceDataParallelLearner:
         table = (S * N)()
         self._opened = []
         for r in range(N):
-            if r == self.rank:
+            if _emulated is not None:
+                ptrs = [getattr(emu_rings[r].memory, f).data_ptr() for f in _RING_FIELDS]
+            elif r == self.rank:
                 ptrs = own
             else:
                 ptrs = []
@@ -459,7 +471,7 @@ class DeviceDataParallelLearner:
             _lib.call("dqn_dp_owned", s2, self.owner.data_ptr(), self.local_idx.data_ptr(),
                       self.td_all.data_ptr(), K, self.rank, self.eps, self.idx_c.data_ptr(),
                       self.td_c.data_ptr(), self.n_c.data_ptr(), self.mem._max_p.data_ptr(),
-                      flags.data_ptr())
+                      flags.data_ptr(), self.sums.data_ptr())
             _lib.call("dqn_tree_update_n", s2, tree.nodes.data_ptr(), tree.depth,
                       ring._size_dev.data_ptr(), self.idx_c.data_ptr(), self.td_c.data_ptr(), K,
                       self.n_c.data_ptr(), self.alpha, self.eps, None, flags.data_ptr())

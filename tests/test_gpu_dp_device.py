@@ -225,7 +225,7 @@ def test_owned_strata_update_matches_host_update_priorities(P):
         fl = torch.zeros(1, dtype=torch.int32, device="cuda")
         _lib.call("dqn_dp_owned", st, od.data_ptr(), ld.data_ptr(), tdd.data_ptr(), K, rank, 0.01,
                   idx_c.data_ptr(), td_c.data_ptr(), n_c.data_ptr(), mem._max_p.data_ptr(),
-                  fl.data_ptr())
+                  fl.data_ptr(), None)
         _lib.call("dqn_tree_update_n", st, mem.tree.nodes.data_ptr(), mem.tree.depth,
                   mem.memory._size_dev.data_ptr(), idx_c.data_ptr(), td_c.data_ptr(), K,
                   n_c.data_ptr(), 0.6, 0.01, None, fl.data_ptr())
@@ -235,3 +235,135 @@ def test_owned_strata_update_matches_host_update_priorities(P):
         assert torch.equal(mem.tree.nodes, ref.tree.nodes)
         assert mem.max_priority == max(1.0, float((np.abs(td) + 0.01).max()))
         assert fl.item() == 0
+
+
+class _Hub:
+    """Host-side collectives for ranks that are threads of this process: each
+    rank synchronises its stream, posts its buffer, and copies the combined
+    result once every rank has posted.  Kernels never wait on another rank."""
+
+    def __init__(self, n):
+        import threading
+        self.n = n
+        self.lock = threading.Lock()
+        self.barriers = {}
+        self.slots = {}
+
+    def barrier(self, name):
+        import threading
+        with self.lock:
+            if name not in self.barriers:
+                self.barriers[name] = threading.Barrier(self.n)
+            return self.barriers[name]
+
+
+class _EmuComm:
+    def __init__(self, hub, rank, name):
+        self.hub, self.rank, self.name = hub, rank, name
+
+    def _exchange(self, t):
+        torch.cuda.current_stream().synchronize()
+        self.hub.slots[(self.name, self.rank)] = t.detach().clone()
+        b = self.hub.barrier(self.name)
+        b.wait()
+        vals = [self.hub.slots[(self.name, r)] for r in range(self.hub.n)]
+        b.wait()
+        return vals
+
+    def all_gather(self, send, recv, stream):
+        recv.copy_(torch.cat([v.reshape(-1) for v in self._exchange(send)]))
+        torch.cuda.current_stream().synchronize()
+
+    def all_reduce(self, t, op, stream, out=None):
+        from paper_1804_05834_b200 import nccl
+        vals = self._exchange(t)
+        acc = vals[0].clone()
+        for v in vals[1:]:
+            acc = acc + v if op == nccl.NCCL_SUM else torch.maximum(acc, v)
+        (t if out is None else out).copy_(acc)
+        torch.cuda.current_stream().synchronize()
+
+    def close(self):
+        pass
+
+
+def test_emulated_world2_equals_global_batch_update(P, monkeypatch):
+    """Two ranks as threads on this GPU, collectives emulated on the host:
+    both ranks agree on the sampled strata, weights and TD errors; the summed
+    per-rank gradients equal the gradient of ONE batch-64 update over the
+    same transitions and weights (the loss is a sum); each shard's tree gets
+    exactly its owned strata in global batch order; max_priority becomes the
+    global running max on every shard."""
+    import threading
+    from paper_1804_05834_b200 import agent, dp
+    from tests.helpers import rel_norm
+    monkeypatch.setattr(agent, "USE_GRAPH", False)
+    N, k, cap = 2, 32, 200
+    K = N * k
+    hub = _Hub(N)
+    shards, nets, learners = [], [], []
+    for r in range(N):
+        on, tg, mem, opt, cfg = _learner(P, seed=40 + r, cap=cap)
+        shards.append(mem)
+        nets.append((on, tg, opt, cfg))
+    mp0 = [m.max_priority for m in shards]
+    before = [m.tree.nodes.clone() for m in shards]
+    for r in range(N):
+        names = iter(["main", "td"])
+        on, tg, opt, cfg = nets[r]
+        opt.enqueue_apply = lambda flags: None          # keep the reduced gradients
+        learners.append(dp.DeviceDataParallelLearner(
+            on, tg, shards[r], opt, cfg,
+            _emulated=(r, N, lambda r=r, names=names: _EmuComm(hub, r, next(names)), shards)))
+    u = np.random.default_rng(11).random(K)
+    out, errs = [None] * N, []
+
+    def run(r):
+        try:
+            out[r] = learners[r].step(u, 0.7)
+        except Exception as e:          # pragma: no cover - surfaced below
+            errs.append(e)
+    th = [threading.Thread(target=run, args=(r,)) for r in range(N)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    a, b = out
+    assert np.array_equal(a.indices, b.indices) and np.array_equal(a.owner, b.owner)
+    assert np.array_equal(a.weights, b.weights) and np.array_equal(a.td_errors, b.td_errors)
+    assert set(a.owner.tolist()) == {0, 1}
+    g = [n[0].flat_grads.clone() for n in nets]
+    assert torch.equal(g[0], g[1])
+    # the same transitions and weights through one batch-64 update
+    cfg64 = P.RunConfig(double=True, dueling=True, batch_size=K, beta_end_step=1000)
+    on64 = P.build_network("atari", (84, 84, 4), 4, True)
+    tg64 = P.build_network("atari", (84, 84, 4), 4, True)
+    P.init_params(on64, 1)
+    P.init_params(tg64, 2)
+    opt64 = P.RmsProp(on64)
+    plan = agent._StepPlan(on64, tg64, shards[0], opt64, cfg64)
+    local = a.indices // N
+    for j in range(K):
+        m = shards[int(a.owner[j])].memory
+        plan.x[j].copy_(m.states[local[j]])
+        plan.x[K + j].copy_(m.next_states[local[j]])
+        plan.a[j] = m.actions[local[j]]
+        plan.r[j] = m.rewards[local[j]]
+        plan.t[j] = m.terminals[local[j]]
+    plan.w.copy_(torch.as_tensor(a.weights))
+    plan.enqueue_learn(priorities=False)
+    torch.cuda.synchronize()
+    td64 = plan.d_out[K:2 * K].cpu().numpy()
+    assert rel_norm(a.td_errors, td64) < 1e-5
+    assert rel_norm(g[0].cpu().numpy(), on64.flat_grads.cpu().numpy()) < 1e-5
+    # owner-side priority updates in global batch order
+    for r in range(N):
+        ref = P.PrioritizedReplay(cap, (84, 84, 4), P.PriorityConfig(0.6, 0.01, P.LinearSchedule(0.4, 1, 10)))
+        ref.memory._set_size(cap)
+        ref.tree.nodes.copy_(before[r])
+        m = a.owner == r
+        ref.update_priorities(local[m], a.td_errors[m])
+        assert torch.equal(shards[r].tree.nodes, ref.tree.nodes)
+    want_max = max(max(mp0), float((np.abs(a.td_errors) + 0.01).max()))
+    assert [s.max_priority for s in shards] == [want_max] * N
