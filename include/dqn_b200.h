@@ -239,6 +239,18 @@ int dqn_clip_gradients(void *stream, float *g, int64_t n, double max_norm, doubl
 /* sync_target (optim.py:78-89): bitwise copy of the flat parameter buffer. */
 int dqn_sync_target(void *stream, float *dst, const float *src, int64_t n);
 
+/* The learner's three forwards of trunk layers [0, upto) in one launch per
+ * layer (tcgen05 layers; others fall back to two launches): online rows
+ * [0, k) and [k, 2k) of on_bind (batch 2k: [s; s'], network.py:90-100) and
+ * the target binding (batch k, its x = s'), same net geometry, online and
+ * target parameters.  scratch: dqn_net_forward_group_scratch(net, upto, k)
+ * floats, the last 16384 (split-K tile counters) zeroed once. */
+int64_t dqn_net_forward_group_scratch(const dqn_net_desc *net, int32_t upto, int32_t batch);
+int dqn_net_forward_group(void *stream, const dqn_net_desc *net, const float *on_params,
+                          const dqn_binding *on_bind, const float *tg_params,
+                          const dqn_binding *tg_bind, int32_t upto, float *scratch,
+                          int64_t scratch_floats, int32_t *flags);
+
 /* ---- data-parallel learner (algorithm in dp.py) --------
  * N ranks (one per GPU), rank r owns replay shard r (global transition g at
  * rank g % N, slot g / N) with its own sum tree; K = k * N strata per global

@@ -158,6 +158,16 @@ class _StepPlan:
         # graph.  Off by default: measured 1-2 % slower (the update is mostly
         # SM-time bound and the target forward on the side stream is critical)
         hi = -8 if USE_PRIORITY else 0
+        # DQN_B200_GROUPED_FWD=1: online [s; s'] and target s' forwards of the
+        # trunk as one launch per layer (dqn_net_forward_group).  Off by
+        # default: measured 5 % slower than the two concurrent PDL chains
+        self.grouped = (self.fused_head and self.double
+                        and os.environ.get("DQN_B200_GROUPED_FWD", "0") == "1")
+        self.grp_scratch = None
+        if self.grouped:
+            n = int(_lib.lib.dqn_net_forward_group_scratch(C.byref(self.on_desc),
+                                                           self.head_layer, k))
+            self.grp_scratch = torch.zeros(n, dtype=torch.float32, device=dev)
         self.side = torch.cuda.Stream(priority=0)
         self.tree_stream = torch.cuda.Stream(priority=hi)
         self.capture_stream = torch.cuda.Stream(priority=hi)
@@ -219,9 +229,12 @@ class _StepPlan:
         e_in.record(s0)
         with torch.cuda.stream(s1):
             s1.wait_event(e_in)
-            tg.forward_into(self.x[k:], self.tg_bind, upto=self.head_layer if self.fused_head else None)
-            e_tg = ev()
-            e_tg.record(s1)
+            e_tg = None
+            if not self.grouped:
+                tg.forward_into(self.x[k:], self.tg_bind,
+                                upto=self.head_layer if self.fused_head else None)
+                e_tg = ev()
+                e_tg.record(s1)
             e_xt = None
             if self.xt is not None:              # read by the last wgrad only
                 self.on_view.struct.x = self.x.data_ptr()
@@ -230,11 +243,21 @@ class _StepPlan:
                 e_xt = ev()
                 e_xt.record(s1)
         upto = self.head_layer if self.fused_head else None
-        if self.double:
+        if self.grouped:
+            xs = self.x[k:]
+            self.on_bind.x, self.tg_bind.x = self.x, xs
+            self.on_bind.struct.x, self.tg_bind.struct.x = self.x.data_ptr(), xs.data_ptr()
+            g = self.grp_scratch
+            _lib.call("dqn_net_forward_group", st, C.byref(self.on_desc), on.flat_values.data_ptr(),
+                      C.byref(self.on_bind.struct), tg.flat_values.data_ptr(),
+                      C.byref(self.tg_bind.struct), self.head_layer, g.data_ptr(), g.numel(),
+                      self.flags.data_ptr())
+        elif self.double:
             on.forward_into(self.x, self.on_bind, upto=upto)
         else:
             on.forward_into(self.x[:k], self.on_bind, upto=upto)
-        s0.wait_event(e_tg)
+        if e_tg is not None:
+            s0.wait_event(e_tg)
         nA = self.nA
         out = self.d_out
         for v in (self.on_view, self.on_wview):

@@ -25,6 +25,11 @@ int tc_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const flo
                       const dqn_binding *b);
 int tc_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
                    const dqn_binding *b, int32_t *flags);
+int tc_layer_forward_group(cudaStream_t st, const dqn_net_desc *net, int l,
+                           const float *on_params, const dqn_binding *on_b,
+                           const float *tg_params, const dqn_binding *tg_b, float *scratch,
+                           int *counters);
+int64_t tc_forward_group_scratch(const dqn_net_desc *net, int upto, int batch);
 
 // tcgen05 trunk for supported geometries unless the descriptor asks for SIMT
 static bool use_tc(const dqn_net_desc *net, int l, int phase) {
@@ -110,6 +115,41 @@ extern "C" int dqn_net_forward(void *stream, const dqn_net_desc *net, const floa
   if (st) return st;
   for (int l = 0; l < net->n_layers; ++l) {
     st = layer_forward(as_stream(stream), net, l, params, bind, flags);
+    if (st) return st;
+  }
+  return DQN_OK;
+}
+
+extern "C" int64_t dqn_net_forward_group_scratch(const dqn_net_desc *net, int32_t upto,
+                                                 int32_t batch) {
+  if (!net || upto < 0 || upto > net->n_layers || batch < 1) return -1;
+  return tc_forward_group_scratch(net, upto, batch) + kTileCounters;
+}
+
+extern "C" int dqn_net_forward_group(void *stream, const dqn_net_desc *net,
+                                     const float *on_params, const dqn_binding *on_bind,
+                                     const float *tg_params, const dqn_binding *tg_bind,
+                                     int32_t upto, float *scratch, int64_t scratch_floats,
+                                     int32_t *flags) {
+  int st = check_binding(net, on_bind);
+  if (st) return st;
+  st = check_binding(net, tg_bind);
+  if (st) return st;
+  if (upto < 0 || upto > net->n_layers || on_bind->batch != 2 * tg_bind->batch || !scratch ||
+      scratch_floats < dqn_net_forward_group_scratch(net, upto, tg_bind->batch)) {
+    set_error("forward_group: need on batch = 2 x target batch, upto <= layers, scratch");
+    return DQN_ERR_INVALID_ARG;
+  }
+  cudaStream_t s = as_stream(stream);
+  int *counters = reinterpret_cast<int *>(scratch + scratch_floats - kTileCounters);
+  for (int l = 0; l < upto; ++l) {
+    if (use_tc(net, l, 0)) {
+      st = tc_layer_forward_group(s, net, l, on_params, on_bind, tg_params, tg_bind, scratch,
+                                  counters);
+    } else {
+      st = layer_forward(s, net, l, on_params, on_bind, flags);
+      if (!st) st = layer_forward(s, net, l, tg_params, tg_bind, flags);
+    }
     if (st) return st;
   }
   return DQN_OK;

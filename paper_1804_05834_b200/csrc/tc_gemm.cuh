@@ -348,6 +348,7 @@ struct Gather {
 // Policies derive from this; it supplies the B gather form a policy does not
 // use (never called: the Gather uses the form of its layout).
 struct PolBase {
+  __device__ int rows(int) const { return 0x7fffffff; }   // problem height (grouped launches)
   __device__ void note_bias(float) const {}      // BIAS_FROM_B: the written bias gradient
   __device__ int b_koff(int) const { return 0; }
   __device__ float4 b_ld(long long, int) const { return make_float4(0.f, 0.f, 0.f, 0.f); }
@@ -443,6 +444,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   __shared__ unsigned long long tr_mma[2];
 #endif
   TC_MARK(0)
+  // problems of different heights share the grid: tiles past a problem's
+  // rows exit before touching TMEM, barriers or split-K counters
+  if ((int)blockIdx.x * BM >= p.rows((int)blockIdx.z / p.ksplits)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(

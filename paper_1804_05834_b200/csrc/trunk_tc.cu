@@ -132,6 +132,64 @@ struct FwdPol : tc::PolBase {
   }
 };
 
+// ------------------------------------------------ grouped trunk forward
+// The learner's online [s; s'] and target s' forwards of one trunk layer in
+// ONE launch: problem 0 = online (2 x batch images),
+// problem 1 = target (batch images, its tiles past M1 exit at entry);
+// problem p = blockIdx.z / splits selects input, weights, bias and output.
+// The problem rides in the top byte of the row bases, so the per-element code
+// is FwdPol's.
+template <typename InT, int BN_>
+struct FwdGroupPol : tc::PolBase {
+  static constexpr bool U8 = sizeof(InT) == 1;
+  static constexpr bool SPLIT_A = !U8, SPLIT_B = true, BIAS_FROM_B = false;
+  static constexpr bool B_MNC = true;
+  static constexpr int BN = BN_;
+  static constexpr int PSHIFT = 56;
+  static constexpr long long PMASK = (1LL << PSHIFT) - 1;
+  const InT *x0, *x1;
+  const float *w0, *w1, *bias0, *bias1;
+  float *y0, *y1, *partial;
+  float *bias_out, *bias_partial;       // unused
+  int *counters;
+  Geo g;
+  int M, M1, N, K, klen, relu, ksplits;   // M = problem 0 rows (the grid), M1 = problem 1 rows
+  __device__ int rows(int p) const { return p ? M1 : M; }
+  __device__ int kbeg(int z) const { return z * klen; }
+  __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
+  __device__ long long a_row(int m, int p) const {
+    return m < rows(p) ? (pixel_base(g, m) | ((long long)p << PSHIFT)) : -1;
+  }
+  __device__ void a16(long long base, int k, int ke, float (&v)[16]) const {
+    if (k >= ke) return zero16(v);
+    const InT *x = (base >> PSHIFT) ? x1 : x0;
+    ld16(x + (base & PMASK) + patch_off(g, k), v);
+  }
+  __device__ long long b_row(int n, int p) const {
+    return n < N ? ((long long)n | ((long long)p << PSHIFT)) : -1;
+  }
+  __device__ void b4(long long base, int k, int ke, float4 (&v)[4]) const {
+    const float *w = (base >> PSHIFT) ? w1 : w0;
+    const long long n = base & PMASK;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) v[t] = (k + t < ke) ? ld4(w + (int64_t)(k + t) * N + n) : zero4();
+  }
+  __device__ void final4(int m, int n, float4 v, int p) const {
+    if (m >= rows(p)) return;
+    const float *bias = p ? bias1 : bias0;
+    float *y = p ? y1 : y0;
+    float t[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float u = U8 ? __fdiv_rn(t[j], 255.0f) : t[j];
+      u = __fadd_rn(u, bias[n + j]);
+      if (relu && u < 0.f) u = 0.f;
+      t[j] = u;
+    }
+    st4(y + (int64_t)m * N + n, make_float4(t[0], t[1], t[2], t[3]));
+  }
+};
+
 // --------------------------------------------------------- linear dgrad
 // dX[m, f] = sum_co dY[m, co] * W[f, co]  (W row-major [F][Cout])
 template <int BN_>
@@ -383,6 +441,38 @@ int fwd_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const f
   return DQN_ERR_UNSUPPORTED;
 }
 
+template <typename InT, int BN>
+int fwd_group_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *const x[2],
+                     const float *const w[2], const float *const b[2], float *const y[2],
+                     float *scratch, int *counters, int batch) {
+  FwdGroupPol<InT, BN> p{};
+  p.counters = counters;
+  p.x0 = x[0]; p.x1 = x[1];
+  p.w0 = w[0]; p.w1 = w[1];
+  p.bias0 = b[0]; p.bias1 = b[1];
+  p.y0 = y[0]; p.y1 = y[1];
+  p.partial = scratch;
+  p.g = geo_of(L);
+  p.M1 = batch * L.out_h * L.out_w;
+  p.M = 2 * p.M1;
+  p.N = L.out_c;
+  p.K = L.fh * L.fw * L.in_c;
+  p.klen = fwd_klen(p.K);
+  p.relu = L.relu;
+  p.ksplits = ceil_div(p.K, p.klen);
+  return tc::launch(st, p, 2 * p.ksplits, "tc_fwd_group");
+}
+
+template <typename InT>
+int fwd_group_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *const x[2],
+                       const float *const w[2], const float *const b[2], float *const y[2],
+                       float *scratch, int *counters, int batch) {
+  const int N = L.out_c;
+  if (N == 32) return fwd_group_launch<InT, 32>(st, L, x, w, b, y, scratch, counters, batch);
+  if (N % 64 == 0) return fwd_group_launch<InT, 64>(st, L, x, w, b, y, scratch, counters, batch);
+  return DQN_ERR_UNSUPPORTED;
+}
+
 template <int BN>
 int lin_dgrad_launch(cudaStream_t st, const float *dy, const float *w, const float *mask,
                      float *out, float *partial, int *counters, int M, int N, int K) {
@@ -551,6 +641,38 @@ int tc_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const floa
                                   counters_of(b), b->batch);
   return fwd_dispatch<float>(st, L, (const float *)in, params, b->act[l], b->scratch,
                               counters_of(b), b->batch);
+}
+
+// The grouped forward of trunk layer l: online on_b (batch 2k, [s; s']) and
+// target tg_b (batch k) in one launch.
+int tc_layer_forward_group(cudaStream_t st, const dqn_net_desc *net, int l,
+                           const float *on_params, const dqn_binding *on_b,
+                           const float *tg_params, const dqn_binding *tg_b, float *scratch,
+                           int *counters) {
+  const dqn_layer_desc &L = net->layer[l];
+  const int k = tg_b->batch;
+  const float *w[2] = {on_params + L.w_off, tg_params + L.w_off};
+  const float *b[2] = {on_params + L.b_off, tg_params + L.b_off};
+  float *y[2] = {on_b->act[l], tg_b->act[l]};
+  if (l == 0 && net->input_u8) {
+    const uint8_t *x[2] = {(const uint8_t *)on_b->x, (const uint8_t *)tg_b->x};
+    return fwd_group_dispatch<uint8_t>(st, L, x, w, b, y, scratch, counters, k);
+  }
+  const float *x[2] = {l == 0 ? (const float *)on_b->x : on_b->act[l - 1],
+                       l == 0 ? (const float *)tg_b->x : tg_b->act[l - 1]};
+  return fwd_group_dispatch<float>(st, L, x, w, b, y, scratch, counters, k);
+}
+
+// split-K partials of the grouped forward: two problems of 2k rows (grid)
+int64_t tc_forward_group_scratch(const dqn_net_desc *net, int upto, int batch) {
+  int64_t m = 0;
+  for (int l = 0; l < upto; ++l) {
+    const dqn_layer_desc &L = net->layer[l];
+    const int K = L.fh * L.fw * L.in_c;
+    const int ks = ceil_div(K, fwd_klen(K));
+    if (ks > 1) m = std::max(m, (int64_t)2 * ks * 2 * batch * L.out_h * L.out_w * L.out_c);
+  }
+  return m;
 }
 
 int tc_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,

@@ -137,3 +137,21 @@ def test_im2col_t_u8_bit_exact(P):
     _lib.call("dqn_net_im2col_t", _lib.stream_ptr(), C.byref(desc), C.byref(b.struct))
     want = _im2col_t_np(x, 8, 8, 4, 4)
     assert np.array_equal(xt.cpu().numpy().reshape(want.shape), want)
+
+
+def test_grouped_forward_matches_two_stream_forward(P, monkeypatch):
+    """DQN_B200_GROUPED_FWD=1 (online [s; s'] and target s' trunk forwards as
+    one launch per layer, dqn_net_forward_group) computes the same rows with
+    the same split-K order as the two per-network launches: bit-identical."""
+    runs = []
+    for grouped in ("1", "0"):
+        monkeypatch.setenv("DQN_B200_GROUPED_FWD", grouped)
+        on, tg, mem, opt, cfg = learner(P, **CASES["cfg4"])
+        res = P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(3))
+        plan = next(p for p in P.agent._PLANS.values() if p.online is on)
+        assert plan.grouped == (grouped == "1")
+        runs.append((res, on.flat_values.clone(), tg.binding(32).act[-2].clone()))
+    (ra, wa, ta), (rb, wb, tb) = runs
+    assert np.array_equal(ra.td_errors, rb.td_errors)
+    assert torch.equal(ta, tb)
+    assert torch.equal(wa, wb)
