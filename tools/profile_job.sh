@@ -13,3 +13,5 @@ timeout 900 ncu --profile-from-start off --set full --import-source on --clock-c
   -k regex:tc_gemm -o gpurun_out/step_gemms python tools/profile_step.py \
   > gpurun_out/ncu_gemms.log 2>&1
 tail -2 gpurun_out/ncu_gemms.log
+timeout 600 python tools/kernel_bench.py gpurun_out/kernel_bench.json > gpurun_out/kb.log 2>&1
+tail -1 gpurun_out/kb.log
