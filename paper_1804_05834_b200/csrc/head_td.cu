@@ -49,6 +49,12 @@ struct HeadTdArgs {
   int32_t *flags;
 };
 
+// DQN_B200_HEAD_TWO_PHASE=0 selects the last-CTA form (head_q_td + head_bwd_wgrad)
+inline bool head_two_phase() {
+  const char *e = getenv("DQN_B200_HEAD_TWO_PHASE");   // read per call (graph capture time)
+  return !(e && e[0] == '0');
+}
+
 // K1: Q heads of both networks (one warp per row: lane-strided fmaf chains,
 // fixed shuffle tree read from lane 0), then -- in the last CTA to finish --
 // the TD block (td_loss_kernel's per-row arithmetic and 256-slot statistics
@@ -220,13 +226,223 @@ __global__ void __launch_bounds__(kHeadCta) head_bwd_wgrad_kernel(const HeadTdAr
   }
 }
 
+// ---- two-phase form for learner batches (k * (nA + 1) <= kGsMax) ----------
+// K1q: the Q heads only (CTA per row, features split over 8 warps).
+// K2t: every CTA recomputes the k-row TD block into shared memory (a few
+// hundred L2 bytes and fp64 ops per row), so no CTA waits on a last-arrival
+// ticket; CTA 0 alone stores targets / TD / losses / dq / statistics; then
+// head dX (first nb_dx CTAs) and head wgrad (the rest, 32-feature x 8-row-
+// group tiles).  Same formulas as head_q_td + head_bwd_wgrad; the Q-head and
+// wgrad sums run in a different fixed order (not bit-identical to that form).
+constexpr int kGsMax = 2048;
+
+template <int NA>
+__global__ void __launch_bounds__(kHeadCta) head_q_kernel(const HeadTdArgs p) {
+  // one CTA per Q row; warp w owns features [w F/8, (w+1) F/8) (lane-strided,
+  // every load of the row in flight at once); partial sums of the 8 warps are
+  // added in warp order
+  pdl_begin();
+  constexpr int NO = NA + 1, NW = kHeadCta / 32;
+  __shared__ float s_part[NW][NO];
+  const int F = p.F;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x;
+  const bool on = r < p.on.rows;
+  const int row = on ? r : r - p.on.rows;
+  const float *xr = (on ? p.on.x : p.tg.x) + (int64_t)row * F;
+  const float *wv = on ? p.on.wv : p.tg.wv, *wa = on ? p.on.wa : p.tg.wa;
+  const float *bv = on ? p.on.bv : p.tg.bv, *ba = on ? p.on.ba : p.tg.ba;
+  const int per = (F + NW - 1) / NW, f0 = warp * per, f1 = min(F, f0 + per);
+  float acc[NO];
+#pragma unroll
+  for (int o = 0; o < NO; ++o) acc[o] = 0.f;
+#pragma unroll 4
+  for (int f = f0 + lane; f < f1; f += 32) {
+    const float xv = __ldg(xr + f);
+    if (p.dueling) acc[NA] = fmaf(xv, __ldg(wv + f), acc[NA]);
+#pragma unroll
+    for (int a = 0; a < NA; ++a) acc[a] = fmaf(xv, __ldg(wa + (int64_t)f * NA + a), acc[a]);
+  }
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) acc[o] = __fadd_rn(acc[o], __shfl_down_sync(0xffffffffu, acc[o], s));
+    if (lane == 0) s_part[warp][o] = acc[o];
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+    float v = s_part[0][o];
+    for (int w = 1; w < NW; ++w) v = __fadd_rn(v, s_part[w][o]);
+    acc[o] = v;
+  }
+  bool bad = false;
+  float *qr = (on ? p.on.q : p.tg.q) + (int64_t)row * NA;
+  if (p.dueling) {
+    const float v = __fadd_rn(acc[NA], bv[0]);
+    float adv[NA], sum = 0.f;
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      adv[a] = __fadd_rn(acc[a], ba[a]);
+      sum = __fadd_rn(sum, adv[a]);
+    }
+    const float mean = __fdiv_rn(sum, (float)NA);
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      const float qa = __fsub_rn(__fadd_rn(v, adv[a]), mean);
+      bad |= !isfinite(qa);
+      qr[a] = qa;
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      const float qa = __fadd_rn(acc[a], ba[a]);
+      bad |= !isfinite(qa);
+      qr[a] = qa;
+    }
+  }
+  if (bad) raise_flag(p.flags, DQN_FLAG_NONFINITE_OUT);
+}
+
+template <int NA>
+__global__ void __launch_bounds__(kHeadCta) head_td_bwd_kernel(const HeadTdArgs p, int nb_dx) {
+  pdl_begin();
+  constexpr int NO = NA + 1;
+  const int F = p.F, k = p.k, t = threadIdx.x;
+  const int no = p.dueling ? NA + 1 : NA;
+  __shared__ float s_gs[kGsMax];
+  __shared__ double s_abs[kHeadCta], s_loss[kHeadCta];
+  const bool writer = blockIdx.x == 0;
+  const float *q_on = p.on.q, *q_next_on = p.on.q + (int64_t)k * NA;
+  double acc_abs = 0.0, acc_loss = 0.0;
+  for (int j = t; j < k; j += kHeadCta) {
+    int64_t a;
+    double y, d, loss;
+    float gf;
+    td_core(j, q_on, q_next_on, p.tg.q, p.actions, p.rewards, p.terminals, p.weights, NA,
+            p.gamma, p.td_flags, a, y, d, loss, gf);
+    // dq row j is gf at the taken action, 0 elsewhere; branch gradients as
+    // head_q_td_kernel derives them from that row (sums in the same order)
+    float *gs = s_gs + j * NO;
+    if (p.dueling) {
+      float gv = 0.f;
+      for (int c = 0; c < NA; ++c) gv = __fadd_rn(gv, c == a ? gf : 0.f);
+      gs[0] = gv;
+      const float gvn = __fdiv_rn(gv, (float)NA);
+      for (int c = 0; c < NA; ++c) gs[c + 1] = __fsub_rn(c == a ? gf : 0.f, gvn);
+    } else {
+      for (int c = 0; c < NA; ++c) gs[c] = c == a ? gf : 0.f;
+    }
+    if (writer) {
+      p.targets[j] = y;
+      p.td[j] = d;
+      p.losses[j] = loss;
+      for (int c = 0; c < NA; ++c) p.dq[(int64_t)j * NA + c] = (c == a) ? gf : 0.f;
+      acc_abs = __dadd_rn(acc_abs, fabs(d));
+      acc_loss = __dadd_rn(acc_loss, loss);
+    }
+  }
+  __syncthreads();
+  if (writer && p.stats) {
+    s_abs[t] = acc_abs;
+    s_loss[t] = acc_loss;
+    __syncthreads();
+    for (int s = kHeadCta / 2; s > 0; s >>= 1) {
+      if (t < s) {
+        s_abs[t] = __dadd_rn(s_abs[t], s_abs[t + s]);
+        s_loss[t] = __dadd_rn(s_loss[t], s_loss[t + s]);
+      }
+      __syncthreads();
+    }
+    if (t == 0) {
+      p.stats[0] = s_abs[0];
+      p.stats[1] = s_loss[0];
+    }
+  }
+  if ((int)blockIdx.x < nb_dx) {
+    const int e = blockIdx.x * kHeadCta + t;
+    if (e >= k * F) return;
+    const int row = e / F, f = e - row * F;
+    const float *gs = s_gs + row * NO;
+    float v;
+    if (p.dueling) {
+      float s = 0.f;
+#pragma unroll
+      for (int a = 0; a < NA; ++a) s = fmaf(gs[a + 1], __ldg(p.on.wa + (int64_t)f * NA + a), s);
+      v = __fadd_rn(__fmul_rn(gs[0], __ldg(p.on.wv + f)), s);
+    } else {
+      float s = 0.f;
+#pragma unroll
+      for (int a = 0; a < NA; ++a) s = fmaf(gs[a], __ldg(p.on.wa + (int64_t)f * NA + a), s);
+      v = s;
+    }
+    if (p.mask != nullptr && !(p.mask[e] > 0.f)) v = 0.f;
+    p.dx[e] = v;
+    return;
+  }
+  // head wgrad: CTA = 32 features (f = F is the bias row) x 8 row groups;
+  // each thread sums its rows (all loads in flight), the 8 group partials are
+  // added in group order
+  __shared__ float s_w[kHeadCta / 32][32][NO];
+  const int fl = t & 31, rg = t >> 5;
+  const int f = (blockIdx.x - nb_dx) * 32 + fl;
+  const int rows_per = (k + 7) / 8, r0 = rg * rows_per, r1 = min(k, r0 + rows_per);
+  float acc[NO];
+#pragma unroll
+  for (int o = 0; o < NO; ++o) acc[o] = 0.f;
+  if (f <= F) {
+#pragma unroll 4
+    for (int r = r0; r < r1; ++r) {
+      const float xv = f < F ? __ldg(p.on.x + (int64_t)r * F + f) : 1.f;
+      const float *gs = s_gs + r * NO;
+#pragma unroll
+      for (int o = 0; o < NO; ++o)
+        if (o < no) acc[o] = fmaf(xv, gs[o], acc[o]);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < NO; ++o) s_w[rg][fl][o] = acc[o];
+  __syncthreads();
+  if (rg != 0 || f > F) return;
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+    if (o >= no) break;
+    float s = s_w[0][fl][o];
+    for (int g = 1; g < kHeadCta / 32; ++g) s = __fadd_rn(s, s_w[g][fl][o]);
+    if (p.dueling) {
+      if (o == 0) {
+        if (f < F) acc_grad(&p.gwv[f], s, p.flags); else acc_grad(&p.gbv[0], s, p.flags);
+      } else {
+        if (f < F) acc_grad(&p.gwa[(int64_t)f * NA + o - 1], s, p.flags);
+        else acc_grad(&p.gba[o - 1], s, p.flags);
+      }
+    } else {
+      if (f < F) acc_grad(&p.gwa[(int64_t)f * NA + o], s, p.flags);
+      else acc_grad(&p.gba[o], s, p.flags);
+    }
+  }
+}
+
 template <int NA>
 int launch_head_td(cudaStream_t st, const HeadTdArgs &p) {
   const int R = p.on.rows + p.tg.rows;
-  launch_k(head_q_td_kernel<NA>, (R + kHeadCta / 32 - 1) / (kHeadCta / 32), kHeadCta, 0, st, p);
-  DQN_LAUNCH_CHECK("head_q_td");
   const int nb_dx = p.dx ? (p.k * p.F + kHeadCta - 1) / kHeadCta : 0;
   const int nb_w = (p.F + 1 + kHeadCta - 1) / kHeadCta;
+  if (p.k * (NA + 1) <= kGsMax && head_two_phase()) {
+    const char *only = getenv("DQN_B200_HEAD_ONLY");      // diagnostic: "q" or "td"
+    if (!only || only[0] != 't') {
+      launch_k(head_q_kernel<NA>, R, kHeadCta, 0, st, p);
+      DQN_LAUNCH_CHECK("head_q");
+    }
+    if (!only || only[0] != 'q') {
+      launch_k(head_td_bwd_kernel<NA>, nb_dx + (p.F + 1 + 31) / 32, kHeadCta, 0, st, p, nb_dx);
+      DQN_LAUNCH_CHECK("head_td_bwd");
+    }
+    return DQN_OK;
+  }
+  launch_k(head_q_td_kernel<NA>, (R + kHeadCta / 32 - 1) / (kHeadCta / 32), kHeadCta, 0, st, p);
+  DQN_LAUNCH_CHECK("head_q_td");
   launch_k(head_bwd_wgrad_kernel<NA>, nb_dx + nb_w, kHeadCta, 0, st, p, nb_dx);
   DQN_LAUNCH_CHECK("head_bwd_wgrad");
   return DQN_OK;

@@ -155,3 +155,20 @@ def test_grouped_forward_matches_two_stream_forward(P, monkeypatch):
     assert np.array_equal(ra.td_errors, rb.td_errors)
     assert torch.equal(ta, tb)
     assert torch.equal(wa, wb)
+
+
+@pytest.mark.parametrize("name", ["cfg4", "cfg4_huber", "cfg1"])
+def test_head_two_phase_matches_last_cta_form(P, name, monkeypatch):
+    """The two-phase head (Q heads, then every CTA recomputes the TD block)
+    against the last-CTA-ticket form: same formulas, sums in another fixed
+    order (1e-5, as the fused vs per-layer head)."""
+    runs = []
+    for two in ("1", "0"):
+        monkeypatch.setenv("DQN_B200_HEAD_TWO_PHASE", two)
+        on, tg, mem, opt, cfg = learner(P, **CASES[name])
+        res = P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(3))
+        runs.append((res, on.flat_values.clone()))
+    (ra, wa), (rb, wb) = runs
+    for f in ("targets", "td_errors", "losses"):
+        assert rel_norm(getattr(ra, f), getattr(rb, f)) < 1e-5, f
+    assert rel_norm(wa.cpu().numpy(), wb.cpu().numpy()) < 1e-5

@@ -63,3 +63,26 @@ for _ in range(200):
 e1.record()
 torch.cuda.synchronize()
 print(f"whole update  {e0.elapsed_time(e1) / 200 * 1e3:7.2f} us (graph replay)")
+
+# the fused head (K1: both Q heads + TD block, K2: head backward + wgrad)
+import ctypes as C  # noqa: E402
+from paper_1804_05834_b200 import _lib  # noqa: E402
+
+
+def head():
+    out = pl.d_out
+    _lib.call("dqn_head_td", _lib.stream_ptr(), C.byref(on.desc_for(pl.x)), on.flat_values.data_ptr(),
+              on.flat_grads.data_ptr(), C.byref(pl.on_bind.struct), C.byref(pl.on_view.struct),
+              C.byref(tg.desc_for(pl.x)), tg.flat_values.data_ptr(), C.byref(pl.tg_bind.struct),
+              pl.a.data_ptr(), pl.r.data_ptr(), pl.t.data_ptr(), pl.w.data_ptr(), pl.gamma,
+              pl.flags_td, out[:k].data_ptr(), out[k:2 * k].data_ptr(), out[2 * k:3 * k].data_ptr(),
+              out[3 * k:].data_ptr(), pl.head_work.data_ptr(), pl.flags.data_ptr())
+
+
+print(f"head_td (K1+K2) {timeit(head):7.2f} us")
+for only in ("q", "td"):
+    os.environ["DQN_B200_HEAD_ONLY"] = only
+    print(f"head only {only:3s}    {timeit(head):7.2f} us")
+os.environ.pop("DQN_B200_HEAD_ONLY")
+print(f"rms_apply+sync {timeit(lambda: (opt.enqueue_apply(pl.flags), P.sync_target(on, tg))):7.2f} us")
+print(f"empty kernel   {timeit(lambda: _lib.call('dqn_sync_target', _lib.stream_ptr(), tg.flat_values.data_ptr(), on.flat_values.data_ptr(), 0)):7.2f} us")
