@@ -314,6 +314,19 @@ int dqn_ipc_handle(void *ptr, uint8_t *handle64);
 int dqn_ipc_open(const uint8_t *handle64, void **ptr);
 int dqn_ipc_close(void *ptr);
 
+/* dqn_tree_sample followed by dqn_ring_gather of the sampled slots (states,
+ * next states, metadata) in ONE launch: each gather CTA descends its own
+ * query, one extra CTA row computes the batch-normalised IS weights.  Same
+ * results as the two calls (replay.py:104-115, 215-230); 16-byte aligned
+ * frames (slot_bytes % 16 == 0). */
+int dqn_sample_gather(void *stream, const double *nodes, int32_t depth, const int64_t *size,
+                      const double *u, int32_t k, const double *beta, int64_t *idx,
+                      double *prob, double *weight, int32_t *flags, const uint8_t *states,
+                      const uint8_t *next_states, int64_t slot_bytes, const int64_t *actions,
+                      const double *rewards, const uint8_t *terminals, uint8_t *out_states,
+                      uint8_t *out_next_states, int64_t *out_actions, double *out_rewards,
+                      uint8_t *out_terminals);
+
 /* CUDA-graph plumbing for the learner (no reference counterpart: the
  * reference runs eagerly).  Instantiate a captured cudaGraph_t, optionally
  * honouring per-kernel-node priorities (every launch of this library carries

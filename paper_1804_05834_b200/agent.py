@@ -168,6 +168,8 @@ class _StepPlan:
             n = int(_lib.lib.dqn_net_forward_group_scratch(C.byref(self.on_desc),
                                                            self.head_layer, k))
             self.grp_scratch = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.fused_sample = (ring.slot_bytes % 16 == 0 and ring.states.dtype == torch.uint8
+                             and os.environ.get("DQN_B200_FUSED_SAMPLE", "1") != "0")
         self.side = torch.cuda.Stream(priority=0)
         self.tree_stream = torch.cuda.Stream(priority=hi)
         self.capture_stream = torch.cuda.Stream(priority=hi)
@@ -185,13 +187,26 @@ class _StepPlan:
         torch = _lib.require_cuda()
         st = _lib.stream_ptr()
         k, ring = self.k, self.ring
-        if self.per:
+        if self.per and self.fused_sample:
+            # descent + IS weights + frame gather in one launch
             self.d_in.copy_(self.h_in, non_blocking=True)
-            self.memory.sample_indices(self.d_in[:k], k, self.d_in[k:], self.idx, self.prob,
-                                       self.w, self.flags)
+            tree = self.memory.tree
+            _lib.call("dqn_sample_gather", st, tree.nodes.data_ptr(), tree.depth,
+                      ring._size_dev.data_ptr(), self.d_in.data_ptr(), k,
+                      self.d_in[k:].data_ptr(), self.idx.data_ptr(), self.prob.data_ptr(),
+                      self.w.data_ptr(), self.flags.data_ptr(), ring.states.data_ptr(),
+                      ring.next_states.data_ptr(), ring.slot_bytes, ring.actions.data_ptr(),
+                      ring.rewards.data_ptr(), ring.terminals.data_ptr(), self.x.data_ptr(),
+                      self.x[k:].data_ptr(), self.a.data_ptr(), self.r.data_ptr(),
+                      self.t.data_ptr())
         else:
-            self.idx.copy_(self.h_idx, non_blocking=True)
-        ring.gather_into(self.idx, k, self.x[:k], self.x[k:], self.a, self.r, self.t)
+            if self.per:
+                self.d_in.copy_(self.h_in, non_blocking=True)
+                self.memory.sample_indices(self.d_in[:k], k, self.d_in[k:], self.idx, self.prob,
+                                           self.w, self.flags)
+            else:
+                self.idx.copy_(self.h_idx, non_blocking=True)
+            ring.gather_into(self.idx, k, self.x[:k], self.x[k:], self.a, self.r, self.t)
         # priorities are updated inside enqueue_learn, beside the backward pass
         self.enqueue_learn(priorities=self.per)
         if self.grad_clip > 0.0:

@@ -161,6 +161,96 @@ __global__ void tree_sample_kernel(const double *__restrict__ nodes, int depth,
   if (j < k) weight[j] = __ddiv_rn(w, red[0]);                    // w /= w.max()
 }
 
+// PrioritizedReplay.sample + ReplayMemory._gather in ONE launch (the
+// learner's first kernel): CTA (x, j, which) for j < k descends query j
+// itself (thread 0; the same arithmetic as tree_sample_kernel) and copies its
+// share of state / next state j, CTA (0, j, 0) also the metadata; the extra
+// CTA row y = k descends all k queries for the IS weights (batch max) and
+// writes idx / prob / weight.  Results identical to tree_sample + ring_gather.
+__global__ void __launch_bounds__(kGatherThreads)
+sample_gather_kernel(const double *__restrict__ nodes, int depth, const int64_t *__restrict__ size_p,
+                     const double *__restrict__ u, int k, const double *__restrict__ beta_p,
+                     int64_t *__restrict__ idx, double *__restrict__ prob,
+                     double *__restrict__ weight, int32_t *flags, const int4 *__restrict__ states,
+                     const int4 *__restrict__ next_states, int64_t slot_vecs,
+                     int4 *__restrict__ out_s, int4 *__restrict__ out_s2,
+                     const int64_t *__restrict__ actions, const double *__restrict__ rewards,
+                     const uint8_t *__restrict__ terminals, int64_t *out_a, double *out_r,
+                     uint8_t *out_t) {
+  pdl_begin();   // programmatic dependent launch (common.cuh)
+  const int j = blockIdx.y;
+  const double total = nodes[1];
+  const bool ok = total > 0.0;
+  if (j == k) {                                   // the weights CTA
+    if (blockIdx.x != 0 || blockIdx.z != 0) return;
+    __shared__ double red[kGatherThreads / 32];
+    double mx = 0.0;
+    const double beta = *beta_p, size = (double)*size_p, seg = __ddiv_rn(total, (double)k);
+    const double hi = nextafter(total, 0.0);
+    for (int q = threadIdx.x; q < k; q += blockDim.x) {
+      if (!ok) {
+        idx[q] = 0; prob[q] = 0.0; weight[q] = 0.0;
+        continue;
+      }
+      double leaf;
+      const int64_t i = tree_descend(nodes, depth, __dmul_rn(__dadd_rn((double)q, u[q]), seg), hi,
+                                     &leaf);
+      const double p = __ddiv_rn(leaf, total);
+      const double w = pow(__dmul_rn(size, p), -beta);
+      idx[q] = i;
+      prob[q] = p;
+      weight[q] = w;
+      mx = fmax(mx, w);
+    }
+    if (!ok) {
+      if (threadIdx.x == 0) raise_flag(flags, DQN_FLAG_ZERO_TOTAL);
+      return;
+    }
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v = red[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+      red[0] = v;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < k; q += blockDim.x) weight[q] = __ddiv_rn(weight[q], red[0]);
+    return;
+  }
+  __shared__ int64_t s_slot;
+  if (threadIdx.x == 0) {
+    int64_t i = 0;
+    if (ok)
+      i = tree_descend(nodes, depth,
+                       __dmul_rn(__dadd_rn((double)j, u[j]), __ddiv_rn(total, (double)k)),
+                       nextafter(total, 0.0));
+    s_slot = i;
+    if (blockIdx.x == 0 && blockIdx.z == 0) {
+      if (out_a) out_a[j] = actions[i];
+      if (out_r) out_r[j] = rewards[i];
+      if (out_t) out_t[j] = terminals[i];
+    }
+  }
+  __syncthreads();
+  const int64_t slot = s_slot;
+  const int which = blockIdx.z;
+  const int4 *s = (which ? next_states : states) + slot * slot_vecs;
+  int4 *d = (which ? out_s2 : out_s) + (int64_t)j * slot_vecs;
+  const int64_t base = (int64_t)blockIdx.x * kGatherChunk + threadIdx.x;
+  int4 v[kGatherUnroll];
+#pragma unroll
+  for (int uu = 0; uu < kGatherUnroll; ++uu) {
+    const int64_t e = base + uu * kGatherThreads;
+    if (e < slot_vecs) v[uu] = __ldg(s + e);
+  }
+#pragma unroll
+  for (int uu = 0; uu < kGatherUnroll; ++uu) {
+    const int64_t e = base + uu * kGatherThreads;
+    if (e < slot_vecs) d[e] = v[uu];
+  }
+}
+
 // Large-k variant, pass 1: per-query descent, raw weights, per-CTA max.
 __global__ void tree_sample_raw_kernel(const double *__restrict__ nodes, int depth,
                                        const int64_t *__restrict__ size_p,
@@ -686,6 +776,32 @@ extern "C" int dqn_tree_sample(void *stream, const double *nodes, int32_t depth,
   DQN_LAUNCH_CHECK("tree_sample_raw");
   launch_k(tree_sample_norm_kernel, grid_for(k, 256), 256, 0, st, weight, k, scratch, blocks);
   DQN_LAUNCH_CHECK("tree_sample_norm");
+  return DQN_OK;
+}
+
+extern "C" int dqn_sample_gather(void *stream, const double *nodes, int32_t depth,
+                                 const int64_t *size, const double *u, int32_t k,
+                                 const double *beta, int64_t *idx, double *prob, double *weight,
+                                 int32_t *flags, const uint8_t *states,
+                                 const uint8_t *next_states, int64_t slot_bytes,
+                                 const int64_t *actions, const double *rewards,
+                                 const uint8_t *terminals, uint8_t *out_states,
+                                 uint8_t *out_next_states, int64_t *out_actions,
+                                 double *out_rewards, uint8_t *out_terminals) {
+  DQN_CHECK_ARG(nodes && size && u && beta && idx && prob && weight && k >= 1 && depth >= 1 &&
+                    depth < 40 && states && next_states && out_states && out_next_states &&
+                    slot_bytes > 0 && slot_bytes % 16 == 0 && (uintptr_t)states % 16 == 0 &&
+                    (uintptr_t)next_states % 16 == 0 && (uintptr_t)out_states % 16 == 0 &&
+                    (uintptr_t)out_next_states % 16 == 0 && k < 65535,
+                "sample_gather: bad args (16-byte aligned frames)");
+  const int64_t vecs = slot_bytes / 16;
+  dim3 grid((unsigned)((vecs + kGatherChunk - 1) / kGatherChunk), (unsigned)k + 1, 2);
+  launch_k(sample_gather_kernel, grid, kGatherThreads, 0, as_stream(stream), nodes, depth, size,
+           u, k, beta, idx, prob, weight, flags, reinterpret_cast<const int4 *>(states),
+           reinterpret_cast<const int4 *>(next_states), vecs,
+           reinterpret_cast<int4 *>(out_states), reinterpret_cast<int4 *>(out_next_states),
+           actions, rewards, terminals, out_actions, out_rewards, out_terminals);
+  DQN_LAUNCH_CHECK("sample_gather");
   return DQN_OK;
 }
 

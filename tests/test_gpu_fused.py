@@ -172,3 +172,31 @@ def test_head_two_phase_matches_last_cta_form(P, name, monkeypatch):
     for f in ("targets", "td_errors", "losses"):
         assert rel_norm(getattr(ra, f), getattr(rb, f)) < 1e-5, f
     assert rel_norm(wa.cpu().numpy(), wb.cpu().numpy()) < 1e-5
+
+
+def test_fused_sample_gather_matches_two_launches(P, monkeypatch):
+    """dqn_sample_gather (descent + IS weights + frame gather in one launch)
+    against dqn_tree_sample + dqn_ring_gather: identical indices, weights,
+    gathered batch and update."""
+    runs = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("DQN_B200_FUSED_SAMPLE", fused)
+        on, tg, mem, opt, cfg = learner(P, **CASES["cfg4"])
+        rng = np.random.default_rng(8)
+        res = [P.learn_step(on, tg, mem, opt, cfg, 10 + s, rng) for s in range(3)]
+        plan = next(p for p in P.agent._PLANS.values() if p.online is on)
+        assert plan.fused_sample == (fused == "1")
+        runs.append((res, plan.idx.clone(), plan.w.clone(), plan.x.clone(), plan.a.clone(),
+                     on.flat_values.clone(), mem.tree.nodes.clone()))
+    a, b = runs
+    for ra, rb in zip(a[0], b[0]):
+        assert np.array_equal(ra.td_errors, rb.td_errors)
+    for ta, tb in zip(a[1:], b[1:]):
+        assert torch.equal(ta, tb)
+
+
+def test_fused_sample_gather_zero_total_raises(P):
+    on, tg, mem, opt, cfg = learner(P, **CASES["cfg4"])
+    mem.tree.load_leaves(np.zeros(mem.capacity))
+    with pytest.raises(ValueError):
+        P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(0))
