@@ -380,9 +380,18 @@ bool conv_ok(const dqn_layer_desc &L) {
 }
 
 // forward split length: a function of K only (batch-independent rows)
+inline int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 inline int fwd_klen(int K) {
-  if (K >= 2048) return ceil_div(ceil_div(K, 8), tc::BK) * tc::BK;   // 8 splits (fc1: 416)
-  if (K >= 512) return 192;
+  static const int s_long = env_int("DQN_B200_FWD_SPLITS", 8);      // diagnostic overrides
+  static const int kl_mid = env_int("DQN_B200_FWD_KLEN", 256);
+  // measured in the learner's graph: conv2 / conv3 (K = 512 / 576) best at
+  // 256-k splits, fc1 (K = 3136) at 8 splits
+  if (K >= 2048) return ceil_div(ceil_div(K, s_long), tc::BK) * tc::BK;   // 8 splits (fc1: 448)
+  if (K >= 512) return kl_mid;
   return K;
 }
 
@@ -486,7 +495,8 @@ int lin_dgrad_launch(cudaStream_t st, const float *dy, const float *w, const flo
   p.M = M;
   p.N = N;
   p.K = K;
-  split_k(ceil_div(M, tc::BM) * ceil_div(N, BN), K, BN, 16, p.klen, p.ksplits);
+  static const int cap = env_int("DQN_B200_DGRAD_CAP", 16);
+  split_k(ceil_div(M, tc::BM) * ceil_div(N, BN), K, BN, cap, p.klen, p.ksplits);
   return tc::launch(st, p, p.ksplits, "tc_lin_dgrad");
 }
 
@@ -521,7 +531,8 @@ int conv_dgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const float *dy,
   p.N = L.in_c;
   p.K = (L.fh / L.sh) * (L.fw / L.sw) * L.out_c;
   // split K until phases x tiles x splits fill the machine
-  split_k(L.sh * L.sw * ceil_div(p.M, tc::BM) * ceil_div(p.N, BN), p.K, BN, 16, p.klen, p.ksplits);
+  static const int cap = env_int("DQN_B200_CDGRAD_CAP", 4);   // measured best in the learner
+  split_k(L.sh * L.sw * ceil_div(p.M, tc::BM) * ceil_div(p.N, BN), p.K, BN, cap, p.klen, p.ksplits);
   return tc::launch(st, p, L.sh * L.sw * p.ksplits, "tc_conv_dgrad");
 }
 
@@ -541,9 +552,14 @@ int conv_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const 
   return DQN_ERR_UNSUPPORTED;
 }
 
-inline void wgrad_split(int M, int N, int K, int bn, int &klen, int &splits) {
-  // ~2 CTA waves over the machine, split lengths a multiple of BK
-  split_k(ceil_div(M, tc::BM) * ceil_div(N, bn), K, bn, 128, klen, splits);
+inline void wgrad_split(int M, int N, int K, int bn, bool u8, int &klen, int &splits) {
+  // split lengths a multiple of BK, count from the latency model, capped
+  // (measured in the learner's graph: the model alone picks ~67 splits for
+  // conv1's K = 12,800, whose last-arrival fixup then tails the update; 32
+  // is 6 % faster end to end)
+  static const int cap_f = env_int("DQN_B200_WGRAD_CAP", 32);
+  static const int cap_u8 = env_int("DQN_B200_WGRAD_CAP_U8", 32);
+  split_k(ceil_div(M, tc::BM) * ceil_div(N, bn), K, bn, u8 ? cap_u8 : cap_f, klen, splits);
 }
 
 template <typename InT, int BN>
@@ -563,7 +579,7 @@ int wgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const u
   p.K = batch * L.out_h * L.out_w;
   p.xt = (xt && p.K % 16 == 0) ? xt : nullptr;      // whole 16-pixel runs only
   int splits;
-  wgrad_split(p.M, p.N, p.K, BN, p.klen, splits);
+  wgrad_split(p.M, p.N, p.K, BN, sizeof(InT) == 1, p.klen, splits);
   p.partial = scratch;
   p.bias_partial = scratch + (int64_t)splits * p.M * p.N;
   p.ksplits = splits;
@@ -585,8 +601,10 @@ int wgrad_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const
 int64_t wgrad_scratch_tc(const dqn_layer_desc &L, int batch) {
   const int M = L.fh * L.fw * L.in_c, N = L.out_c, K = batch * L.out_h * L.out_w;
   const int bn = N == 32 ? 32 : 64;
-  int klen, splits;
-  wgrad_split(M, N, K, bn, klen, splits);
+  int klen, s0, s1;
+  wgrad_split(M, N, K, bn, false, klen, s0);
+  wgrad_split(M, N, K, bn, true, klen, s1);
+  const int splits = s0 > s1 ? s0 : s1;      // either input type
   return (int64_t)splits * M * N + (int64_t)splits * N;
 }
 
