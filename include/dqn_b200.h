@@ -50,7 +50,7 @@ typedef enum {
 #define DQN_FLAG_BAD_PRIORITY   0x10 /* SumTree.set with negative / non-finite value */
 
 const char *dqn_last_error(void);
-int dqn_abi_version(void);             /* 2 */
+int dqn_abi_version(void);             /* 3 */
 /* 1 if this library was built with the tcgen05 (sm_100a UMMA) conv trunk */
 int dqn_has_tcgen05(void);
 /* kernels launched (or captured) through this library so far, all threads */
@@ -195,13 +195,17 @@ int64_t dqn_head_td_work_bytes(int32_t batch, int32_t n_actions);
  * exactly as dqn_td_loss (targets/td/losses/stats, dq into on_view->dact[L-1]),
  * the head backward into on_view->dact[L-2] (masked by the hidden ReLU) and
  * the head weight gradient added to on_grads.  Linear or dueling heads with
- * at most 18 actions and batch <= 1024; DQN_ERR_UNSUPPORTED otherwise. */
+ * at most 18 actions and batch <= 1024; DQN_ERR_UNSUPPORTED otherwise.
+ * host_out (optional, pinned host memory mapped for the device): also gets
+ * [targets | td | losses | stats] (3 batch + 2 doubles), written by the
+ * kernel itself -- no device-to-host copy in the learner's graph. */
 int dqn_head_td(void *stream, const dqn_net_desc *on_net, const float *on_params,
                 float *on_grads, const dqn_binding *on_bind, const dqn_binding *on_view,
                 const dqn_net_desc *tg_net, const float *tg_params, const dqn_binding *tg_bind,
                 const int64_t *actions, const double *rewards, const uint8_t *terminals,
                 const double *weights, double gamma, int32_t td_flags, double *targets,
-                double *td, double *losses, double *stats, void *work, int32_t *flags);
+                double *td, double *losses, double *stats, void *work, int32_t *flags,
+                double *host_out);
 
 #define DQN_TD_DOUBLE 0x1
 #define DQN_TD_HUBER 0x2
@@ -228,9 +232,12 @@ int dqn_rmsprop_step(void *stream, float *w, float *g, float *acc, int64_t n,
 /* The update of dqn_rmsprop_step without the finiteness scan, for gradients
  * whose producers raised DQN_FLAG_NONFINITE_GRAD as they wrote them
  * (dqn_net_layer phase 2 with a flag word, dqn_head_td): skipped on any error
- * flag, exactly as dqn_rmsprop_step. */
+ * flag, exactly as dqn_rmsprop_step.  flag_out (optional, pinned host memory):
+ * receives the step's flag word once every earlier kernel of the stream has
+ * completed (the learner's completion signal, polled by the host). */
 int dqn_rmsprop_apply(void *stream, float *w, float *g, float *acc, int64_t n, float lr,
-                      float rho, float one_minus_rho, float eps, int32_t *flags);
+                      float rho, float one_minus_rho, float eps, int32_t *flags,
+                      int32_t *flag_out);
 
 /* clip_gradients (optim.py:61-75): fp64 global L2 norm into *norm_out; if
  * norm > max_norm, g *= f32(max_norm / norm). */

@@ -70,7 +70,7 @@ _SIGS = {
     "dqn_head_td_work_bytes": ([i32, i32], i64),
     "dqn_head_td": ([vp, C.POINTER(NetDesc), vp, vp, C.POINTER(Binding), C.POINTER(Binding),
                      C.POINTER(NetDesc), vp, C.POINTER(Binding), vp, vp, vp, vp, f64, i32,
-                     vp, vp, vp, vp, vp, vp], C.c_int),
+                     vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "dqn_net_im2col_t": ([vp, C.POINTER(NetDesc), C.POINTER(Binding)], C.c_int),
     "dqn_net_forward": ([vp, C.POINTER(NetDesc), vp, C.POINTER(Binding), vp], C.c_int),
     "dqn_net_backward": ([vp, C.POINTER(NetDesc), vp, C.POINTER(Binding), vp], C.c_int),
@@ -79,7 +79,7 @@ _SIGS = {
     "dqn_td_loss": ([vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, f64, i32, vp, vp, vp, vp, vp],
                     C.c_int),
     "dqn_rmsprop_step": ([vp, vp, vp, vp, i64, f32, f32, f32, f32, vp], C.c_int),
-    "dqn_rmsprop_apply": ([vp, vp, vp, vp, i64, f32, f32, f32, f32, vp], C.c_int),
+    "dqn_rmsprop_apply": ([vp, vp, vp, vp, i64, f32, f32, f32, f32, vp, vp], C.c_int),
     "dqn_clip_gradients": ([vp, vp, i64, f64, vp], C.c_int),
     "dqn_sync_target": ([vp, vp, vp, i64], C.c_int),
     "dqn_net_forward_group_scratch": ([vp, C.c_int, C.c_int], i64),

@@ -170,6 +170,10 @@ class _StepPlan:
             self.grp_scratch = torch.zeros(n, dtype=torch.float32, device=dev)
         self.fused_sample = (ring.slot_bytes % 16 == 0 and ring.states.dtype == torch.uint8
                              and os.environ.get("DQN_B200_FUSED_SAMPLE", "1") != "0")
+        self.zero_copy = (k * (self.nA + 1) <= 2048
+                          and os.environ.get("DQN_B200_ZEROCOPY", "1") != "0"
+                          and os.environ.get("DQN_B200_HEAD_TWO_PHASE", "1") != "0")
+        self._host_out = None
         self.side = torch.cuda.Stream(priority=0)
         self.tree_stream = torch.cuda.Stream(priority=hi)
         self.capture_stream = torch.cuda.Stream(priority=hi)
@@ -187,13 +191,23 @@ class _StepPlan:
         torch = _lib.require_cuda()
         st = _lib.stream_ptr()
         k, ring = self.k, self.ring
+        # zero-copy I/O: the draws are read from pinned host memory by the
+        # first kernel, TdResult and the flag word are written to pinned host
+        # memory by the head and the optimizer kernels -- no memcpy nodes
+        zc = (io and self.zero_copy and self.per and self.fused_sample and self.fused_head
+              and self.grad_clip == 0.0)
+        self._host_out = self.h_out if zc else None
         if self.per and self.fused_sample:
-            # descent + IS weights + frame gather in one launch
-            self.d_in.copy_(self.h_in, non_blocking=True)
+            # descent + IS weights + frame gather in one launch, reading the
+            # draws where they are (pinned host buffer, or a device slot)
+            src = self.h_in
+            if not zc and src.device.type == "cpu":
+                self.d_in.copy_(self.h_in, non_blocking=True)
+                src = self.d_in
             tree = self.memory.tree
             _lib.call("dqn_sample_gather", st, tree.nodes.data_ptr(), tree.depth,
-                      ring._size_dev.data_ptr(), self.d_in.data_ptr(), k,
-                      self.d_in[k:].data_ptr(), self.idx.data_ptr(), self.prob.data_ptr(),
+                      ring._size_dev.data_ptr(), src.data_ptr(), k,
+                      src[k:].data_ptr(), self.idx.data_ptr(), self.prob.data_ptr(),
                       self.w.data_ptr(), self.flags.data_ptr(), ring.states.data_ptr(),
                       ring.next_states.data_ptr(), ring.slot_bytes, ring.actions.data_ptr(),
                       ring.rewards.data_ptr(), ring.terminals.data_ptr(), self.x.data_ptr(),
@@ -214,8 +228,8 @@ class _StepPlan:
         else:
             # every gradient of the update came from launches that flagged
             # non-finite values into self.flags as they wrote them
-            self.opt.enqueue_apply(self.flags)
-        if io:
+            self.opt.enqueue_apply(self.flags, flag_out=self.h_flags if zc else None)
+        if io and not zc:
             self.h_out.copy_(self.d_out, non_blocking=True)
             self.h_flags.copy_(self.flags, non_blocking=True)
         del torch
@@ -288,7 +302,8 @@ class _StepPlan:
                       self.a.data_ptr(), self.r.data_ptr(), self.t.data_ptr(), self.w.data_ptr(),
                       self.gamma, self.flags_td, out[:k].data_ptr(), out[k:2 * k].data_ptr(),
                       out[2 * k:3 * k].data_ptr(), out[3 * k:].data_ptr(),
-                      self.head_work.data_ptr(), self.flags.data_ptr())
+                      self.head_work.data_ptr(), self.flags.data_ptr(),
+                      None if self._host_out is None else self._host_out.data_ptr())
             first = self.head_layer - 1
         else:
             q_on = self.on_bind.act[-1]

@@ -47,6 +47,7 @@ struct HeadTdArgs {
   float *gs;               // work: [k][nA + 1] branch gradients (gv, ga) or g
   int *ticket;             // work: CTA arrival counter (0 at rest)
   int32_t *flags;
+  double *host_out;        // optional pinned host copy: targets | td | losses | stats
 };
 
 // DQN_B200_HEAD_TWO_PHASE=0 selects the last-CTA form (head_q_td + head_bwd_wgrad)
@@ -338,6 +339,11 @@ __global__ void __launch_bounds__(kHeadCta) head_td_bwd_kernel(const HeadTdArgs 
       p.targets[j] = y;
       p.td[j] = d;
       p.losses[j] = loss;
+      if (p.host_out) {
+        p.host_out[j] = y;
+        p.host_out[k + j] = d;
+        p.host_out[2 * k + j] = loss;
+      }
       for (int c = 0; c < NA; ++c) p.dq[(int64_t)j * NA + c] = (c == a) ? gf : 0.f;
       acc_abs = __dadd_rn(acc_abs, fabs(d));
       acc_loss = __dadd_rn(acc_loss, loss);
@@ -358,8 +364,13 @@ __global__ void __launch_bounds__(kHeadCta) head_td_bwd_kernel(const HeadTdArgs 
     if (t == 0) {
       p.stats[0] = s_abs[0];
       p.stats[1] = s_loss[0];
+      if (p.host_out) {
+        p.host_out[3 * k] = s_abs[0];
+        p.host_out[3 * k + 1] = s_loss[0];
+      }
     }
   }
+  if (writer && p.host_out) __threadfence_system();     // before any later completion signal
   if ((int)blockIdx.x < nb_dx) {
     const int e = blockIdx.x * kHeadCta + t;
     if (e >= k * F) return;
@@ -429,6 +440,10 @@ int launch_head_td(cudaStream_t st, const HeadTdArgs &p) {
   const int R = p.on.rows + p.tg.rows;
   const int nb_dx = p.dx ? (p.k * p.F + kHeadCta - 1) / kHeadCta : 0;
   const int nb_w = (p.F + 1 + kHeadCta - 1) / kHeadCta;
+  if (p.host_out && !(p.k * (NA + 1) <= kGsMax && head_two_phase())) {
+    set_error("head_td: host_out needs the two-phase form (batch * (nA + 1) <= %d)", kGsMax);
+    return DQN_ERR_UNSUPPORTED;
+  }
   if (p.k * (NA + 1) <= kGsMax && head_two_phase()) {
     const char *only = getenv("DQN_B200_HEAD_ONLY");      // diagnostic: "q" or "td"
     if (!only || only[0] != 't') {
@@ -499,7 +514,7 @@ extern "C" int dqn_head_td(void *stream, const dqn_net_desc *on_net, const float
                            const int64_t *actions, const double *rewards,
                            const uint8_t *terminals, const double *weights, double gamma,
                            int32_t td_flags, double *targets, double *td, double *losses,
-                           double *stats, void *work, int32_t *flags) {
+                           double *stats, void *work, int32_t *flags, double *host_out) {
   DQN_CHECK_ARG(on_net && on_params && on_grads && on_bind && on_view && tg_net && tg_params &&
                     tg_bind && actions && rewards && terminals && weights && targets && td &&
                     losses && work,
@@ -547,6 +562,7 @@ extern "C" int dqn_head_td(void *stream, const dqn_net_desc *on_net, const float
   p.ticket = reinterpret_cast<int *>(work);
   p.gs = reinterpret_cast<float *>(reinterpret_cast<char *>(work) + 256);
   p.flags = flags;
+  p.host_out = host_out;
   if (!p.dq) {
     set_error("head_td: on_view has no head gradient buffer");
     return DQN_ERR_INVALID_ARG;

@@ -76,8 +76,15 @@ __device__ __forceinline__ void rms_one(float &w, float &g, float &a, float lr, 
 
 __global__ void rms_apply_kernel(float *__restrict__ w, float *__restrict__ g,
                                  float *__restrict__ acc, int64_t n, float lr, float rho,
-                                 float omr, float eps, const int32_t *__restrict__ flags) {
+                                 float omr, float eps, const int32_t *__restrict__ flags,
+                                 int32_t *flag_out) {
   pdl_begin();   // programmatic dependent launch (common.cuh)
+  // completion signal for the host: every earlier kernel of the update has
+  // finished (and its host-memory results were fenced) once this runs
+  if (flag_out && blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence_system();
+    *(volatile int32_t *)flag_out = *flags;
+  }
   // optim.py:38-40: a non-finite gradient aborts the step before any update;
   // any earlier failure of this step (the reference would have raised before
   // reaching the optimizer) does too.  Flags are sticky until the host reads.
@@ -182,7 +189,8 @@ extern "C" int dqn_rmsprop_step(void *stream, float *w, float *g, float *acc, in
   launch_k(rms_scan_kernel, blocks, 256, 0, st, g, n, flags);
   DQN_LAUNCH_CHECK("rms_scan");
   const int blocks4 = (int)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, 148 * 4));
-  launch_k(rms_apply_kernel, blocks4, 256, 0, st, w, g, acc, n, lr, rho, one_minus_rho, eps, flags);
+  launch_k(rms_apply_kernel, blocks4, 256, 0, st, w, g, acc, n, lr, rho, one_minus_rho, eps, flags,
+           (int32_t *)nullptr);
   DQN_LAUNCH_CHECK("rms_apply");
   return DQN_OK;
 }
@@ -192,14 +200,18 @@ extern "C" int dqn_rmsprop_step(void *stream, float *w, float *g, float *acc, in
 // the step is skipped on any error flag exactly as in dqn_rmsprop_step.
 extern "C" int dqn_rmsprop_apply(void *stream, float *w, float *g, float *acc, int64_t n,
                                  float lr, float rho, float one_minus_rho, float eps,
-                                 int32_t *flags) {
+                                 int32_t *flags, int32_t *flag_out) {
   DQN_CHECK_ARG(w && g && acc && flags && n >= 0, "rmsprop: bad args");
   DQN_CHECK_ARG(((uintptr_t)w | (uintptr_t)g | (uintptr_t)acc) % 16 == 0,
                 "rmsprop: buffers must be 16-byte aligned");
   if (n == 0) return DQN_OK;
-  const int blocks4 = (int)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, 148 * 4));
+  static const int cap = [] {
+    const char *e = getenv("DQN_B200_RMS_BLOCKS");     // diagnostic
+    return e ? atoi(e) : 148 * 8;                       // measured best in the learner graph
+  }();
+  const int blocks4 = (int)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, cap));
   launch_k(rms_apply_kernel, blocks4, 256, 0, as_stream(stream), w, g, acc, n, lr, rho,
-           one_minus_rho, eps, flags);
+           one_minus_rho, eps, flags, flag_out);
   DQN_LAUNCH_CHECK("rms_apply");
   return DQN_OK;
 }

@@ -54,15 +54,17 @@ class RmsProp:
                   float(self._lr32), float(self._rho32), float(self._omr32), float(self._eps32),
                   (flags if flags is not None else self._flags).data_ptr())
 
-    def enqueue_apply(self, flags) -> None:
+    def enqueue_apply(self, flags, flag_out=None) -> None:
         """Device-side step without the finiteness scan: for gradients whose
         producers flagged non-finite values into ``flags`` as they wrote them
-        (the learner's wgrad / fused-head launches); skipped on any flag."""
+        (the learner's wgrad / fused-head launches); skipped on any flag.
+        ``flag_out`` (pinned host tensor) receives the flag word from the
+        kernel itself (the learner's completion signal)."""
         net = self.net
         _lib.call("dqn_rmsprop_apply", _lib.stream_ptr(), net.flat_values.data_ptr(),
                   net.flat_grads.data_ptr(), self.flat_acc.data_ptr(), net.n_flat,
                   float(self._lr32), float(self._rho32), float(self._omr32), float(self._eps32),
-                  flags.data_ptr())
+                  flags.data_ptr(), None if flag_out is None else flag_out.data_ptr())
 
     def step(self) -> None:
         """Apply one update from the accumulated gradients, then zero them."""

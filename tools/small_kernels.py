@@ -76,7 +76,7 @@ def head():
               C.byref(tg.desc_for(pl.x)), tg.flat_values.data_ptr(), C.byref(pl.tg_bind.struct),
               pl.a.data_ptr(), pl.r.data_ptr(), pl.t.data_ptr(), pl.w.data_ptr(), pl.gamma,
               pl.flags_td, out[:k].data_ptr(), out[k:2 * k].data_ptr(), out[2 * k:3 * k].data_ptr(),
-              out[3 * k:].data_ptr(), pl.head_work.data_ptr(), pl.flags.data_ptr())
+              out[3 * k:].data_ptr(), pl.head_work.data_ptr(), pl.flags.data_ptr(), None)
 
 
 print(f"head_td (K1+K2) {timeit(head):7.2f} us")
