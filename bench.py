@@ -440,8 +440,10 @@ def run_ours(args):
             "transitions_per_sec": value * k,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": plan.h2d_bytes,
                     "d2h_bytes_per_step": plan.d2h_bytes,
-                    "path": "paper_1804_05834_b200.learn_step (host rng draws -> pinned H2D -> "
-                            "CUDA graph -> D2H TdResult)"},
+                    "path": "paper_1804_05834_b200.learn_step (host rng draws in pinned memory, "
+                            "read by the graph's first kernel -> CUDA graph -> TdResult and flag "
+                            "word written to pinned memory by the head / optimizer kernels; the "
+                            "bytes crossing the host link are counted as h2d / d2h)"},
             "roofline": roof,
             "step_roofline": {"bound": "hbm", "t_roof_us": T_ROOF_US,
                               "frac": T_ROOF_US / (ms_per_step * 1e3),
