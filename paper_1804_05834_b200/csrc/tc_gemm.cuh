@@ -362,6 +362,11 @@ struct PolBase {
 // different bindings never share counters.
 constexpr int kMaxTiles = 16384;
 
+// Split-K reducers per tile: the last R = budget / tiles + 1 arrivals (<= 8,
+// <= splits) each reduce a slice; R - 1 of them wait for the final arrival
+// on their SM, at most `budget` CTAs per launch (deadlock-free beside another
+// launch).  A kernel argument: DQN_B200_REDUCERS (default 60, at most 60).
+
 // Shared/tensor memory plan of a policy.
 template <class Pol>
 struct Plan {
@@ -422,7 +427,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 template <class Pol>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const int launch_id,
-                                                               const int cluster_ks) {
+                                                               const int cluster_ks, const int reducer_budget) {
   using PL = Plan<Pol>;
   constexpr int nacc = kNacc;
   constexpr int BN = Pol::BN, STAGES = PL::STAGES, NA = PL::NA, NB = PL::NB, RB = PL::RB;
@@ -738,7 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
     __syncthreads();
     const int tile = (zp * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     const int tiles = gridDim.x * gridDim.y * (gridDim.z / ks);
-    int R = 60 / tiles + 1;
+    int R = reducer_budget / tiles + 1;
     R = R > 8 ? 8 : R;
     R = R > ks ? ks : R;
     int *arrive = p.counters + 2 * tile, *finished = arrive + 1;
@@ -876,6 +881,15 @@ inline bool cluster_splitk_enabled() {
   return on;
 }
 
+inline int reducer_budget() {
+  static const int b = [] {
+    const char *e = getenv("DQN_B200_REDUCERS");
+    int v = e ? atoi(e) : 60;
+    return v < 0 ? 0 : (v > 60 ? 60 : v);
+  }();
+  return b;
+}
+
 template <class Pol>
 int launch(cudaStream_t st, const Pol &p, int splits, const char *what) {
   const int bytes = smem_bytes<Pol>();
@@ -918,7 +932,7 @@ int launch(cudaStream_t st, const Pol &p, int splits, const char *what) {
   attr[2].val.clusterDim.z = cks ? cks : 1;
   cfg.attrs = attr;
   cfg.numAttrs = cks ? 3 : 2;
-  cudaLaunchKernelEx(&cfg, tc_gemm_kernel<Pol>, p, launch_id, cks);
+  cudaLaunchKernelEx(&cfg, tc_gemm_kernel<Pol>, p, launch_id, cks, reducer_budget());
   DQN_LAUNCH_CHECK(what);
   return DQN_OK;
 }

@@ -408,7 +408,7 @@ inline void split_k(int tiles, int K, int bn, int cap, int &klen, int &splits) {
     const int kl = ceil_div(ceil_div(K, s), tc::BK) * tc::BK;
     if (ceil_div(K, kl) != s) continue;              // same split as a smaller s
     const int waves = ceil_div(tiles * s, kNumSMs);
-    const int R = std::min({60 / tiles + 1, 8, s});
+    const int R = std::min({tc::reducer_budget() / tiles + 1, 8, s});
     double t = waves * (3.0 + (kl / tc::BK - 1) * 0.8);
     if (s > 1) t += 1.5 + (double)s * tc::BM * bn * 4 / (70e3 * R);
     if (t < best - 1e-9) {
