@@ -219,14 +219,14 @@ sample_gather_kernel(const double *__restrict__ nodes, int depth, const int64_t 
     return;
   }
   __shared__ int64_t s_slot;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {                         // warp 0: eight levels per round trip
     int64_t i = 0;
     if (ok)
-      i = tree_descend(nodes, depth,
-                       __dmul_rn(__dadd_rn((double)j, u[j]), __ddiv_rn(total, (double)k)),
-                       nextafter(total, 0.0));
-    s_slot = i;
-    if (blockIdx.x == 0 && blockIdx.z == 0) {
+      i = warp_tree_descend(nodes, depth,
+                            __dmul_rn(__dadd_rn((double)j, u[j]), __ddiv_rn(total, (double)k)),
+                            nextafter(total, 0.0));
+    if (threadIdx.x == 0) s_slot = i;
+    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.z == 0) {
       if (out_a) out_a[j] = actions[i];
       if (out_r) out_r[j] = rewards[i];
       if (out_t) out_t[j] = terminals[i];

@@ -85,4 +85,61 @@ static __device__ __forceinline__ int64_t tree_descend(const double *__restrict_
 }
 
 
+// The same descent by one full warp, eight levels per dependent round trip:
+// the 2 + 4 + ... + 256 nodes of the eight levels below the current node are
+// loaded by the 32 lanes at once (level l's node o sits in lane o % 32, slot
+// o / 32), then the eight compare / subtract steps run exactly as above with
+// each left-child sum taken from its lane by a shuffle.  Every lane returns
+// the leaf index; *leaf_value gets nodes[leaf].
+static __device__ __forceinline__ double wsel(const double *r, int slot) {
+  double v = r[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i)
+    if (slot == i) v = r[i];
+  return v;
+}
+
+static __device__ __forceinline__ int64_t warp_tree_descend(const double *__restrict__ nodes,
+                                                            int depth, double q, double hi,
+                                                            double *leaf_value = nullptr) {
+  const int lane = threadIdx.x & 31;
+  q = fmin(fmax(q, 1e-300), hi);
+  int64_t n = 1;
+  int l = 0;
+  double leaf = 0.0;
+  while (l < depth) {
+    const int G = depth - l < 8 ? depth - l : 8;
+    // r[g][s]: node (n << (g + 1)) + 32 s + lane of level g + 1 below n
+    double r[8][8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+#pragma unroll
+      for (int sl = 0; sl < 8; ++sl) {
+        const int cnt = 2 << g;                       // nodes at this level
+        const int o = 32 * sl + lane;
+        r[g][sl] = (g < G && o < cnt) ? __ldg(nodes + (n << (g + 1)) + o) : 0.0;
+      }
+    }
+    int64_t p = 0;                                    // offset inside the level
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      if (g >= G) break;
+      const int o = (int)(2 * p);                     // left child of the path node
+      const double mine = wsel(r[g], o >> 5);
+      const double ls = __shfl_sync(0xffffffffu, mine, o & 31);
+      const bool right = q > ls;
+      if (right) q = __dsub_rn(q, ls);
+      p = 2 * p + (right ? 1 : 0);
+      if (g == G - 1 && leaf_value) {
+        const int ol = (int)p;
+        leaf = __shfl_sync(0xffffffffu, wsel(r[g], ol >> 5), ol & 31);
+      }
+    }
+    n = (n << G) + p;
+    l += G;
+  }
+  if (leaf_value) *leaf_value = leaf;
+  return n - (int64_t(1) << depth);
+}
+
 }  // namespace dqn

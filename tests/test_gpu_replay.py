@@ -240,3 +240,54 @@ def test_update_bulk_path_partial_update_then_index_error(P):
     got = mem.tree.nodes.cpu().numpy()
     assert ulp_diff(got[ref.tree.base:], ref.tree.nodes[ref.tree.base:]).max() <= 1
     assert mem.max_priority == max_before             # untouched on the raising call
+
+
+@pytest.mark.parametrize("cap", [1000, 300_000, 1 << 20])
+def test_sample_gather_equals_sample_then_gather(cap):
+    """dqn_sample_gather (warp descent, eight levels per round trip, fused
+    with the frame gather) against dqn_tree_sample + dqn_ring_gather at tree
+    depths 10, 19 and 20: identical indices, probabilities, weights, bytes."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1804_05834_b200 as P
+    from paper_1804_05834_b200 import _lib
+    mem = P.PrioritizedReplay(cap, (16,), P.PriorityConfig(0.6, 0.01, P.LinearSchedule(0.4, 1, 10)))
+    ring = mem.memory
+    rng = np.random.default_rng(cap)
+    ring.states.copy_(torch.as_tensor(rng.integers(0, 256, (cap, 16), dtype=np.uint8)))
+    ring.next_states.copy_(torch.as_tensor(rng.integers(0, 256, (cap, 16), dtype=np.uint8)))
+    ring.actions.copy_(torch.as_tensor(rng.integers(0, 4, cap)))
+    ring.rewards.copy_(torch.as_tensor(rng.standard_normal(cap)))
+    ring._set_size(cap)
+    leaves = rng.random(cap) ** 3
+    leaves[rng.integers(0, cap, cap // 10)] = 0.0
+    mem.tree.load_leaves(leaves)
+    k = 32
+    u = torch.as_tensor(np.concatenate([rng.random(k), [0.55]]), device="cuda")
+    outs = []
+    for fused in (True, False):
+        idx = torch.zeros(k, dtype=torch.int64, device="cuda")
+        prob = torch.zeros(k, dtype=torch.float64, device="cuda")
+        w = torch.zeros(k, dtype=torch.float64, device="cuda")
+        x = torch.zeros((2 * k, 16), dtype=torch.uint8, device="cuda")
+        a = torch.zeros(k, dtype=torch.int64, device="cuda")
+        r = torch.zeros(k, dtype=torch.float64, device="cuda")
+        t = torch.zeros(k, dtype=torch.bool, device="cuda")
+        fl = torch.zeros(1, dtype=torch.int32, device="cuda")
+        st = _lib.stream_ptr()
+        if fused:
+            _lib.call("dqn_sample_gather", st, mem.tree.nodes.data_ptr(), mem.tree.depth,
+                      ring._size_dev.data_ptr(), u.data_ptr(), k, u[k:].data_ptr(),
+                      idx.data_ptr(), prob.data_ptr(), w.data_ptr(), fl.data_ptr(),
+                      ring.states.data_ptr(), ring.next_states.data_ptr(), ring.slot_bytes,
+                      ring.actions.data_ptr(), ring.rewards.data_ptr(), ring.terminals.data_ptr(),
+                      x.data_ptr(), x[k:].data_ptr(), a.data_ptr(), r.data_ptr(), t.data_ptr())
+        else:
+            mem.sample_indices(u[:k], k, u[k:], idx, prob, w, fl)
+            ring.gather_into(idx, k, x[:k], x[k:], a, r, t)
+        torch.cuda.synchronize()
+        assert fl.item() == 0
+        outs.append((idx, prob, w, x, a, r, t))
+    for p_, q_ in zip(*outs):
+        assert torch.equal(p_, q_)
+    assert mem.tree.depth >= 10
