@@ -30,6 +30,8 @@ int tc_layer_forward_group(cudaStream_t st, const dqn_net_desc *net, int l,
                            const float *tg_params, const dqn_binding *tg_b, float *scratch,
                            int *counters);
 int64_t tc_forward_group_scratch(const dqn_net_desc *net, int upto, int batch);
+int lin_wgrad_smallk(cudaStream_t st, const float *x, const float *dy, int B, int F, int N,
+                     float *gw, float *gb, int32_t *flags);
 
 // tcgen05 trunk for supported geometries unless the descriptor asks for SIMT
 static bool use_tc(const dqn_net_desc *net, int l, int phase) {
@@ -55,8 +57,20 @@ static int layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const
   return simt_layer_backward(st, net, l, params, b);
 }
 // flags (optional): every written gradient is checked for non-finite values
+// opt-in: measured neutral in the learner (the wgrad runs beside the dgrad chain)
+static bool lin_wgrad_simt_enabled() {
+  const char *e = getenv("DQN_B200_LIN_WGRAD_SIMT");
+  return e && e[0] == '1';
+}
 static int layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
                        const dqn_binding *b, int32_t *flags) {
+  const dqn_layer_desc &L = net->layer[l];
+  // hidden linear layers at learner batch sizes: the small-K FMA kernel
+  if (L.kind == DQN_LAYER_LINEAR && l != net->n_layers - 1 && l > 0 && b->batch <= 64 &&
+      net->algo != 1 && lin_wgrad_simt_enabled())
+    return lin_wgrad_smallk(st, b->act[l - 1], b->dact[l], b->batch,
+                            L.in_h * L.in_w * L.in_c, L.out_c, grads + L.w_off,
+                            grads + L.b_off, flags);
   if (use_tc(net, l, 2)) return tc_layer_wgrad(st, net, l, grads, b, flags);
   return simt_layer_wgrad(st, net, l, grads, b, flags);
 }

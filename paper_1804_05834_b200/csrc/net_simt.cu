@@ -667,6 +667,88 @@ int simt_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const f
   return launch_dgrad(st, L, b->dact[l], params, mask, out, b->scratch, b->batch);
 }
 
+// ------------------------------------------------ small-K linear wgrad
+// dW[F][N] += X^T dY and db[N] += sum_r dY[r] for a linear layer at learner
+// batch sizes (B <= 64 rows, network.py:124-126 / layers.py:157-160): an
+// outer-product sum that is bandwidth-bound on dW (read-modify-write), so
+// plain fp32 FMAs (exact products, sequential sum over rows) instead of a
+// tensor-core GEMM with a half-empty 64-k block per CTA.  CTA = 64 features x
+// 128 outputs, all B rows of both operands in shared memory, 4 x 8 outputs
+// per thread; non-finite results raise DQN_FLAG_NONFINITE_GRAD.
+constexpr int kLwF = 64, kLwN = 128, kLwMaxB = 64;
+
+__global__ void __launch_bounds__(256)
+lin_wgrad_smallk_kernel(const float *__restrict__ x, const float *__restrict__ dy, int B, int F,
+                        int N, float *__restrict__ gw, float *__restrict__ gb, int32_t *flags) {
+  pdl_begin();
+  __shared__ __align__(16) float xs[kLwMaxB][kLwF];
+  __shared__ __align__(16) float ys[kLwMaxB][kLwN];
+  const int f0 = blockIdx.x * kLwF, n0 = blockIdx.y * kLwN, t = threadIdx.x;
+  for (int i = t; i < B * kLwF; i += 256) {
+    const int r = i / kLwF, c = i - r * kLwF;
+    xs[r][c] = f0 + c < F ? x[(int64_t)r * F + f0 + c] : 0.f;
+  }
+  for (int i = t; i < B * kLwN; i += 256) {
+    const int r = i / kLwN, c = i - r * kLwN;
+    ys[r][c] = n0 + c < N ? dy[(int64_t)r * N + n0 + c] : 0.f;
+  }
+  __syncthreads();
+  const int tf = (t >> 4) * 4, tn = (t & 15) * 8;     // 16 x 16 threads, 4 x 8 outputs each
+  float acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  for (int r = 0; r < B; ++r) {
+    const float4 a = *reinterpret_cast<const float4 *>(&xs[r][tf]);
+    const float4 b0 = *reinterpret_cast<const float4 *>(&ys[r][tn]);
+    const float4 b1 = *reinterpret_cast<const float4 *>(&ys[r][tn + 4]);
+    const float av[4] = {a.x, a.y, a.z, a.w};
+    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+  }
+  const bool vec = (N % 4 == 0) && n0 + tn + 8 <= N;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int f = f0 + tf + i;
+    if (f >= F) break;
+    float *row = gw + (int64_t)f * N + n0 + tn;
+    if (vec) {
+      float4 *p4 = reinterpret_cast<float4 *>(row);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float4 v = p4[h];
+        v.x = __fadd_rn(v.x, acc[i][4 * h]);
+        v.y = __fadd_rn(v.y, acc[i][4 * h + 1]);
+        v.z = __fadd_rn(v.z, acc[i][4 * h + 2]);
+        v.w = __fadd_rn(v.w, acc[i][4 * h + 3]);
+        p4[h] = v;
+        note_grad4(flags, v);
+      }
+    } else {
+      for (int j = 0; j < 8; ++j)
+        if (n0 + tn + j < N) acc_grad(row + j, acc[i][j], flags);
+    }
+  }
+  if (blockIdx.x == 0 && gb != nullptr && t < kLwN && n0 + t < N) {
+    float sb = 0.f;
+    for (int r = 0; r < B; ++r) sb = __fadd_rn(sb, ys[r][t]);
+    acc_grad(gb + n0 + t, sb, flags);
+  }
+}
+
+int lin_wgrad_smallk(cudaStream_t st, const float *x, const float *dy, int B, int F, int N,
+                     float *gw, float *gb, int32_t *flags) {
+  if (B < 1 || B > kLwMaxB) return DQN_ERR_UNSUPPORTED;
+  dim3 grid((F + kLwF - 1) / kLwF, (N + kLwN - 1) / kLwN);
+  launch_k(lin_wgrad_smallk_kernel, grid, 256, 0, st, x, dy, B, F, N, gw, gb, flags);
+  DQN_LAUNCH_CHECK("lin_wgrad_smallk");
+  return DQN_OK;
+}
+
 int simt_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
                      const dqn_binding *b, int32_t *flags) {
   const dqn_layer_desc &L = net->layer[l];

@@ -200,3 +200,16 @@ def test_fused_sample_gather_zero_total_raises(P):
     mem.tree.load_leaves(np.zeros(mem.capacity))
     with pytest.raises(ValueError):
         P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(0))
+
+
+def test_linear_wgrad_simt_matches_tcgen05(P, monkeypatch):
+    """DQN_B200_LIN_WGRAD_SIMT=1 (fc1 weight gradient as a small-K FMA
+    kernel) against the tcgen05 wgrad: same gradient within 1e-5."""
+    runs = []
+    for simt in ("1", "0"):
+        monkeypatch.setenv("DQN_B200_LIN_WGRAD_SIMT", simt)
+        on, tg, mem, opt, cfg = learner(P, **CASES["cfg4"])
+        opt.enqueue_apply = lambda flags, flag_out=None: None    # keep the gradients
+        P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(3))
+        runs.append(on.flat_grads.clone())
+    assert rel_norm(runs[0].cpu().numpy(), runs[1].cpu().numpy()) < 1e-5
