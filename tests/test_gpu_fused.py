@@ -206,6 +206,7 @@ def test_linear_wgrad_simt_matches_tcgen05(P, monkeypatch):
     """DQN_B200_LIN_WGRAD_SIMT=1 (fc1 weight gradient as a small-K FMA
     kernel) against the tcgen05 wgrad: same gradient within 1e-5."""
     runs = []
+    monkeypatch.setenv("DQN_B200_ZEROCOPY", "0")     # the stubbed optimizer writes no host flag
     for simt in ("1", "0"):
         monkeypatch.setenv("DQN_B200_LIN_WGRAD_SIMT", simt)
         on, tg, mem, opt, cfg = learner(P, **CASES["cfg4"])
