@@ -476,6 +476,8 @@ def learn_step_collect(plan: _StepPlan) -> TdResult:
     _wait_result(plan)
     k = plan.k
     f = int(plan.h_flags_np[0])
+    if f == _SENTINEL:      # the update's completion word was never written
+        raise RuntimeError("learner update finished without reporting its status word")
     if f:
         plan.flags.zero_()
         if f & _lib.FLAG_ZERO_TOTAL:
