@@ -15,6 +15,7 @@
 // reference given the same uniforms.
 #include "common.cuh"
 #include "tree_descend.cuh"
+#include "bulk_copy.cuh"
 
 #include <math.h>
 
@@ -79,6 +80,33 @@ ring_gather_vec_kernel(const int4 *__restrict__ states, const int4 *__restrict__
   for (int u = 0; u < kGatherUnroll; ++u) {
     int64_t e = base + u * kGatherThreads;
     if (e < slot_vecs) d[e] = v[u];
+  }
+}
+
+// The same gather through the TMA bulk-copy engine: one CTA per (sample,
+// state | next state), one thread moves the whole slot global -> shared ->
+// global (cp.async.bulk); thread 1 copies the sample's metadata.
+__global__ void __launch_bounds__(32)
+ring_gather_tma_kernel(const uint8_t *__restrict__ states, const uint8_t *__restrict__ next_states,
+                       int64_t slot_bytes, const int64_t *__restrict__ idx,
+                       uint8_t *__restrict__ out_s, uint8_t *__restrict__ out_s2,
+                       const int64_t *__restrict__ actions, const double *__restrict__ rewards,
+                       const uint8_t *__restrict__ terminals, int64_t *out_a, double *out_r,
+                       uint8_t *out_t) {
+  pdl_begin();
+  extern __shared__ __align__(128) uint8_t slot_buf[];
+  __shared__ uint64_t bar;
+  const int j = blockIdx.x, which = blockIdx.y;
+  const int64_t slot = __ldg(idx + j);
+  if (threadIdx.x == 0) bc_mbar_init(&bar);
+  __syncthreads();
+  if (threadIdx.x == 0)
+    bulk_copy_via_smem(slot_buf, &bar, (which ? next_states : states) + slot * slot_bytes,
+                       (which ? out_s2 : out_s) + (int64_t)j * slot_bytes, (uint32_t)slot_bytes);
+  if (threadIdx.x == 1 && which == 0) {
+    if (out_a) out_a[j] = actions[slot];
+    if (out_r) out_r[j] = rewards[slot];
+    if (out_t) out_t[j] = terminals[slot];
   }
 }
 
@@ -167,6 +195,7 @@ __global__ void tree_sample_kernel(const double *__restrict__ nodes, int depth,
 // share of state / next state j, CTA (0, j, 0) also the metadata; the extra
 // CTA row y = k descends all k queries for the IS weights (batch max) and
 // writes idx / prob / weight.  Results identical to tree_sample + ring_gather.
+template <bool TMA>
 __global__ void __launch_bounds__(kGatherThreads)
 sample_gather_kernel(const double *__restrict__ nodes, int depth, const int64_t *__restrict__ size_p,
                      const double *__restrict__ u, int k, const double *__restrict__ beta_p,
@@ -235,6 +264,19 @@ sample_gather_kernel(const double *__restrict__ nodes, int depth, const int64_t 
   __syncthreads();
   const int64_t slot = s_slot;
   const int which = blockIdx.z;
+  if constexpr (TMA) {             // one CTA per frame: the TMA engine moves the slot
+    extern __shared__ __align__(128) uint8_t slot_buf[];
+    __shared__ uint64_t bar;
+    if (threadIdx.x == 0) {
+      bc_mbar_init(&bar);
+      const int64_t bytes = slot_vecs * 16;
+      bulk_copy_via_smem(slot_buf, &bar,
+                         reinterpret_cast<const uint8_t *>(which ? next_states : states) + slot * bytes,
+                         reinterpret_cast<uint8_t *>(which ? out_s2 : out_s) + (int64_t)j * bytes,
+                         (uint32_t)bytes);
+    }
+    return;
+  }
   const int4 *s = (which ? next_states : states) + slot * slot_vecs;
   int4 *d = (which ? out_s2 : out_s) + (int64_t)j * slot_vecs;
   const int64_t base = (int64_t)blockIdx.x * kGatherChunk + threadIdx.x;
@@ -714,6 +756,13 @@ extern "C" int dqn_ring_gather(void *stream, const uint8_t *states, const uint8_
   const bool vec = (out_states || out_next_states) && slot_bytes % 16 == 0 &&
                    ((uintptr_t)states % 16 == 0) && ((uintptr_t)next_states % 16 == 0) &&
                    ((uintptr_t)out_states % 16 == 0) && ((uintptr_t)out_next_states % 16 == 0);
+  if (vec && out_states && out_next_states && slot_bytes <= 48 * 1024 && tma_gather_enabled()) {
+    launch_k(ring_gather_tma_kernel, dim3((unsigned)k, 2), 32, (size_t)slot_bytes, st, states,
+             next_states, slot_bytes, idx, out_states, out_next_states, actions, rewards,
+             terminals, out_actions, out_rewards, out_terminals);
+    DQN_LAUNCH_CHECK("ring_gather_tma");
+    return DQN_OK;
+  }
   if (vec) {   // frames + metadata in one launch
     const int64_t vecs = slot_bytes / 16;
     dim3 grid((unsigned)((vecs + kGatherChunk - 1) / kGatherChunk), (unsigned)k, 2);
@@ -795,8 +844,17 @@ extern "C" int dqn_sample_gather(void *stream, const double *nodes, int32_t dept
                     (uintptr_t)out_next_states % 16 == 0 && k < 65535,
                 "sample_gather: bad args (16-byte aligned frames)");
   const int64_t vecs = slot_bytes / 16;
+  if (slot_bytes <= 48 * 1024 && tma_gather_enabled()) {
+    launch_k(sample_gather_kernel<true>, dim3(1, (unsigned)k + 1, 2), 32, (size_t)slot_bytes,
+             as_stream(stream), nodes, depth, size, u, k, beta, idx, prob, weight, flags,
+             reinterpret_cast<const int4 *>(states), reinterpret_cast<const int4 *>(next_states),
+             vecs, reinterpret_cast<int4 *>(out_states), reinterpret_cast<int4 *>(out_next_states),
+             actions, rewards, terminals, out_actions, out_rewards, out_terminals);
+    DQN_LAUNCH_CHECK("sample_gather_tma");
+    return DQN_OK;
+  }
   dim3 grid((unsigned)((vecs + kGatherChunk - 1) / kGatherChunk), (unsigned)k + 1, 2);
-  launch_k(sample_gather_kernel, grid, kGatherThreads, 0, as_stream(stream), nodes, depth, size,
+  launch_k(sample_gather_kernel<false>, grid, kGatherThreads, 0, as_stream(stream), nodes, depth, size,
            u, k, beta, idx, prob, weight, flags, reinterpret_cast<const int4 *>(states),
            reinterpret_cast<const int4 *>(next_states), vecs,
            reinterpret_cast<int4 *>(out_states), reinterpret_cast<int4 *>(out_next_states),

@@ -557,9 +557,12 @@ inline void wgrad_split(int M, int N, int K, int bn, bool u8, int &klen, int &sp
   // (measured in the learner's graph: the model alone picks ~67 splits for
   // conv1's K = 12,800, whose last-arrival fixup then tails the update; 32
   // is 6 % faster end to end)
-  static const int cap_f = env_int("DQN_B200_WGRAD_CAP", 32);
+  // (applies to learner-sized reductions, K <= 64k: large batches keep the
+  // model's count -- conv1 at B = 4096, K = 1.6M, is 2.3x slower at 32)
+  static const int cap_f = env_int("DQN_B200_WGRAD_CAP", 128);
   static const int cap_u8 = env_int("DQN_B200_WGRAD_CAP_U8", 32);
-  split_k(ceil_div(M, tc::BM) * ceil_div(N, bn), K, bn, u8 ? cap_u8 : cap_f, klen, splits);
+  const int cap = (u8 && K <= 65536) ? cap_u8 : cap_f;
+  split_k(ceil_div(M, tc::BM) * ceil_div(N, bn), K, bn, cap, klen, splits);
 }
 
 template <typename InT, int BN>
