@@ -444,7 +444,9 @@ template <typename InT>
 int fwd_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *params,
                  float *y, float *scratch, int *counters, int batch) {
   const int N = L.out_c;
-  if (N == 32) return fwd_launch<InT, 32>(st, L, x, params, y, scratch, counters, batch);
+  static const int bn_max = env_int("DQN_B200_FWD_BN", 64);          // diagnostic
+  if (N == 32 || (bn_max <= 32 && N % 32 == 0))
+    return fwd_launch<InT, 32>(st, L, x, params, y, scratch, counters, batch);
   if (N == 64) return fwd_launch<InT, 64>(st, L, x, params, y, scratch, counters, batch);
   if (N % 64 == 0) return fwd_launch<InT, 64>(st, L, x, params, y, scratch, counters, batch);
   return DQN_ERR_UNSUPPORTED;
@@ -504,7 +506,10 @@ int lin_dgrad(cudaStream_t st, const float *dy, const float *w, const float *mas
               float *partial, int *counters, int M, int N, int K) {
   // tiles of at most 64 columns: two [big | small] accumulator pairs + the A
   // stages fit in TMEM
+  // measured in the learner: fc1 dgrad (N = 3136) best at 32 columns per tile
+  static const int bn_max = env_int("DQN_B200_LIN_DGRAD_BN", 32);
   for (int bn : {64, 32, 16}) {
+    if (bn > bn_max) continue;
     if (N % bn) continue;
     switch (bn) {
       case 64: return lin_dgrad_launch<64>(st, dy, w, mask, out, partial, counters, M, N, K);
@@ -540,6 +545,9 @@ bool dgrad_tile_ok(int C) { return C == 16 || C == 32 || C == 48 || C % 64 == 0;
 
 int conv_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
                const float *mask, float *out, float *scratch, int *counters, int batch) {
+  static const int bn_max = env_int("DQN_B200_CONV_DGRAD_BN", 64);   // diagnostic
+  if (bn_max <= 32 && L.in_c % 32 == 0 && L.in_c > 32)
+    return conv_dgrad_launch<32>(st, L, dy, w, mask, out, scratch, counters, batch);
   switch (L.in_c) {
     case 16: return conv_dgrad_launch<16>(st, L, dy, w, mask, out, scratch, counters, batch);
     case 32: return conv_dgrad_launch<32>(st, L, dy, w, mask, out, scratch, counters, batch);
@@ -594,7 +602,8 @@ int wgrad_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const
                    const float *dy, float *grads, float *scratch, int *counters, int batch,
                    int32_t *flags) {
   const int N = L.out_c;
-  if (N == 32)
+  static const int bn_max = env_int("DQN_B200_WGRAD_BN", 64);         // diagnostic
+  if (N == 32 || (bn_max <= 32 && N % 32 == 0))
     return wgrad_launch<InT, 32>(st, L, x, xt, dy, grads, scratch, counters, batch, flags);
   if (N % 64 == 0)
     return wgrad_launch<InT, 64>(st, L, x, xt, dy, grads, scratch, counters, batch, flags);
@@ -603,11 +612,13 @@ int wgrad_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const
 
 int64_t wgrad_scratch_tc(const dqn_layer_desc &L, int batch) {
   const int M = L.fh * L.fw * L.in_c, N = L.out_c, K = batch * L.out_h * L.out_w;
-  const int bn = N == 32 ? 32 : 64;
-  int klen, s0, s1;
-  wgrad_split(M, N, K, bn, false, klen, s0);
-  wgrad_split(M, N, K, bn, true, klen, s1);
-  const int splits = s0 > s1 ? s0 : s1;      // either input type
+  int klen, splits = 1;
+  for (int bn : {32, 64})                    // either tile width and input type
+    for (bool u8 : {false, true}) {
+      int sp;
+      wgrad_split(M, N, K, bn, u8, klen, sp);
+      splits = std::max(splits, sp);
+    }
   return (int64_t)splits * M * N + (int64_t)splits * N;
 }
 
