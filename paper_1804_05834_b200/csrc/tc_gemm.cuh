@@ -378,7 +378,10 @@ struct Plan {
   static constexpr int STAGES_SMEM = (200 * 1024) / B_BYTES;
   static constexpr int STAGES_TMEM = (kTmemCols - 2 * kNacc * BN) / A_COLS;
   static constexpr int S0 = STAGES_SMEM < STAGES_TMEM ? STAGES_SMEM : STAGES_TMEM;
-  static constexpr int STAGES = S0 > 4 ? 4 : S0;
+  // an even ring: the two producer groups alternate k-blocks, so every slot
+  // stays with one group (an odd ring hands slots back and forth between the
+  // groups -- measured: LinDgradPol<32> with 3 stages raced)
+  static constexpr int STAGES = (S0 > 4 ? 4 : S0) & ~1;
   static_assert(STAGES >= kGroups, "one ring slot per producer group at least");
   static_assert(RB <= 256 && RB % 16 == 0 && BN % 16 == 0, "MMA N limits");
   static constexpr int ACC_MAX = kTmemCols - STAGES * A_COLS;   // columns for accumulators

@@ -5,6 +5,9 @@ reference's geometry / phase-order errors."""
 
 from __future__ import annotations
 
+import os
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -136,3 +139,22 @@ def test_errors(P):
     net.params()[0].weight.values.fill_(float("nan"))
     with pytest.raises(P.NonFiniteError):
         net.forward(np.ones((1, 24, 24, 4), np.float32))
+
+
+@pytest.mark.parametrize("bn", ["32", "64"])
+def test_fc1_dgrad_tiles_correct_and_deterministic(bn, monkeypatch):
+    """fc1's dgrad through the tcgen05 engine in 32- and 64-column tiles
+    against an fp64 reference, over repeated launches.  Regression test for
+    an odd producer ring (3 stages at 32 columns) that raced: every launch
+    must agree bit for bit and stay at 3xTF32 accuracy."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import subprocess
+    import sys
+    env = dict(os.environ, DQN_B200_LIN_DGRAD_BN=bn)
+    out = subprocess.run([sys.executable, "tools/lin_dgrad_check.py"], env=env, capture_output=True,
+                         text=True, timeout=300, cwd=str(Path(__file__).resolve().parent.parent))
+    line = [l for l in out.stdout.splitlines() if l.startswith("BN=")]
+    assert line, out.stdout + out.stderr
+    err = float(line[0].split("rel err ")[1].split()[0])
+    assert "deterministic True" in line[0] and err < 1e-5, line[0]
