@@ -45,7 +45,8 @@ for r in rows:
             u = d["Metric Unit"]
             us = v / 1000 if u in ("ns", "nsecond") else (v if u in ("us", "usecond") else v * 1000)
             recs.append((clean(d["Kernel Name"]), us))
-starts = [i for i, (n, _) in enumerate(recs) if n.startswith("tree_sample_kernel")]
+starts = [i for i, (n, _) in enumerate(recs)
+          if n.startswith("tree_sample_kernel") or n.startswith("sample_gather_kernel")]
 updates = []
 for a in starts:
     seg = []
