@@ -379,8 +379,12 @@ struct Plan {
   static constexpr int STAGES_TMEM = (kTmemCols - 2 * kNacc * BN) / A_COLS;
   static constexpr int S0 = STAGES_SMEM < STAGES_TMEM ? STAGES_SMEM : STAGES_TMEM;
   // an even ring: the two producer groups alternate k-blocks, so every slot
-  // stays with one group (an odd ring hands slots back and forth between the
-  // groups -- measured: LinDgradPol<32> with 3 stages raced)
+  // stays with one group, and a group is never more than one phase ahead of a
+  // slot's empty barrier.  With an odd ring a slot alternates between groups:
+  // group 0 can reach its use 2 of slot 0 (waiting for parity 1) before use 0
+  // completed -- the barrier is still in phase 0, parity 0 != 1, so the
+  // parity wait passes at once and the slot is overwritten under the MMAs
+  // (measured: LinDgradPol<32> with 3 stages raced).
   static constexpr int STAGES = (S0 > 4 ? 4 : S0) & ~1;
   static_assert(STAGES >= kGroups, "one ring slot per producer group at least");
   static_assert(RB <= 256 && RB % 16 == 0 && BN % 16 == 0, "MMA N limits");
