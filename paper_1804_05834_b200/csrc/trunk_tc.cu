@@ -445,7 +445,9 @@ int fwd_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const f
                  float *y, float *scratch, int *counters, int batch) {
   const int N = L.out_c;
   static const int bn_max = env_int("DQN_B200_FWD_BN", 64);          // diagnostic
-  if (N == 32 || (bn_max <= 32 && N % 32 == 0))
+  static const int bn_lin = env_int("DQN_B200_FWD_BN_LINEAR", 64);   // diagnostic
+  const int bmax = L.kind == DQN_LAYER_LINEAR ? bn_lin : bn_max;
+  if (N == 32 || (bmax <= 32 && N % 32 == 0))
     return fwd_launch<InT, 32>(st, L, x, params, y, scratch, counters, batch);
   if (N == 64) return fwd_launch<InT, 64>(st, L, x, params, y, scratch, counters, batch);
   if (N % 64 == 0) return fwd_launch<InT, 64>(st, L, x, params, y, scratch, counters, batch);
