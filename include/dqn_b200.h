@@ -321,6 +321,17 @@ int dqn_ipc_handle(void *ptr, uint8_t *handle64);
 int dqn_ipc_open(const uint8_t *handle64, void **ptr);
 int dqn_ipc_close(void *ptr);
 
+/* ReplayMemory.store_many (replay.py:91-102): n staged transitions into slots
+ * (cursor + i) % capacity (raw state bytes, any ring dtype; n <= capacity);
+ * the sources may be pinned host memory, read in place.  *size_dev (optional)
+ * = new_size.  The PER tree half is dqn_tree_store. */
+int dqn_ring_store(void *stream, uint8_t *states, uint8_t *next_states, int64_t slot_bytes,
+                   int64_t *actions, double *rewards, uint8_t *terminals, int64_t capacity,
+                   int64_t cursor, int32_t n, const uint8_t *src_states,
+                   const uint8_t *src_next_states, const int64_t *src_actions,
+                   const double *src_rewards, const uint8_t *src_terminals, int64_t *size_dev,
+                   int64_t new_size);
+
 /* dqn_tree_sample followed by dqn_ring_gather of the sampled slots (states,
  * next states, metadata) in ONE launch: each gather CTA descends its own
  * query, one extra CTA row computes the batch-normalised IS weights.  Same

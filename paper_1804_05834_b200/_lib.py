@@ -100,6 +100,8 @@ _SIGS = {
     "dqn_ipc_handle": ([vp, vp], C.c_int),
     "dqn_ipc_open": ([vp, C.POINTER(C.c_void_p)], C.c_int),
     "dqn_ipc_close": ([vp], C.c_int),
+    "dqn_ring_store": ([vp, vp, vp, i64, vp, vp, vp, i64, i64, C.c_int, vp, vp, vp, vp, vp, vp,
+                        i64], C.c_int),
     "dqn_sample_gather": ([vp, vp, C.c_int, vp, vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, i64, vp,
                            vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "dqn_graph_instantiate": ([vp, C.c_int, C.POINTER(C.c_void_p)], C.c_int),

@@ -46,9 +46,19 @@ static int64_t scratch_need(const dqn_net_desc *net, int batch) {
   return (a > b ? a : b) + kTileCounters;
 }
 
+// diagnostic: route forwards of at most this many rows to the SIMT kernels
+// (measured at batch 1, desk net: SIMT 90 us vs tcgen05 65 us -> off)
+static int small_batch_rows() {
+  static const int n = [] {
+    const char *e = getenv("DQN_B200_SIMT_FWD_ROWS");
+    return e ? atoi(e) : 0;
+  }();
+  return n;
+}
 static int layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
                          const dqn_binding *b, int32_t *flags) {
-  if (use_tc(net, l, 0)) return tc_layer_forward(st, net, l, params, b);
+  if (b->batch > small_batch_rows() && use_tc(net, l, 0))
+    return tc_layer_forward(st, net, l, params, b);
   return simt_layer_forward(st, net, l, params, b, flags);
 }
 static int layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,

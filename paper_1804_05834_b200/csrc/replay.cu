@@ -140,6 +140,38 @@ __global__ void ring_gather_meta_kernel(const int64_t *__restrict__ actions,
   if (out_t) out_t[j] = terminals[s];
 }
 
+// ReplayMemory.store_many (replay.py:91-102) for n staged transitions: slot
+// (cursor + i) % capacity <- transition i, raw bytes of each state (any ring
+// dtype); the sources may be pinned host memory read in place.  CTA (i, w)
+// copies state (w = 0) / next state (w = 1) of transition i; CTA (i, 0)
+// also the metadata, CTA (0, 0) the new size.
+__global__ void __launch_bounds__(256)
+ring_store_kernel(uint8_t *__restrict__ states, uint8_t *__restrict__ next_states,
+                  int64_t slot_bytes, int64_t *__restrict__ actions, double *__restrict__ rewards,
+                  uint8_t *__restrict__ terminals, int64_t capacity, int64_t cursor,
+                  const uint8_t *__restrict__ src_s, const uint8_t *__restrict__ src_s2,
+                  const int64_t *__restrict__ src_a, const double *__restrict__ src_r,
+                  const uint8_t *__restrict__ src_t, int64_t *size_dev, int64_t new_size) {
+  pdl_begin();
+  const int i = blockIdx.x, w = blockIdx.y;
+  const int64_t slot = (cursor + i) % capacity;
+  const uint8_t *src = (w ? src_s2 : src_s) + (int64_t)i * slot_bytes;
+  uint8_t *dst = (w ? next_states : states) + slot * slot_bytes;
+  if (slot_bytes % 16 == 0 && ((uintptr_t)src | (uintptr_t)dst) % 16 == 0) {
+    const int4 *s4 = reinterpret_cast<const int4 *>(src);
+    int4 *d4 = reinterpret_cast<int4 *>(dst);
+    for (int64_t e = threadIdx.x; e < slot_bytes / 16; e += blockDim.x) d4[e] = s4[e];
+  } else {
+    for (int64_t e = threadIdx.x; e < slot_bytes; e += blockDim.x) dst[e] = src[e];
+  }
+  if (w == 0 && threadIdx.x == 0) {
+    actions[slot] = src_a[i];
+    rewards[slot] = src_r[i];
+    terminals[slot] = src_t[i] ? 1 : 0;
+    if (i == 0 && size_dev) *size_dev = new_size;
+  }
+}
+
 // --------------------------------------------------------------- sum tree
 
 // tree_descend (SumTree.find descent) lives in tree_descend.cuh (shared with dp.cu)
@@ -730,6 +762,27 @@ inline int grid_for(int64_t n, int threads, int cap = 148 * 16) {
 }  // namespace dqn
 
 using namespace dqn;
+
+extern "C" int dqn_ring_store(void *stream, uint8_t *states, uint8_t *next_states,
+                              int64_t slot_bytes, int64_t *actions, double *rewards,
+                              uint8_t *terminals, int64_t capacity, int64_t cursor, int32_t n,
+                              const uint8_t *src_states, const uint8_t *src_next_states,
+                              const int64_t *src_actions, const double *src_rewards,
+                              const uint8_t *src_terminals, int64_t *size_dev,
+                              int64_t new_size) {
+  DQN_CHECK_ARG(states && next_states && actions && rewards && terminals && slot_bytes > 0 &&
+                    capacity >= 1 && cursor >= 0 && cursor < capacity && n >= 0 &&
+                    n <= capacity && (n == 0 || (src_states && src_next_states && src_actions &&
+                                                  src_rewards && src_terminals)),
+                "ring_store: bad args");
+  if (n == 0) return DQN_OK;
+  launch_k(ring_store_kernel, dim3((unsigned)n, 2), 256, 0, as_stream(stream), states,
+           next_states, slot_bytes, actions, rewards, terminals, capacity, cursor, src_states,
+           src_next_states, src_actions, src_rewards, src_terminals, size_dev, new_size);
+  DQN_LAUNCH_CHECK("ring_store");
+  return DQN_OK;
+}
+
 
 extern "C" int dqn_ring_fill_hash(void *stream, uint8_t *frames, int64_t slot0, int64_t nslots,
                                   int64_t slot_bytes, uint64_t counter_base) {

@@ -206,6 +206,24 @@ class ReplayMemory:
         self._set_size(min(self.size + n, self.capacity))
         return slots
 
+    def store_staged(self, states, next_states, actions, rewards, terminals, n: int) -> None:
+        """Insert n staged transitions in one launch (dqn_ring_store): tensors
+        in the ring's state dtype / int64 / float64 / uint8, pinned host
+        memory (read in place by the kernel) or device memory; same ring
+        semantics as ``store`` called n times."""
+        if n <= 0:
+            return
+        if n > self.capacity:
+            raise ValueError("more staged transitions than slots")
+        new_size = min(self.size + n, self.capacity)
+        _lib.call("dqn_ring_store", _lib.stream_ptr(), self.states.data_ptr(),
+                  self.next_states.data_ptr(), self.slot_bytes, self.actions.data_ptr(),
+                  self.rewards.data_ptr(), self.terminals.data_ptr(), self.capacity, self.cursor,
+                  int(n), states.data_ptr(), next_states.data_ptr(), actions.data_ptr(),
+                  rewards.data_ptr(), terminals.data_ptr(), self._size_dev.data_ptr(), new_size)
+        self.cursor = (self.cursor + n) % self.capacity
+        self.size = new_size
+
     def fill_synthetic(self, seed: int, n: int | None = None, n_actions: int = 4) -> None:
         """Bench/test input: hash frames generated in HBM (synth.py), host
         metadata streams.  Fills slots [0, n) and sets size = cursor = n."""
@@ -383,6 +401,16 @@ class PrioritizedReplay:
                   self.tree.depth, self.capacity, slot0, len(slots), self._max_p.data_ptr(),
                   float(self.config.alpha))
         return slots
+
+    def store_staged(self, states, next_states, actions, rewards, terminals, n: int) -> None:
+        """``ReplayMemory.store_staged`` + the new leaves at max priority."""
+        if n <= 0:
+            return
+        slot0 = self.memory.cursor
+        self.memory.store_staged(states, next_states, actions, rewards, terminals, n)
+        _lib.call("dqn_tree_store", _lib.stream_ptr(), self.tree.nodes.data_ptr(),
+                  self.tree.depth, self.capacity, slot0, int(n), self._max_p.data_ptr(),
+                  float(self.config.alpha))
 
     def fill_synthetic(self, seed: int, n: int | None = None, n_actions: int = 4,
                        warmup: bool = True) -> None:
