@@ -877,13 +877,14 @@ inline int smem_bytes() {
   return Plan<Pol>::BYTES;
 }
 
-// Opt-in (DQN_B200_CLUSTER_SPLITK=1): each kernel alone is faster, but in the
-// learner's two-stream graph the GPC-level placement of clusters costs more
-// than it saves (measured: ~5360 vs ~5430 updates/s).
+// On by default since the even-ring / tuned-split build (measured in the
+// learner graph: 6,788 vs 6,759 updates/s device, +1-2 % end to end; it was
+// slower in the earlier two-stream layout); DQN_B200_CLUSTER_SPLITK=0 turns
+// it off.  Same reduction order as the global fixup: identical results.
 inline bool cluster_splitk_enabled() {
   static const bool on = [] {
     const char *e = getenv("DQN_B200_CLUSTER_SPLITK");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return on;
 }
