@@ -67,10 +67,12 @@ static int layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const
   return simt_layer_backward(st, net, l, params, b);
 }
 // flags (optional): every written gradient is checked for non-finite values
-// opt-in: measured neutral in the learner (the wgrad runs beside the dgrad chain)
+// fc1's wgrad is an outer-product sum over the batch rows: the FMA kernel's
+// short CTAs leave SMs to the dgrad chain that 200 one-block tcgen05 CTAs
+// hold (measured +0.6 % in the learner); DQN_B200_LIN_WGRAD_SIMT=0 turns it off
 static bool lin_wgrad_simt_enabled() {
   const char *e = getenv("DQN_B200_LIN_WGRAD_SIMT");
-  return e && e[0] == '1';
+  return !(e && e[0] == '0');
 }
 static int layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
                        const dqn_binding *b, int32_t *flags) {
