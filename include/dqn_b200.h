@@ -310,6 +310,12 @@ int dqn_dp_owned(void *stream, const int64_t *owner, const int64_t *local_idx,
                  const double *td_all, int32_t K, int32_t rank, double eps, int64_t *idx_c,
                  double *td_c, int32_t *n_c, double *max_p, const int32_t *flags,
                  const double *sums);
+/* The update's results for the host, written by the device into pinned host
+ * memory: host_out = [td | w | owner | local idx] (4 K doubles), then
+ * *host_flag = *flags (fenced; the host's completion signal). */
+int dqn_dp_report(void *stream, const double *td_all, const double *w_all, const int64_t *owner,
+                  const int64_t *local_idx, int32_t K, const int32_t *flags, double *host_out,
+                  int32_t *host_flag);
 /* dqn_tree_update with the batch length read from device memory (*k_dev <= k_max <= 256). */
 int dqn_tree_update_n(void *stream, double *nodes, int32_t depth, const int64_t *size,
                       const int64_t *idx, const double *td, int32_t k_max, const int32_t *k_dev,

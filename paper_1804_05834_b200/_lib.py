@@ -93,6 +93,7 @@ _SIGS = {
                        vp, vp], C.c_int),
     "dqn_dp_owned": ([vp, vp, vp, vp, C.c_int, C.c_int, C.c_double, vp, vp, vp, vp, vp, vp],
                      C.c_int),
+    "dqn_dp_report": ([vp, vp, vp, vp, vp, C.c_int, vp, vp, vp], C.c_int),
     "dqn_tree_update_n": ([vp, vp, C.c_int, vp, vp, vp, C.c_int, vp, C.c_double, C.c_double, vp,
                            vp], C.c_int),
     "dqn_dev_alloc": ([i64, C.POINTER(C.c_void_p)], C.c_int),

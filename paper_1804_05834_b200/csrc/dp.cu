@@ -259,6 +259,29 @@ __global__ void dp_owned_kernel(const int64_t *__restrict__ owner,
   }
 }
 
+// Results of a global update for the host, written into pinned host memory
+// by the device (zero-copy): [td | w | owner | local idx] as doubles, then
+// the status word last (fenced), which the host polls.
+__global__ void dp_report_kernel(const double *__restrict__ td_all,
+                                 const double *__restrict__ w_all,
+                                 const int64_t *__restrict__ owner,
+                                 const int64_t *__restrict__ local_idx, int K,
+                                 const int32_t *__restrict__ flags, double *host_out,
+                                 int32_t *host_flag) {
+  pdl_begin();
+  for (int j = threadIdx.x; j < K; j += blockDim.x) {
+    host_out[j] = td_all[j];
+    host_out[K + j] = w_all[j];
+    host_out[2 * K + j] = (double)owner[j];
+    host_out[3 * K + j] = (double)local_idx[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    *(volatile int32_t *)host_flag = *flags;
+  }
+}
+
 }  // namespace
 }  // namespace dqn
 
@@ -373,4 +396,15 @@ extern "C" int dqn_ipc_open(const uint8_t *handle64, void **ptr) {
 extern "C" int dqn_ipc_close(void *ptr) {
   if (!ptr) return DQN_OK;
   return cuda_status(cudaIpcCloseMemHandle(ptr), "ipc_close");
+}
+
+extern "C" int dqn_dp_report(void *stream, const double *td_all, const double *w_all,
+                             const int64_t *owner, const int64_t *local_idx, int32_t K,
+                             const int32_t *flags, double *host_out, int32_t *host_flag) {
+  DQN_CHECK_ARG(td_all && w_all && owner && local_idx && flags && host_out && host_flag && K >= 1,
+                "dp_report: bad args");
+  launch_k(dp_report_kernel, 1, 256, 0, as_stream(stream), td_all, w_all, owner, local_idx, K,
+           flags, host_out, host_flag);
+  DQN_LAUNCH_CHECK("dp_report");
+  return DQN_OK;
 }

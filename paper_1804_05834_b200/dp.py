@@ -446,12 +446,14 @@ class DeviceDataParallelLearner:
         st = _lib.stream_ptr()
         tree, ring = self.mem.tree, self.mem.memory
         flags = p.flags
-        self.d_in.copy_(self.h_in, non_blocking=True)
+        # the draws are read where they are: pinned host memory (zero-copy) or,
+        # in the bench's device loop, a device slot
+        src = self.h_in
         _lib.call("dqn_dp_shard_info", st, tree.nodes.data_ptr(), ring._size_dev.data_ptr(),
                   self.mem._max_p.data_ptr(), self.info.data_ptr())
         self.comm.all_gather(self.info, self.info_all, st)
         # routing with the owner descent fused in -> (index, leaf) table
-        _lib.call("dqn_dp_route", st, self.info_all.data_ptr(), N, self.d_in.data_ptr(), K,
+        _lib.call("dqn_dp_route", st, self.info_all.data_ptr(), N, src.data_ptr(), K,
                   self.owner.data_ptr(), self.q_local.data_ptr(), self.sums.data_ptr(),
                   flags.data_ptr(), tree.nodes.data_ptr(), tree.depth, self.rank,
                   self.table.data_ptr())
@@ -460,7 +462,7 @@ class DeviceDataParallelLearner:
         _lib.call("dqn_dp_gather", st, self.rings.data_ptr(), self.owner.data_ptr(),
                   self.table.data_ptr(), k, self.rank, ring.slot_bytes, p.x.data_ptr(),
                   p.a.data_ptr(), p.r.data_ptr(), p.t.data_ptr(), self.sums.data_ptr(),
-                  self.d_in[K:].data_ptr(), K, self.local_idx.data_ptr(), self.w_all.data_ptr(),
+                  src[K:].data_ptr(), K, self.local_idx.data_ptr(), self.w_all.data_ptr(),
                   p.w.data_ptr())
 
         def td_branch():
@@ -486,13 +488,10 @@ class DeviceDataParallelLearner:
             self.opt.enqueue_step(flags)
         else:
             self.opt.enqueue_apply(flags)
-        r = self.d_res
-        r[:K].copy_(self.td_all)
-        r[K:2 * K].copy_(self.w_all)
-        r[2 * K:3 * K].copy_(self.owner)
-        r[3 * K:].copy_(self.local_idx)
-        self.h_res.copy_(r, non_blocking=True)
-        self.h_flags.copy_(flags, non_blocking=True)
+        # results and the status word straight into pinned host memory
+        _lib.call("dqn_dp_report", st, self.td_all.data_ptr(), self.w_all.data_ptr(),
+                  self.owner.data_ptr(), self.local_idx.data_ptr(), K, flags.data_ptr(),
+                  self.h_res.data_ptr(), self.h_flags.data_ptr())
 
     def step(self, u: np.ndarray, beta: float) -> DpStepResult:
         from . import _lib, agent
@@ -509,8 +508,18 @@ class DeviceDataParallelLearner:
         else:
             self.enqueue()
         self.calls += 1
-        agent._device_sync()
-        f = int(self.h_flags_np[0])
+        hf = self.h_flags_np
+        for _ in range(200_000):               # the report kernel writes it last
+            if hf[0] != agent._SENTINEL:
+                break
+        else:
+            agent._device_sync()
+        f = int(hf[0])
+        if f == agent._SENTINEL:
+            agent._device_sync()
+            f = int(hf[0])
+            if f == agent._SENTINEL:
+                raise RuntimeError("data-parallel update finished without its status word")
         if f:
             self.plan.flags.zero_()
             if f & _lib.FLAG_ZERO_TOTAL:
