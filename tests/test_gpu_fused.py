@@ -214,3 +214,22 @@ def test_linear_wgrad_simt_matches_tcgen05(P, monkeypatch):
         P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(3))
         runs.append(on.flat_grads.clone())
     assert rel_norm(runs[0].cpu().numpy(), runs[1].cpu().numpy()) < 1e-5
+
+
+def test_conv1_wgrad_simt_matches_tcgen05(P, monkeypatch):
+    """The uint8 first conv's weight gradient by the FMA reduction over the
+    transposed patch operand (opt-in) against the tcgen05 wgrad (default):
+    same gradients (conv1 and everything else) within 1e-5."""
+    runs = []
+    monkeypatch.setenv("DQN_B200_ZEROCOPY", "0")     # the stubbed optimizer writes no host flag
+    for simt in ("1", "0"):
+        monkeypatch.setenv("DQN_B200_CONV1_WGRAD_SIMT", simt)
+        on, tg, mem, opt, cfg = learner(P, **CASES["cfg4"])
+        opt.enqueue_apply = lambda flags, flag_out=None: None    # keep the gradients
+        P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(3))
+        g = dict(on.named_tensors())
+        runs.append((on.flat_grads.clone(), g["conv1.weight"].grad.clone(), g["conv1.bias"].grad.clone()))
+    (fa, wa, ba), (fb, wb, bb) = runs
+    assert rel_norm(wa.cpu().numpy(), wb.cpu().numpy()) < 1e-5
+    assert rel_norm(ba.cpu().numpy(), bb.cpu().numpy()) < 1e-5
+    assert rel_norm(fa.cpu().numpy(), fb.cpu().numpy()) < 1e-5
