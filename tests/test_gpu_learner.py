@@ -228,3 +228,22 @@ def test_sampler_1m_ring_learn_step(P):
     idx, prob, w = O.per_indices(ref, n, 32, mem.beta(10), u)
     assert np.array_equal(plan.idx.cpu().numpy(), idx)
     assert ulp_diff(plan.w.cpu().numpy(), w).max() <= 4
+
+
+@pytest.mark.parametrize("name", ["cfg4", "cfg3"])
+def test_long_run_bit_reproducible(P, name):
+    """Two identical learners, 60 graph-replayed updates each (the learner's
+    streams, split-K fixups, cluster reductions and producer rings all in
+    play): every TD error, every parameter and the whole tree bit-identical.
+    Guards against pipeline races (an odd producer ring raced once)."""
+    kw = CASES[name]
+    runs = []
+    for _ in range(2):
+        on, tg, mem, opt, cfg = device_learner(P, **kw)
+        rng = np.random.default_rng(2024)
+        tds = [P.learn_step(on, tg, mem, opt, cfg, 100 + s, rng).td_errors for s in range(60)]
+        runs.append((np.concatenate(tds), on.flat_values.cpu().numpy(),
+                     opt.flat_acc.cpu().numpy(),
+                     mem.tree.nodes.cpu().numpy() if hasattr(mem, "tree") else np.zeros(1)))
+    for a, b in zip(runs[0], runs[1]):
+        assert np.array_equal(a, b)
