@@ -56,10 +56,12 @@ ring_gather_vec_kernel(const int4 *__restrict__ states, const int4 *__restrict__
                        const uint8_t *__restrict__ terminals, int64_t *out_a, double *out_r,
                        uint8_t *out_t) {
   pdl_begin();   // programmatic dependent launch (common.cuh)
-  const int j = blockIdx.y;
-  const int which = blockIdx.z;
+  // blockIdx.x = sample * chunks + chunk (grid.y would cap k at 65,535)
+  const int64_t nchunks = (slot_vecs + kGatherChunk - 1) / kGatherChunk;
+  const int64_t j = blockIdx.x / nchunks, chunk = blockIdx.x - j * nchunks;
+  const int which = blockIdx.y;
   const int64_t slot = __ldg(idx + j);
-  if (blockIdx.x == 0 && which == 0 && threadIdx.x == 0) {   // the sample's metadata
+  if (chunk == 0 && which == 0 && threadIdx.x == 0) {   // the sample's metadata
     if (out_a) out_a[j] = actions[slot];
     if (out_r) out_r[j] = rewards[slot];
     if (out_t) out_t[j] = terminals[slot];
@@ -68,8 +70,8 @@ ring_gather_vec_kernel(const int4 *__restrict__ states, const int4 *__restrict__
   int4 *dst = which ? out_s2 : out_s;
   if (dst == nullptr) return;
   const int4 *s = src + slot * slot_vecs;
-  int4 *d = dst + (int64_t)j * slot_vecs;
-  const int64_t base = (int64_t)blockIdx.x * kGatherChunk + threadIdx.x;
+  int4 *d = dst + j * slot_vecs;
+  const int64_t base = chunk * kGatherChunk + threadIdx.x;
   int4 v[kGatherUnroll];
 #pragma unroll
   for (int u = 0; u < kGatherUnroll; ++u) {
@@ -115,14 +117,13 @@ __global__ void ring_gather_bytes_kernel(const uint8_t *__restrict__ states,
                                          int64_t slot_bytes, const int64_t *__restrict__ idx,
                                          uint8_t *__restrict__ out_s, uint8_t *__restrict__ out_s2) {
   pdl_begin();   // programmatic dependent launch (common.cuh)
-  const int j = blockIdx.y;
-  const int which = blockIdx.z;
+  const int64_t j = blockIdx.x;                 // one CTA per sample and frame
+  const int which = blockIdx.y;
   const uint8_t *src = which ? next_states : states;
   uint8_t *dst = which ? out_s2 : out_s;
   if (dst == nullptr) return;
   const int64_t slot = idx[j];
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < slot_bytes;
-       e += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t e = threadIdx.x; e < slot_bytes; e += blockDim.x)
     dst[j * slot_bytes + e] = src[slot * slot_bytes + e];
 }
 
@@ -818,7 +819,7 @@ extern "C" int dqn_ring_gather(void *stream, const uint8_t *states, const uint8_
   }
   if (vec) {   // frames + metadata in one launch
     const int64_t vecs = slot_bytes / 16;
-    dim3 grid((unsigned)((vecs + kGatherChunk - 1) / kGatherChunk), (unsigned)k, 2);
+    dim3 grid((unsigned)((vecs + kGatherChunk - 1) / kGatherChunk * k), 2);
     launch_k(ring_gather_vec_kernel, grid, kGatherThreads, 0, st, 
         reinterpret_cast<const int4 *>(states), reinterpret_cast<const int4 *>(next_states), vecs,
         idx, reinterpret_cast<int4 *>(out_states), reinterpret_cast<int4 *>(out_next_states),
@@ -828,8 +829,7 @@ extern "C" int dqn_ring_gather(void *stream, const uint8_t *states, const uint8_
   }
   if (out_states || out_next_states) {
     {
-      dim3 grid((unsigned)((slot_bytes + 255) / 256 < 64 ? (slot_bytes + 255) / 256 : 64),
-                (unsigned)k, 2);
+      dim3 grid((unsigned)k, 2);
       launch_k(ring_gather_bytes_kernel, grid, 256, 0, st, states, next_states, slot_bytes, idx,
                                                      out_states, out_next_states);
     }
