@@ -62,17 +62,22 @@ def _td_flags(config) -> int:
 
 def _targets_only(batch: SampleBatch, online, target, gamma: float, double: bool):
     torch = _lib.require_cuda()
-    k = len(batch)
-    q_tg = target.forward(batch.next_states).contiguous().clone()
+
+    def dev(x, dtype):      # tensors or array-likes (duck-typed nets / batches)
+        t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x))
+        return t.to(device="cuda", dtype=dtype).contiguous()
+
+    k = len(batch.rewards)
+    q_tg = dev(target.forward(batch.next_states), torch.float32).clone()
     if double:
-        q_on2 = online.forward(batch.next_states).contiguous().clone()
+        q_on2 = dev(online.forward(batch.next_states), torch.float32).clone()
     else:
         q_on2 = q_tg
     out = [torch.empty(k, dtype=torch.float64, device="cuda") for _ in range(3)]
     dq = torch.empty_like(q_tg)
     acts = torch.zeros(k, dtype=torch.int64, device="cuda")
-    r = batch.rewards.to(device="cuda", dtype=torch.float64).contiguous()
-    t = batch.terminals.to(device="cuda", dtype=torch.bool).contiguous()
+    r = dev(batch.rewards, torch.float64)
+    t = dev(batch.terminals, torch.bool)
     w = torch.ones(k, dtype=torch.float64, device="cuda")
     _lib.call("dqn_td_loss", _lib.stream_ptr(), q_on2.data_ptr(), q_on2.data_ptr(),
               q_tg.data_ptr(), acts.data_ptr(), r.data_ptr(), t.data_ptr(), w.data_ptr(), k,

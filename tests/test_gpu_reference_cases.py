@@ -180,3 +180,60 @@ def test_single_transition_delta_shrinks_monotonically(P):
     deltas = [P.learn_step(on, tg, mem, opt, cfg, i, rng).mean_abs_td for i in range(100)]
     assert all(b <= a + 1e-7 for a, b in zip(deltas, deltas[1:]))
     assert deltas[-1] < 1e-3 < deltas[0]
+
+
+class _TableNet:
+    """Q-table lookup 'network' (the reference test's TableNet): forward maps
+    integer state indices to Q rows."""
+
+    def __init__(self, table):
+        self.table = np.asarray(table, dtype=np.float64)
+        self.output_shape = (self.table.shape[1],)
+
+    def forward(self, states):
+        return self.table[np.asarray(states, dtype=np.int64)]
+
+
+def _value_iteration(trans, rew, term, gamma, tol=1e-10):
+    q = np.zeros((len(trans), len(trans[0])))
+    while True:
+        prev = q.copy()
+        for s in range(len(trans)):
+            for a in range(len(trans[0])):
+                q[s, a] = rew[s][a] + (0.0 if term[s][a] else gamma * prev[trans[s][a]].max())
+        if np.max(np.abs(q - prev)) < tol:
+            return q
+
+
+def _batch(P, rewards, next_states, terminals, actions=None):
+    k = len(rewards)
+    return P.SampleBatch(states=np.zeros(k), actions=np.zeros(k, np.int64) if actions is None
+                         else np.asarray(actions), rewards=np.asarray(rewards, np.float64),
+                         next_states=np.asarray(next_states),
+                         terminals=np.asarray(terminals, bool), indices=np.arange(k),
+                         probabilities=np.full(k, 1.0 / k), weights=np.ones(k))
+
+
+def test_criterion06_bellman_target_oracle(P):
+    """compute_target_dqn / _double on the exact Q* of TabularChain reproduce
+    Q* (the Bellman fixed point, test_acceptance.py:206-229); the Double-DQN
+    bootstrap never exceeds the max bootstrap over 10k random rows."""
+    env = P.TabularChain()
+    gamma = 0.99
+    q_star = _value_iteration(env.TRANSITIONS, env.REWARDS, env.TERMINAL, gamma)
+    net = _TableNet(q_star)
+    for s in (1, 2, 3):
+        for a in (0, 1):
+            b = _batch(P, [env.REWARDS[s][a]], [env.TRANSITIONS[s][a]], [env.TERMINAL[s][a]], [a])
+            y_dqn = float(P.compute_target_dqn(b, net, gamma)[0])
+            y_double = float(P.compute_target_double(b, net, net, gamma)[0])
+            assert abs(y_dqn - q_star[s, a]) < 1e-6       # Q in fp32 on the device
+            assert abs(y_double - q_star[s, a]) < 1e-6
+    rng = np.random.default_rng(17)
+    k = 10_000
+    online = _TableNet(rng.standard_normal((k, 5)))
+    target = _TableNet(rng.standard_normal((k, 5)))
+    b = _batch(P, rng.standard_normal(k), np.arange(k), np.zeros(k, dtype=bool))
+    yd = P.compute_target_double(b, online, target, 0.99).cpu().numpy()
+    ym = P.compute_target_dqn(b, target, 0.99).cpu().numpy()
+    assert np.all(yd <= ym + 1e-12)
