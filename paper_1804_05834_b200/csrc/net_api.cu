@@ -32,6 +32,8 @@ int tc_layer_forward_group(cudaStream_t st, const dqn_net_desc *net, int l,
 int64_t tc_forward_group_scratch(const dqn_net_desc *net, int upto, int batch);
 int lin_wgrad_smallk(cudaStream_t st, const float *x, const float *dy, int B, int F, int N,
                      float *gw, float *gb, int32_t *flags);
+int small_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
+                        const dqn_binding *b);
 int conv_wgrad_u8_smallk(cudaStream_t st, const uint8_t *xt, const float *dy, int M, int N, int P,
                          float *gw, float *gb, float *scratch, int64_t scratch_floats,
                          int32_t *flags);
@@ -49,19 +51,25 @@ static int64_t scratch_need(const dqn_net_desc *net, int batch) {
   return (a > b ? a : b) + kTileCounters;
 }
 
-// diagnostic: route forwards of at most this many rows to the SIMT kernels
-// (measured at batch 1, desk net: SIMT 90 us vs tcgen05 65 us -> off)
+// opt-in (DQN_B200_SMALL_FWD_ROWS=n): forwards of at most n rows use the
+// small-batch SIMT kernel for hidden conv / linear layers.  Measured at batch
+// 1: conv layers 4-15 us, but a linear layer is a single output pixel (N/32
+// CTAs walking K = 2048-3136 serially: 35-53 us), so the act forward is
+// faster on the tcgen05 path (desk 59 vs 64 us, Atari 65 vs 112 us) -> off.
 static int small_batch_rows() {
   static const int n = [] {
-    const char *e = getenv("DQN_B200_SIMT_FWD_ROWS");
+    const char *e = getenv("DQN_B200_SMALL_FWD_ROWS");
     return e ? atoi(e) : 0;
   }();
   return n;
 }
 static int layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
                          const dqn_binding *b, int32_t *flags) {
-  if (b->batch > small_batch_rows() && use_tc(net, l, 0))
-    return tc_layer_forward(st, net, l, params, b);
+  const dqn_layer_desc &L = net->layer[l];
+  if (b->batch <= small_batch_rows() && l != net->n_layers - 1 && net->algo != 1 &&
+      (L.kind == DQN_LAYER_CONV || L.kind == DQN_LAYER_LINEAR))
+    return small_layer_forward(st, net, l, params, b);
+  if (use_tc(net, l, 0)) return tc_layer_forward(st, net, l, params, b);
   return simt_layer_forward(st, net, l, params, b, flags);
 }
 static int layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,

@@ -623,6 +623,75 @@ int launch_col2im(cudaStream_t st, const float *dpatch, const Geo &g, int batch,
 }
 
 // Called by dqn_net_forward for layers the tcgen05 trunk does not own.
+// ------------------------------------------------ small-batch forward
+// Acting (select_action at batch 1, evaluate): a latency-bound forward.  One
+// CTA per (output pixel, 32 output channels): lane = channel (weight rows
+// W[k][n0..n0+31] load coalesced, the input element is a warp broadcast),
+// the 8 warps split the reduction length, partial sums combined in warp
+// order; bias + ReLU fused.  A linear layer is the full-size conv of its
+// input (fh = in_h, fw = in_w), so one kernel serves both.
+template <typename InT>
+__global__ void __launch_bounds__(256)
+small_fwd_kernel(const InT *__restrict__ x, const float *__restrict__ w,
+                 const float *__restrict__ bias, float *__restrict__ y, Geo g, int relu) {
+  pdl_begin();
+  __shared__ float part[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ngrp = (g.N + 31) / 32;
+  const int pix = blockIdx.x / ngrp, n = (blockIdx.x - pix * ngrp) * 32 + lane;
+  const int P = g.OH * g.OW, img = pix / P, pp = pix - img * P;
+  const int oy = pp / g.OW, ox = pp - oy * g.OW;
+  const int64_t base = (((int64_t)img * g.H + (int64_t)oy * g.sh) * g.W + (int64_t)ox * g.sw) * g.C;
+  const int K = g.fh * g.fw * g.C, rowlen = g.fw * g.C;
+  const int per = (K + 7) / 8, k0 = warp * per, k1 = min(K, k0 + per);
+  float a0 = 0.f, a1 = 0.f;                      // two chains, summed at the end
+  int k = k0;
+  for (; k + 1 < k1; k += 2) {
+    const int i0 = k / rowlen, i1 = (k + 1) / rowlen;
+    float x0 = (float)x[base + (int64_t)i0 * g.W * g.C + (k - i0 * rowlen)];
+    float x1 = (float)x[base + (int64_t)i1 * g.W * g.C + (k + 1 - i1 * rowlen)];
+    if (sizeof(InT) == 1) {
+      x0 = __fdiv_rn(x0, 255.0f);
+      x1 = __fdiv_rn(x1, 255.0f);
+    }
+    if (n < g.N) {
+      a0 = fmaf(x0, __ldg(w + (int64_t)k * g.N + n), a0);
+      a1 = fmaf(x1, __ldg(w + (int64_t)(k + 1) * g.N + n), a1);
+    }
+  }
+  if (k < k1) {
+    const int i0 = k / rowlen;
+    float x0 = (float)x[base + (int64_t)i0 * g.W * g.C + (k - i0 * rowlen)];
+    if (sizeof(InT) == 1) x0 = __fdiv_rn(x0, 255.0f);
+    if (n < g.N) a0 = fmaf(x0, __ldg(w + (int64_t)k * g.N + n), a0);
+  }
+  part[warp][lane] = __fadd_rn(a0, a1);
+  __syncthreads();
+  if (warp != 0 || n >= g.N) return;
+  float v = part[0][lane];
+#pragma unroll
+  for (int q = 1; q < 8; ++q) v = __fadd_rn(v, part[q][lane]);
+  v = __fadd_rn(v, bias[n]);
+  if (relu && v < 0.f) v = 0.f;
+  y[(int64_t)pix * g.N + n] = v;
+}
+
+int small_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
+                        const dqn_binding *b) {
+  const dqn_layer_desc &L = net->layer[l];
+  const Geo g = geo_of(L);
+  const int64_t blocks = (int64_t)b->batch * g.OH * g.OW * ((g.N + 31) / 32);
+  const void *in = (l == 0) ? b->x : b->act[l - 1];
+  if (l == 0 && net->input_u8)
+    launch_k(small_fwd_kernel<uint8_t>, (unsigned)blocks, 256, 0, st, (const uint8_t *)in,
+             params + L.w_off, params + L.b_off, b->act[l], g, (int)L.relu);
+  else
+    launch_k(small_fwd_kernel<float>, (unsigned)blocks, 256, 0, st, (const float *)in,
+             params + L.w_off, params + L.b_off, b->act[l], g, (int)L.relu);
+  DQN_LAUNCH_CHECK("small_fwd");
+  return DQN_OK;
+}
+
 int simt_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
                        const dqn_binding *b, int32_t *flags) {
   const dqn_layer_desc &L = net->layer[l];

@@ -158,3 +158,20 @@ def test_fc1_dgrad_tiles_correct_and_deterministic(bn, monkeypatch):
     assert line, out.stdout + out.stderr
     err = float(line[0].split("rel err ")[1].split()[0])
     assert "deterministic True" in line[0] and err < 1e-5, line[0]
+
+
+@pytest.mark.parametrize("rows_env", ["0", "4"])
+def test_small_batch_forward_matches_batched(rows_env):
+    """Small forwards -- batch <= 4 on the default tcgen05 path, and through
+    the opt-in small-batch SIMT kernel (DQN_B200_SMALL_FWD_ROWS=4; a
+    subprocess: the switch is read once) -- against the same rows inside a
+    batch-64 forward (tcgen05)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import subprocess
+    import sys
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, DQN_B200_SMALL_FWD_ROWS=rows_env)
+    out = subprocess.run([sys.executable, "tools/small_fwd_check.py"], env=env, cwd=str(root),
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.startswith("OK"), out.stdout + out.stderr
