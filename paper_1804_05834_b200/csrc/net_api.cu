@@ -66,8 +66,12 @@ static int small_batch_rows() {
 static int layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
                          const dqn_binding *b, int32_t *flags) {
   const dqn_layer_desc &L = net->layer[l];
-  if (b->batch <= small_batch_rows() && l != net->n_layers - 1 && net->algo != 1 &&
-      (L.kind == DQN_LAYER_CONV || L.kind == DQN_LAYER_LINEAR))
+  const bool hidden = l != net->n_layers - 1 && net->algo != 1 &&
+                      (L.kind == DQN_LAYER_CONV || L.kind == DQN_LAYER_LINEAR);
+  // acting-sized batches: layers without a tcgen05 kernel (e.g. the desk
+  // net's 16-filter conv1: 24.3 -> 4.1 us at batch 1) take the small-batch
+  // kernel instead of the batched SIMT GEMM; tcgen05 layers stay (faster)
+  if (hidden && ((b->batch <= 4 && !use_tc(net, l, 0)) || b->batch <= small_batch_rows()))
     return small_layer_forward(st, net, l, params, b);
   if (use_tc(net, l, 0)) return tc_layer_forward(st, net, l, params, b);
   return simt_layer_forward(st, net, l, params, b, flags);

@@ -633,7 +633,10 @@ int launch_col2im(cudaStream_t st, const float *dpatch, const Geo &g, int batch,
 template <typename InT>
 __global__ void __launch_bounds__(256)
 small_fwd_kernel(const InT *__restrict__ x, const float *__restrict__ w,
-                 const float *__restrict__ bias, float *__restrict__ y, Geo g, int relu) {
+                 const float *__restrict__ bias, float *__restrict__ y, Geo g, int relu,
+                 float *__restrict__ partial) {
+  // partial != nullptr: split-K over blockIdx.y (one output pixel layers);
+  // the block writes its 32 partial sums, small_fwd_reduce_kernel finishes
   pdl_begin();
   __shared__ float part[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -643,7 +646,9 @@ small_fwd_kernel(const InT *__restrict__ x, const float *__restrict__ w,
   const int oy = pp / g.OW, ox = pp - oy * g.OW;
   const int64_t base = (((int64_t)img * g.H + (int64_t)oy * g.sh) * g.W + (int64_t)ox * g.sw) * g.C;
   const int K = g.fh * g.fw * g.C, rowlen = g.fw * g.C;
-  const int per = (K + 7) / 8, k0 = warp * per, k1 = min(K, k0 + per);
+  const int kspan = (K + gridDim.y - 1) / gridDim.y;
+  const int kb = blockIdx.y * kspan, ke = min(K, kb + kspan);
+  const int per = (ke - kb + 7) / 8, k0 = kb + warp * per, k1 = min(ke, k0 + per);
   float a0 = 0.f, a1 = 0.f;                      // two chains, summed at the end
   int k = k0;
   for (; k + 1 < k1; k += 2) {
@@ -671,9 +676,28 @@ small_fwd_kernel(const InT *__restrict__ x, const float *__restrict__ w,
   float v = part[0][lane];
 #pragma unroll
   for (int q = 1; q < 8; ++q) v = __fadd_rn(v, part[q][lane]);
+  if (partial) {
+    const int64_t npix = gridDim.x / ngrp;                             // [split][pix][n]
+    partial[((int64_t)blockIdx.y * npix + pix) * g.N + n] = v;
+    return;
+  }
   v = __fadd_rn(v, bias[n]);
   if (relu && v < 0.f) v = 0.f;
   y[(int64_t)pix * g.N + n] = v;
+}
+
+// splits summed in split order, then bias + ReLU
+__global__ void small_fwd_reduce_kernel(const float *__restrict__ partial, int splits,
+                                        int64_t outputs, int N, const float *__restrict__ bias,
+                                        float *__restrict__ y, int relu) {
+  pdl_begin();
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o >= outputs) return;
+  float v = partial[o];
+  for (int s = 1; s < splits; ++s) v = __fadd_rn(v, partial[(int64_t)s * outputs + o]);
+  v = __fadd_rn(v, bias[o % N]);
+  if (relu && v < 0.f) v = 0.f;
+  y[o] = v;
 }
 
 int small_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
@@ -681,14 +705,32 @@ int small_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const f
   const dqn_layer_desc &L = net->layer[l];
   const Geo g = geo_of(L);
   const int64_t blocks = (int64_t)b->batch * g.OH * g.OW * ((g.N + 31) / 32);
+  const int K = g.fh * g.fw * g.C;
+  // few output blocks (linear layers): split K so that about one wave runs,
+  // at least 64 reduction steps per warp
+  int splits = 1;
+  if (blocks < kNumSMs)
+    splits = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs / blocks, K / (8 * 64)));
+  const int64_t outputs = (int64_t)b->batch * g.OH * g.OW * g.N;
+  float *partial = nullptr;
+  if (splits > 1) {
+    if ((int64_t)splits * outputs > b->scratch_floats) splits = 1;
+    else partial = b->scratch;
+  }
   const void *in = (l == 0) ? b->x : b->act[l - 1];
+  const dim3 grid((unsigned)blocks, (unsigned)splits);
   if (l == 0 && net->input_u8)
-    launch_k(small_fwd_kernel<uint8_t>, (unsigned)blocks, 256, 0, st, (const uint8_t *)in,
-             params + L.w_off, params + L.b_off, b->act[l], g, (int)L.relu);
+    launch_k(small_fwd_kernel<uint8_t>, grid, 256, 0, st, (const uint8_t *)in, params + L.w_off,
+             params + L.b_off, b->act[l], g, (int)L.relu, partial);
   else
-    launch_k(small_fwd_kernel<float>, (unsigned)blocks, 256, 0, st, (const float *)in,
-             params + L.w_off, params + L.b_off, b->act[l], g, (int)L.relu);
+    launch_k(small_fwd_kernel<float>, grid, 256, 0, st, (const float *)in, params + L.w_off,
+             params + L.b_off, b->act[l], g, (int)L.relu, partial);
   DQN_LAUNCH_CHECK("small_fwd");
+  if (partial) {
+    launch_k(small_fwd_reduce_kernel, (unsigned)((outputs + 255) / 256), 256, 0, st, partial,
+             splits, outputs, g.N, params + L.b_off, b->act[l], (int)L.relu);
+    DQN_LAUNCH_CHECK("small_fwd_reduce");
+  }
   return DQN_OK;
 }
 
