@@ -46,3 +46,24 @@ def test_product_path_refuses_without_gpu(monkeypatch):
     monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         _lib.require_cuda()
+
+
+def test_product_path_fails_loudly_without_the_library(tmp_path):
+    """No CPU fallback: importing the package with the CUDA library missing
+    raises ImportError; without a GPU every constructor raises."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DQN_B200_LIB=str(tmp_path / "missing.so"))
+    r = subprocess.run([sys.executable, "-c", "import paper_1804_05834_b200"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0 and "ImportError" in r.stderr
+    probe = ("import torch, paper_1804_05834_b200 as P\n"
+             "if torch.cuda.is_available():\n    print('GPU')\nelse:\n"
+             "    try:\n        P.build_network('atari', (84, 84, 4), 4, True)\n"
+             "        print('NO-RAISE')\n"
+             "    except Exception as e:\n        print('RAISED', type(e).__name__)\n")
+    r = subprocess.run([sys.executable, "-c", probe], cwd=root, capture_output=True, text=True,
+                       timeout=300)
+    assert r.stdout.startswith("GPU") or r.stdout.startswith("RAISED"), r.stdout + r.stderr
