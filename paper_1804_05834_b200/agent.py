@@ -199,8 +199,8 @@ class _StepPlan:
         # zero-copy I/O: the draws are read from pinned host memory by the
         # first kernel, TdResult and the flag word are written to pinned host
         # memory by the head and the optimizer kernels -- no memcpy nodes
-        zc = (io and self.zero_copy and self.per and self.fused_sample and self.fused_head
-              and self.grad_clip == 0.0)
+        zc = (io and self.zero_copy and self.fused_head and self.grad_clip == 0.0
+              and (self.fused_sample or not self.per))
         self._host_out = self.h_out if zc else None
         if self.per and self.fused_sample:
             # descent + IS weights + frame gather in one launch, reading the
@@ -219,13 +219,16 @@ class _StepPlan:
                       self.x[k:].data_ptr(), self.a.data_ptr(), self.r.data_ptr(),
                       self.t.data_ptr())
         else:
+            idx = self.idx
             if self.per:
                 self.d_in.copy_(self.h_in, non_blocking=True)
                 self.memory.sample_indices(self.d_in[:k], k, self.d_in[k:], self.idx, self.prob,
                                            self.w, self.flags)
+            elif zc:
+                idx = self.h_idx                  # uniform draws read in place (pinned)
             else:
                 self.idx.copy_(self.h_idx, non_blocking=True)
-            ring.gather_into(self.idx, k, self.x[:k], self.x[k:], self.a, self.r, self.t)
+            ring.gather_into(idx, k, self.x[:k], self.x[k:], self.a, self.r, self.t)
         # priorities are updated inside enqueue_learn, beside the backward pass
         self.enqueue_learn(priorities=self.per)
         if self.grad_clip > 0.0:
@@ -355,6 +358,11 @@ class _StepPlan:
         if self.grad_clip > 0.0:
             _lib.call("dqn_clip_gradients", st, on.flat_grads.data_ptr(), on.n_flat,
                       self.grad_clip, self.norm.data_ptr())
+
+    def last_indices(self):
+        """Replay slots sampled by the last update (device tensor for PER;
+        for uniform replay the host draws, which zero-copy reads in place)."""
+        return self.idx if self.per else self.h_idx
 
     def run(self, use_graph: bool) -> None:
         if use_graph and self.graph_exec is not None:   # hot path: one graph launch

@@ -88,7 +88,7 @@ def test_one_step_parity(P, name):
     res = P.learn_step(on, tg, mem, opt, cfg, 100, np.random.default_rng(1000))
     ores = O.learn_step(o_on, o_tg, o_mem, o_opt, o_cfg, 100, rng=np.random.default_rng(1000))
     plan = next(p for p in P.agent._PLANS.values() if p.online is on)
-    assert np.array_equal(plan.idx.cpu().numpy(), ores["batch"].indices)
+    assert np.array_equal(plan.last_indices().cpu().numpy(), ores["batch"].indices)
     assert rel_norm(res.targets, ores["targets"]) < TIGHT
     assert rel_norm(res.td_errors, ores["td_errors"]) < TIGHT
     assert rel_norm(res.losses, ores["losses"]) < TIGHT
