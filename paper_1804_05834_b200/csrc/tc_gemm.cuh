@@ -39,6 +39,8 @@
 
 #include "common.cuh"
 
+#include <cuda.h>
+
 #include <stdlib.h>
 
 namespace dqn {
@@ -85,6 +87,20 @@ __device__ __forceinline__ void fence_barrier_init() {
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// TMA 2-D tile load (cp.async.bulk.tensor), completing on an mbarrier
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -348,6 +364,8 @@ struct Gather {
 // Policies derive from this; it supplies the B gather form a policy does not
 // use (never called: the Gather uses the form of its layout).
 struct PolBase {
+  static constexpr bool B_TMA = false;   // B hi tiles by TMA tensor loads (K-major dense B)
+  __device__ const CUtensorMap *b_map() const { return nullptr; }
   __device__ int rows(int) const { return 0x7fffffff; }   // problem height (grouped launches)
   __device__ void note_bias(float) const {}      // BIAS_FROM_B: the written bias gradient
   __device__ int b_koff(int) const { return 0; }
@@ -433,7 +451,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 template <class Pol>
-__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const int launch_id,
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ Pol p,
+                                                               const int launch_id,
                                                                const int cluster_ks, const int reducer_budget) {
   using PL = Plan<Pol>;
   constexpr int nacc = kNacc;
@@ -445,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
   // empty[s]: the MMAs reading slot s completed (tcgen05.commit); done: all
   // MMAs of every group
   __shared__ uint64_t full[STAGES], empty[STAGES], done;
+  __shared__ uint64_t tbar[Pol::B_TMA ? STAGES : 1];     // TMA B tile landed
   __shared__ uint32_t tmem_slot;
   __shared__ float bias_red[Pol::BIAS_FROM_B ? kGroups : 1][Pol::BIAS_FROM_B ? BN : 1][kKc];
 
@@ -476,6 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], kGroupThreads);
       mbar_init(&empty[s], 1);
+      if constexpr (Pol::B_TMA) mbar_init(&tbar[s], 1);
     }
     mbar_init(&done, kGroups);
     fence_barrier_init();
@@ -540,9 +561,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
           for (int j = 0; j < 16; ++j) av[h][j] = 0.f;
         }
       }
-      gb.fetch(bv, k0, kend, [&](int k) { return p.b_koff(k); },
-               [&](long long b, int ko) { return p.b_ld(b, ko); },
-               [&](long long b, int k, int ke, float4 (&v)[4]) { p.b4(b, k, ke, v); });
+      if constexpr (!Pol::B_TMA)
+        gb.fetch(bv, k0, kend, [&](int k) { return p.b_koff(k); },
+                 [&](long long b, int ko) { return p.b_ld(b, ko); },
+                 [&](long long b, int k, int ke, float4 (&v)[4]) { p.b4(b, k, ke, v); });
     };
     auto put = [&](int kb) {
       const int s = kb % STAGES, use = kb / STAGES;
@@ -555,6 +577,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
       if (tk) tk_[(kb >> 1) * 4 + 1] = gtimer();
 #endif
       tc_fence_after();
+      if constexpr (Pol::B_TMA) {
+        // the B hi tile by TMA: one 4-k x BN-row box per 16-byte k-chunk,
+        // straight into the canonical K-major layout's hi rows (chunk c at
+        // c * RB * 16, row r at r * 16); rows / k beyond the tensor are zeros
+        if (threadIdx.x % kGroupThreads == 0 && !TC_SKIP(16)) {
+          fence_proxy_async();
+          mbar_expect_tx(&tbar[s], (uint32_t)(BN * BK * 4));
+          const int k0 = kbeg + kb * BK;
+#pragma unroll 1
+          for (int c = 0; c < kKc; ++c)
+            tma_load_2d(sbase + s * B_BYTES + c * RB * 16, p.b_map(), k0 + 4 * c, n0, &tbar[s]);
+        }
+      }
 #ifdef DQN_TC_TRACE
       if (kb == 0 && threadIdx.x == 0) tr_[5] = gtimer();
 #endif
@@ -574,7 +609,25 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Pol p, const
             }
           }
         }
-        if (!TC_SKIP(16)) gb.store(bv, sbase + s * B_BYTES, BN * 16, NB, want_bias);
+        if constexpr (Pol::B_TMA) {
+          if (!TC_SKIP(16)) {
+            // lo = x - trunc_tf32(x) of the landed hi rows, into rows BN.. of each chunk
+            mbar_wait(&tbar[s], use & 1);
+            const uint32_t tb = sbase + s * B_BYTES;
+            for (int i = threadIdx.x % kGroupThreads; i < BN * kKc; i += kGroupThreads) {
+              const int c = i / BN, r = i - c * BN;
+              const uint32_t a = tb + (uint32_t)(c * RB * 16 + r * 16);
+              float4 h;
+              asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                           : "=f"(h.x), "=f"(h.y), "=f"(h.z), "=f"(h.w) : "r"(a));
+              asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a + BN * 16),
+                           "f"(tf32_lo(h.x)), "f"(tf32_lo(h.y)), "f"(tf32_lo(h.z)), "f"(tf32_lo(h.w))
+                           : "memory");
+            }
+          }
+        } else {
+          if (!TC_SKIP(16)) gb.store(bv, sbase + s * B_BYTES, BN * 16, NB, want_bias);
+        }
         tmem_wait_st();
       }
       fence_proxy_async();

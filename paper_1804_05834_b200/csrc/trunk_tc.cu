@@ -218,6 +218,15 @@ struct LinDgradPol : tc::PolBase {
   }
 };
 
+// The same with B's hi tiles loaded by TMA tensor loads (W is dense and
+// K-major: rows n = input features, k = output channels, row stride K).
+template <int BN_>
+struct LinDgradTmaPol : LinDgradPol<BN_> {
+  static constexpr bool B_TMA = true;
+  CUtensorMap map;
+  __device__ const CUtensorMap *b_map() const { return &map; }
+};
+
 // ----------------------------------------------------------- conv dgrad
 // One stride phase (py, px) per blockIdx.z: rows are the input pixels
 // (img, yq, xq) with y = yq*sh + py, x = xq*sw + px; k = (ti, tj, co).
@@ -486,9 +495,72 @@ int fwd_group_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *cons
   return DQN_ERR_UNSUPPORTED;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                   const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      (void)cudaGetLastError();
+      f = nullptr;
+    }
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// 2-D map of a row-major [rows][K] fp32 matrix with 4 x BN boxes (one
+// 16-byte k-chunk of BN rows); out-of-range elements read as zero
+static bool make_kmajor_map(CUtensorMap *m, const float *base, int K, int rows, int bn) {
+  const EncodeTiledFn fn = encode_tiled();
+  if (!fn || ((uintptr_t)base % 16) || (K % 4)) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)K * 4};
+  const cuuint32_t box[2] = {4, (cuuint32_t)bn};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool tma_b_enabled() {
+  static const bool on = env_int("DQN_B200_TMA_B", 1) == 1;
+  return on;
+}
+
+template <int BN>
+int lin_dgrad_launch_tma(cudaStream_t st, const float *dy, const float *w, const float *mask,
+                         float *out, float *partial, int *counters, int M, int N, int K,
+                         int cap) {
+  LinDgradTmaPol<BN> p{};
+  if (!make_kmajor_map(&p.map, w, K, N, BN)) return DQN_ERR_UNSUPPORTED;
+  p.counters = counters;
+  p.dy = dy;
+  p.w = w;
+  p.mask = mask;
+  p.out = out;
+  p.partial = partial;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  split_k(ceil_div(M, tc::BM) * ceil_div(N, BN), K, BN, cap, p.klen, p.ksplits);
+  return tc::launch(st, p, p.ksplits, "tc_lin_dgrad_tma");
+}
+
 template <int BN>
 int lin_dgrad_launch(cudaStream_t st, const float *dy, const float *w, const float *mask,
                      float *out, float *partial, int *counters, int M, int N, int K) {
+  if (tma_b_enabled()) {
+    static const int cap = env_int("DQN_B200_DGRAD_CAP", 16);
+    const int rc = lin_dgrad_launch_tma<BN>(st, dy, w, mask, out, partial, counters, M, N, K, cap);
+    if (rc != DQN_ERR_UNSUPPORTED) return rc;
+  }
   LinDgradPol<BN> p{};
   p.counters = counters;
   p.dy = dy;

@@ -142,22 +142,32 @@ def test_errors(P):
 
 
 @pytest.mark.parametrize("bn", ["32", "64"])
-def test_fc1_dgrad_tiles_correct_and_deterministic(bn, monkeypatch):
+def test_fc1_dgrad_tiles_correct_and_deterministic(bn, tmp_path):
     """fc1's dgrad through the tcgen05 engine in 32- and 64-column tiles
     against an fp64 reference, over repeated launches.  Regression test for
     an odd producer ring (3 stages at 32 columns) that raced: every launch
-    must agree bit for bit and stay at 3xTF32 accuracy."""
+    must agree bit for bit and stay at 3xTF32 accuracy.  B (the weights)
+    arrives by TMA tensor loads by default and by register staging with
+    DQN_B200_TMA_B=0; the two must be bit-identical (subprocesses: the switch
+    is read once)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import subprocess
     import sys
-    env = dict(os.environ, DQN_B200_LIN_DGRAD_BN=bn)
-    out = subprocess.run([sys.executable, "tools/lin_dgrad_check.py"], env=env, capture_output=True,
-                         text=True, timeout=300, cwd=str(Path(__file__).resolve().parent.parent))
-    line = [l for l in out.stdout.splitlines() if l.startswith("BN=")]
-    assert line, out.stdout + out.stderr
-    err = float(line[0].split("rel err ")[1].split()[0])
-    assert "deterministic True" in line[0] and err < 1e-5, line[0]
+    dumps = []
+    for tma in ("1", "0"):
+        dump = tmp_path / f"fc1_dgrad_{tma}.pt"
+        env = dict(os.environ, DQN_B200_LIN_DGRAD_BN=bn, DQN_B200_TMA_B=tma,
+                   LIN_DGRAD_DUMP=str(dump))
+        out = subprocess.run([sys.executable, "tools/lin_dgrad_check.py"], env=env,
+                             capture_output=True, text=True, timeout=300,
+                             cwd=str(Path(__file__).resolve().parent.parent))
+        line = [l for l in out.stdout.splitlines() if l.startswith("BN=")]
+        assert line, out.stdout + out.stderr
+        err = float(line[0].split("rel err ")[1].split()[0])
+        assert "deterministic True" in line[0] and err < 1e-5, (tma, line[0])
+        dumps.append(torch.load(dump))
+    assert torch.equal(dumps[0], dumps[1])
 
 
 @pytest.mark.parametrize("rows_env", ["0", "4"])

@@ -15,6 +15,7 @@ from paper_1804_05834_b200 import _lib  # noqa: E402
 net = P.build_network("atari", (84, 84, 4), 4, True)
 P.init_params(net, 1)
 B = 32
+torch.manual_seed(0)
 x = torch.randint(0, 256, (B, 84, 84, 4), dtype=torch.uint8, device="cuda")
 bind = net.binding(B)
 net.forward_into(x, bind)
@@ -39,3 +40,14 @@ if bad.any():
     rows, cols = torch.nonzero(bad, as_tuple=True)
     print("bad rows", sorted(set(rows.tolist()))[:10], "cols", sorted(set((cols // 32).tolist()))[:20],
           "count", int(bad.sum()))
+if os.environ.get("LIN_DGRAD_DUMP"):
+    torch.save(outs[0].cpu(), os.environ["LIN_DGRAD_DUMP"])
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+for _ in range(20):
+    net.layer_into(bind, fc1, 1)
+e0.record()
+for _ in range(200):
+    net.layer_into(bind, fc1, 1)
+e1.record()
+torch.cuda.synchronize()
+print(f"fc1 dgrad {e0.elapsed_time(e1) / 200 * 1000:.2f} us/launch (incl. host launch overhead)")
