@@ -102,6 +102,16 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// TMA 4-D tile load (coordinates innermost first)
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                            int c2, int c3, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -365,7 +375,8 @@ struct Gather {
 // use (never called: the Gather uses the form of its layout).
 struct PolBase {
   static constexpr bool B_TMA = false;   // B hi tiles by TMA tensor loads (K-major dense B)
-  __device__ const CUtensorMap *b_map() const { return nullptr; }
+  // issue the TMA load of B's hi rows n0.. for the 4-k chunk at k (problem zp)
+  __device__ void b_tma(uint32_t, int, int, int, uint64_t *) const {}
   __device__ int rows(int) const { return 0x7fffffff; }   // problem height (grouped launches)
   __device__ void note_bias(float) const {}      // BIAS_FROM_B: the written bias gradient
   __device__ int b_koff(int) const { return 0; }
@@ -587,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           const int k0 = kbeg + kb * BK;
 #pragma unroll 1
           for (int c = 0; c < kKc; ++c)
-            tma_load_2d(sbase + s * B_BYTES + c * RB * 16, p.b_map(), k0 + 4 * c, n0, &tbar[s]);
+            p.b_tma(sbase + s * B_BYTES + c * RB * 16, n0, k0 + 4 * c, zp, &tbar[s]);
         }
       }
 #ifdef DQN_TC_TRACE

@@ -170,6 +170,31 @@ def test_fc1_dgrad_tiles_correct_and_deterministic(bn, tmp_path):
     assert torch.equal(dumps[0], dumps[1])
 
 
+def test_conv_dgrad_tma_matches_register_staging(tmp_path):
+    """conv2 / conv3 dgrad (stride phases, split K, ragged batch) against an
+    fp64 reference with the weights by 4-D TMA tensor loads (opt-in,
+    DQN_B200_TMA_B_CONV=1) and by register staging (default): 3xTF32 accuracy,
+    repeatable, and the two bit-identical."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import subprocess
+    import sys
+    dumps = []
+    for tma in ("1", "0"):
+        dump = tmp_path / f"conv_dgrad_{tma}.pt"
+        env = dict(os.environ, DQN_B200_TMA_B_CONV=tma, CONV_DGRAD_DUMP=str(dump))
+        out = subprocess.run([sys.executable, "tools/conv_dgrad_check.py"], env=env,
+                             capture_output=True, text=True, timeout=300,
+                             cwd=str(Path(__file__).resolve().parent.parent))
+        line = [l for l in out.stdout.splitlines() if l.startswith("WORST")]
+        assert line, out.stdout + out.stderr
+        assert float(line[0].split()[1]) < 1e-5, (tma, out.stdout)
+        dumps.append(torch.load(dump))
+    assert dumps[0].keys() == dumps[1].keys()
+    for k in dumps[0]:
+        assert torch.equal(dumps[0][k], dumps[1][k]), k
+
+
 @pytest.mark.parametrize("rows_env", ["0", "4"])
 def test_small_batch_forward_matches_batched(rows_env):
     """Small forwards -- batch <= 4 on the default tcgen05 path, and through
