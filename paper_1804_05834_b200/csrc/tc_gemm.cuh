@@ -577,6 +577,24 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
                  [&](long long b, int ko) { return p.b_ld(b, ko); },
                  [&](long long b, int k, int ke, float4 (&v)[4]) { p.b4(b, k, ke, v); });
     };
+    // the B hi tile of k-block kb by TMA (group leader): one 4-k x BN-row box
+    // per 16-byte k-chunk, straight into the canonical K-major layout's hi
+    // rows (chunk c at c * RB * 16, row r at r * 16); rows / k beyond the
+    // tensor are zeros.  Issued one k-block ahead, right after the previous
+    // block's MMAs, so the load overlaps that block's A store and MMAs.
+    auto issue_b = [&](int kb) {
+      if constexpr (Pol::B_TMA) {
+        if (TC_SKIP(16)) return;
+        const int s = kb % STAGES, use = kb / STAGES;
+        if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);  // MMAs of kb - STAGES done
+        fence_proxy_async();
+        mbar_expect_tx(&tbar[s], (uint32_t)(BN * BK * 4));
+        const int k0 = kbeg + kb * BK;
+#pragma unroll 1
+        for (int c = 0; c < kKc; ++c)
+          p.b_tma(sbase + s * B_BYTES + c * RB * 16, n0, k0 + 4 * c, zp, &tbar[s]);
+      }
+    };
     auto put = [&](int kb) {
       const int s = kb % STAGES, use = kb / STAGES;
 #ifdef DQN_TC_TRACE
@@ -588,19 +606,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       if (tk) tk_[(kb >> 1) * 4 + 1] = gtimer();
 #endif
       tc_fence_after();
-      if constexpr (Pol::B_TMA) {
-        // the B hi tile by TMA: one 4-k x BN-row box per 16-byte k-chunk,
-        // straight into the canonical K-major layout's hi rows (chunk c at
-        // c * RB * 16, row r at r * 16); rows / k beyond the tensor are zeros
-        if (threadIdx.x % kGroupThreads == 0 && !TC_SKIP(16)) {
-          fence_proxy_async();
-          mbar_expect_tx(&tbar[s], (uint32_t)(BN * BK * 4));
-          const int k0 = kbeg + kb * BK;
-#pragma unroll 1
-          for (int c = 0; c < kKc; ++c)
-            p.b_tma(sbase + s * B_BYTES + c * RB * 16, n0, k0 + 4 * c, zp, &tbar[s]);
-        }
-      }
 #ifdef DQN_TC_TRACE
       if (kb == 0 && threadIdx.x == 0) tr_[5] = gtimer();
 #endif
@@ -674,8 +679,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 #ifdef DQN_TC_TRACE
         if (tk) tk_[(kb >> 1) * 4 + 3] = gtimer();
 #endif
+        if (kb + kGroups < nk) issue_b(kb + kGroups);
       }
     };
+    if (group < nk && threadIdx.x % kGroupThreads == 0) issue_b(group);
     if (group < nk) fetch(group);
     for (int kb = group; kb < nk; kb += kGroups) {
       put(kb);
