@@ -100,7 +100,7 @@ def val(r, n):
 labels = ["conv1.fwd (batch 32, target)", "conv2.fwd (batch 32, target)",
           "conv3.fwd (batch 32, target)", "fc1.fwd (batch 32, target)",
           "conv1.fwd (batch 64)", "conv2.fwd (batch 64)", "conv3.fwd (batch 64)",
-          "fc1.fwd (batch 64)", "fc1.wgrad (batch 32)", "fc1.dgrad (batch 32)",
+          "fc1.fwd (batch 64)", "fc1.dgrad (batch 32)",
           "conv3.wgrad (batch 32)", "conv3.dgrad (batch 32)", "conv2.wgrad (batch 32)",
           "conv2.dgrad (batch 32)", "conv1.wgrad (batch 32)"]
 L = [f"# {tag} — every tcgen05 GEMM of one learner update, `ncu --set full`", "",
