@@ -492,6 +492,10 @@ def learn_step_collect(plan: _StepPlan) -> TdResult:
     if f == _SENTINEL:      # the update's completion word was never written
         raise RuntimeError("learner update finished without reporting its status word")
     if f:
+        # the step was aborted on the device; let the update's remaining
+        # launches finish before raising
+        torch = _lib.require_cuda()
+        torch.cuda.current_stream().synchronize()
         plan.flags.zero_()
         if f & _lib.FLAG_ZERO_TOTAL:
             raise ValueError("zero total priority; nothing can be sampled")

@@ -99,10 +99,11 @@ def test_learner_aborts_on_gradient_overflow(P):
     skips the update, learn_step raises (optim.py:38-40 semantics)."""
     on, tg, mem, opt, cfg = learner(P, dueling=True, double=True, per=True)
     mem.memory.rewards.fill_(1e38)
-    before = on.flat_values.clone()
+    before, acc = on.flat_values.clone(), opt.flat_acc.clone()
     with pytest.raises(P.NonFiniteError):
         P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(0))
     assert torch.equal(before, on.flat_values)
+    assert torch.equal(acc, opt.flat_acc)
 
 
 def _im2col_t_np(x, fh, fw, sh, sw):
