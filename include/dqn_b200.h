@@ -222,6 +222,20 @@ int dqn_td_loss(void *stream, const float *q_online, const float *q_next_online,
                 int32_t n_actions, double gamma, int32_t flags, double *targets,
                 double *td, double *losses, float *dq, double *stats);
 
+/* Frame-deduplicated ring gather (replaces ReplayMemory._gather,
+ * replay.py:104-115, for rings that keep each H x W frame once; the
+ * reference itself stores full stacks).  frames: pool of
+ * frame_bytes-byte planes; ids: per ring slot 2*stack int64 pool ids (state
+ * planes, then next-state planes).  Writes the k sampled transitions'
+ * channel-last stacks (frame_bytes * stack bytes each, byte-identical to a
+ * full-stack ring holding the same transitions) and, where given, their
+ * action / reward / terminal.  Indices must be valid slots. */
+int dqn_frame_gather(void *stream, const uint8_t *frames, int64_t frame_bytes,
+                     const int64_t *ids, int stack, const int64_t *indices, int k,
+                     const int64_t *actions, const double *rewards, const bool *terminals,
+                     uint8_t *out_states, uint8_t *out_next_states, int64_t *out_actions,
+                     double *out_rewards, bool *out_terminals);
+
 /* RmsProp.step (optim.py:36-47) over a flat buffer: finite scan of all grads,
  * then (only if all finite) acc = acc*rho; acc += (1-rho)*g*g;
  * w -= (lr*g)/(sqrt(acc)+eps); g = 0 -- fp32, no FMA, bit-exact given g.

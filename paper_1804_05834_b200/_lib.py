@@ -80,6 +80,8 @@ _SIGS = {
                     C.c_int),
     "dqn_rmsprop_step": ([vp, vp, vp, vp, i64, f32, f32, f32, f32, vp], C.c_int),
     "dqn_rmsprop_apply": ([vp, vp, vp, vp, i64, f32, f32, f32, f32, vp, vp], C.c_int),
+    "dqn_frame_gather": ([vp, vp, i64, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp],
+                         C.c_int),
     "dqn_clip_gradients": ([vp, vp, i64, f64, vp], C.c_int),
     "dqn_sync_target": ([vp, vp, vp, i64], C.c_int),
     "dqn_net_forward_group_scratch": ([vp, C.c_int, C.c_int], i64),

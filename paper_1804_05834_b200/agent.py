@@ -113,7 +113,7 @@ class _StepPlan:
         self.nA = online.output_shape[-1]
         dev = "cuda"
         ring = self.ring
-        self.x = torch.empty((2 * k,) + ring.state_shape, dtype=ring.states.dtype, device=dev)
+        self.x = torch.empty((2 * k,) + ring.state_shape, dtype=ring.state_dtype, device=dev)
         self.a = torch.empty(k, dtype=torch.int64, device=dev)
         self.r = torch.empty(k, dtype=torch.float64, device=dev)
         self.t = torch.empty(k, dtype=torch.bool, device=dev)
@@ -173,7 +173,8 @@ class _StepPlan:
             n = int(_lib.lib.dqn_net_forward_group_scratch(C.byref(self.on_desc),
                                                            self.head_layer, k))
             self.grp_scratch = torch.zeros(n, dtype=torch.float32, device=dev)
-        self.fused_sample = (ring.slot_bytes % 16 == 0 and ring.states.dtype == torch.uint8
+        self.fused_sample = (ring.fused_ok and ring.slot_bytes % 16 == 0
+                             and ring.state_dtype == torch.uint8
                              and os.environ.get("DQN_B200_FUSED_SAMPLE", "1") != "0")
         self.zero_copy = (k * (self.nA + 1) <= 2048
                           and os.environ.get("DQN_B200_ZEROCOPY", "1") != "0"

@@ -142,6 +142,8 @@ class ReplayMemory:
     whose CUDA IPC handles other processes can map (the data-parallel
     learner's peer gather, dp.py)."""
 
+    fused_ok = True           # slots the learner's fused sample + gather can read
+
     def __init__(self, capacity: int, state_shape: tuple[int, ...], dtype=np.uint8,
                  shareable: bool = False):
         if capacity < 1:
@@ -173,6 +175,10 @@ class ReplayMemory:
         self.size = 0
         self._size_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
         self._scratch = {}
+
+    @property
+    def state_dtype(self):
+        return self.states.dtype
 
     # -- insertion ------------------------------------------------------
     def _set_size(self, n: int) -> None:
@@ -363,9 +369,19 @@ class PrioritizedReplay:
     """Ring + sum tree over p^alpha (replay.py:184-241)."""
 
     def __init__(self, capacity: int, state_shape: tuple[int, ...],
-                 config: PriorityConfig | None = None, dtype=np.uint8, shareable: bool = False):
+                 config: PriorityConfig | None = None, dtype=np.uint8, shareable: bool = False,
+                 frame_dedup: bool = False, frame_capacity: int | None = None):
+        """``frame_dedup=True`` keeps each frame once (frame_ring.py; uint8,
+        same sampled bytes, ~1/8 of the footprint for episodic streams)."""
         torch = _torch()
-        self.memory = ReplayMemory(capacity, state_shape, dtype=dtype, shareable=shareable)
+        if frame_dedup:
+            from .frame_ring import FrameDedupMemory
+            if shareable:
+                raise ValueError("the frame-deduplicated ring is not shareable")
+            self.memory = FrameDedupMemory(capacity, state_shape, dtype=dtype,
+                                           frame_capacity=frame_capacity)
+        else:
+            self.memory = ReplayMemory(capacity, state_shape, dtype=dtype, shareable=shareable)
         self.config = config or PriorityConfig()
         self.tree = SumTree(capacity)
         self._max_p = torch.ones(1, dtype=torch.float64, device="cuda")   # raw p-space

@@ -1,0 +1,105 @@
+"""Frame-deduplicated ring (frame_ring.py, dqn_frame_gather) against the
+full-stack ring holding the same transitions (the reference's storage,
+replay.py:83-115): sampled bytes and metadata identical, learn_step on it
+bit-identical, footprint ~1/8 for an episodic stream."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1804_05834_b200 as P
+    return P
+
+
+def episodic(rng, n, shape, max_len=9):
+    """Transitions of an Atari-like stream: an episode starts from one frame
+    repeated, each step shifts one new frame into the stack."""
+    h, w, s = shape
+    out = []
+    while len(out) < n:
+        stack = [rng.integers(0, 256, (h, w), dtype=np.uint8)] * s
+        for _ in range(int(rng.integers(1, max_len + 1))):
+            nxt = stack[1:] + [rng.integers(0, 256, (h, w), dtype=np.uint8)]
+            out.append((np.stack(stack, -1), int(rng.integers(0, 4)),
+                        float(rng.choice([-1.0, 0.0, 1.0])), np.stack(nxt, -1),
+                        bool(rng.random() < 0.1)))
+            stack = nxt
+    return out[:n]
+
+
+def _pair(P, cap, shape, stream, as_float=False):
+    from paper_1804_05834_b200.frame_ring import FrameDedupMemory
+    full = P.ReplayMemory(cap, shape)
+    dedup = FrameDedupMemory(cap, shape)
+    for s, a, r, s2, t in stream:
+        if as_float:
+            s, s2 = s.astype(np.float32) / np.float32(255.0), s2.astype(np.float32) / np.float32(255.0)
+        tr = P.Transition(s, a, r, s2, t)
+        assert full.store(tr) == dedup.store(tr)
+    return full, dedup
+
+
+@pytest.mark.parametrize("shape", [(84, 84, 4), (10, 10, 4), (10, 10, 3), (9, 7, 4)])
+def test_gather_matches_full_stack_ring(P, shape):
+    rng = np.random.default_rng(sum(shape))
+    cap = 40
+    full, dedup = _pair(P, cap, shape, episodic(rng, 3 * cap + 7, shape))
+    assert full.size == dedup.size == cap and full.cursor == dedup.cursor
+    idx = rng.integers(0, cap, 300)
+    a, b = full.sample_uniform(300, np.random.default_rng(1)), dedup.sample_uniform(300, np.random.default_rng(1))
+    for f in ("states", "next_states", "actions", "rewards", "terminals", "indices"):
+        assert torch.equal(getattr(a, f), getattr(b, f)), f
+    ti = torch.as_tensor(idx, device="cuda")
+    out = [torch.empty((300,) + shape, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    dedup.gather_into(ti, 300, out[0], out[1], None, None, None)
+    assert torch.equal(out[0], full.states[ti]) and torch.equal(out[1], full.next_states[ti])
+
+
+def test_float_frames_and_footprint(P):
+    rng = np.random.default_rng(7)
+    shape, cap = (84, 84, 4), 64
+    stream = episodic(rng, 2 * cap, shape, max_len=40)
+    full, dedup = _pair(P, cap, shape, stream, as_float=True)
+    ti = torch.arange(cap, device="cuda")
+    s, s2 = torch.empty_like(full.states), torch.empty_like(full.next_states)
+    dedup.gather_into(ti, cap, s, s2, None, None, None)
+    assert torch.equal(s, full.states) and torch.equal(s2, full.next_states)
+    full_bytes = 2 * cap * full.slot_bytes
+    assert dedup.resident_bytes < 0.3 * full_bytes, (dedup.resident_bytes, full_bytes)
+
+
+def test_learn_step_identical_on_dedup_ring(P):
+    """The learner over PrioritizedReplay(frame_dedup=True) -- the graph's
+    gather through dqn_frame_gather -- gives the same TdResults and
+    parameters as over the full-stack ring, bit for bit."""
+    rng = np.random.default_rng(11)
+    shape, cap = (24, 24, 4), 256
+    stream = episodic(rng, 300, shape)
+    runs = []
+    for dedup in (False, True):
+        cfg = P.RunConfig(batch_size=32, double=True, dueling=True, beta_end_step=1000)
+        on = P.build_network("desk", shape, 3, True)
+        tg = P.build_network("desk", shape, 3, True)
+        P.init_params(on, 1)
+        P.sync_target(on, tg)
+        opt = P.RmsProp(on, cfg.learning_rate, cfg.rms_decay, cfg.rms_epsilon)
+        mem = P.PrioritizedReplay(cap, shape, P.PriorityConfig(0.6, 0.01, cfg.beta_schedule()),
+                                  frame_dedup=dedup)
+        for s, a, r, s2, t in stream:
+            mem.store(P.Transition(s, a % 3, r, s2, t))
+        g = np.random.default_rng(5)
+        res = [P.learn_step(on, tg, mem, opt, cfg, 100 + i, g) for i in range(4)]
+        runs.append((res, on.flat_values.clone(), mem.tree.nodes.clone()))
+    (ra, wa, na), (rb, wb, nb) = runs
+    for x, y in zip(ra, rb):
+        assert np.array_equal(x.td_errors, y.td_errors) and np.array_equal(x.losses, y.losses)
+    assert torch.equal(wa, wb) and torch.equal(na, nb)

@@ -85,6 +85,23 @@ def main():
     add("ring_gather k=4096", us, bytes_=2 * 2 * k * 28224 + k * (8 + 8 + 8 + 8 + 1),
         note="frames read+write, metadata")
 
+    # --- frame-deduplicated ring gather, k = 4096: a 1M-slot ring whose
+    # pool holds ~1.1 frames per slot (an episodic stream), filled directly
+    from paper_1804_05834_b200.frame_ring import FrameDedupMemory
+    fcap = cap + cap // 10
+    dd = FrameDedupMemory(cap, (84, 84, 4), frame_capacity=fcap)
+    for c0 in range(0, fcap, 1 << 18):
+        c1 = min(fcap, c0 + (1 << 18))
+        dd.frames[c0:c1] = torch.randint(0, 256, (c1 - c0, 84 * 84), dtype=torch.uint8,
+                                         device="cuda")
+    dd.ids.copy_(torch.randint(0, fcap, dd.ids.shape, dtype=torch.int64, device="cuda"))
+    dd._set_size(cap)
+    us = dev_time_us(lambda: dd.gather_into(idx, k, s, s2, a, r, t))
+    add("frame_dedup_gather k=4096", us,
+        bytes_=2 * k * (4 * 7056 + 28224) + k * (2 * 4 * 8 + 8 + 8 + 8 + 1),
+        note="4 pool frames read + stack written per state; 7.8 GB pool instead of a 56 GB ring")
+    del dd
+
     # --- frame preprocessing: 1024 raw 210x160 RGB frames -> 84x84 f32
     from paper_1804_05834_b200 import frames as FR
     nf = 1024
