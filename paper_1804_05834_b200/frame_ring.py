@@ -172,9 +172,43 @@ class FrameDedupMemory(ReplayMemory):
         return i
 
     def store_many(self, states, actions, rewards, next_states, terminals) -> np.ndarray:
-        slots = [self.store(Transition(states[j], actions[j], rewards[j], next_states[j],
-                                       terminals[j])) for j in range(len(actions))]
-        return np.asarray(slots, dtype=np.int64)
+        """Batched ``store``: ids assigned on the host in order, then the new
+        planes in one pinned upload and one scatter per array."""
+        torch = _torch()
+        n = len(actions)
+        if n == 0:
+            return np.zeros(0, dtype=np.int64)
+        slots = (self.cursor + np.arange(n)) % self.capacity
+        new_ids, new_planes = [], []
+        for j in range(n):
+            planes = _planes(states[j], self.stack) + _planes(next_states[j], self.stack)
+            for p in planes:
+                if len(p) != self.frame_bytes:
+                    raise GeometryError(f"frame of {len(p)} B, ring holds {self.frame_bytes} B frames")
+            for fid, p in self.index.assign(int(slots[j]), planes):
+                new_ids.append(fid)
+                new_planes.append(p)
+        # a pool id can be reassigned within the batch only after its last
+        # reference went away: the last upload of an id is the one that counts
+        if new_ids:
+            buf = torch.empty((len(new_ids), self.frame_bytes), dtype=torch.uint8).pin_memory()
+            buf.numpy()[:] = np.frombuffer(b"".join(new_planes), dtype=np.uint8).reshape(
+                len(new_ids), self.frame_bytes)
+            last = {fid: i for i, fid in enumerate(new_ids)}
+            keep = torch.as_tensor(sorted(last.values()), dtype=torch.int64)
+            ids_t = torch.as_tensor([new_ids[i] for i in keep.tolist()], dtype=torch.int64)
+            self.frames.index_copy_(0, ids_t.to("cuda"), buf[keep].to("cuda", non_blocking=True))
+        # a batch longer than the ring keeps its last `capacity` transitions
+        # (scatters with repeated slots would leave an unspecified winner)
+        m = min(n, self.capacity)
+        sl = torch.as_tensor(slots[n - m:], device="cuda")
+        self.ids.index_copy_(0, sl, torch.as_tensor(self.index.ids[slots[n - m:]]).to("cuda"))
+        self.actions[sl] = torch.as_tensor(np.asarray(actions)[n - m:], dtype=torch.int64).to("cuda")
+        self.rewards[sl] = torch.as_tensor(np.asarray(rewards)[n - m:], dtype=torch.float64).to("cuda")
+        self.terminals[sl] = torch.as_tensor(np.asarray(terminals)[n - m:], dtype=torch.bool).to("cuda")
+        self.cursor = int((self.cursor + n) % self.capacity)
+        self._set_size(min(self.size + n, self.capacity))
+        return slots
 
     def store_staged(self, *args, **kwargs) -> None:
         raise NotImplementedError("the frame-deduplicated ring stores through store()")

@@ -202,12 +202,17 @@ class ReplayMemory:
         torch = _torch()
         n = len(actions)
         slots = (self.cursor + np.arange(n)) % self.capacity
-        sl = torch.as_tensor(slots, device="cuda")
-        self.states[sl] = _frames(states, self.states.dtype).reshape((n,) + self.state_shape)
-        self.next_states[sl] = _frames(next_states, self.states.dtype).reshape((n,) + self.state_shape)
-        self.actions[sl] = _to_device(actions, torch.int64)
-        self.rewards[sl] = _to_device(rewards, torch.float64)
-        self.terminals[sl] = _to_device(terminals, torch.bool)
+        # a batch longer than the ring keeps its last `capacity` transitions
+        # (scatters with repeated slots would leave an unspecified winner)
+        m = min(n, self.capacity)
+        sl = torch.as_tensor(slots[n - m:], device="cuda")
+        tail = slice(n - m, n)
+        self.states[sl] = _frames(states, self.states.dtype).reshape((n,) + self.state_shape)[tail]
+        self.next_states[sl] = _frames(next_states, self.states.dtype).reshape(
+            (n,) + self.state_shape)[tail]
+        self.actions[sl] = _to_device(actions, torch.int64)[tail]
+        self.rewards[sl] = _to_device(rewards, torch.float64)[tail]
+        self.terminals[sl] = _to_device(terminals, torch.bool)[tail]
         self.cursor = int((self.cursor + n) % self.capacity)
         self._set_size(min(self.size + n, self.capacity))
         return slots

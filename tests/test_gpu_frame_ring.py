@@ -103,3 +103,39 @@ def test_learn_step_identical_on_dedup_ring(P):
     for x, y in zip(ra, rb):
         assert np.array_equal(x.td_errors, y.td_errors) and np.array_equal(x.losses, y.losses)
     assert torch.equal(wa, wb) and torch.equal(na, nb)
+
+
+def test_store_many_matches_store(P):
+    """The batched insert (one upload for the batch, pool ids possibly freed
+    and reused inside it) leaves the same sampled bytes as per-transition
+    stores and as the full-stack ring."""
+    from paper_1804_05834_b200.frame_ring import FrameDedupMemory
+    rng = np.random.default_rng(21)
+    shape, cap = (84, 84, 4), 16
+    stream = episodic(rng, 70, shape, max_len=5)
+    full, one = _pair(P, cap, shape, stream)
+    many = FrameDedupMemory(cap, shape, frame_capacity=2 * cap + 16)
+    for c0 in range(0, len(stream), 23):               # batches that wrap the ring
+        chunk = stream[c0:c0 + 23]
+        many.store_many([c[0] for c in chunk], [c[1] for c in chunk], [c[2] for c in chunk],
+                        [c[3] for c in chunk], [c[4] for c in chunk])
+    assert many.cursor == full.cursor and many.size == full.size
+    # the full-stack ring's batched insert with batches longer than the ring
+    batched = P.ReplayMemory(cap, shape)
+    for c0 in range(0, len(stream), 23):
+        chunk = stream[c0:c0 + 23]
+        batched.store_many(np.stack([c[0] for c in chunk]), [c[1] for c in chunk],
+                           [c[2] for c in chunk], np.stack([c[3] for c in chunk]),
+                           [c[4] for c in chunk])
+    for f in ("states", "next_states", "actions", "rewards", "terminals"):
+        assert torch.equal(getattr(batched, f), getattr(full, f)), f
+    ti = torch.arange(cap, device="cuda")
+    for mem in (one, many):
+        s, s2 = torch.empty_like(full.states), torch.empty_like(full.next_states)
+        a = torch.empty(cap, dtype=torch.int64, device="cuda")
+        r = torch.empty(cap, dtype=torch.float64, device="cuda")
+        t = torch.empty(cap, dtype=torch.bool, device="cuda")
+        mem.gather_into(ti, cap, s, s2, a, r, t)
+        assert torch.equal(s, full.states) and torch.equal(s2, full.next_states)
+        assert torch.equal(a, full.actions) and torch.equal(r, full.rewards)
+        assert torch.equal(t, full.terminals)
