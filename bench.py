@@ -3,6 +3,7 @@ updates/s and sampled transitions/s, Dueling+Double+PER, batch 32, 1M
 synthetic Atari transitions).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--mode auto|single|dp|replicas]
 
 Our arm (default) prints ONE JSON line on rank 0:
   value      device-timed updates/s, inputs (ring, tree, pre-drawn uniforms)
@@ -14,15 +15,23 @@ Our arm (default) prints ONE JSON line on rank 0:
   roofline   the dominant layer phase (GEMM) of the step, timed alone with
              CUDA events on its stream, vs MEASURED_PEAKS.json;
   cpu_baseline  the CPU oracle port of the reference learn_step on this
-             host's cores for a bounded sample.
-``--impl reference`` times that CPU path alone and prints its own line.
-Under torchrun (N > 1) the default is N independent learners, one per GPU
-(the population-of-seeds mode: each rank owns its own 1M ring, tree and
-networks; no data-path collective; weak scaling).  ``--mode dp`` runs the
-cfg5 data-parallel learner instead (paper_1804_05834_b200/dp.py: replay
-sharded across the ranks, global stratified PER over all-gathered shard
-totals, per-GPU batch 32, NCCL gradient all-reduce; host-orchestrated, see
-DESIGN.md §6).  Rank 0 reports the max-over-ranks time.
+             host's cores for a bounded sample (all BLAS threads, and one
+             pinned core under ``single_core``).
+``--impl reference`` times that CPU path alone and prints its own line; it
+never imports this package (the synthetic data generator is loaded from its
+file), so no CUDA library of ours is loaded in that arm.
+
+Multi-GPU.  ``--gpus N`` (N > 1) outside torchrun launches N ranks itself
+through torch.distributed.run (and refuses when fewer than N GPUs are
+visible); under torchrun each rank reads RANK / WORLD_SIZE / LOCAL_RANK.  The
+default for N > 1 is the cfg5 data-parallel learner (``--mode dp``,
+paper_1804_05834_b200/dp.py: replay sharded across the ranks, global
+stratified PER over all-gathered shard totals, per-GPU batch 32, frames read
+from the owners' rings over NVLink, NCCL gradient all-reduce, one CUDA graph
+per rank and update); ``--mode replicas`` runs N independent learners (the
+population of seeds, no data-path collective).  Both are weak scaling; rank 0
+reports the max-over-ranks device time.  NCCL_DEBUG=INFO (INIT, ENV) goes to
+stderr for N > 1.
 """
 
 from __future__ import annotations
@@ -120,13 +129,24 @@ class ClockSampler:
 # CPU side: the oracle port of the reference learn_step
 # --------------------------------------------------------------------------
 
-def cpu_learner(cfg_name: str, seed: int = 0, pool: int = 2048):
+def load_synth():
+    """The synthetic-data generator, loaded straight from its file so the CPU
+    arm never imports the package (whose __init__ loads libdqn_b200.so)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "dqn_bench_synth", REPO / "paper_1804_05834_b200" / "synth.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def cpu_learner(cfg_name: str, batch: int = 32, seed: int = 0, pool: int = 2048):
     """Oracle learner at the bench config.  The 1M-leaf fp64 tree is real; the
     frame store is a pool of ``pool`` synthetic transitions addressed by
     slot % pool (the reference's float32 ring would need 226 GB of host RAM;
     gather cost per sample is unchanged: one fancy-index copy per state)."""
     from oracle import deepq_oracle as O
-    from paper_1804_05834_b200 import synth
+    synth = load_synth()
     c = CONFIGS[cfg_name]
     cap = c["capacity"]
     shape = (84, 84, 4)
@@ -161,7 +181,7 @@ def cpu_learner(cfg_name: str, seed: int = 0, pool: int = 2048):
         mem.max_priority = float((td + 0.01).max())
     else:
         mem = ring
-    lcfg = O.LearnCfg(double=c["double"])
+    lcfg = O.LearnCfg(double=c["double"], batch_size=batch)
     return on, tg, mem, opt, lcfg, O
 
 
@@ -174,9 +194,9 @@ def blas_threads() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_time(cfg_name: str, steps: int, warmup: int, budget_s: float | None):
+def cpu_time(cfg_name: str, steps: int, warmup: int, budget_s: float | None, batch: int = 32):
     """Time the oracle learn_step; returns (updates/s, steps timed)."""
-    on, tg, mem, opt, lcfg, O = cpu_learner(cfg_name)
+    on, tg, mem, opt, lcfg, O = cpu_learner(cfg_name, batch)
     rng = np.random.default_rng(np.random.SeedSequence([0, 2]))
     for s in range(warmup):
         O.learn_step(on, tg, mem, opt, lcfg, 50_000 + s, rng=rng)
@@ -193,25 +213,95 @@ def cpu_time(cfg_name: str, steps: int, warmup: int, budget_s: float | None):
     return n / (time.perf_counter() - t0), n
 
 
+def cpu_time_single_core(cfg_name: str, steps: int, warmup: int, budget_s: float | None,
+                         batch: int = 32):
+    """The same, pinned to one core with one BLAS thread (BASELINE.md §3.1's
+    1-core setting: taskset -c <cpu> + OPENBLAS_NUM_THREADS=1)."""
+    from threadpoolctl import threadpool_limits
+    cpus = sorted(os.sched_getaffinity(0))
+    try:
+        os.sched_setaffinity(0, {cpus[0]})
+        with threadpool_limits(limits=1):
+            return cpu_time(cfg_name, steps, warmup, budget_s, batch)
+    finally:
+        os.sched_setaffinity(0, set(cpus))
+
+
+def cpu_baseline_obj(cfg_name: str, batch: int, steps: int, warmup: int,
+                     budget_s: float | None, budget_1core_s: float | None) -> dict:
+    """cpu_baseline: the oracle port of the reference learn_step on this host,
+    all BLAS threads (value) and one pinned core (single_core)."""
+    ups, n = cpu_time(cfg_name, steps, warmup, budget_s, batch)
+    cores = blas_threads()
+    ups1, n1 = cpu_time_single_core(cfg_name, max(3, steps // 3), 2, budget_1core_s, batch)
+    what = (f"({cfg_name}, batch {batch}, 1M-leaf fp64 tree, pooled frame store, "
+            f"numpy/OpenBLAS")
+    return {"value": ups, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{n} oracle learn_step updates {what} {cores} threads)",
+            "cpu": cpu_model(), "nproc": os.cpu_count(),
+            "single_core": {"value": ups1, "unit": UNIT, "cores": 1,
+                            "sample": f"{n1} oracle learn_step updates {what} 1 thread, "
+                                      f"pinned to one core)"}}
+
+
+def bench_config(cfg_name: str, capacity: int, batch: int, world: int, mode: str) -> dict:
+    """The ``config`` object, identical in both arms for the same command."""
+    c = CONFIGS[cfg_name]
+    if world == 1 and mode != "dp":
+        workload, par = c["desc"], "single GPU"
+    elif mode == "replicas":
+        workload, par = c["desc"] + f" (population of {world} independent learners)", \
+            f"replicas x{world}"
+    else:
+        workload = (f"cfg5: Dueling + Double + PER data-parallel, replay sharded over {world} "
+                    f"GPUs, per-GPU batch {batch}")
+        par = f"dp{world}"
+    return {"workload": workload, "capacity": capacity, "global_batch": batch * world,
+            "per_gpu_batch": batch, "parallelism": par,
+            "l2": "inputs larger than L2 (56 GB u8 ring); parameters stay L2-resident across "
+                  "updates as in training"}
+
+
 def run_reference(args):
+    """--impl reference: the reference learn_step's CPU path (the oracle port,
+    see module doc) on this host, on the same config / metric / unit as our
+    arm.  At N > 1 the comparator is cfg5's global batch 32 N in one process
+    (the reference has no data-parallel mode), its value counted in the same
+    unit as our DP arm (batch-32 learner updates/s = global updates/s x N)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    ups, n = cpu_time(args.config, args.steps, args.warmup, None)
+    n_gpus = max(world, args.gpus)
+    mode = resolve_mode(args, n_gpus)
+    per_rank = n_gpus if mode == "dp" else 1
+    batch = args.batch * per_rank
+    cap = args.capacity or CONFIGS[args.config]["capacity"]
+    ups, n = cpu_time(args.config, args.steps, args.warmup, None, batch)
     cores = blas_threads()
-    sample = (f"{n} oracle learn_step updates ({args.config}, batch 32, 1M-leaf fp64 tree, "
-              f"pooled frame store) after {args.warmup} warm-up, numpy/OpenBLAS {cores} threads")
+    ups1, n1 = cpu_time_single_core(args.config, max(3, args.steps // 4), 2, 20.0, batch)
+    value = ups * per_rank if mode == "dp" else ups
+    what = (f"({args.config}, batch {batch}, 1M-leaf fp64 tree, pooled frame store) after "
+            f"{args.warmup} warm-up, numpy/OpenBLAS")
     line = {
-        "impl": "reference", "metric": METRIC, "value": ups, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus,
         "steps": n, "warmup": args.warmup, "ms_per_step": 1000.0 / ups, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": CONFIGS[args.config]["desc"], "global_batch": 32,
-                   "parallelism": "host cpu"},
-        "transitions_per_sec": ups * 32,
-        "cpu_baseline": {"value": ups, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample, "cpu": cpu_model()},
-        "e2e": {"value": ups, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": bench_config(args.config, cap, args.batch, n_gpus, mode),
+        "transitions_per_sec": ups * batch,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{n} oracle learn_step updates {what} {cores} threads",
+                         "cpu": cpu_model(), "nproc": os.cpu_count(),
+                         "single_core": {"value": ups1 * (per_rank if mode == "dp" else 1),
+                                         "unit": UNIT, "cores": 1,
+                                         "sample": f"{n1} updates {what} 1 thread, pinned"}},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if mode == "dp":
+        line["note"] = (f"the reference has no data-parallel mode: one learn_step at global batch "
+                        f"{batch} per step, value = updates/s x {per_rank} (batch-{args.batch} "
+                        f"learner updates/s, our DP arm's unit)")
+    elif mode == "replicas":
+        line["note"] = "one CPU learner; the population mode's value on the GPU arm is summed over GPUs"
     print(json.dumps(line), flush=True)
 
 
@@ -416,13 +506,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        ups, n = cpu_time(args.config, 1 << 30, 2, args.cpu_budget)
-        cores = blas_threads()
-        cpu = {"value": ups, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": (f"{n} oracle learn_step updates in ~{args.cpu_budget:.0f} s ({args.config}, "
-                          f"batch 32, 1M-leaf fp64 tree, pooled frame store), numpy/OpenBLAS "
-                          f"{cores} threads"),
-               "cpu": cpu_model()}
+        cpu = cpu_baseline_obj(args.config, k, 1 << 30, 2, args.cpu_budget, args.cpu_budget_1core)
 
     if rank == 0:
         clocks = clk.summary()
@@ -431,12 +515,8 @@ def run_ours(args):
             "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (hash-generated u8 84x84x4 frames, seeded metadata, random-init nets)",
-            "config": {"workload": c["desc"], "capacity": cap, "global_batch": k * world,
-                       "per_gpu_batch": k,
-                       "parallelism": "single GPU" if world == 1 else f"replicas x{world}",
-                       "l2": "inputs larger than L2 (56 GB u8 ring); parameters stay L2-resident "
-                             "across updates as in training",
-                       "fill_seconds": round(t_fill, 2)},
+            "config": bench_config(args.config, cap, k, world, "single" if world == 1 else "replicas"),
+            "fill_seconds": round(t_fill, 2),
             "transitions_per_sec": value * k,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": plan.h2d_bytes,
                     "d2h_bytes_per_step": plan.d2h_bytes,
@@ -560,25 +640,56 @@ def run_dp(args):
     e2e = world * args.steps / (float(t.item()) / 1e3)
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT + " (batch-32 updates, all GPUs)",
+            "metric": METRIC, "value": value, "unit": UNIT,
+            "unit_note": "batch-32 learner updates/s summed over the GPUs (= global updates/s x N)",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (hash-generated u8 frames per shard, random-init nets)",
-            "config": {"workload": "cfg5 Dueling+Double+PER data-parallel, replay sharded",
-                       "capacity": cap * world, "global_batch": K, "per_gpu_batch": k,
-                       "parallelism": f"dp{world} (sharded PER, peer-ring gather, NCCL allreduce)",
-                       "l2": "1M-slot ring (56 GB) >> L2: sampled rows come from HBM"},
+            "config": bench_config("cfg4", cap * world, k, world, "dp"),
+            "exchange": "sharded PER (shard totals all-gathered), frames read from the owners' "
+                        "rings over NVLink (CUDA-IPC), NCCL gradient all-reduce",
             "transitions_per_sec": value * k,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * (K + 1),
                     "d2h_bytes_per_step": 8 * 4 * K + 4,
                     "path": "dp.DeviceDataParallelLearner.step (one graph launch per update)"},
             "gpu_launches": launches * args.steps, "launches_per_step": launches,
-            "clocks": clk.summary(), "cpu_baseline": None,
+            "clocks": clk.summary(),
+            "cpu_baseline": (cpu_baseline_obj("cfg4", k, 1 << 30, 2, args.cpu_budget,
+                                              args.cpu_budget_1core)
+                             if world == 1 and not args.no_cpu else None),
         }
         print(json.dumps(line), flush=True)
     learner.close()
     dist.destroy_process_group()
+
+
+def resolve_mode(args, n_gpus: int) -> str:
+    """N = 1: the single-GPU learner (cfg4); N > 1: the cfg5 data-parallel
+    learner unless --mode replicas asks for the population of seeds."""
+    if args.mode == "auto":
+        return "single" if n_gpus == 1 else "dp"
+    return args.mode
+
+
+def spawn_ranks(n: int) -> int:
+    """``python bench.py --gpus N`` outside torchrun: launch N ranks (one per
+    GPU) through torch.distributed.run on this node and return its exit code.
+    Refuses loudly when this box has fewer than N GPUs."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {n} requested but only {have} "
+                          f"CUDA device(s) are visible; refusing to time fewer GPUs"}), flush=True)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -591,18 +702,31 @@ def main():
     ap.add_argument("--capacity", type=int, default=0)
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget-1core", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--mode", default="auto", choices=["auto", "single", "replicas", "dp"],
-                    help="auto/replicas: one independent learner per GPU (population of "
-                         "seeds; N = 1 is the single-GPU learner); dp: the cfg5 "
-                         "data-parallel learner (sharded PER, NCCL gradient all-reduce)")
+                    help="auto: N = 1 -> the single-GPU learner, N > 1 -> dp; dp: the cfg5 "
+                         "data-parallel learner (sharded PER, NCCL gradient all-reduce); "
+                         "replicas: one independent learner per GPU (population of seeds)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    world = dist_env()[1]
+    rank, world, _ = dist_env()
     if args.impl == "reference":
         run_reference(args)
-    elif args.mode == "dp":
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
+    if world > 1 and args.gpus not in (1, world):
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    args.gpus = world
+    if world > 1:
+        # communicator set-up lines (ranks, NVLS / P2P transport) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    mode = resolve_mode(args, world)
+    if mode == "dp":
         run_dp(args)
     else:
         run_ours(args)
