@@ -228,6 +228,12 @@ def test_sampler_1m_ring_learn_step(P):
     idx, prob, w = O.per_indices(ref, n, 32, mem.beta(10), u)
     assert np.array_equal(plan.idx.cpu().numpy(), idx)
     assert ulp_diff(plan.w.cpu().numpy(), w).max() <= 4
+    # release the 56 GB ring (cached plans reference their memories)
+    for key in [k for k, p in P.agent._PLANS.items() if p.memory is mem]:
+        del P.agent._PLANS[key]
+    del plan, mem
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("name", ["cfg4", "cfg3"])
