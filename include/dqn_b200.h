@@ -50,7 +50,7 @@ typedef enum {
 #define DQN_FLAG_BAD_PRIORITY   0x10 /* SumTree.set with negative / non-finite value */
 
 const char *dqn_last_error(void);
-int dqn_abi_version(void);             /* 3 */
+int dqn_abi_version(void);             /* 4 */
 /* 1 if this library was built with the tcgen05 (sm_100a UMMA) conv trunk */
 int dqn_has_tcgen05(void);
 /* kernels launched (or captured) through this library so far, all threads */
@@ -145,23 +145,9 @@ typedef struct {
   float *dx;               /* input gradient (NULL = skip, as the learner does) */
   float *scratch;
   int64_t scratch_floats;
-  /* optional: layer 0's transposed im2col of x (uint8 input only), filled by
-   * dqn_net_im2col_t; when set, layer 0's wgrad reads its patch operand from
-   * it as contiguous rows instead of gathering bytes (NULL = gather) */
-  uint8_t *xt;
 } dqn_binding;
 
 int64_t dqn_net_scratch_floats(const dqn_net_desc *net, int32_t batch);
-
-/* Bytes of layer 0's transposed im2col for `batch` (0 when the network's
- * input is not uint8 or layer 0 is not a tcgen05 convolution). */
-int64_t dqn_net_im2col_t_bytes(const dqn_net_desc *net, int32_t batch);
-
-/* bind->xt[r][pix] = x patch element r of output pixel pix for layer 0
- * (r < fh*fw*C, pix < batch*OH*OW): the wgrad operand of layers.py:250-255
- * laid out along the reduction.  Run it anywhere between the batch gather
- * and the wgrad (the learner puts it beside the forward pass). */
-int dqn_net_im2col_t(void *stream, const dqn_net_desc *net, const dqn_binding *bind);
 
 /* Network.forward (network.py:90-104): all layers front to back. */
 int dqn_net_forward(void *stream, const dqn_net_desc *net, const float *params,
@@ -210,6 +196,8 @@ int dqn_head_td(void *stream, const dqn_net_desc *on_net, const float *on_params
 #define DQN_TD_DOUBLE 0x1
 #define DQN_TD_HUBER 0x2
 #define DQN_TD_REWARD_CLIP 0x4
+/* dqn_head_td only: the last-CTA head form instead of the two-phase form */
+#define DQN_TD_HEAD_LAST_CTA 0x8
 
 /* compute_target_double / compute_target_dqn (agent.py:58-73) and the loss
  * block of learn_step (agent.py:110-124): argmax (first max), y = r + (t ? 0 :
@@ -259,18 +247,6 @@ int dqn_clip_gradients(void *stream, float *g, int64_t n, double max_norm, doubl
 
 /* sync_target (optim.py:78-89): bitwise copy of the flat parameter buffer. */
 int dqn_sync_target(void *stream, float *dst, const float *src, int64_t n);
-
-/* The learner's three forwards of trunk layers [0, upto) in one launch per
- * layer (tcgen05 layers; others fall back to two launches): online rows
- * [0, k) and [k, 2k) of on_bind (batch 2k: [s; s'], network.py:90-100) and
- * the target binding (batch k, its x = s'), same net geometry, online and
- * target parameters.  scratch: dqn_net_forward_group_scratch(net, upto, k)
- * floats, the last 16384 (split-K tile counters) zeroed once. */
-int64_t dqn_net_forward_group_scratch(const dqn_net_desc *net, int32_t upto, int32_t batch);
-int dqn_net_forward_group(void *stream, const dqn_net_desc *net, const float *on_params,
-                          const dqn_binding *on_bind, const float *tg_params,
-                          const dqn_binding *tg_bind, int32_t upto, float *scratch,
-                          int64_t scratch_floats, int32_t *flags);
 
 /* ---- data-parallel learner (algorithm in dp.py) --------
  * N ranks (one per GPU), rank r owns replay shard r (global transition g at

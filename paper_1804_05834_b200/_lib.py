@@ -27,7 +27,7 @@ OK, ERR_INVALID_ARG, ERR_GEOMETRY, ERR_INDEX, ERR_EMPTY, ERR_ZERO_TOTAL, ERR_NON
     ERR_CUDA, ERR_UNSUPPORTED = range(9)
 FLAG_INDEX, FLAG_ZERO_TOTAL, FLAG_NONFINITE_GRAD, FLAG_NONFINITE_OUT, FLAG_BAD_PRIORITY = \
     0x1, 0x2, 0x4, 0x8, 0x10
-TD_DOUBLE, TD_HUBER, TD_REWARD_CLIP = 0x1, 0x2, 0x4
+TD_DOUBLE, TD_HUBER, TD_REWARD_CLIP, TD_HEAD_LAST_CTA = 0x1, 0x2, 0x4, 0x8
 LAYER_CONV, LAYER_LINEAR, LAYER_DUELING = 0, 1, 2
 MAX_LAYERS = 8
 
@@ -49,7 +49,7 @@ class NetDesc(C.Structure):
 class Binding(C.Structure):
     _fields_ = [("batch", i32), ("pad_", i32), ("x", vp), ("act", vp * MAX_LAYERS),
                 ("dact", vp * MAX_LAYERS), ("dx", vp), ("scratch", vp),
-                ("scratch_floats", i64), ("xt", vp)]
+                ("scratch_floats", i64)]
 
 
 _SIGS = {
@@ -66,12 +66,10 @@ _SIGS = {
     "dqn_tree_set": ([vp, vp, i32, i64, vp, vp, i32, vp], C.c_int),
     "dqn_tree_rebuild": ([vp, vp, i32], C.c_int),
     "dqn_net_scratch_floats": ([C.POINTER(NetDesc), i32], i64),
-    "dqn_net_im2col_t_bytes": ([C.POINTER(NetDesc), i32], i64),
     "dqn_head_td_work_bytes": ([i32, i32], i64),
     "dqn_head_td": ([vp, C.POINTER(NetDesc), vp, vp, C.POINTER(Binding), C.POINTER(Binding),
                      C.POINTER(NetDesc), vp, C.POINTER(Binding), vp, vp, vp, vp, f64, i32,
                      vp, vp, vp, vp, vp, vp, vp], C.c_int),
-    "dqn_net_im2col_t": ([vp, C.POINTER(NetDesc), C.POINTER(Binding)], C.c_int),
     "dqn_net_forward": ([vp, C.POINTER(NetDesc), vp, C.POINTER(Binding), vp], C.c_int),
     "dqn_net_backward": ([vp, C.POINTER(NetDesc), vp, C.POINTER(Binding), vp], C.c_int),
     "dqn_net_wgrad": ([vp, C.POINTER(NetDesc), vp, C.POINTER(Binding)], C.c_int),
@@ -84,8 +82,6 @@ _SIGS = {
                          C.c_int),
     "dqn_clip_gradients": ([vp, vp, i64, f64, vp], C.c_int),
     "dqn_sync_target": ([vp, vp, vp, i64], C.c_int),
-    "dqn_net_forward_group_scratch": ([vp, C.c_int, C.c_int], i64),
-    "dqn_net_forward_group": ([vp, vp, vp, vp, vp, vp, C.c_int, vp, i64, vp], C.c_int),
     "dqn_dp_shard_info": ([vp, vp, vp, vp, vp], C.c_int),
     "dqn_dp_route": ([vp, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_int, C.c_int, vp],
                      C.c_int),

@@ -146,43 +146,22 @@ class _StepPlan:
         self.head_layer = len(units) - 1
         self.fused_head = (len(units) >= 2 and units[-1]["kind"] in (_lib.LAYER_LINEAR,
                                                                      _lib.LAYER_DUELING)
-                           and self.nA <= 18 and k <= 1024
-                           and os.environ.get("DQN_B200_FUSED_HEAD", "1") != "0")
+                           and self.nA <= 18 and k <= 1024 and FUSED_HEAD)
         self.head_work = torch.zeros(int(_lib.lib.dqn_head_td_work_bytes(k, self.nA)),
                                      dtype=torch.uint8, device=dev)
-        # conv1's wgrad reads its uint8 patch operand from a transposed im2col
-        # built beside the forward pass (dqn_net_im2col_t), not byte gathers
         self.on_desc = online.desc_for(self.x)
-        nb = int(_lib.lib.dqn_net_im2col_t_bytes(C.byref(self.on_desc), k))
-        self.xt = torch.empty(nb, dtype=torch.uint8, device=dev) if nb > 0 else None
-        if self.xt is not None:
-            self.on_view.struct.xt = self.xt.data_ptr()
-        # DQN_B200_PRIO=1: the capture stream (dgrad chain) and the priority-
-        # update stream run at the highest priority, the side stream (target
-        # forward, wgrads) at the lowest, node priorities honoured by the
-        # graph.  Off by default: measured 1-2 % slower (the update is mostly
-        # SM-time bound and the target forward on the side stream is critical)
-        hi = -8 if USE_PRIORITY else 0
-        # DQN_B200_GROUPED_FWD=1: online [s; s'] and target s' forwards of the
-        # trunk as one launch per layer (dqn_net_forward_group).  Off by
-        # default: measured 5 % slower than the two concurrent PDL chains
-        self.grouped = (self.fused_head and self.double
-                        and os.environ.get("DQN_B200_GROUPED_FWD", "0") == "1")
-        self.grp_scratch = None
-        if self.grouped:
-            n = int(_lib.lib.dqn_net_forward_group_scratch(C.byref(self.on_desc),
-                                                           self.head_layer, k))
-            self.grp_scratch = torch.zeros(n, dtype=torch.float32, device=dev)
         self.fused_sample = (ring.fused_ok and ring.slot_bytes % 16 == 0
-                             and ring.state_dtype == torch.uint8
-                             and os.environ.get("DQN_B200_FUSED_SAMPLE", "1") != "0")
-        self.zero_copy = (k * (self.nA + 1) <= 2048
-                          and os.environ.get("DQN_B200_ZEROCOPY", "1") != "0"
-                          and os.environ.get("DQN_B200_HEAD_TWO_PHASE", "1") != "0")
+                             and ring.state_dtype == torch.uint8 and FUSED_SAMPLE)
+        # the head's form is fixed when the plan is built (and so in its graph)
+        self.head_two_phase = HEAD_TWO_PHASE
+        if not self.head_two_phase:
+            self.flags_td |= _lib.TD_HEAD_LAST_CTA
+        # zero-copy results are written by the two-phase head's kernels
+        self.zero_copy = k * (self.nA + 1) <= 2048 and self.head_two_phase
         self._host_out = None
-        self.side = torch.cuda.Stream(priority=0)
-        self.tree_stream = torch.cuda.Stream(priority=hi)
-        self.capture_stream = torch.cuda.Stream(priority=hi)
+        self.side = torch.cuda.Stream()
+        self.tree_stream = torch.cuda.Stream()
+        self.capture_stream = torch.cuda.Stream()
         self.graph = None
         self.graph_exec = None
         self.dev = torch.cuda.current_device()
@@ -252,8 +231,6 @@ class _StepPlan:
         beside the rest of the dgrad chain as soon as that layer's output
         gradient exists (it has its own scratch / split-K counters); the first
         layer's wgrad, which has no dgrad beside it, stays on the main stream.
-        conv1's transposed patch operand (im2col_t) is built after the target
-        forward: it is read only by the last wgrad.
         With ``priorities`` the sum-tree update (replay.py:232-241) runs on a
         third stream as soon as the TD errors exist and joins before the
         optimizer, which still sees its error flags first."""
@@ -267,35 +244,16 @@ class _StepPlan:
         e_in.record(s0)
         with torch.cuda.stream(s1):
             s1.wait_event(e_in)
-            e_tg = None
-            if not self.grouped:
-                tg.forward_into(self.x[k:], self.tg_bind,
-                                upto=self.head_layer if self.fused_head else None)
-                e_tg = ev()
-                e_tg.record(s1)
-            e_xt = None
-            if self.xt is not None:              # read by the last wgrad only
-                self.on_view.struct.x = self.x.data_ptr()
-                _lib.call("dqn_net_im2col_t", _lib.stream_ptr(), C.byref(self.on_desc),
-                          C.byref(self.on_view.struct))
-                e_xt = ev()
-                e_xt.record(s1)
+            tg.forward_into(self.x[k:], self.tg_bind,
+                            upto=self.head_layer if self.fused_head else None)
+            e_tg = ev()
+            e_tg.record(s1)
         upto = self.head_layer if self.fused_head else None
-        if self.grouped:
-            xs = self.x[k:]
-            self.on_bind.x, self.tg_bind.x = self.x, xs
-            self.on_bind.struct.x, self.tg_bind.struct.x = self.x.data_ptr(), xs.data_ptr()
-            g = self.grp_scratch
-            _lib.call("dqn_net_forward_group", st, C.byref(self.on_desc), on.flat_values.data_ptr(),
-                      C.byref(self.on_bind.struct), tg.flat_values.data_ptr(),
-                      C.byref(self.tg_bind.struct), self.head_layer, g.data_ptr(), g.numel(),
-                      self.flags.data_ptr())
-        elif self.double:
+        if self.double:
             on.forward_into(self.x, self.on_bind, upto=upto)
         else:
             on.forward_into(self.x[:k], self.on_bind, upto=upto)
-        if e_tg is not None:
-            s0.wait_event(e_tg)
+        s0.wait_event(e_tg)
         nA = self.nA
         out = self.d_out
         for v in (self.on_view, self.on_wview):
@@ -341,8 +299,6 @@ class _StepPlan:
             if layer == 0:
                 # conv1 has no dgrad: its wgrad takes the main stream (and the
                 # dgrad binding's scratch) instead of queueing behind conv2's
-                if e_xt is not None:
-                    s0.wait_event(e_xt)
                 on.layer_into(self.on_view, 0, 2, self.flags)
                 break
             with torch.cuda.stream(s1):           # wgrad of `layer` once its grad exists
@@ -384,7 +340,11 @@ class _StepPlan:
 
 _PLANS: dict = {}
 USE_GRAPH = os.environ.get("DQN_B200_GRAPH", "1") != "0"
-USE_PRIORITY = os.environ.get("DQN_B200_PRIO", "0") == "1"
+# Launch-form switches, read when a step plan is built (tests compare the
+# forms; each alternative was measured and the defaults are the fastest):
+FUSED_HEAD = True       # Q heads + TD block + head backward/wgrad in dqn_head_td
+HEAD_TWO_PHASE = True   # its two-phase form (else the last-CTA-ticket form)
+FUSED_SAMPLE = True     # sum-tree descent + frame gather in one launch
 _GRAPH_LAUNCH = _lib.lib.dqn_graph_launch
 
 
@@ -402,7 +362,7 @@ class _Exec:
     def __init__(self, graph):
         self.ptr = C.c_void_p()
         _lib.call("dqn_graph_instantiate", C.c_void_p(graph.raw_cuda_graph()),
-                  1 if USE_PRIORITY else 0, C.byref(self.ptr))
+                  0, C.byref(self.ptr))
         self._fin = weakref.finalize(self, _lib.lib.dqn_graph_destroy, self.ptr)
 
     @property

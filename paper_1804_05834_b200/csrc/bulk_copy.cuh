@@ -46,9 +46,9 @@ static __device__ __forceinline__ void bulk_copy_via_smem(void *smem, uint64_t *
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-inline bool tma_gather_enabled() {
-  const char *e = getenv("DQN_B200_TMA_GATHER");       // read per call (capture time)
-  return !(e && e[0] == '0');
-}
+// the frame gathers use the bulk-copy engine (measured +0.3 % device / +1 %
+// end to end over register copies); the register path remains for slots
+// that are not 16-byte multiples
+inline bool tma_gather_enabled() { return true; }
 
 }  // namespace dqn

@@ -50,11 +50,10 @@ struct HeadTdArgs {
   double *host_out;        // optional pinned host copy: targets | td | losses | stats
 };
 
-// DQN_B200_HEAD_TWO_PHASE=0 selects the last-CTA form (head_q_td + head_bwd_wgrad)
-inline bool head_two_phase() {
-  const char *e = getenv("DQN_B200_HEAD_TWO_PHASE");   // read per call (graph capture time)
-  return !(e && e[0] == '0');
-}
+// td_flags & DQN_TD_HEAD_LAST_CTA selects the last-CTA form (head_q_td +
+// head_bwd_wgrad) instead of the two-phase form -- an explicit argument, so a
+// captured graph's form is fixed by its caller, not by the environment
+inline bool head_two_phase(int td_flags) { return !(td_flags & DQN_TD_HEAD_LAST_CTA); }
 
 // K1: Q heads of both networks (one warp per row: lane-strided fmaf chains,
 // fixed shuffle tree read from lane 0), then -- in the last CTA to finish --
@@ -440,20 +439,15 @@ int launch_head_td(cudaStream_t st, const HeadTdArgs &p) {
   const int R = p.on.rows + p.tg.rows;
   const int nb_dx = p.dx ? (p.k * p.F + kHeadCta - 1) / kHeadCta : 0;
   const int nb_w = (p.F + 1 + kHeadCta - 1) / kHeadCta;
-  if (p.host_out && !(p.k * (NA + 1) <= kGsMax && head_two_phase())) {
+  if (p.host_out && !(p.k * (NA + 1) <= kGsMax && head_two_phase(p.td_flags))) {
     set_error("head_td: host_out needs the two-phase form (batch * (nA + 1) <= %d)", kGsMax);
     return DQN_ERR_UNSUPPORTED;
   }
-  if (p.k * (NA + 1) <= kGsMax && head_two_phase()) {
-    const char *only = getenv("DQN_B200_HEAD_ONLY");      // diagnostic: "q" or "td"
-    if (!only || only[0] != 't') {
-      launch_k(head_q_kernel<NA>, R, kHeadCta, 0, st, p);
-      DQN_LAUNCH_CHECK("head_q");
-    }
-    if (!only || only[0] != 'q') {
-      launch_k(head_td_bwd_kernel<NA>, nb_dx + (p.F + 1 + 31) / 32, kHeadCta, 0, st, p, nb_dx);
-      DQN_LAUNCH_CHECK("head_td_bwd");
-    }
+  if (p.k * (NA + 1) <= kGsMax && head_two_phase(p.td_flags)) {
+    launch_k(head_q_kernel<NA>, R, kHeadCta, 0, st, p);
+    DQN_LAUNCH_CHECK("head_q");
+    launch_k(head_td_bwd_kernel<NA>, nb_dx + (p.F + 1 + 31) / 32, kHeadCta, 0, st, p, nb_dx);
+    DQN_LAUNCH_CHECK("head_td_bwd");
     return DQN_OK;
   }
   launch_k(head_q_td_kernel<NA>, (R + kHeadCta / 32 - 1) / (kHeadCta / 32), kHeadCta, 0, st, p);

@@ -860,157 +860,6 @@ int lin_wgrad_smallk(cudaStream_t st, const float *x, const float *dy, int B, in
   return DQN_OK;
 }
 
-// -------------------------------------------- uint8 conv wgrad, small batch
-// dW[t][c] += (sum_p xt[t][p] * dY[p][c]) / 255, db[c] += sum_p dY[p][c] for
-// the first (uint8-input) conv at learner batch sizes, from the transposed
-// patch operand xt [M taps][P pixels] (dqn_net_im2col_t).  A long-K,
-// tiny-output reduction (M x N = 256 x 32 over P = 12,800): CTA b sums a
-// pixel range into registers (one tap per thread, all channels), staging
-// 64-pixel chunks of xt (transposed: consecutive taps per pixel) and dY in
-// shared memory; a second kernel adds the CTA partials in CTA order
-// (deterministic) and applies the 1/255 and the gradient flags.
-constexpr int kCwChunk = 64;
-
-template <int NN>
-__global__ void __launch_bounds__(256)
-conv_wgrad_u8_partial_kernel(const uint8_t *__restrict__ xt, const float *__restrict__ dy, int M,
-                             int P, int pix_per_cta, float *__restrict__ partial) {
-  // thread (g = t % 64, cg = t / 64): taps g, g + 64, g + 128, g + 192 of this
-  // 256-tap block, channels 8 cg .. 8 cg + 7 (+ 32 per extra tile for NN = 64).
-  // xs keeps xt's [tap][pixel] layout, rows padded to 17 words: lane g of a
-  // warp reads word (g + 64 i) * 17 + pp / 4 -> 32 distinct banks; ys reads
-  // are warp-wide broadcasts.
-  pdl_begin();
-  constexpr int CT = NN / 32, RW = kCwChunk / 4 + 1;  // channel tiles, padded row words
-  __shared__ uint32_t xs[256 * RW];
-  __shared__ __align__(16) float ys[kCwChunk][NN];
-  const int t = threadIdx.x, tap0 = blockIdx.y * 256;
-  const int g = t & 63, c8 = 8 * (t >> 6);
-  const int p_begin = blockIdx.x * pix_per_cta, p_end = min(P, p_begin + pix_per_cta);
-  float acc[4][8 * CT];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int c = 0; c < 8 * CT; ++c) acc[i][c] = 0.f;
-  float bacc = 0.f;
-  for (int p0 = p_begin; p0 < p_end; p0 += kCwChunk) {
-    const int np = min(kCwChunk, p_end - p0);
-    // all loads of the chunk in flight first: xt rows as 16-byte pieces
-    // (16 pixels of one tap; p0 and P are multiples of 16), dY as float4
-    uint4 xv[4];
-    constexpr int YV = kCwChunk * NN / 4 / 256;           // float4 of dY per thread
-    float4 yv[YV];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = t + 256 * u, tr = i >> 2, q = i & 3;   // tap row, 16-pixel piece
-      const bool ok = tap0 + tr < M && 16 * q < np;
-      xv[u] = ok ? *reinterpret_cast<const uint4 *>(xt + (int64_t)(tap0 + tr) * P + p0 + 16 * q)
-                 : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < YV; ++u) {
-      const int i = t + 256 * u, pp = i / (NN / 4), c4 = i - pp * (NN / 4);
-      yv[u] = pp < np ? *reinterpret_cast<const float4 *>(dy + (int64_t)(p0 + pp) * NN + 4 * c4)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = t + 256 * u, tr = i >> 2, q = i & 3;
-      uint32_t *row = xs + tr * RW + 4 * q;
-      row[0] = xv[u].x; row[1] = xv[u].y; row[2] = xv[u].z; row[3] = xv[u].w;
-    }
-#pragma unroll
-    for (int u = 0; u < YV; ++u) {
-      const int i = t + 256 * u, pp = i / (NN / 4), c4 = i - pp * (NN / 4);
-      *reinterpret_cast<float4 *>(&ys[pp][4 * c4]) = yv[u];
-    }
-    __syncthreads();
-    for (int pq = 0; pq < np; pq += 4) {                // 4 pixels per step
-      uint32_t xw[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) xw[i] = xs[(g + 64 * i) * RW + (pq >> 2)];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int pp = pq + j;
-        float av[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) av[i] = (float)((xw[i] >> (8 * j)) & 0xff);
-#pragma unroll
-        for (int ct = 0; ct < CT; ++ct) {
-          const float4 b0 = *reinterpret_cast<const float4 *>(&ys[pp][32 * ct + c8]);
-          const float4 b1 = *reinterpret_cast<const float4 *>(&ys[pp][32 * ct + c8 + 4]);
-          const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int c = 0; c < 8; ++c) acc[i][8 * ct + c] = fmaf(av[i], bv[c], acc[i][8 * ct + c]);
-        }
-      }
-    }
-    if (blockIdx.y == 0 && t < NN)
-      for (int pp = 0; pp < np; ++pp) bacc = __fadd_rn(bacc, ys[pp][t]);
-    __syncthreads();
-  }
-  float *out = partial + (int64_t)blockIdx.x * ((int64_t)M * NN + NN);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int tap = tap0 + g + 64 * i;
-    if (tap >= M) continue;
-#pragma unroll
-    for (int ct = 0; ct < CT; ++ct) {
-      float *o = out + (int64_t)tap * NN + 32 * ct + c8;
-      *reinterpret_cast<float4 *>(o) =
-          make_float4(acc[i][8 * ct], acc[i][8 * ct + 1], acc[i][8 * ct + 2], acc[i][8 * ct + 3]);
-      *reinterpret_cast<float4 *>(o + 4) = make_float4(acc[i][8 * ct + 4], acc[i][8 * ct + 5],
-                                                       acc[i][8 * ct + 6], acc[i][8 * ct + 7]);
-    }
-  }
-  if (blockIdx.y == 0 && t < NN) out[(int64_t)M * NN + t] = bacc;
-}
-
-// one warp per output: lane l adds partials l, l + 32, ... in order, then a
-// fixed shuffle tree -- deterministic, every partial load in flight at once
-__global__ void conv_wgrad_u8_reduce_kernel(const float *__restrict__ partial, int nblk, int M,
-                                            int N, float *__restrict__ gw,
-                                            float *__restrict__ gb, int32_t *flags) {
-  pdl_begin();
-  const int64_t stride = (int64_t)M * N + N;
-  const int lane = threadIdx.x & 31;
-  const int64_t o = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
-  if (o >= stride) return;
-  float s = 0.f;
-  for (int b = lane; b < nblk; b += 32) s = __fadd_rn(s, partial[(int64_t)b * stride + o]);
-  for (int k = 16; k; k >>= 1) s = __fadd_rn(s, __shfl_down_sync(0xffffffffu, s, k));
-  if (lane != 0) return;
-  if (o < (int64_t)M * N)
-    acc_grad(gw + o, __fdiv_rn(s, 255.0f), flags);
-  else if (gb)
-    acc_grad(gb + (o - (int64_t)M * N), s, flags);
-}
-
-int conv_wgrad_u8_smallk(cudaStream_t st, const uint8_t *xt, const float *dy, int M, int N, int P,
-                         float *gw, float *gb, float *scratch, int64_t scratch_floats,
-                         int32_t *flags) {
-  if ((N != 32 && N != 64) || P % 16 != 0 || ((uintptr_t)xt % 16) || ((uintptr_t)dy % 16))
-    return DQN_ERR_UNSUPPORTED;
-  const int64_t per = (int64_t)M * N + N;
-  int nblk = (int)std::min<int64_t>({(int64_t)kNumSMs, (int64_t)(P + kCwChunk - 1) / kCwChunk,
-                                     scratch_floats / per});
-  if (nblk < 8) return DQN_ERR_UNSUPPORTED;
-  int ppc = (P + nblk - 1) / nblk;
-  ppc = (ppc + kCwChunk - 1) / kCwChunk * kCwChunk;     // chunks start on 64-pixel boundaries
-  nblk = (P + ppc - 1) / ppc;
-  dim3 grid((unsigned)nblk, (unsigned)((M + 255) / 256));
-  if (N == 32)
-    launch_k(conv_wgrad_u8_partial_kernel<32>, grid, 256, 0, st, xt, dy, M, P, ppc, scratch);
-  else
-    launch_k(conv_wgrad_u8_partial_kernel<64>, grid, 256, 0, st, xt, dy, M, P, ppc, scratch);
-  DQN_LAUNCH_CHECK("conv_wgrad_u8_partial");
-  launch_k(conv_wgrad_u8_reduce_kernel, (int)((per + 7) / 8), 256, 0, st, scratch, nblk, M, N, gw,
-           gb, flags);
-  DQN_LAUNCH_CHECK("conv_wgrad_u8_reduce");
-  return DQN_OK;
-}
 
 int simt_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads,
                      const dqn_binding *b, int32_t *flags) {

@@ -394,7 +394,7 @@ constexpr int kMaxTiles = 16384;
 // Split-K reducers per tile: the last R = budget / tiles + 1 arrivals (<= 8,
 // <= splits) each reduce a slice; R - 1 of them wait for the final arrival
 // on their SM, at most `budget` CTAs per launch (deadlock-free beside another
-// launch).  A kernel argument: DQN_B200_REDUCERS (default 60, at most 60).
+// launch).  A kernel argument (reducer_budget(): 60).
 
 // Shared/tensor memory plan of a policy.
 template <class Pol>
@@ -948,26 +948,13 @@ inline int smem_bytes() {
   return Plan<Pol>::BYTES;
 }
 
-// On by default since the even-ring / tuned-split build (measured in the
-// learner graph: 6,788 vs 6,759 updates/s device, +1-2 % end to end; it was
-// slower in the earlier two-stream layout); DQN_B200_CLUSTER_SPLITK=0 turns
-// it off.  Same reduction order as the global fixup: identical results.
-inline bool cluster_splitk_enabled() {
-  static const bool on = [] {
-    const char *e = getenv("DQN_B200_CLUSTER_SPLITK");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
+// Split-K across thread-block clusters (measured in the learner graph: 6,788
+// vs 6,759 updates/s device, +1-2 % end to end).  Same reduction order as
+// the global fixup: identical results.
+inline bool cluster_splitk_enabled() { return true; }
 
-inline int reducer_budget() {
-  static const int b = [] {
-    const char *e = getenv("DQN_B200_REDUCERS");
-    int v = e ? atoi(e) : 60;
-    return v < 0 ? 0 : (v > 60 ? 60 : v);
-  }();
-  return b;
-}
+// split-K reducers per launch (fewer measured -1 to -6 %)
+inline int reducer_budget() { return 60; }
 
 template <class Pol>
 int launch(cudaStream_t st, const Pol &p, int splits, const char *what) {

@@ -205,10 +205,7 @@ extern "C" int dqn_rmsprop_apply(void *stream, float *w, float *g, float *acc, i
   DQN_CHECK_ARG(((uintptr_t)w | (uintptr_t)g | (uintptr_t)acc) % 16 == 0,
                 "rmsprop: buffers must be 16-byte aligned");
   if (n == 0) return DQN_OK;
-  static const int cap = [] {
-    const char *e = getenv("DQN_B200_RMS_BLOCKS");     // diagnostic
-    return e ? atoi(e) : 148 * 8;                       // measured best in the learner graph
-  }();
+  constexpr int cap = 148 * 8;                          // measured best in the learner graph
   const int blocks4 = (int)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, cap));
   launch_k(rms_apply_kernel, blocks4, 256, 0, as_stream(stream), w, g, acc, n, lr, rho,
            one_minus_rho, eps, flags, flag_out);

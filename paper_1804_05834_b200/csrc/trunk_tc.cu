@@ -24,6 +24,8 @@
 #include <algorithm>
 
 namespace dqn {
+bool conv1_wgrad_u8_ok(const dqn_net_desc *net);
+int64_t conv1_wgrad_u8_scratch(const dqn_net_desc *net, int batch);
 namespace {
 
 __device__ __forceinline__ float4 ld4(const float *p) {
@@ -120,64 +122,6 @@ struct FwdPol : tc::PolBase {
     for (int t = 0; t < 4; ++t) v[t] = (k + t < ke) ? ld4(w + (int64_t)(k + t) * N + n) : zero4();
   }
   __device__ void final4(int m, int n, float4 v, int) const {
-    float t[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float u = U8 ? __fdiv_rn(t[j], 255.0f) : t[j];
-      u = __fadd_rn(u, bias[n + j]);
-      if (relu && u < 0.f) u = 0.f;
-      t[j] = u;
-    }
-    st4(y + (int64_t)m * N + n, make_float4(t[0], t[1], t[2], t[3]));
-  }
-};
-
-// ------------------------------------------------ grouped trunk forward
-// The learner's online [s; s'] and target s' forwards of one trunk layer in
-// ONE launch: problem 0 = online (2 x batch images),
-// problem 1 = target (batch images, its tiles past M1 exit at entry);
-// problem p = blockIdx.z / splits selects input, weights, bias and output.
-// The problem rides in the top byte of the row bases, so the per-element code
-// is FwdPol's.
-template <typename InT, int BN_>
-struct FwdGroupPol : tc::PolBase {
-  static constexpr bool U8 = sizeof(InT) == 1;
-  static constexpr bool SPLIT_A = !U8, SPLIT_B = true, BIAS_FROM_B = false;
-  static constexpr bool B_MNC = true;
-  static constexpr int BN = BN_;
-  static constexpr int PSHIFT = 56;
-  static constexpr long long PMASK = (1LL << PSHIFT) - 1;
-  const InT *x0, *x1;
-  const float *w0, *w1, *bias0, *bias1;
-  float *y0, *y1, *partial;
-  float *bias_out, *bias_partial;       // unused
-  int *counters;
-  Geo g;
-  int M, M1, N, K, klen, relu, ksplits;   // M = problem 0 rows (the grid), M1 = problem 1 rows
-  __device__ int rows(int p) const { return p ? M1 : M; }
-  __device__ int kbeg(int z) const { return z * klen; }
-  __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
-  __device__ long long a_row(int m, int p) const {
-    return m < rows(p) ? (pixel_base(g, m) | ((long long)p << PSHIFT)) : -1;
-  }
-  __device__ void a16(long long base, int k, int ke, float (&v)[16]) const {
-    if (k >= ke) return zero16(v);
-    const InT *x = (base >> PSHIFT) ? x1 : x0;
-    ld16(x + (base & PMASK) + patch_off(g, k), v);
-  }
-  __device__ long long b_row(int n, int p) const {
-    return n < N ? ((long long)n | ((long long)p << PSHIFT)) : -1;
-  }
-  __device__ void b4(long long base, int k, int ke, float4 (&v)[4]) const {
-    const float *w = (base >> PSHIFT) ? w1 : w0;
-    const long long n = base & PMASK;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) v[t] = (k + t < ke) ? ld4(w + (int64_t)(k + t) * N + n) : zero4();
-  }
-  __device__ void final4(int m, int n, float4 v, int p) const {
-    if (m >= rows(p)) return;
-    const float *bias = p ? bias1 : bias0;
-    float *y = p ? y1 : y0;
     float t[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -298,25 +242,6 @@ struct ConvDgradPol : tc::PolBase {
   }
 };
 
-// The same with B's hi tiles loaded by TMA from a 4-D map of the weights
-// {co, c, fx, fy}: the 4-k chunk at k is tap (ti, tj) of this phase, output
-// channels co..co+3, input channels n0..; k past the last tap lands outside
-// the filter (fy >= fh) and reads as zeros (A is zero there anyway)
-template <int BN_>
-struct ConvDgradTmaPol : ConvDgradPol<BN_> {
-  static constexpr bool B_TMA = true;
-  CUtensorMap map;
-  __device__ void b_tma(uint32_t dst, int n0, int k, int zp, uint64_t *bar) const {
-    const Geo &g = this->g;
-    int py, px, hq, wq;
-    this->phase(zp, py, px, hq, wq);
-    const int tw = g.fw / g.sw;
-    const int tap = k / g.N, co = k - tap * g.N;
-    const int ti = tap / tw, tj = tap - ti * tw;
-    tc::tma_load_4d(dst, &map, co, n0, px + g.sw * tj, py + g.sh * ti, bar);
-  }
-};
-
 // ------------------------------------------------------------------ wgrad
 // C[r, co] = sum_pix im2col(x)[pix, r] * dY[pix, co]; the reduction runs
 // over pixels, so both operands are gathered 4 pixels at a time; the bias
@@ -328,7 +253,6 @@ struct WgradPol : tc::PolBase {
   static constexpr bool B_MNC = true;
   static constexpr int BN = BN_;
   const InT *x;
-  const uint8_t *xt;              // optional transposed im2col [M][K] (uint8 input)
   int32_t *flags;                 // non-finite gradients are flagged as written (or nullptr)
   const float *dy;
   float *grad, *partial;
@@ -340,20 +264,12 @@ struct WgradPol : tc::PolBase {
   __device__ int kend(int z) const { return min(K, (z + 1) * klen); }
   __device__ long long a_row(int r, int) const {
     if (r >= M) return -1;
-    return xt ? (long long)r * K : patch_off(g, r);
+    return patch_off(g, r);
   }
-  // patch element r at pixels pix..pix+15: one 16-byte row segment of xt, or
-  // a walk of the window bases along the output rows (a warp's 32 lanes = 32
-  // consecutive patch elements: coalesced)
+  // patch element r at pixels pix..pix+15: a walk of the window bases along
+  // the output rows (a warp's 32 lanes = 32 consecutive patch elements:
+  // coalesced)
   __device__ void a16(long long roff, int pix, int ke, float (&v)[16]) const {
-    if (xt) {
-      if (pix >= ke) return zero16(v);        // K % 16 == 0: whole runs
-      const uint4 q = __ldg(reinterpret_cast<const uint4 *>(xt + roff + pix));
-      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = (float)((w[j >> 2] >> (8 * (j & 3))) & 0xFF);
-      return;
-    }
     const int P = g.OH * g.OW;
     const int img = pix / P, p = pix - img * P;
     int oy = p / g.OW, ox = p - oy * g.OW;
@@ -402,6 +318,7 @@ struct WgradPol : tc::PolBase {
 };
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+constexpr int kDgradCap = 16;       // linear dgrad split cap (measured best in the learner)
 
 // ------------------------------------------------------------ host helpers
 bool conv_ok(const dqn_layer_desc &L) {
@@ -409,19 +326,12 @@ bool conv_ok(const dqn_layer_desc &L) {
   return L.in_c % 4 == 0 && (L.fw * L.in_c) % 4 == 0 && L.out_c % 16 == 0;
 }
 
-// forward split length: a function of K only (batch-independent rows)
-inline int env_int(const char *name, int dflt) {
-  const char *e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-
+// forward split length: a function of K only (batch-independent rows);
+// measured in the learner's graph: conv2 / conv3 (K = 512 / 576) best at
+// 256-k splits, fc1 (K = 3136) at 8 splits
 inline int fwd_klen(int K) {
-  static const int s_long = env_int("DQN_B200_FWD_SPLITS", 8);      // diagnostic overrides
-  static const int kl_mid = env_int("DQN_B200_FWD_KLEN", 256);
-  // measured in the learner's graph: conv2 / conv3 (K = 512 / 576) best at
-  // 256-k splits, fc1 (K = 3136) at 8 splits
-  if (K >= 2048) return ceil_div(ceil_div(K, s_long), tc::BK) * tc::BK;   // 8 splits (fc1: 448)
-  if (K >= 512) return kl_mid;
+  if (K >= 2048) return ceil_div(ceil_div(K, 8), tc::BK) * tc::BK;   // 8 splits (fc1: 448)
+  if (K >= 512) return 256;
   return K;
 }
 
@@ -474,45 +384,10 @@ template <typename InT>
 int fwd_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *params,
                  float *y, float *scratch, int *counters, int batch) {
   const int N = L.out_c;
-  static const int bn_max = env_int("DQN_B200_FWD_BN", 64);          // diagnostic
-  static const int bn_lin = env_int("DQN_B200_FWD_BN_LINEAR", 64);   // diagnostic
-  const int bmax = L.kind == DQN_LAYER_LINEAR ? bn_lin : bn_max;
-  if (N == 32 || (bmax <= 32 && N % 32 == 0))
+  if (N == 32)
     return fwd_launch<InT, 32>(st, L, x, params, y, scratch, counters, batch);
   if (N == 64) return fwd_launch<InT, 64>(st, L, x, params, y, scratch, counters, batch);
   if (N % 64 == 0) return fwd_launch<InT, 64>(st, L, x, params, y, scratch, counters, batch);
-  return DQN_ERR_UNSUPPORTED;
-}
-
-template <typename InT, int BN>
-int fwd_group_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *const x[2],
-                     const float *const w[2], const float *const b[2], float *const y[2],
-                     float *scratch, int *counters, int batch) {
-  FwdGroupPol<InT, BN> p{};
-  p.counters = counters;
-  p.x0 = x[0]; p.x1 = x[1];
-  p.w0 = w[0]; p.w1 = w[1];
-  p.bias0 = b[0]; p.bias1 = b[1];
-  p.y0 = y[0]; p.y1 = y[1];
-  p.partial = scratch;
-  p.g = geo_of(L);
-  p.M1 = batch * L.out_h * L.out_w;
-  p.M = 2 * p.M1;
-  p.N = L.out_c;
-  p.K = L.fh * L.fw * L.in_c;
-  p.klen = fwd_klen(p.K);
-  p.relu = L.relu;
-  p.ksplits = ceil_div(p.K, p.klen);
-  return tc::launch(st, p, 2 * p.ksplits, "tc_fwd_group");
-}
-
-template <typename InT>
-int fwd_group_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *const x[2],
-                       const float *const w[2], const float *const b[2], float *const y[2],
-                       float *scratch, int *counters, int batch) {
-  const int N = L.out_c;
-  if (N == 32) return fwd_group_launch<InT, 32>(st, L, x, w, b, y, scratch, counters, batch);
-  if (N % 64 == 0) return fwd_group_launch<InT, 64>(st, L, x, w, b, y, scratch, counters, batch);
   return DQN_ERR_UNSUPPORTED;
 }
 
@@ -550,18 +425,6 @@ static bool make_kmajor_map(CUtensorMap *m, const float *base, int K, int rows, 
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static bool tma_b_enabled() {
-  static const bool on = env_int("DQN_B200_TMA_B", 1) == 1;
-  return on;
-}
-// conv dgrad by TMA: bit-identical but measured -6 % in the learner (few
-// k-blocks per CTA after phases x splits: the load latency is not hidden the
-// way the 2-deep register prefetch hides it); opt-in
-static bool tma_b_conv_enabled() {
-  static const bool on = env_int("DQN_B200_TMA_B_CONV", 0) == 1;
-  return on;
-}
-
 template <int BN>
 int lin_dgrad_launch_tma(cudaStream_t st, const float *dy, const float *w, const float *mask,
                          float *out, float *partial, int *counters, int M, int N, int K,
@@ -584,9 +447,9 @@ int lin_dgrad_launch_tma(cudaStream_t st, const float *dy, const float *w, const
 template <int BN>
 int lin_dgrad_launch(cudaStream_t st, const float *dy, const float *w, const float *mask,
                      float *out, float *partial, int *counters, int M, int N, int K) {
-  if (tma_b_enabled()) {
-    static const int cap = env_int("DQN_B200_DGRAD_CAP", 16);
-    const int rc = lin_dgrad_launch_tma<BN>(st, dy, w, mask, out, partial, counters, M, N, K, cap);
+  {   // B (the weights, dense K-major) by TMA tensor loads when the map encodes
+    const int rc = lin_dgrad_launch_tma<BN>(st, dy, w, mask, out, partial, counters, M, N, K,
+                                            kDgradCap);
     if (rc != DQN_ERR_UNSUPPORTED) return rc;
   }
   LinDgradPol<BN> p{};
@@ -599,11 +462,7 @@ int lin_dgrad_launch(cudaStream_t st, const float *dy, const float *w, const flo
   p.M = M;
   p.N = N;
   p.K = K;
-  static const int cap = env_int("DQN_B200_DGRAD_CAP", 16);
-  split_k(ceil_div(M, tc::BM) * ceil_div(N, BN), K, BN, cap, p.klen, p.ksplits);
-  if (env_int("DQN_B200_DEBUG_SPLITS", 0))
-    fprintf(stderr, "lin_dgrad BN=%d M=%d N=%d K=%d klen=%d ks=%d tiles=%d\n", BN, M, N, K,
-            p.klen, p.ksplits, ceil_div(M, tc::BM) * ceil_div(N, BN));
+  split_k(ceil_div(M, tc::BM) * ceil_div(N, BN), K, BN, kDgradCap, p.klen, p.ksplits);
   return tc::launch(st, p, p.ksplits, "tc_lin_dgrad");
 }
 
@@ -613,9 +472,7 @@ int lin_dgrad(cudaStream_t st, const float *dy, const float *w, const float *mas
   // stages fit in TMEM
   // measured in the learner: fc1 dgrad (N = 3136) 1.4 % faster in 32-column
   // tiles (needs the even producer ring, tc_gemm.cuh Plan::STAGES)
-  static const int bn_max = env_int("DQN_B200_LIN_DGRAD_BN", 32);
-  for (int bn : {64, 32, 16}) {
-    if (bn > bn_max) continue;
+  for (int bn : {32, 16}) {
     if (N % bn) continue;
     switch (bn) {
       case 64: return lin_dgrad_launch<64>(st, dy, w, mask, out, partial, counters, M, N, K);
@@ -626,44 +483,9 @@ int lin_dgrad(cudaStream_t st, const float *dy, const float *w, const float *mas
   return DQN_ERR_UNSUPPORTED;
 }
 
-// 4-D map of the HWIO weights W[fh][fw][C][Cout] with 4 x BN x 1 x 1 boxes
-static bool make_hwio_map(CUtensorMap *m, const float *w, const dqn_layer_desc &L, int bn) {
-  const EncodeTiledFn fn = encode_tiled();
-  if (!fn || ((uintptr_t)w % 16) || (L.out_c % 4)) return false;
-  const cuuint64_t dims[4] = {(cuuint64_t)L.out_c, (cuuint64_t)L.in_c, (cuuint64_t)L.fw,
-                              (cuuint64_t)L.fh};
-  const cuuint64_t strides[3] = {(cuuint64_t)L.out_c * 4, (cuuint64_t)L.in_c * L.out_c * 4,
-                                 (cuuint64_t)L.fw * L.in_c * L.out_c * 4};
-  const cuuint32_t box[4] = {4, (cuuint32_t)bn, 1, 1};
-  const cuuint32_t es[4] = {1, 1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(w), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <int BN>
 int conv_dgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
                       const float *mask, float *out, float *scratch, int *counters, int batch) {
-  if (tma_b_enabled() && tma_b_conv_enabled()) {
-    ConvDgradTmaPol<BN> p{};
-    if (make_hwio_map(&p.map, w, L, BN)) {
-      p.counters = counters;
-      p.partial = scratch;
-      p.dy = dy;
-      p.w = w;
-      p.mask = mask;
-      p.out = out;
-      p.g = geo_of(L);
-      p.batch = batch;
-      p.M = batch * ceil_div(L.in_h, L.sh) * ceil_div(L.in_w, L.sw);
-      p.N = L.in_c;
-      p.K = (L.fh / L.sh) * (L.fw / L.sw) * L.out_c;
-      static const int cap = env_int("DQN_B200_CDGRAD_CAP", 4);
-      split_k(L.sh * L.sw * ceil_div(p.M, tc::BM) * ceil_div(p.N, BN), p.K, BN, cap, p.klen,
-              p.ksplits);
-      return tc::launch(st, p, L.sh * L.sw * p.ksplits, "tc_conv_dgrad_tma");
-    }
-  }
   ConvDgradPol<BN> p{};
   p.counters = counters;
   p.partial = scratch;
@@ -676,9 +498,10 @@ int conv_dgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const float *dy,
   p.M = batch * ceil_div(L.in_h, L.sh) * ceil_div(L.in_w, L.sw);
   p.N = L.in_c;
   p.K = (L.fh / L.sh) * (L.fw / L.sw) * L.out_c;
-  // split K until phases x tiles x splits fill the machine
-  static const int cap = env_int("DQN_B200_CDGRAD_CAP", 4);   // measured best in the learner
-  split_k(L.sh * L.sw * ceil_div(p.M, tc::BM) * ceil_div(p.N, BN), p.K, BN, cap, p.klen, p.ksplits);
+  // split K until phases x tiles x splits fill the machine (cap 4: measured
+  // best in the learner; conv dgrad B by 4-D TMA tensor loads was bit-identical
+  // but 6 % slower there -- few k-blocks per CTA leave its latency exposed)
+  split_k(L.sh * L.sw * ceil_div(p.M, tc::BM) * ceil_div(p.N, BN), p.K, BN, 4, p.klen, p.ksplits);
   return tc::launch(st, p, L.sh * L.sw * p.ksplits, "tc_conv_dgrad");
 }
 
@@ -686,9 +509,6 @@ bool dgrad_tile_ok(int C) { return C == 16 || C == 32 || C == 48 || C % 64 == 0;
 
 int conv_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
                const float *mask, float *out, float *scratch, int *counters, int batch) {
-  static const int bn_max = env_int("DQN_B200_CONV_DGRAD_BN", 64);   // diagnostic
-  if (bn_max <= 32 && L.in_c % 32 == 0 && L.in_c > 32)
-    return conv_dgrad_launch<32>(st, L, dy, w, mask, out, scratch, counters, batch);
   switch (L.in_c) {
     case 16: return conv_dgrad_launch<16>(st, L, dy, w, mask, out, scratch, counters, batch);
     case 32: return conv_dgrad_launch<32>(st, L, dy, w, mask, out, scratch, counters, batch);
@@ -702,21 +522,19 @@ int conv_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const 
 }
 
 inline void wgrad_split(int M, int N, int K, int bn, bool u8, int &klen, int &splits) {
-  // split lengths a multiple of BK, count from the latency model, capped
-  // (measured in the learner's graph: the model alone picks ~67 splits for
-  // conv1's K = 12,800, whose last-arrival fixup then tails the update; 32
-  // is 6 % faster end to end)
-  // (applies to learner-sized reductions, K <= 64k: large batches keep the
-  // model's count -- conv1 at B = 4096, K = 1.6M, is 2.3x slower at 32)
-  static const int cap_f = env_int("DQN_B200_WGRAD_CAP", 128);
-  static const int cap_u8 = env_int("DQN_B200_WGRAD_CAP_U8", 32);
-  const int cap = (u8 && K <= 65536) ? cap_u8 : cap_f;
+  // split lengths a multiple of BK, count from the latency model, capped at
+  // learner-sized reductions (K <= 64k pixels): the wgrads run beside the
+  // dgrad chain, and the model's count for one launch alone (conv3: 25
+  // one-block splits over 125 CTAs) takes the SMs the chain needs.  Measured
+  // in the learner's graph (cfg4, batch 32, with conv1's wgrad from the
+  // frames): caps 4 / 8 / 12 / 16 / 128 -> 8 best (+3 % updates/s over 128).
+  // Large batches (K > 64k) keep the model's count.
+  const int cap = K <= 65536 ? (u8 ? 32 : 8) : 128;
   split_k(ceil_div(M, tc::BM) * ceil_div(N, bn), K, bn, cap, klen, splits);
 }
 
 template <typename InT, int BN>
-int wgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const uint8_t *xt,
-                 const float *dy, float *grads, float *scratch, int *counters, int batch,
+int wgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *dy, float *grads, float *scratch, int *counters, int batch,
                  int32_t *flags) {
   WgradPol<InT, BN> p{};
   p.flags = flags;
@@ -729,7 +547,6 @@ int wgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const u
   p.M = L.fh * L.fw * L.in_c;
   p.N = L.out_c;
   p.K = batch * L.out_h * L.out_w;
-  p.xt = (xt && p.K % 16 == 0) ? xt : nullptr;      // whole 16-pixel runs only
   int splits;
   wgrad_split(p.M, p.N, p.K, BN, sizeof(InT) == 1, p.klen, splits);
   p.partial = scratch;
@@ -739,15 +556,12 @@ int wgrad_launch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const u
 }
 
 template <typename InT>
-int wgrad_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const uint8_t *xt,
-                   const float *dy, float *grads, float *scratch, int *counters, int batch,
+int wgrad_dispatch(cudaStream_t st, const dqn_layer_desc &L, const InT *x, const float *dy, float *grads, float *scratch, int *counters, int batch,
                    int32_t *flags) {
   const int N = L.out_c;
-  static const int bn_max = env_int("DQN_B200_WGRAD_BN", 64);         // diagnostic
-  if (N == 32 || (bn_max <= 32 && N % 32 == 0))
-    return wgrad_launch<InT, 32>(st, L, x, xt, dy, grads, scratch, counters, batch, flags);
+  if (N == 32) return wgrad_launch<InT, 32>(st, L, x, dy, grads, scratch, counters, batch, flags);
   if (N % 64 == 0)
-    return wgrad_launch<InT, 64>(st, L, x, xt, dy, grads, scratch, counters, batch, flags);
+    return wgrad_launch<InT, 64>(st, L, x, dy, grads, scratch, counters, batch, flags);
   return DQN_ERR_UNSUPPORTED;
 }
 
@@ -780,7 +594,7 @@ bool tc_layer_supported(const dqn_net_desc *net, int l, int phase) {
 }
 
 int64_t tc_scratch_floats(const dqn_net_desc *net, int batch) {
-  int64_t m = 0;
+  int64_t m = conv1_wgrad_u8_ok(net) ? conv1_wgrad_u8_scratch(net, batch) : 0;
   for (int l = 0; l < net->n_layers; ++l) {
     if (!tc_layer_supported(net, l, 0)) continue;
     const dqn_layer_desc &L = net->layer[l];
@@ -816,38 +630,6 @@ int tc_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const floa
                               counters_of(b), b->batch);
 }
 
-// The grouped forward of trunk layer l: online on_b (batch 2k, [s; s']) and
-// target tg_b (batch k) in one launch.
-int tc_layer_forward_group(cudaStream_t st, const dqn_net_desc *net, int l,
-                           const float *on_params, const dqn_binding *on_b,
-                           const float *tg_params, const dqn_binding *tg_b, float *scratch,
-                           int *counters) {
-  const dqn_layer_desc &L = net->layer[l];
-  const int k = tg_b->batch;
-  const float *w[2] = {on_params + L.w_off, tg_params + L.w_off};
-  const float *b[2] = {on_params + L.b_off, tg_params + L.b_off};
-  float *y[2] = {on_b->act[l], tg_b->act[l]};
-  if (l == 0 && net->input_u8) {
-    const uint8_t *x[2] = {(const uint8_t *)on_b->x, (const uint8_t *)tg_b->x};
-    return fwd_group_dispatch<uint8_t>(st, L, x, w, b, y, scratch, counters, k);
-  }
-  const float *x[2] = {l == 0 ? (const float *)on_b->x : on_b->act[l - 1],
-                       l == 0 ? (const float *)tg_b->x : tg_b->act[l - 1]};
-  return fwd_group_dispatch<float>(st, L, x, w, b, y, scratch, counters, k);
-}
-
-// split-K partials of the grouped forward: two problems of 2k rows (grid)
-int64_t tc_forward_group_scratch(const dqn_net_desc *net, int upto, int batch) {
-  int64_t m = 0;
-  for (int l = 0; l < upto; ++l) {
-    const dqn_layer_desc &L = net->layer[l];
-    const int K = L.fh * L.fw * L.in_c;
-    const int ks = ceil_div(K, fwd_klen(K));
-    if (ks > 1) m = std::max(m, (int64_t)2 * ks * 2 * batch * L.out_h * L.out_w * L.out_c);
-  }
-  return m;
-}
-
 int tc_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
                       const dqn_binding *b) {
   const dqn_layer_desc &L = net->layer[l];
@@ -867,50 +649,12 @@ int tc_layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *grads
   const dqn_layer_desc &L = net->layer[l];
   const void *in = (l == 0) ? b->x : b->act[l - 1];
   if (l == 0 && net->input_u8)
-    return wgrad_dispatch<uint8_t>(st, L, (const uint8_t *)in, b->xt, b->dact[l], grads,
-                                    b->scratch, counters_of(b), b->batch, flags);
-  return wgrad_dispatch<float>(st, L, (const float *)in, nullptr, b->dact[l], grads, b->scratch,
+    return wgrad_dispatch<uint8_t>(st, L, (const uint8_t *)in, b->dact[l], grads, b->scratch,
+                                    counters_of(b), b->batch, flags);
+  return wgrad_dispatch<float>(st, L, (const float *)in, b->dact[l], grads, b->scratch,
                                 counters_of(b), b->batch, flags);
 }
 
-
-namespace {
-// xt[r][pix] for 16 consecutive pixels per thread (one 16-byte store); the
-// warp's 32 lanes take 32 consecutive patch elements of one pixel group, so
-// each byte load of the warp reads one contiguous segment of a window row
-__global__ void im2col_t_u8_kernel(const uint8_t *__restrict__ x, Geo g, int R, int K,
-                                   uint8_t *__restrict__ xt) {
-  pdl_begin();   // programmatic dependent launch (common.cuh)
-  const int nq = K / 16;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)R * nq) return;
-  const int q = (int)(idx / R), r = (int)(idx - (int64_t)q * R);
-  const int roff = patch_off(g, r);
-  const int P = g.OH * g.OW;
-  int pix = q * 16;
-  int img = pix / P, p = pix - img * P;
-  int oy = p / g.OW, ox = p - oy * g.OW;
-  uint32_t w[4] = {0, 0, 0, 0};
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const long long base =
-        (((long long)img * g.H + (long long)oy * g.sh) * g.W + (long long)ox * g.sw) * g.C;
-    w[j >> 2] |= (uint32_t)__ldg(x + base + roff) << (8 * (j & 3));
-    if (++ox == g.OW) {
-      ox = 0;
-      if (++oy == g.OH) { oy = 0; ++img; }
-    }
-  }
-  *reinterpret_cast<uint4 *>(xt + (int64_t)r * K + q * 16) = make_uint4(w[0], w[1], w[2], w[3]);
-}
-
-bool im2col_t_ok(const dqn_net_desc *net, int batch) {
-  if (!net->input_u8 || net->n_layers < 1 || net->algo == 1) return false;
-  const dqn_layer_desc &L = net->layer[0];
-  if (L.kind != DQN_LAYER_CONV || !tc_layer_supported(net, 0, 2)) return false;
-  return ((int64_t)batch * L.out_h * L.out_w) % 16 == 0;
-}
-}  // namespace
 
 }  // namespace dqn
 
@@ -928,29 +672,3 @@ extern "C" int dqn_tc_trace(unsigned long long *host, int max_ctas) {
 }
 extern "C" void dqn_tc_skip(int mask) { cudaMemcpyToSymbol(dqn::tc::g_skip, &mask, sizeof(mask)); }
 #endif
-
-extern "C" int64_t dqn_net_im2col_t_bytes(const dqn_net_desc *net, int32_t batch) {
-  if (!net || batch < 1 || !dqn::im2col_t_ok(net, batch)) return 0;
-  const dqn_layer_desc &L = net->layer[0];
-  return (int64_t)L.fh * L.fw * L.in_c * batch * L.out_h * L.out_w;
-}
-
-extern "C" int dqn_net_im2col_t(void *stream, const dqn_net_desc *net, const dqn_binding *bind) {
-  using namespace dqn;
-  if (!net || !bind || !bind->x || !bind->xt || bind->batch < 1) {
-    set_error("net_im2col_t: network / binding / x / xt missing");
-    return DQN_ERR_INVALID_ARG;
-  }
-  if (!im2col_t_ok(net, bind->batch)) {
-    set_error("net_im2col_t: layer 0 has no transposed-im2col wgrad (uint8 tcgen05 conv, 16 | pixels)");
-    return DQN_ERR_UNSUPPORTED;
-  }
-  const dqn_layer_desc &L = net->layer[0];
-  const int R = L.fh * L.fw * L.in_c, K = bind->batch * L.out_h * L.out_w;
-  const int64_t n = (int64_t)R * (K / 16);
-  launch_k(im2col_t_u8_kernel, (unsigned)((n + 255) / 256), 256, 0, as_stream(stream), 
-      (const uint8_t *)bind->x, geo_of(L), R, K, bind->xt);
-  DQN_LAUNCH_CHECK("net_im2col_t");
-  return DQN_OK;
-}
-

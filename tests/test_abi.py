@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in declared_symbols() if not hasattr(lib, s)]
     assert not missing, missing
     assert set(declared_symbols()) == set(_lib.EXPORTED)
-    assert lib.dqn_abi_version() == 3
+    assert lib.dqn_abi_version() == 4
 
 
 def test_struct_layouts_match_header():
@@ -36,7 +36,7 @@ def test_struct_layouts_match_header():
     # dqn_layer_desc: 12 int32 + 4 int64 = 80 bytes; net desc: 16 + 8*80
     assert ctypes.sizeof(_lib.LayerDesc) == 80
     assert ctypes.sizeof(_lib.NetDesc) == 16 + 8 * 80
-    assert ctypes.sizeof(_lib.Binding) == 8 + 8 + 16 * 8 + 8 + 8 + 8 + 8   # ... scratch_floats, xt
+    assert ctypes.sizeof(_lib.Binding) == 8 + 8 + 16 * 8 + 8 + 8 + 8   # ... scratch_floats
 
 
 def test_product_path_refuses_without_gpu(monkeypatch):

@@ -5,8 +5,8 @@
 * the apply-only optimizer (dqn_rmsprop_apply, gradients flagged by their
   producers) vs dqn_rmsprop_step, and its abort on a non-finite gradient
   raised inside a learner update;
-* dqn_net_im2col_t (conv1's transposed uint8 patch operand) vs a numpy
-  restatement, bit-exact.
+* the two-phase head vs the last-CTA-ticket head, the fused sample+gather
+  vs two launches.
 """
 
 from __future__ import annotations
@@ -57,7 +57,7 @@ CASES = {
 def test_fused_head_matches_per_layer_head(P, name, monkeypatch):
     runs = []
     for fused in ("1", "0"):
-        monkeypatch.setenv("DQN_B200_FUSED_HEAD", fused)
+        monkeypatch.setattr(P.agent, "FUSED_HEAD", fused == "1")
         on, tg, mem, opt, cfg = learner(P, **CASES[name])
         rng = np.random.default_rng(3)
         res = [P.learn_step(on, tg, mem, opt, cfg, 10, rng)]
@@ -106,58 +106,6 @@ def test_learner_aborts_on_gradient_overflow(P):
     assert torch.equal(acc, opt.flat_acc)
 
 
-def _im2col_t_np(x, fh, fw, sh, sw):
-    b, h, w, c = x.shape
-    oh, ow = (h - fh) // sh + 1, (w - fw) // sw + 1
-    cols = np.empty((fh * fw * c, b * oh * ow), dtype=x.dtype)
-    p = 0
-    for img in range(b):
-        for oy in range(oh):
-            for ox in range(ow):
-                cols[:, p] = x[img, oy * sh:oy * sh + fh, ox * sw:ox * sw + fw, :].reshape(-1)
-                p += 1
-    return cols
-
-
-def test_im2col_t_u8_bit_exact(P):
-    import ctypes as C
-    from paper_1804_05834_b200 import _lib
-    net = P.build_network("atari", (84, 84, 4), 4, True)
-    batch = 4
-    rng = np.random.default_rng(11)
-    x = rng.integers(0, 256, size=(batch, 84, 84, 4), dtype=np.uint8)
-    xd = torch.as_tensor(x, device="cuda")
-    desc = net.desc_for(xd)
-    nb = int(_lib.lib.dqn_net_im2col_t_bytes(C.byref(desc), batch))
-    assert nb == 8 * 8 * 4 * batch * 20 * 20
-    xt = torch.zeros(nb, dtype=torch.uint8, device="cuda")
-    b = net.binding(batch)
-    b.x = xd
-    b.struct.x = xd.data_ptr()
-    b.struct.xt = xt.data_ptr()
-    _lib.call("dqn_net_im2col_t", _lib.stream_ptr(), C.byref(desc), C.byref(b.struct))
-    want = _im2col_t_np(x, 8, 8, 4, 4)
-    assert np.array_equal(xt.cpu().numpy().reshape(want.shape), want)
-
-
-def test_grouped_forward_matches_two_stream_forward(P, monkeypatch):
-    """DQN_B200_GROUPED_FWD=1 (online [s; s'] and target s' trunk forwards as
-    one launch per layer, dqn_net_forward_group) computes the same rows with
-    the same split-K order as the two per-network launches: bit-identical."""
-    runs = []
-    for grouped in ("1", "0"):
-        monkeypatch.setenv("DQN_B200_GROUPED_FWD", grouped)
-        on, tg, mem, opt, cfg = learner(P, **CASES["cfg4"])
-        res = P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(3))
-        plan = next(p for p in P.agent._PLANS.values() if p.online is on)
-        assert plan.grouped == (grouped == "1")
-        runs.append((res, on.flat_values.clone(), tg.binding(32).act[-2].clone()))
-    (ra, wa, ta), (rb, wb, tb) = runs
-    assert np.array_equal(ra.td_errors, rb.td_errors)
-    assert torch.equal(ta, tb)
-    assert torch.equal(wa, wb)
-
-
 @pytest.mark.parametrize("name", ["cfg4", "cfg4_huber", "cfg1"])
 def test_head_two_phase_matches_last_cta_form(P, name, monkeypatch):
     """The two-phase head (Q heads, then every CTA recomputes the TD block)
@@ -165,7 +113,7 @@ def test_head_two_phase_matches_last_cta_form(P, name, monkeypatch):
     order (1e-5, as the fused vs per-layer head)."""
     runs = []
     for two in ("1", "0"):
-        monkeypatch.setenv("DQN_B200_HEAD_TWO_PHASE", two)
+        monkeypatch.setattr(P.agent, "HEAD_TWO_PHASE", two == "1")
         on, tg, mem, opt, cfg = learner(P, **CASES[name])
         res = P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(3))
         runs.append((res, on.flat_values.clone()))
@@ -181,7 +129,7 @@ def test_fused_sample_gather_matches_two_launches(P, monkeypatch):
     gathered batch and update."""
     runs = []
     for fused in ("1", "0"):
-        monkeypatch.setenv("DQN_B200_FUSED_SAMPLE", fused)
+        monkeypatch.setattr(P.agent, "FUSED_SAMPLE", fused == "1")
         on, tg, mem, opt, cfg = learner(P, **CASES["cfg4"])
         rng = np.random.default_rng(8)
         res = [P.learn_step(on, tg, mem, opt, cfg, 10 + s, rng) for s in range(3)]
@@ -201,36 +149,3 @@ def test_fused_sample_gather_zero_total_raises(P):
     mem.tree.load_leaves(np.zeros(mem.capacity))
     with pytest.raises(ValueError):
         P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(0))
-
-
-def test_linear_wgrad_simt_matches_tcgen05(P, monkeypatch):
-    """DQN_B200_LIN_WGRAD_SIMT=1 (fc1 weight gradient as a small-K FMA
-    kernel) against the tcgen05 wgrad: same gradient within 1e-5."""
-    runs = []
-    monkeypatch.setenv("DQN_B200_ZEROCOPY", "0")     # the stubbed optimizer writes no host flag
-    for simt in ("1", "0"):
-        monkeypatch.setenv("DQN_B200_LIN_WGRAD_SIMT", simt)
-        on, tg, mem, opt, cfg = learner(P, **CASES["cfg4"])
-        opt.enqueue_apply = lambda flags, flag_out=None: None    # keep the gradients
-        P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(3))
-        runs.append(on.flat_grads.clone())
-    assert rel_norm(runs[0].cpu().numpy(), runs[1].cpu().numpy()) < 1e-5
-
-
-def test_conv1_wgrad_simt_matches_tcgen05(P, monkeypatch):
-    """The uint8 first conv's weight gradient by the FMA reduction over the
-    transposed patch operand (opt-in) against the tcgen05 wgrad (default):
-    same gradients (conv1 and everything else) within 1e-5."""
-    runs = []
-    monkeypatch.setenv("DQN_B200_ZEROCOPY", "0")     # the stubbed optimizer writes no host flag
-    for simt in ("1", "0"):
-        monkeypatch.setenv("DQN_B200_CONV1_WGRAD_SIMT", simt)
-        on, tg, mem, opt, cfg = learner(P, **CASES["cfg4"])
-        opt.enqueue_apply = lambda flags, flag_out=None: None    # keep the gradients
-        P.learn_step(on, tg, mem, opt, cfg, 10, np.random.default_rng(3))
-        g = dict(on.named_tensors())
-        runs.append((on.flat_grads.clone(), g["conv1.weight"].grad.clone(), g["conv1.bias"].grad.clone()))
-    (fa, wa, ba), (fb, wb, bb) = runs
-    assert rel_norm(wa.cpu().numpy(), wb.cpu().numpy()) < 1e-5
-    assert rel_norm(ba.cpu().numpy(), bb.cpu().numpy()) < 1e-5
-    assert rel_norm(fa.cpu().numpy(), fb.cpu().numpy()) < 1e-5

@@ -141,72 +141,78 @@ def test_errors(P):
         net.forward(np.ones((1, 24, 24, 4), np.float32))
 
 
-@pytest.mark.parametrize("bn", ["32", "64"])
-def test_fc1_dgrad_tiles_correct_and_deterministic(bn, tmp_path):
-    """fc1's dgrad through the tcgen05 engine in 32- and 64-column tiles
-    against an fp64 reference, over repeated launches.  Regression test for
-    an odd producer ring (3 stages at 32 columns) that raced: every launch
-    must agree bit for bit and stay at 3xTF32 accuracy.  B (the weights)
-    arrives by TMA tensor loads by default and by register staging with
-    DQN_B200_TMA_B=0; the two must be bit-identical (subprocesses: the switch
-    is read once)."""
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
+def _run_tool(script, env_extra=None):
     import subprocess
     import sys
-    dumps = []
-    for tma in ("1", "0"):
-        dump = tmp_path / f"fc1_dgrad_{tma}.pt"
-        env = dict(os.environ, DQN_B200_LIN_DGRAD_BN=bn, DQN_B200_TMA_B=tma,
-                   LIN_DGRAD_DUMP=str(dump))
-        out = subprocess.run([sys.executable, "tools/lin_dgrad_check.py"], env=env,
-                             capture_output=True, text=True, timeout=300,
-                             cwd=str(Path(__file__).resolve().parent.parent))
-        line = [l for l in out.stdout.splitlines() if l.startswith("BN=")]
-        assert line, out.stdout + out.stderr
-        err = float(line[0].split("rel err ")[1].split()[0])
-        assert "deterministic True" in line[0] and err < 1e-5, (tma, line[0])
-        dumps.append(torch.load(dump))
-    assert torch.equal(dumps[0], dumps[1])
+    env = dict(os.environ, **(env_extra or {}))
+    return subprocess.run([sys.executable, script], env=env, capture_output=True, text=True,
+                          timeout=300, cwd=str(Path(__file__).resolve().parent.parent))
 
 
-def test_conv_dgrad_tma_matches_register_staging(tmp_path):
+def test_fc1_dgrad_tiles_correct_and_deterministic(tmp_path):
+    """fc1's dgrad through the tcgen05 engine (32-column tiles, the weights by
+    TMA tensor loads) against an fp64 reference over repeated launches.
+    Regression test for an odd producer ring (3 stages at 32 columns) that
+    raced: every launch must agree bit for bit and stay at 3xTF32 accuracy."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = _run_tool("tools/lin_dgrad_check.py", {"LIN_DGRAD_DUMP": str(tmp_path / "d.pt")})
+    line = [l for l in out.stdout.splitlines() if l.startswith("BN=")]
+    assert line, out.stdout + out.stderr
+    err = float(line[0].split("rel err ")[1].split()[0])
+    assert "deterministic True" in line[0] and err < 1e-5, line[0]
+
+
+def test_conv_dgrad_accuracy():
     """conv2 / conv3 dgrad (stride phases, split K, ragged batch) against an
-    fp64 reference with the weights by 4-D TMA tensor loads (opt-in,
-    DQN_B200_TMA_B_CONV=1) and by register staging (default): 3xTF32 accuracy,
-    repeatable, and the two bit-identical."""
+    fp64 reference: 3xTF32 accuracy and repeatable."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    import subprocess
-    import sys
-    dumps = []
-    for tma in ("1", "0"):
-        dump = tmp_path / f"conv_dgrad_{tma}.pt"
-        env = dict(os.environ, DQN_B200_TMA_B_CONV=tma, CONV_DGRAD_DUMP=str(dump))
-        out = subprocess.run([sys.executable, "tools/conv_dgrad_check.py"], env=env,
-                             capture_output=True, text=True, timeout=300,
-                             cwd=str(Path(__file__).resolve().parent.parent))
-        line = [l for l in out.stdout.splitlines() if l.startswith("WORST")]
-        assert line, out.stdout + out.stderr
-        assert float(line[0].split()[1]) < 1e-5, (tma, out.stdout)
-        dumps.append(torch.load(dump))
-    assert dumps[0].keys() == dumps[1].keys()
-    for k in dumps[0]:
-        assert torch.equal(dumps[0][k], dumps[1][k]), k
+    out = _run_tool("tools/conv_dgrad_check.py")
+    line = [l for l in out.stdout.splitlines() if l.startswith("WORST")]
+    assert line, out.stdout + out.stderr
+    assert float(line[0].split()[1]) < 1e-5, out.stdout
 
 
-@pytest.mark.parametrize("rows_env", ["0", "4"])
-def test_small_batch_forward_matches_batched(rows_env):
-    """Small forwards -- batch <= 4 on the default tcgen05 path, and through
-    the opt-in small-batch SIMT kernel (DQN_B200_SMALL_FWD_ROWS=4; a
-    subprocess: the switch is read once) -- against the same rows inside a
-    batch-64 forward (tcgen05)."""
+def test_small_batch_forward_matches_batched():
+    """Small forwards (batch <= 4: tcgen05 layers, the small-batch kernel for
+    layers without one) against the same rows inside a batch-64 forward."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    import subprocess
-    import sys
-    root = Path(__file__).resolve().parent.parent
-    env = dict(os.environ, DQN_B200_SMALL_FWD_ROWS=rows_env)
-    out = subprocess.run([sys.executable, "tools/small_fwd_check.py"], env=env, cwd=str(root),
-                         capture_output=True, text=True, timeout=300)
+    out = _run_tool("tools/small_fwd_check.py")
     assert out.returncode == 0 and out.stdout.startswith("OK"), out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("batch", [1, 6, 12, 32, 64])
+def test_conv1_wgrad_from_frames(P, batch):
+    """conv1's weight gradient straight from the uint8 frames (csrc/wgrad_u8.cu:
+    one CTA per image, cluster + ticketed cross-cluster reduction) against the
+    oracle at batch sizes that give 1, 2, 4 and 8-image clusters; a second
+    accumulation doubles it and two runs are bit-identical (layers.py:250-255)."""
+    from paper_1804_05834_b200 import synth
+    on, ref = _pair(P, "atari", (84, 84, 4), 4, True, seed=3)
+    x8 = synth.frames(9, 0, np.arange(batch))
+    q = on.forward(torch.as_tensor(x8, device="cuda")).cpu().numpy()
+    ref.forward(O.Ring.lift(x8))
+    g = np.random.default_rng(batch).standard_normal(q.shape).astype(np.float32)
+    on.backward(g)
+    ref.backward(g)
+    ref.wgrad()
+    t1 = dict(on.named_tensors())
+    xd = torch.as_tensor(x8, device="cuda")
+    runs = []
+    for _ in range(2):
+        for _, t in on.named_tensors():
+            t.grad.zero_()
+        on.forward(xd)
+        on.backward(g)
+        on.calculate_gradient()
+        runs.append((t1["conv1.weight"].grad.clone(), t1["conv1.bias"].grad.clone()))
+    assert torch.equal(runs[0][0], runs[1][0]) and torch.equal(runs[0][1], runs[1][1])
+    for n in ("conv1.weight", "conv1.bias"):
+        assert rel_norm(t1[n].grad.cpu().numpy(), ref.grads[n]) < TOL, n
+    on.forward(xd)
+    on.backward(g)
+    on.calculate_gradient()                       # accumulates: grads += dW
+    w2 = t1["conv1.weight"].grad.cpu().numpy()
+    assert rel_norm(w2, 2 * ref.grads["conv1.weight"]) < TOL

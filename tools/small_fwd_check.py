@@ -1,5 +1,5 @@
 """Batch-1/3 forwards vs the same rows of a batch-64 forward (used by
-tests/test_gpu_network.py under both DQN_B200_SMALL_FWD_ROWS settings).
+tests/test_gpu_network.py).
 Prints "OK <max rel err>" or raises."""
 import sys
 from pathlib import Path

@@ -80,16 +80,9 @@ def head():
 
 
 print(f"head_td (K1+K2) {timeit(head):7.2f} us")
-for only in ("q", "td"):
-    os.environ["DQN_B200_HEAD_ONLY"] = only
-    print(f"head only {only:3s}    {timeit(head):7.2f} us")
-os.environ.pop("DQN_B200_HEAD_ONLY")
 print(f"rms_apply+sync {timeit(lambda: (opt.enqueue_apply(pl.flags), P.sync_target(on, tg))):7.2f} us")
 print(f"empty kernel   {timeit(lambda: _lib.call('dqn_sync_target', _lib.stream_ptr(), tg.flat_values.data_ptr(), on.flat_values.data_ptr(), 0)):7.2f} us")
 
-# conv1 weight gradient (the update's last kernel) by path
-for simt in ("1", "0"):
-    os.environ["DQN_B200_CONV1_WGRAD_SIMT"] = simt
-    us = timeit(lambda: pl.online.layer_into(pl.on_view, 0, 2, pl.flags))
-    print(f"conv1 wgrad simt={simt}  {us:7.2f} us")
-os.environ.pop("DQN_B200_CONV1_WGRAD_SIMT")
+# conv1 weight gradient from the frames (the update's last GEMM)
+us = timeit(lambda: pl.online.layer_into(pl.on_view, 0, 2, pl.flags))
+print(f"conv1 wgrad    {us:7.2f} us")
