@@ -178,8 +178,13 @@ def main():
                 note="3xTF32 on tcgen05 (implementation FLOPs are 2-3x the algorithmic)")
     net.flat_grads.zero_()
     path = sys.argv[1] if len(sys.argv) > 1 else str(ROOT / "gpurun_out" / "kernel_bench.json")
+    out["clocks"] = CLOCKS.summary() if CLOCKS is not None else None
     json.dump(out, open(path, "w"), indent=1)
 
 
+CLOCKS = None
+
 if __name__ == "__main__":
-    main()
+    import bench          # the bench's nvidia-smi sampler (clocks + throttle reasons)
+    with bench.ClockSampler(0) as CLOCKS:
+        main()

@@ -12,6 +12,7 @@ L = [f"# {title}", "",
      "CUDA-graph replays of each call, no host launch overhead).  Peaks from MEASURED_PEAKS.json:",
      f"HBM copy {d['hbm_peak_gbps']:.1f} GB/s, dense bf16 {d['bf16_peak_tflops']:.1f} TFLOP/s (the GEMMs",
      "compute 3xTF32: their implementation tensor work is 2-3x the algorithmic FLOPs below).", "",
+     f"Clocks during the run (nvidia-smi sampler of bench.py): {d.get('clocks')}", "",
      "| kernel | us | algorithmic | achieved | of peak | note |", "|---|---|---|---|---|---|"]
 for r in d["kernels"]:
     if "gbps" in r:
