@@ -63,7 +63,8 @@ struct W1Args {
   int *counters;               // [cl] slice tickets (zero between launches)
   int32_t *flags;
   int H, W, C, OH, OW, fw, sh, sw;
-  int P, PS, PP, PP8, R, img_bytes, img_smem, cl, nclusters;   // PS CTAs per image, PP pixels each
+  int P, PS, PP, PP8, R, img_bytes, img_smem, cl, nclusters;   // PS units per image, PP pixels each
+  int units;                   // batch * PS (image, pixel-range) units over the grid
 };
 
 __device__ __forceinline__ uint32_t w1_chunk(int RB, int row, int k) {
@@ -87,7 +88,6 @@ __global__ void __launch_bounds__(kW1Threads, 1) conv1_wgrad_u8_kernel(const __g
   __shared__ int gbase[128];                 // image byte offset of each 4-pixel group
 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int img = blockIdx.x / a.PS, pbase = (blockIdx.x % a.PS) * a.PP;
   W1_MARK(0)
   uint8_t *simg = smem;
   const uint32_t bbase = tc::smem_u32(smem + a.img_smem);
@@ -99,12 +99,6 @@ __global__ void __launch_bounds__(kW1Threads, 1) conv1_wgrad_u8_kernel(const __g
                  "r"(512)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  // pixels come in groups of 4 consecutive output columns (OW % 4 == 0):
-  // group g starts at output pixel pbase + 4 g, its pixels SWC bytes apart
-  for (int g = t; g < a.PP / 4; g += kW1Threads) {
-    const int p = pbase + 4 * g, oy = p / a.OW, ox = p - oy * a.OW;
-    gbase[g] = (oy * a.sh * a.W + ox * a.sw) * a.C;
   }
   if (t == 32) {
     tc::mbar_init(&empty[0], 1);
@@ -121,63 +115,6 @@ __global__ void __launch_bounds__(kW1Threads, 1) conv1_wgrad_u8_kernel(const __g
   const uint32_t tmem = tmem_slot;
   W1_MARK(1)
 
-  if (t == 0) {
-    tc::mbar_expect_tx(&imgbar, (uint32_t)a.img_bytes);
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(tc::smem_u32(simg)),
-        "l"(a.x + (int64_t)img * a.img_bytes), "r"((uint32_t)a.img_bytes),
-        "r"(tc::smem_u32(&imgbar))
-        : "memory");
-  }
-
-  // ---- B = [dY_hi ; dY_lo], K-major over the image's pixels (+ bias sums)
-  const int q = t % NQ;
-  float bs[4] = {0.f, 0.f, 0.f, 0.f};
-  {
-    const float *dyi = a.dy + ((int64_t)img * a.P + pbase) * N + 4 * q;
-    const int units = (a.PP8 / 4) * NQ;
-    for (int u = t; u < units; u += kW1Threads) {
-      const int pq = u / NQ, p0 = 4 * pq;
-      float4 v[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (p0 + j < a.PP) {
-          const float *src = dyi + (int64_t)(p0 + j) * N;
-          asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(v[j].x), "=f"(v[j].y), "=f"(v[j].z), "=f"(v[j].w)
-                       : "l"(src));
-        } else {
-          v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-      // channel 4q + i over pixels p0..p0+3; lanes rotate i so one store
-      // instruction of the warp covers all 8 rows of a core matrix
-      const int rot = pq & 3;
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const int i = (s + rot) & 3;
-        const float4 c = i == 0 ? make_float4(v[0].x, v[1].x, v[2].x, v[3].x)
-                         : i == 1 ? make_float4(v[0].y, v[1].y, v[2].y, v[3].y)
-                         : i == 2 ? make_float4(v[0].z, v[1].z, v[2].z, v[3].z)
-                                  : make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
-        const int row = 4 * q + i;
-        tc::st_shared_v4(bbase + w1_chunk(RB, row, p0), c);
-        tc::st_shared_v4(bbase + w1_chunk(RB, N + row, p0),
-                         make_float4(tc::tf32_lo(c.x), tc::tf32_lo(c.y), tc::tf32_lo(c.z),
-                                     tc::tf32_lo(c.w)));
-        bs[i] = __fadd_rn(bs[i], __fadd_rn(__fadd_rn(c.x, c.y), __fadd_rn(c.z, c.w)));
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) bias_red[t / NQ][4 * q + i] = bs[i];
-  tc::fence_proxy_async();                   // B (generic stores) -> tensor-core reads
-  W1_MARK(2)
-  tc::mbar_wait(&imgbar, 0);
-  W1_MARK(3)
-
-  // ---- A blocks in TMEM, MMAs
   // warp w: TMEM lane quarter w % 4; its 4 sub-groups (w / 4) cover the MT x 4
   // 16-pixel slices of a 64-pixel block
   const int quarter = warp & 3, sub = warp >> 2;
@@ -188,57 +125,130 @@ __global__ void __launch_bounds__(kW1Threads, 1) conv1_wgrad_u8_kernel(const __g
   const int fy = r / rowlen;
   const int roff = fy * a.W * a.C + (r - fy * rowlen);   // (fx, c) is r - fy * rowlen
   const int ngroups = a.PP / 4;
-  for (int kb = 0; kb < nkb; ++kb) {
-    const int s = kb & 1;
-    if (kb >= 2) tc::mbar_wait(&empty[s], ((kb - 2) >> 1) & 1);
-    tc::tc_fence_after();
+  const int q = t % NQ;
+  float bs[4] = {0.f, 0.f, 0.f, 0.f};
+  int g = 0;                                 // k-blocks issued by this CTA so far
+
+  // units (image, pixel half) blockIdx.x, + gridDim.x, ...: every unit's
+  // products accumulate into the same TMEM pairs (one partial per CTA)
+  int it = 0;
+  for (int unit = blockIdx.x; unit < a.units; unit += gridDim.x, ++it) {
+    const int img = unit / a.PS, pbase = (unit % a.PS) * a.PP;
+    if (it > 0) tc::mbar_wait(&done, (it - 1) & 1);     // the last unit's MMAs read B / A
+    // pixels come in groups of 4 consecutive output columns (OW % 4 == 0):
+    // group gg starts at output pixel pbase + 4 gg, its pixels SWC bytes apart
+    for (int gg = t; gg < ngroups; gg += kW1Threads) {
+      const int p = pbase + 4 * gg, oy = p / a.OW, ox = p - oy * a.OW;
+      gbase[gg] = (oy * a.sh * a.W + ox * a.sw) * a.C;
+    }
+    if (t == 0) {
+      tc::mbar_expect_tx(&imgbar, (uint32_t)a.img_bytes);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(tc::smem_u32(simg)),
+          "l"(a.x + (int64_t)img * a.img_bytes), "r"((uint32_t)a.img_bytes),
+          "r"(tc::smem_u32(&imgbar))
+          : "memory");
+    }
+
+    // ---- B = [dY_hi ; dY_lo], K-major over the unit's pixels (+ bias sums)
+    {
+      const float *dyi = a.dy + ((int64_t)img * a.P + pbase) * N + 4 * q;
+      const int nu = (a.PP8 / 4) * NQ;
+      for (int u = t; u < nu; u += kW1Threads) {
+        const int pq = u / NQ, p0 = 4 * pq;
+        float4 v[4];
 #pragma unroll
-    for (int j = 0; j < MT; ++j) {
-      const int slice = sub * MT + j, cs = slice & 3;
-      const int g0 = (kb * A_COLS + cs * 16) / 4;
-      float v[16];
+        for (int j = 0; j < 4; ++j) {
+          if (p0 + j < a.PP) {
+            const float *src = dyi + (int64_t)(p0 + j) * N;
+            asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(v[j].x), "=f"(v[j].y), "=f"(v[j].z), "=f"(v[j].w)
+                         : "l"(src));
+          } else {
+            v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+        // channel 4q + i over pixels p0..p0+3; lanes rotate i so one store
+        // instruction of the warp covers all 8 rows of a core matrix
+        const int rot = pq & 3;
 #pragma unroll
-      for (int gi = 0; gi < 4; ++gi) {
-        if (!W1_SKIP(2) && g0 + gi < ngroups) {          // warp-uniform
-          const uint8_t *src = simg + roff + gbase[g0 + gi];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)    // exact uint8 -> fp32: (2^23 | b) - 2^23
-            v[4 * gi + i] = __fsub_rn(__uint_as_float(0x4B000000u | src[i * SWC]), 8388608.f);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) v[4 * gi + i] = 0.f;
+        for (int s = 0; s < 4; ++s) {
+          const int i = (s + rot) & 3;
+          const float4 c = i == 0 ? make_float4(v[0].x, v[1].x, v[2].x, v[3].x)
+                           : i == 1 ? make_float4(v[0].y, v[1].y, v[2].y, v[3].y)
+                           : i == 2 ? make_float4(v[0].z, v[1].z, v[2].z, v[3].z)
+                                    : make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
+          const int row = 4 * q + i;
+          tc::st_shared_v4(bbase + w1_chunk(RB, row, p0), c);
+          tc::st_shared_v4(bbase + w1_chunk(RB, N + row, p0),
+                           make_float4(tc::tf32_lo(c.x), tc::tf32_lo(c.y), tc::tf32_lo(c.z),
+                                       tc::tf32_lo(c.w)));
+          bs[i] = __fadd_rn(bs[i], __fadd_rn(__fadd_rn(c.x, c.y), __fadd_rn(c.z, c.w)));
         }
       }
-      if (!W1_SKIP(4))
-        tc::tmem_st16(tmem + ((uint32_t)(quarter * 32) << 16) +
-                          (uint32_t)(ACC_COLS + (s * MT + mw) * A_COLS + cs * 16), v);
     }
-    tc::tmem_wait_st();
-    tc::tc_fence_before();
-    __syncthreads();
-    if (t == 0) {
+    tc::fence_proxy_async();                 // B (generic stores) -> tensor-core reads
+    __syncthreads();                         // gbase of this unit visible to every thread
+    W1_MARK(2)
+    tc::mbar_wait(&imgbar, it & 1);
+    W1_MARK(3)
+
+    // ---- A blocks in TMEM, MMAs
+    for (int kb = 0; kb < nkb; ++kb, ++g) {
+      const int s = g & 1;
+      if (g >= 2) tc::mbar_wait(&empty[s], ((g - 2) >> 1) & 1);
       tc::tc_fence_after();
-      const int nks = min(8, (a.PP8 - kb * A_COLS) / 8);
-#pragma unroll 1
-      for (int kq = 0; kq < (W1_SKIP(1) ? 0 : nks); ++kq) {
-        const uint64_t bd = tc::make_sdesc(bbase + (uint32_t)((kb * 8 + kq) * 2 * RB * 16),
-                                           RB * 16, 128);
 #pragma unroll
-        for (int m = 0; m < MT; ++m)
-          tc::mma_ts(tmem + (uint32_t)(((kb & 1) * MT + m) * RB),
-                     tmem + (uint32_t)(ACC_COLS + (s * MT + m) * A_COLS + 8 * kq), bd, IDESC,
-                     (kb >= 2 || kq > 0) ? 1u : 0u);
+      for (int j = 0; j < MT; ++j) {
+        const int slice = sub * MT + j, cs = slice & 3;
+        const int g0 = (kb * A_COLS + cs * 16) / 4;
+        float v[16];
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+          if (!W1_SKIP(2) && g0 + gi < ngroups) {          // warp-uniform
+            const uint8_t *src = simg + roff + gbase[g0 + gi];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)    // exact uint8 -> fp32: (2^23 | b) - 2^23
+              v[4 * gi + i] = __fsub_rn(__uint_as_float(0x4B000000u | src[i * SWC]), 8388608.f);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[4 * gi + i] = 0.f;
+          }
+        }
+        if (!W1_SKIP(4))
+          tc::tmem_st16(tmem + ((uint32_t)(quarter * 32) << 16) +
+                            (uint32_t)(ACC_COLS + (s * MT + mw) * A_COLS + cs * 16), v);
       }
-      tc::mma_commit(&empty[s]);
-      if (kb == nkb - 1) tc::mma_commit(&done);
+      tc::tmem_wait_st();
+      tc::tc_fence_before();
+      __syncthreads();
+      if (t == 0) {
+        tc::tc_fence_after();
+        const int nks = min(8, (a.PP8 - kb * A_COLS) / 8);
+#pragma unroll 1
+        for (int kq = 0; kq < (W1_SKIP(1) ? 0 : nks); ++kq) {
+          const uint64_t bd = tc::make_sdesc(bbase + (uint32_t)((kb * 8 + kq) * 2 * RB * 16),
+                                             RB * 16, 128);
+#pragma unroll
+          for (int m = 0; m < MT; ++m)
+            tc::mma_ts(tmem + (uint32_t)(((g & 1) * MT + m) * RB),
+                       tmem + (uint32_t)(ACC_COLS + (s * MT + m) * A_COLS + 8 * kq), bd, IDESC,
+                       (g >= 2 || kq > 0) ? 1u : 0u);
+        }
+        tc::mma_commit(&empty[s]);
+        if (kb == nkb - 1) tc::mma_commit(&done);
+      }
     }
   }
-  tc::mbar_wait(&done, 0);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) bias_red[t / NQ][4 * q + i] = bs[i];
+  tc::mbar_wait(&done, (it - 1) & 1);
   tc::tc_fence_after();
   W1_MARK(4)
 
   // ---- epilogue: this image's partial [R][N] into smem (B is dead)
-  const int npair = nkb < 2 ? 1 : 2;
+  const int npair = g < 2 ? 1 : 2;
   constexpr int SLICES = MT * (N / 16);            // (M-tile, 16-channel group)
   for (int sl = sub; sl < SLICES; sl += 4) {
     const int m = sl / (N / 16), c0 = (sl % (N / 16)) * 16;
@@ -367,7 +377,7 @@ int launch_w1(cudaStream_t st, const W1Args &a, int smem) {
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.cl * a.nclusters);   // = batch * PS
+  cfg.gridDim = dim3(a.cl * a.nclusters);
   cfg.blockDim = dim3(kW1Threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -445,7 +455,10 @@ int conv1_wgrad_u8_tc(cudaStream_t st, const dqn_net_desc *net, const uint8_t *x
   a.PP8 = (a.PP + 7) / 8 * 8;
   a.R = L.fh * L.fw * L.in_c;
   a.img_bytes = L.in_h * L.in_w * L.in_c;
-  const int ctas = batch * a.PS;
+  a.units = batch * a.PS;
+  // one CTA per unit up to 128 CTAs (learner batches); larger batches loop
+  // over units inside the CTA, so the cross-CTA reduction stays <= 128 partials
+  const int ctas = a.units <= 128 ? a.units : 128;
   a.cl = 1;
   for (int c : {8, 4, 2})                   // 8-CTA clusters measured best (vs 1, 2, 4)
     if (ctas % c == 0 && a.R % c == 0) { a.cl = c; break; }
