@@ -326,38 +326,66 @@ sample_gather_kernel(const double *__restrict__ nodes, int depth, const int64_t 
   }
 }
 
-// Large-k variant, pass 1: per-query descent, raw weights, per-CTA max.
-__global__ void tree_sample_raw_kernel(const double *__restrict__ nodes, int depth,
-                                       const int64_t *__restrict__ size_p,
-                                       const double *__restrict__ u, int k,
-                                       const double *__restrict__ beta_p, int64_t *__restrict__ idx,
-                                       double *__restrict__ prob, double *__restrict__ weight,
-                                       double *__restrict__ block_max, int32_t *flags) {
+// Large-k sampler (SURVEY §8(d) microbenchmark; the learner's k <= 1024 use
+// tree_sample_kernel / the fused sample+gather): a persistent grid whose CTAs
+// stage the top kTopLevels levels of the heap (nodes [0, 2^top): 64 KB) in
+// shared memory once, then descend their queries -- the first top - 1
+// levels from shared memory, the remaining levels from global memory four
+// per dependent round trip (tree_descend_from).  Same compare / subtract
+// sequence as the reference's loop (replay.py:172-181): identical indices.
+// Consecutive threads take consecutive strata, so a warp's queries share
+// their upper path and land on neighbouring leaves.
+// Pass 1 also reduces the raw IS weights to a per-CTA max; the last CTA to
+// finish (ticket) reduces those to the batch max for pass 2.
+constexpr int kTopLevels = 13;
+constexpr int kSampleThreads = 512;
+
+__global__ void __launch_bounds__(kSampleThreads)
+tree_sample_raw_kernel(const double *nodes, int depth, const int64_t *size_p, const double *u,
+                       int k, const double *beta_p, int64_t *__restrict__ idx,
+                       double *__restrict__ prob, double *__restrict__ weight,
+                       double *block_max, double *gmax, unsigned int *ticket, int32_t *flags) {
+  // no __restrict__ on the inputs: their loads must stay below the PDL wait
+  extern __shared__ double s_top[];
+  __shared__ double red[kSampleThreads / 32];
+  __shared__ bool s_last;
   pdl_begin();   // programmatic dependent launch (common.cuh)
-  __shared__ double red[32];
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const double total = nodes[1];
+  const int top = depth < kTopLevels ? depth : kTopLevels;
+  for (int i = threadIdx.x; i < (1 << top); i += blockDim.x) s_top[i] = nodes[i];
+  __syncthreads();
+  const double total = s_top[1];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double m = 0.0;
   if (!(total > 0.0)) {
-    if (j == 0) raise_flag(flags, DQN_FLAG_ZERO_TOTAL);
-    if (threadIdx.x == 0) block_max[blockIdx.x] = 1.0;
-    if (j < k) { idx[j] = 0; prob[j] = 0.0; weight[j] = 0.0; }
-    return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) raise_flag(flags, DQN_FLAG_ZERO_TOTAL);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < k; j += stride) {
+      idx[j] = 0; prob[j] = 0.0; weight[j] = 0.0;
+    }
+    m = 1.0;
+  } else {
+    const double beta = *beta_p;
+    const double size = (double)*size_p;
+    const double seg = __ddiv_rn(total, (double)k), hi = nextafter(total, 0.0);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < k; j += stride) {
+      double q = fmin(fmax(__dmul_rn(__dadd_rn((double)j, u[j]), seg), 1e-300), hi);
+      int64_t n = 1;
+      int l = 0;
+      for (; l < top - 1; ++l) {                    // children of level l sit below 2^top
+        const double ls = s_top[2 * n];
+        const bool right = q > ls;
+        if (right) q = __dsub_rn(q, ls);            // q -= left_sum * go_right
+        n = 2 * n + (right ? 1 : 0);
+      }
+      double leaf;
+      const int64_t i = tree_descend_from(nodes, depth, n, l, q, &leaf);
+      const double p = __ddiv_rn(leaf, total);
+      const double w = pow(__dmul_rn(size, p), -beta);
+      idx[j] = i;
+      prob[j] = p;
+      weight[j] = w;
+      m = fmax(m, w);
+    }
   }
-  const double beta = *beta_p;
-  const int64_t size = *size_p;
-  const double seg = __ddiv_rn(total, (double)k);
-  double w = 0.0;
-  if (j < k) {
-    const double q = __dmul_rn(__dadd_rn((double)j, u[j]), seg);
-    double leaf;
-    const int64_t i = tree_descend(nodes, depth, q, nextafter(total, 0.0), &leaf);
-    const double p = __ddiv_rn(leaf, total);
-    w = pow(__dmul_rn((double)size, p), -beta);
-    idx[j] = i;
-    prob[j] = p;
-    weight[j] = w;
-  }
-  double m = w;
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
@@ -365,19 +393,28 @@ __global__ void tree_sample_raw_kernel(const double *__restrict__ nodes, int dep
     double v = red[0];
     for (int i = 1; i < (int)(blockDim.x >> 5); ++i) v = fmax(v, red[i]);
     block_max[blockIdx.x] = v;
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v = fmax(v, __ldcg(block_max + b));
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mx = red[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) mx = fmax(mx, red[i]);
+    *gmax = mx;
+    *ticket = 0;                                    // graph-replay safe
   }
 }
 
-__global__ void tree_sample_norm_kernel(double *__restrict__ weight, int k,
-                                        const double *__restrict__ block_max, int nblocks) {
+__global__ void tree_sample_norm_kernel(double *__restrict__ weight, int k, const double *gmax) {
   pdl_begin();   // programmatic dependent launch (common.cuh)
-  __shared__ double mx;
-  if (threadIdx.x == 0) {
-    double v = block_max[0];
-    for (int i = 1; i < nblocks; ++i) v = fmax(v, block_max[i]);
-    mx = v;
-  }
-  __syncthreads();
+  const double mx = *gmax;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x)
     weight[j] = __ddiv_rn(weight[j], mx);
 }
@@ -859,24 +896,32 @@ extern "C" int dqn_tree_sample(void *stream, const double *nodes, int32_t depth,
     return DQN_OK;
   }
   // Large batches (sampler microbenchmarks; the learner uses k <= 1024): the
-  // normaliser needs a grid-wide max, so two passes with per-CTA maxima in a
-  // process-wide scratch grown outside any graph capture.
+  // normaliser needs a grid-wide max, so two passes; the per-CTA maxima, the
+  // batch max and the pass-1 ticket live in a process-wide scratch allocated
+  // (zeroed) outside any graph capture.
   static std::mutex mu;
   static double *scratch = nullptr;
-  static int scratch_n = 0;
-  const int threads = 256;
-  const int blocks = (k + threads - 1) / threads;
+  const int top = depth < kTopLevels ? depth : kTopLevels;
+  const int smem = (int)sizeof(double) << top;
+  const int blocks = 2 * kNumSMs;                   // persistent: 2 CTAs of 512 per SM
   std::lock_guard<std::mutex> lock(mu);
-  if (scratch_n < blocks) {
-    if (scratch) cudaFree(scratch);
-    int st_ = cuda_status(cudaMalloc(&scratch, sizeof(double) * blocks), "tree_sample scratch");
+  if (!scratch) {
+    int st_ = cuda_status(cudaMalloc(&scratch, sizeof(double) * (blocks + 2)), "tree_sample scratch");
     if (st_) return st_;
-    scratch_n = blocks;
+    st_ = cuda_status(cudaMemset(scratch, 0, sizeof(double) * (blocks + 2)), "tree_sample scratch");
+    if (st_) return st_;
+    st_ = cuda_status(cudaFuncSetAttribute(tree_sample_raw_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)sizeof(double) << kTopLevels),
+                      "tree_sample smem");
+    if (st_) return st_;
   }
-  launch_k(tree_sample_raw_kernel, blocks, threads, 0, st, nodes, depth, size, u, k, beta, idx, prob,
-                                                     weight, scratch, flags);
+  double *gmax = scratch + blocks;
+  unsigned int *ticket = reinterpret_cast<unsigned int *>(scratch + blocks + 1);
+  launch_k(tree_sample_raw_kernel, blocks, kSampleThreads, (size_t)smem, st, nodes, depth, size, u, k,
+           beta, idx, prob, weight, scratch, gmax, ticket, flags);
   DQN_LAUNCH_CHECK("tree_sample_raw");
-  launch_k(tree_sample_norm_kernel, grid_for(k, 256), 256, 0, st, weight, k, scratch, blocks);
+  launch_k(tree_sample_norm_kernel, grid_for(k, 256), 256, 0, st, weight, k, (const double *)gmax);
   DQN_LAUNCH_CHECK("tree_sample_norm");
   return DQN_OK;
 }

@@ -22,12 +22,12 @@ static __device__ __forceinline__ double sel8(const double (&v)[8], int i) {
 // loaded together and the four compare/subtract steps then run exactly as the
 // reference's per-level loop (same operations, same order).  The last group
 // also loads the right children, which yields the leaf value for free.
-static __device__ __forceinline__ int64_t tree_descend(const double *__restrict__ nodes, int depth,
-                                                double q, double hi,
-                                                double *leaf_value = nullptr) {
-  q = fmin(fmax(q, 1e-300), hi);            // np.clip(q, 1e-300, nextafter(total, 0))
-  int64_t n = 1;
-  int l = 0;
+// tree_descend_from: the same from node n at level l with remaining mass q
+// (already clipped) -- the tail of a descent whose top levels ran elsewhere
+// (the shared-memory staged sampler).
+static __device__ __forceinline__ int64_t tree_descend_from(const double *__restrict__ nodes,
+                                                            int depth, int64_t n, int l, double q,
+                                                            double *leaf_value = nullptr) {
   double leaf = -1.0;
   for (; l + 4 <= depth; l += 4) {
     const bool last = l + 4 == depth;
@@ -82,6 +82,13 @@ static __device__ __forceinline__ int64_t tree_descend(const double *__restrict_
   }
   if (leaf_value) *leaf_value = leaf >= 0.0 ? leaf : __ldg(nodes + n);
   return n - (int64_t(1) << depth);
+}
+
+static __device__ __forceinline__ int64_t tree_descend(const double *__restrict__ nodes, int depth,
+                                                double q, double hi,
+                                                double *leaf_value = nullptr) {
+  q = fmin(fmax(q, 1e-300), hi);            // np.clip(q, 1e-300, nextafter(total, 0))
+  return tree_descend_from(nodes, depth, 1, 0, q, leaf_value);
 }
 
 
