@@ -224,6 +224,19 @@ int dqn_frame_gather(void *stream, const uint8_t *frames, int64_t frame_bytes,
                      uint8_t *out_states, uint8_t *out_next_states, int64_t *out_actions,
                      double *out_rewards, bool *out_terminals);
 
+/* PrioritizedReplay.sample + _gather on the frame-deduplicated ring in ONE
+ * launch (replay.py:104-115, 215-230): as dqn_sample_gather (stratified
+ * descent per gather CTA, IS-weight CTA row), the stacks assembled from the
+ * frame pool as dqn_frame_gather does.  Identical to dqn_tree_sample
+ * followed by dqn_frame_gather. */
+int dqn_frame_sample_gather(void *stream, const double *nodes, int32_t depth, const int64_t *size,
+                            const double *u, int32_t k, const double *beta, int64_t *idx,
+                            double *prob, double *weight, int32_t *flags, const uint8_t *frames,
+                            int64_t frame_bytes, const int64_t *ids, int stack,
+                            const int64_t *actions, const double *rewards, const bool *terminals,
+                            uint8_t *out_states, uint8_t *out_next_states, int64_t *out_actions,
+                            double *out_rewards, bool *out_terminals);
+
 /* RmsProp.step (optim.py:36-47) over a flat buffer: finite scan of all grads,
  * then (only if all finite) acc = acc*rho; acc += (1-rho)*g*g;
  * w -= (lr*g)/(sqrt(acc)+eps); g = 0 -- fp32, no FMA, bit-exact given g.

@@ -80,6 +80,8 @@ _SIGS = {
     "dqn_rmsprop_apply": ([vp, vp, vp, vp, i64, f32, f32, f32, f32, vp, vp], C.c_int),
     "dqn_frame_gather": ([vp, vp, i64, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp],
                          C.c_int),
+    "dqn_frame_sample_gather": ([vp, vp, C.c_int, vp, vp, C.c_int, vp, vp, vp, vp, vp, vp, i64, vp,
+                                 C.c_int, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "dqn_clip_gradients": ([vp, vp, i64, f64, vp], C.c_int),
     "dqn_sync_target": ([vp, vp, vp, i64], C.c_int),
     "dqn_dp_shard_info": ([vp, vp, vp, vp, vp], C.c_int),

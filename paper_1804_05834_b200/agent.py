@@ -190,14 +190,18 @@ class _StepPlan:
                 self.d_in.copy_(self.h_in, non_blocking=True)
                 src = self.d_in
             tree = self.memory.tree
-            _lib.call("dqn_sample_gather", st, tree.nodes.data_ptr(), tree.depth,
-                      ring._size_dev.data_ptr(), src.data_ptr(), k,
-                      src[k:].data_ptr(), self.idx.data_ptr(), self.prob.data_ptr(),
-                      self.w.data_ptr(), self.flags.data_ptr(), ring.states.data_ptr(),
-                      ring.next_states.data_ptr(), ring.slot_bytes, ring.actions.data_ptr(),
-                      ring.rewards.data_ptr(), ring.terminals.data_ptr(), self.x.data_ptr(),
-                      self.x[k:].data_ptr(), self.a.data_ptr(), self.r.data_ptr(),
-                      self.t.data_ptr())
+            if hasattr(ring, "sample_gather_fused"):       # frame-deduplicated ring
+                ring.sample_gather_fused(tree, src, k, src[k:], self.idx, self.prob, self.w,
+                                         self.flags, self.x, self.x[k:], self.a, self.r, self.t)
+            else:
+                _lib.call("dqn_sample_gather", st, tree.nodes.data_ptr(), tree.depth,
+                          ring._size_dev.data_ptr(), src.data_ptr(), k,
+                          src[k:].data_ptr(), self.idx.data_ptr(), self.prob.data_ptr(),
+                          self.w.data_ptr(), self.flags.data_ptr(), ring.states.data_ptr(),
+                          ring.next_states.data_ptr(), ring.slot_bytes, ring.actions.data_ptr(),
+                          ring.rewards.data_ptr(), ring.terminals.data_ptr(), self.x.data_ptr(),
+                          self.x[k:].data_ptr(), self.a.data_ptr(), self.r.data_ptr(),
+                          self.t.data_ptr())
         else:
             idx = self.idx
             if self.per:

@@ -149,4 +149,47 @@ static __device__ __forceinline__ int64_t warp_tree_descend(const double *__rest
   return n - (int64_t(1) << depth);
 }
 
+// The IS-weights CTA of the fused sample+gather kernels (replay.py:215-230):
+// descends all k stratified queries, writes idx / P / w and normalises w by
+// the batch max (block-wide reduce; red holds blockDim.x / 32 doubles).
+static __device__ __forceinline__ void sample_is_weights_block(
+    const double *nodes, int depth, const int64_t *size_p, const double *u, int k,
+    const double *beta_p, int64_t *idx, double *prob, double *weight, int32_t *flags,
+    double *red) {
+  const double total = nodes[1];
+  const bool ok = total > 0.0;
+  double mx = 0.0;
+  const double beta = *beta_p, size = (double)*size_p, seg = __ddiv_rn(total, (double)k);
+  const double hi = nextafter(total, 0.0);
+  for (int q = threadIdx.x; q < k; q += blockDim.x) {
+    if (!ok) {
+      idx[q] = 0; prob[q] = 0.0; weight[q] = 0.0;
+      continue;
+    }
+    double leaf;
+    const int64_t i = tree_descend(nodes, depth, __dmul_rn(__dadd_rn((double)q, u[q]), seg), hi,
+                                   &leaf);
+    const double p = __ddiv_rn(leaf, total);
+    const double w = pow(__dmul_rn(size, p), -beta);
+    idx[q] = i;
+    prob[q] = p;
+    weight[q] = w;
+    mx = fmax(mx, w);
+  }
+  if (!ok) {
+    if (threadIdx.x == 0) raise_flag(flags, DQN_FLAG_ZERO_TOTAL);
+    return;
+  }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+    red[0] = v;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < k; q += blockDim.x) weight[q] = __ddiv_rn(weight[q], red[0]);
+}
+
 }  // namespace dqn

@@ -34,7 +34,7 @@ import numpy as np
 
 from . import _lib
 from .errors import ConfigError, GeometryError
-from .replay import ReplayMemory, SampleBatch, Transition, _torch
+from .replay import ReplayMemory, SampleBatch, Transition, _to_device, _torch
 
 
 class FrameIndex:
@@ -107,11 +107,12 @@ class FrameDedupMemory(ReplayMemory):
 
     Same API for callers of the learner path: ``store``, ``gather_into``,
     ``sample_uniform``, ``size`` / ``cursor`` / ``capacity``, the
-    ``actions`` / ``rewards`` / ``terminals`` device arrays.  There are no
-    ``states`` / ``next_states`` arrays (``stack_at`` rebuilds one slot), and
-    the batched staging paths of the full-stack ring are not provided."""
+    ``actions`` / ``rewards`` / ``terminals`` device arrays, the Trainer's
+    staged insert (``store_staged``) and checkpoint export / import
+    (``host_states`` / ``restore``).  There are no ``states`` /
+    ``next_states`` arrays (``stack_at`` rebuilds one slot)."""
 
-    fused_ok = False          # the learner gathers through dqn_frame_gather
+    fused_ok = True           # the learner samples + gathers by dqn_frame_sample_gather
 
     def __init__(self, capacity: int, state_shape: tuple[int, ...], dtype=np.uint8,
                  frame_capacity: int | None = None):
@@ -172,46 +173,113 @@ class FrameDedupMemory(ReplayMemory):
         return i
 
     def store_many(self, states, actions, rewards, next_states, terminals) -> np.ndarray:
-        """Batched ``store``: ids assigned on the host in order, then the new
-        planes in one pinned upload and one scatter per array."""
+        """Batched ``store``: ids assigned on the host in batch order, then
+        the new planes in one pinned upload and one scatter per array.
+
+        Every transition's planes are built and checked before the first
+        assignment (a malformed state raises with nothing changed).  If the
+        pool runs out part-way (ConfigError), the transitions assigned so
+        far are uploaded and the cursor advances past them before the error
+        propagates, so the device table never points at ids the host index
+        no longer holds."""
         torch = _torch()
         n = len(actions)
         if n == 0:
             return np.zeros(0, dtype=np.int64)
-        slots = (self.cursor + np.arange(n)) % self.capacity
-        new_ids, new_planes = [], []
+        planes_all = []
         for j in range(n):
             planes = _planes(states[j], self.stack) + _planes(next_states[j], self.stack)
             for p in planes:
                 if len(p) != self.frame_bytes:
                     raise GeometryError(f"frame of {len(p)} B, ring holds {self.frame_bytes} B frames")
-            for fid, p in self.index.assign(int(slots[j]), planes):
+            planes_all.append(planes)
+        slots = (self.cursor + np.arange(n)) % self.capacity
+        new_ids, new_planes = [], []
+        done, err = n, None
+        for j in range(n):
+            try:
+                ups = self.index.assign(int(slots[j]), planes_all[j])
+            except ConfigError as e:           # pool exhausted: keep transitions 0..j-1
+                done, err = j, e
+                break
+            for fid, p in ups:
                 new_ids.append(fid)
                 new_planes.append(p)
+        if done:
+            self._commit(slots[:done], new_ids, new_planes,
+                         _to_device(actions, torch.int64)[:done],
+                         _to_device(rewards, torch.float64)[:done],
+                         _to_device(terminals, torch.bool)[:done])
+        if err is not None:
+            raise err
+        return slots
+
+    def _commit(self, slots, new_ids, new_planes, actions, rewards, terminals) -> None:
+        """Upload the planes assigned to ``slots`` (host index already
+        updated), write the slots' id rows and metadata, advance the cursor."""
+        torch = _torch()
+        n = len(slots)
         # a pool id can be reassigned within the batch only after its last
         # reference went away: the last upload of an id is the one that counts
         if new_ids:
-            buf = torch.empty((len(new_ids), self.frame_bytes), dtype=torch.uint8).pin_memory()
-            buf.numpy()[:] = np.frombuffer(b"".join(new_planes), dtype=np.uint8).reshape(
-                len(new_ids), self.frame_bytes)
             last = {fid: i for i, fid in enumerate(new_ids)}
-            keep = torch.as_tensor(sorted(last.values()), dtype=torch.int64)
-            ids_t = torch.as_tensor([new_ids[i] for i in keep.tolist()], dtype=torch.int64)
-            self.frames.index_copy_(0, ids_t.to("cuda"), buf[keep].to("cuda", non_blocking=True))
+            keep = sorted(last.values())
+            buf = torch.empty((len(keep), self.frame_bytes), dtype=torch.uint8).pin_memory()
+            buf.numpy()[:] = np.frombuffer(b"".join(new_planes[i] for i in keep),
+                                           dtype=np.uint8).reshape(len(keep), self.frame_bytes)
+            ids_t = torch.as_tensor([new_ids[i] for i in keep], dtype=torch.int64, device="cuda")
+            # (torch's pinned-host allocator keeps buf alive until the copy ran)
+            self.frames.index_copy_(0, ids_t, buf.to("cuda", non_blocking=True))
         # a batch longer than the ring keeps its last `capacity` transitions
         # (scatters with repeated slots would leave an unspecified winner)
         m = min(n, self.capacity)
-        sl = torch.as_tensor(slots[n - m:], device="cuda")
-        self.ids.index_copy_(0, sl, torch.as_tensor(self.index.ids[slots[n - m:]]).to("cuda"))
-        self.actions[sl] = torch.as_tensor(np.asarray(actions)[n - m:], dtype=torch.int64).to("cuda")
-        self.rewards[sl] = torch.as_tensor(np.asarray(rewards)[n - m:], dtype=torch.float64).to("cuda")
-        self.terminals[sl] = torch.as_tensor(np.asarray(terminals)[n - m:], dtype=torch.bool).to("cuda")
+        sl_np = np.asarray(slots[n - m:])
+        sl = torch.as_tensor(sl_np, device="cuda")
+        self.ids.index_copy_(0, sl, torch.as_tensor(self.index.ids[sl_np]).to("cuda"))
+        self.actions[sl] = actions[n - m:]
+        self.rewards[sl] = rewards[n - m:]
+        self.terminals[sl] = terminals[n - m:]
         self.cursor = int((self.cursor + n) % self.capacity)
         self._set_size(min(self.size + n, self.capacity))
-        return slots
 
-    def store_staged(self, *args, **kwargs) -> None:
-        raise NotImplementedError("the frame-deduplicated ring stores through store()")
+    def store_staged(self, states, next_states, actions, rewards, terminals, n: int) -> None:
+        """The Trainer's staged insert (trainer._Staging): ``n`` transitions
+        from pinned host buffers, through the batched host index."""
+        n = int(n)
+        if n <= 0:
+            return
+        self.store_many(states[:n].numpy(), actions[:n], rewards[:n], next_states[:n].numpy(),
+                        terminals[:n])
+
+    def fill_synthetic(self, *args, **kwargs) -> None:
+        raise NotImplementedError("the frame-deduplicated ring is filled through store / "
+                                  "store_many (synthetic fills are per slot, not per frame)")
+
+    # -- checkpoint export / import (checkpoint.py:134-177 'memory') ------
+    def host_states(self, n: int):
+        """(states, next_states) of slots [0, n) as host uint8 arrays -- the
+        full stacks, as the full-stack ring's checkpoint holds them."""
+        torch = _torch()
+        out_s = np.empty((n,) + self.state_shape, dtype=np.uint8)
+        out_n = np.empty_like(out_s)
+        for a in range(0, n, 4096):
+            b = min(n, a + 4096)
+            bt = self._gather(torch.arange(a, b, device="cuda"), None, None)
+            out_s[a:b] = bt.states.cpu().numpy()
+            out_n[a:b] = bt.next_states.cpu().numpy()
+        return out_s, out_n
+
+    def restore(self, n: int, states, next_states, actions, rewards, terminals, cursor: int) -> None:
+        """Refill slots [0, n) from host arrays (a checkpoint's memory
+        section), then set the cursor: the same ring contents as the
+        checkpointed one (frames re-deduplicated in slot order)."""
+        h, w, s = self.state_shape
+        self.index = FrameIndex(self.capacity, self.index.frame_capacity, s)
+        self.cursor = 0
+        self._set_size(0)
+        if n:
+            self.store_many(states, actions, rewards, next_states, terminals)
+        self.cursor = int(cursor)
 
     def gather_into(self, indices, k: int, out_states, out_next_states, out_actions,
                     out_rewards, out_terminals) -> None:
@@ -221,6 +289,18 @@ class FrameDedupMemory(ReplayMemory):
                   self.actions.data_ptr(), self.rewards.data_ptr(), self.terminals.data_ptr(),
                   _lib.ptr(out_states), _lib.ptr(out_next_states), _lib.ptr(out_actions),
                   _lib.ptr(out_rewards), _lib.ptr(out_terminals))
+
+    def sample_gather_fused(self, tree, u, k: int, beta, idx, prob, w, flags, out_states,
+                            out_next_states, out_actions, out_rewards, out_terminals) -> None:
+        """PrioritizedReplay.sample + _gather in one launch (the learner's
+        fused path; dqn_frame_sample_gather)."""
+        _lib.call("dqn_frame_sample_gather", _lib.stream_ptr(), tree.nodes.data_ptr(), tree.depth,
+                  self._size_dev.data_ptr(), _lib.ptr(u), k, _lib.ptr(beta), _lib.ptr(idx),
+                  _lib.ptr(prob), _lib.ptr(w), _lib.ptr(flags), self.frames.data_ptr(),
+                  self.frame_bytes, self.ids.data_ptr(), self.stack, self.actions.data_ptr(),
+                  self.rewards.data_ptr(), self.terminals.data_ptr(), _lib.ptr(out_states),
+                  _lib.ptr(out_next_states), _lib.ptr(out_actions), _lib.ptr(out_rewards),
+                  _lib.ptr(out_terminals))
 
     def _gather(self, indices, probabilities, weights) -> SampleBatch:
         torch = _torch()

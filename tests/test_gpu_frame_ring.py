@@ -77,10 +77,13 @@ def test_float_frames_and_footprint(P):
     assert dedup.resident_bytes < 0.3 * full_bytes, (dedup.resident_bytes, full_bytes)
 
 
-def test_learn_step_identical_on_dedup_ring(P):
+@pytest.mark.parametrize("fused", [True, False])
+def test_learn_step_identical_on_dedup_ring(P, fused, monkeypatch):
     """The learner over PrioritizedReplay(frame_dedup=True) -- the graph's
-    gather through dqn_frame_gather -- gives the same TdResults and
-    parameters as over the full-stack ring, bit for bit."""
+    batch from dqn_frame_sample_gather (descent + stack assembly in one
+    launch) or dqn_tree_sample + dqn_frame_gather -- gives the same TdResults
+    and parameters as over the full-stack ring, bit for bit."""
+    monkeypatch.setattr(P.agent, "FUSED_SAMPLE", fused)
     rng = np.random.default_rng(11)
     shape, cap = (24, 24, 4), 256
     stream = episodic(rng, 300, shape)
@@ -139,3 +142,94 @@ def test_store_many_matches_store(P):
         assert torch.equal(s, full.states) and torch.equal(s2, full.next_states)
         assert torch.equal(a, full.actions) and torch.equal(r, full.rewards)
         assert torch.equal(t, full.terminals)
+
+
+def test_store_many_validates_before_assigning(P):
+    """a malformed state in the middle of a batch raises before
+    any transition is assigned; later stores still match the full ring."""
+    from paper_1804_05834_b200.errors import GeometryError
+    from paper_1804_05834_b200.frame_ring import FrameDedupMemory
+    rng = np.random.default_rng(3)
+    shape, cap = (10, 10, 4), 16
+    stream = episodic(rng, 12, shape)
+    full, dedup = P.ReplayMemory(cap, shape), FrameDedupMemory(cap, shape)
+    cols = list(zip(*stream))
+    bad = list(cols[0])
+    bad[3] = np.zeros((10, 10, 3), dtype=np.uint8)           # wrong stack depth
+    with pytest.raises(GeometryError):
+        dedup.store_many(bad, cols[1], cols[2], cols[3], cols[4])
+    assert dedup.size == 0 and dedup.cursor == 0 and dedup.index.live_frames == 0
+    a = torch.as_tensor(np.asarray(cols[1]), device="cuda")   # device metadata is accepted
+    dedup.store_many(cols[0], a, cols[2], cols[3], cols[4])
+    full.store_many(np.stack(cols[0]), np.asarray(cols[1]), np.asarray(cols[2]),
+                    np.stack(cols[3]), np.asarray(cols[4]))
+    ti = torch.arange(12, device="cuda")
+    s, s2 = (torch.empty((12,) + shape, dtype=torch.uint8, device="cuda") for _ in range(2))
+    dedup.gather_into(ti, 12, s, s2, None, None, None)
+    assert torch.equal(s, full.states[:12]) and torch.equal(s2, full.next_states[:12])
+    assert torch.equal(dedup.actions[:12], full.actions[:12])
+
+
+def test_store_many_pool_exhaustion_keeps_the_assigned_prefix(P):
+    """when the frame pool runs out part-way through a batch, the
+    transitions assigned so far are uploaded and the cursor advances past
+    them before ConfigError propagates (device table == host index)."""
+    from paper_1804_05834_b200.errors import ConfigError
+    from paper_1804_05834_b200.frame_ring import FrameDedupMemory
+    rng = np.random.default_rng(4)
+    shape, cap = (6, 6, 4), 16
+    # independent random stacks: 8 new frames per transition, pool of 3 x 8
+    stream = [(rng.integers(0, 256, shape, dtype=np.uint8), 1, 0.5,
+               rng.integers(0, 256, shape, dtype=np.uint8), False) for _ in range(5)]
+    dedup = FrameDedupMemory(cap, shape, frame_capacity=24)
+    cols = list(zip(*stream))
+    with pytest.raises(ConfigError):
+        dedup.store_many(cols[0], cols[1], cols[2], cols[3], cols[4])
+    assert dedup.size == 3 and dedup.cursor == 3
+    ti = torch.arange(3, device="cuda")
+    s, s2 = (torch.empty((3,) + shape, dtype=torch.uint8, device="cuda") for _ in range(2))
+    dedup.gather_into(ti, 3, s, s2, None, None, None)
+    assert np.array_equal(s.cpu().numpy(), np.stack(cols[0][:3]))
+    assert np.array_equal(s2.cpu().numpy(), np.stack(cols[3][:3]))
+    with pytest.raises(NotImplementedError):
+        dedup.fill_synthetic(0, 4)
+
+
+@pytest.mark.parametrize("alpha", [0.6, 0.0])
+def test_trainer_on_dedup_ring_matches_full_ring(P, alpha):
+    """The Trainer's staged insert through the frame-deduplicated ring: the
+    same records and parameters as the full-stack ring (the learner reads
+    byte-identical batches)."""
+    from tests.test_gpu_checkpoint import small_cfg
+    runs = []
+    for dedup in (False, True):
+        sink = P.RecordCollector()
+        tr = P.Trainer(small_cfg(P, max_steps=400, priority_alpha=alpha), sink=sink,
+                       frame_dedup=dedup)
+        tr.run()
+        runs.append(([r.row() for r in sink.records], tr.online.flat_values.clone()))
+    assert runs[0][0] == runs[1][0]
+    assert torch.equal(runs[0][1], runs[1][1])
+
+
+@pytest.mark.parametrize("src_dedup", [True, False])
+def test_resume_on_dedup_ring(P, tmp_path, src_dedup):
+    """CYRL memory section from / into the frame-deduplicated ring: a run
+    resumed on the dedup ring (from a dedup or a full-ring checkpoint)
+    reproduces the uninterrupted run record for record."""
+    import dataclasses
+    from paper_1804_05834_b200.checkpoint import load_checkpoint
+    from tests.test_gpu_checkpoint import small_cfg
+    full_sink = P.RecordCollector()
+    full = P.Trainer(small_cfg(P, max_steps=400, checkpoint_include_memory=True), sink=full_sink)
+    full.run()
+    sink_a = P.RecordCollector()
+    P.Trainer(small_cfg(P, max_steps=200, checkpoint_include_memory=True), sink=sink_a,
+              out_dir=tmp_path, frame_dedup=src_dedup).run()
+    ck = load_checkpoint(tmp_path / "checkpoint_final.ckpt")
+    ck.config = dataclasses.replace(ck.config, max_steps=400)
+    sink_b = P.RecordCollector()
+    resumed = P.Trainer.from_checkpoint(ck, sink=sink_b, frame_dedup=True)
+    resumed.run()
+    assert [r.row() for r in sink_a.records + sink_b.records] == [r.row() for r in full_sink.records]
+    assert torch.equal(resumed.online.flat_values, full.online.flat_values)
