@@ -64,7 +64,8 @@ def main():
     print(f"last update: {len(last)} kernels, span {span:.1f} us")
     rows = []
     for s, e, n, st in last:
-        nm = n.split("(")[0][:70]
+        nm = n.replace("void ", "").replace("dqn::", "").replace("(anonymous namespace)::", "")
+        nm = nm.replace("tc::", "").replace("<unnamed>::", "")[:90]
         rows.append({"start": s - t0, "end": e - t0, "us": e - s, "stream": st, "name": nm})
         print(f"  {s - t0:7.1f} -> {e - t0:7.1f} ({e - s:5.1f} us) s{st:<4} {nm}")
     if a.json:
