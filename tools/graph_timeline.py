@@ -26,7 +26,11 @@ def main():
     ap.add_argument("--cap", type=int, default=100_000)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--json", default="")
+    ap.add_argument("--split-sample", action="store_true",
+                    help="descent and frame gather as two launches (agent.FUSED_SAMPLE = False)")
     a = ap.parse_args()
+    if a.split_sample:
+        P.agent.FUSED_SAMPLE = False
     cfg = P.RunConfig(batch_size=32, beta_end_step=50_000_000)
     on = P.build_network("atari", (84, 84, 4), 4, True)
     tg = P.build_network("atari", (84, 84, 4), 4, True)
