@@ -246,17 +246,16 @@ class _StepPlan:
         ev = torch.cuda.Event
         e_in = ev()
         e_in.record(s0)
+        upto = self.head_layer if self.fused_head else None
+
+        def forward(net, x, bind):
+            net.forward_into(x, bind, upto=upto)
         with torch.cuda.stream(s1):
             s1.wait_event(e_in)
-            tg.forward_into(self.x[k:], self.tg_bind,
-                            upto=self.head_layer if self.fused_head else None)
+            forward(tg, self.x[k:], self.tg_bind)
             e_tg = ev()
             e_tg.record(s1)
-        upto = self.head_layer if self.fused_head else None
-        if self.double:
-            on.forward_into(self.x, self.on_bind, upto=upto)
-        else:
-            on.forward_into(self.x[:k], self.on_bind, upto=upto)
+        forward(on, self.x if self.double else self.x[:k], self.on_bind)
         s0.wait_event(e_tg)
         nA = self.nA
         out = self.d_out

@@ -26,6 +26,10 @@
 namespace dqn {
 bool conv1_wgrad_u8_ok(const dqn_net_desc *net);
 int64_t conv1_wgrad_u8_scratch(const dqn_net_desc *net, int batch);
+bool lin_tc_ok(const dqn_layer_desc &L, int batch);
+int lin_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, const float *params,
+                   float *y, int batch);
+
 namespace {
 
 __device__ __forceinline__ float4 ld4(const float *p) {
@@ -623,6 +627,13 @@ int tc_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const floa
                      const dqn_binding *b) {
   const dqn_layer_desc &L = net->layer[l];
   const void *in = (l == 0) ? b->x : b->act[l - 1];
+  // hidden linear layers at learner batch sizes: the TMA-fed weight-streaming
+  // kernel (lin_tc.cu; measured +0.3 % in the learner -- its dgrad form was
+  // slower than the engine's LinDgradTmaPol there and is not used)
+  if (L.kind == DQN_LAYER_LINEAR && l > 0 && lin_tc_ok(L, b->batch)) {
+    const int rc = lin_tc_forward(st, L, (const float *)in, params, b->act[l], b->batch);
+    if (rc != DQN_ERR_UNSUPPORTED) return rc;
+  }
   if (l == 0 && net->input_u8)
     return fwd_dispatch<uint8_t>(st, L, (const uint8_t *)in, params, b->act[l], b->scratch,
                                   counters_of(b), b->batch);
