@@ -75,6 +75,8 @@ static int layer_wgrad(cudaStream_t st, const dqn_net_desc *net, int l, float *g
                        const dqn_binding *b, int32_t *flags) {
   const dqn_layer_desc &L = net->layer[l];
   // hidden linear layers at learner batch sizes: the small-K FMA kernel
+  // (a tcgen05 form -- both operands TMA-loaded and transposed in smem, one
+  // 32-k stage, 100 CTAs -- measured 18.8 vs 12.9 us and -5 % in the learner)
   if (L.kind == DQN_LAYER_LINEAR && l != net->n_layers - 1 && l > 0 && b->batch <= 64 &&
       net->algo != 1)
     return lin_wgrad_smallk(st, b->act[l - 1], b->dact[l], b->batch,
