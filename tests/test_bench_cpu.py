@@ -46,3 +46,25 @@ def test_gpus_more_than_visible_fails_loudly():
     assert out.returncode != 0
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert "refusing" in line["error"]
+
+
+def test_reference_arm_under_torchrun_world2():
+    """The driver launches `--impl reference` like our arm (torchrun, N ranks):
+    rank 0 alone prints the cfg5 comparator line (global batch 32 N in one
+    process, value in batch-32 updates/s), the other ranks exit 0."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node=2", "--master-addr", "127.0.0.1",
+                          f"--master-port={port}", "bench.py", "--impl", "reference", "--gpus", "2",
+                          "--steps", "3", "--warmup", "3"],
+                         cwd=REPO, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+    assert d["config"]["global_batch"] == 64 and d["config"]["parallelism"] == "dp2"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["value"] > 0
