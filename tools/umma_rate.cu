@@ -69,8 +69,7 @@ __global__ void rate(long long *cycles, int iters) {
 }
 
 template <int N, bool TS>
-void run(long long *d, int sms) {
-  const int iters = 4096;
+void run(long long *d, int sms, int iters = 4096) {
   const int smem = (128 * 32 + N * 32) * 4;
   cudaFuncSetAttribute(rate<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   rate<N, TS><<<sms, 128, smem>>>(d, iters);
@@ -83,6 +82,11 @@ void run(long long *d, int sms) {
   for (int i = 0; i < sms; ++i) mx = h[i] > mx ? h[i] : mx;
   const double cpm = mx / iters;
   const double flop = 2.0 * 128 * N * 8;
+  if (iters < 4096) {      // latency mode: issue of `iters` MMAs -> their commit observed
+    printf("%s N=%3d : %5d MMAs issued -> completion seen after %7.0f cycles (%.2f us)\n",
+           TS ? "TS" : "SS", N, iters, mx, mx / 1965.0);
+    return;
+  }
   printf("%s N=%3d : %6.1f cycles/MMA  -> %7.1f TFLOP/s tf32 at 1.965 GHz x %d SMs\n", TS ? "TS" : "SS", N,
          cpm, flop / cpm * 1.965e9 * sms / 1e12, sms);
 }
@@ -100,5 +104,8 @@ int main() {
   run<64, true>(d, sms);
   run<128, true>(d, sms);
   run<256, true>(d, sms);
+  // latency: one CTA, a short burst of MMAs, issue -> commit arrival
+  for (int n : {1, 2, 4, 8, 16, 32, 64}) run<64, true>(d, 1, n);
+  for (int n : {1, 8, 16}) run<128, false>(d, 1, n);
   return 0;
 }
