@@ -116,9 +116,9 @@ labels = [("sample+gather (batch 32)", "sample_gather"),
           ("conv1.fwd (batch 32, target)", "FwdPol<unsigned char"),
           ("conv2.fwd (batch 32, target)", "FwdPol<float"),
           ("conv3.fwd (batch 32, target)", "FwdPol<float"),
-          ("fc1.fwd (batch 32, target)", "FwdPol<float"),
+          ("fc1.fwd (batch 32, target)", "lin_tc"),
           ("conv1.fwd (batch 64)", "FwdPol<unsigned char"), ("conv2.fwd (batch 64)", "FwdPol<float"),
-          ("conv3.fwd (batch 64)", "FwdPol<float"), ("fc1.fwd (batch 64)", "FwdPol<float"),
+          ("conv3.fwd (batch 64)", "FwdPol<float"), ("fc1.fwd (batch 64)", "lin_tc"),
           ("duel.fwd+td (Q heads)", "head_q"), ("duel.dgrad+wgrad (TD block)", "head_td_bwd"),
           ("tree update (batch 32)", "tree_update"), ("fc1.wgrad (batch 32)", "lin_wgrad"),
           ("fc1.dgrad (batch 32)", "LinDgrad"), ("conv3.wgrad (batch 32)", "WgradPol<float"),
