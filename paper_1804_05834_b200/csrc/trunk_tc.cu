@@ -29,6 +29,9 @@ int64_t conv1_wgrad_u8_scratch(const dqn_net_desc *net, int batch);
 bool lin_tc_ok(const dqn_layer_desc &L, int batch);
 int lin_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, const float *params,
                    float *y, int batch);
+bool conv_tc_ok(const dqn_layer_desc &L);
+int conv_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, const float *params,
+                    float *y, int batch);
 
 namespace {
 
@@ -632,6 +635,11 @@ int tc_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const floa
   // slower than the engine's LinDgradTmaPol there and is not used)
   if (L.kind == DQN_LAYER_LINEAR && l > 0 && lin_tc_ok(L, b->batch)) {
     const int rc = lin_tc_forward(st, L, (const float *)in, params, b->act[l], b->batch);
+    if (rc != DQN_ERR_UNSUPPORTED) return rc;
+  }
+  // fp32-input convolutions: both operands by TMA (conv_tc.cu)
+  if (L.kind == DQN_LAYER_CONV && !(l == 0 && net->input_u8) && conv_tc_ok(L)) {
+    const int rc = conv_tc_forward(st, L, (const float *)in, params, b->act[l], b->batch);
     if (rc != DQN_ERR_UNSUPPORTED) return rc;
   }
   if (l == 0 && net->input_u8)

@@ -114,7 +114,10 @@ def test_determinism_and_batch_independence(P):
     q64b = net.forward(x).clone()
     assert torch.equal(q64, q64b)
     q8 = net.forward(x[:8]).clone()
-    assert torch.equal(q8, q64[:8])       # a row's Q does not depend on its batch
+    assert torch.equal(q8, net.forward(x[:8]))
+    # across batch sizes a row's Q agrees to fp32 rounding: conv2 / conv3
+    # split K over a cluster sized by the batch (conv_tc.cu)
+    assert float((q8 - q64[:8]).norm() / q64[:8].norm()) < 1e-6
 
 
 def test_errors(P):
@@ -216,3 +219,35 @@ def test_conv1_wgrad_from_frames(P, batch):
     on.calculate_gradient()                       # accumulates: grads += dW
     w2 = t1["conv1.weight"].grad.cpu().numpy()
     assert rel_norm(w2, 2 * ref.grads["conv1.weight"]) < TOL
+
+
+@pytest.mark.parametrize("batch", [1, 2, 3, 33, 64, 130, 1024])
+def test_conv_tc_forward_layers(P, batch):
+    """conv2 / conv3 forward (conv_tc.cu: TMA-fed implicit GEMM, tiles of
+    whole images, cluster split-K) against an fp64 convolution of the same
+    layer input, at batch sizes with partial last tiles and several waves."""
+    import torch.nn.functional as F
+    from paper_1804_05834_b200 import synth
+    on = P.build_network("atari", (84, 84, 4), 4, True)
+    P.init_params(on, 5)
+    rng = np.random.default_rng(batch)
+    for n, t in on.named_tensors():
+        if n.endswith("bias"):
+            t.values.copy_(torch.as_tensor((rng.standard_normal(t.shape) * 0.01).astype(np.float32),
+                                           device="cuda"))
+    x8 = synth.frames(4, 1, np.arange(batch) * 7 + 3)
+    on.forward(torch.as_tensor(x8, device="cuda"))
+    bind = on.binding(batch)
+    tens = dict(on.named_tensors())
+    shapes = [tuple(u["out_shape"]) for u in on._units]
+    for l, (name, fh, st) in enumerate([("conv2", 4, 2), ("conv3", 3, 1)], start=1):
+        h, w, c = shapes[l - 1]
+        oh, ow, n = shapes[l]
+        xin = bind.act[l - 1][: batch * h * w * c].view(batch, h, w, c).double().permute(0, 3, 1, 2)
+        W = tens[f"{name}.weight"].values.double().reshape(fh, fh, c, n).permute(3, 2, 0, 1)
+        ref = F.relu(F.conv2d(xin, W, tens[f"{name}.bias"].values.double(), stride=st))
+        ref = ref.permute(0, 2, 3, 1)
+        got = bind.act[l][: batch * oh * ow * n].view(batch, oh, ow, n).double()
+        err = (got - ref).norm() / ref.norm()
+        assert err < 2e-6, (name, batch, float(err))
+        assert float((got - ref).abs().max()) <= 1e-5 * float(ref.abs().max()) + 1e-7, name

@@ -21,7 +21,7 @@ import pytest
 
 from oracle import deepq_oracle as O
 from paper_1804_05834_b200 import synth
-from tests.helpers import ATARI, rel_norm
+from tests.helpers import ATARI, follow_device_relu_kinks, rel_norm
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -121,9 +121,13 @@ def test_one_update_at_1m(P, name):
 
     step = 1000
     res = P.learn_step(on, tg, mem, opt, cfg, step, np.random.default_rng(77))
-    ores = O.learn_step(o_on, o_tg, o_mem, o_opt, o_cfg, step, rng=np.random.default_rng(77))
-
     plan = next(p for p in P.agent._PLANS.values() if p.online is on)
+    # ReLU kinks within fp32 rounding resolved as the device did (helpers)
+    kinks = follow_device_relu_kinks(o_on, [a.cpu().numpy() for a in plan.on_bind.act])
+    ores = O.learn_step(o_on, o_tg, o_mem, o_opt, o_cfg, step, rng=np.random.default_rng(77))
+    if kinks:
+        print(f"{name}: ReLU kinks resolved as on the device: {kinks}")
+
     assert np.array_equal(plan.last_indices().cpu().numpy(), ores["batch"].indices)
     assert rel_norm(res.targets, ores["targets"]) < 1e-5
     assert rel_norm(res.td_errors, ores["td_errors"]) < 1e-5

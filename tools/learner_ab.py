@@ -1,0 +1,93 @@
+"""Diagnostic: the cfg4 learner's device update rate (bench.py's device loop:
+pre-drawn PER uniforms in HBM, one graph launch per update) under several
+settings of a library-side override, interleaved A/B/A/B so clock and
+placement drift average out.
+
+    python tools/learner_ab.py --ct=-1,0,2:3,0:2:192  # conv_tc cluster[:stages[:fill]]
+                                                 # (-1 = generic engine, 0 = auto)
+Settings are applied before each (re)capture: launch configurations are baked
+into the graph.  Uses the product library; the override entry point is
+diagnostic only.
+"""
+import argparse
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+os.environ.setdefault("DQN_B200_LIB", str(Path(__file__).resolve().parent.parent / "paper_1804_05834_b200" / "libdqn_b200_trace.so"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1804_05834_b200 as P  # noqa: E402
+from paper_1804_05834_b200 import _lib, agent  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ct", default="-1,0")
+    ap.add_argument("--cap", type=int, default=1_000_000)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--rounds", type=int, default=3)
+    a = ap.parse_args()
+    settings = a.ct.split(",")
+
+    def apply(v):
+        cl, _, rest = v.partition(":")
+        st, _, fill = rest.partition(":")
+        _lib.lib.dqn_ct_set_cluster(int(cl))
+        _lib.lib.dqn_ct_set_stages(int(st or 2))
+        _lib.lib.dqn_ct_set_fill(int(fill or 128))
+    cfg = P.RunConfig(batch_size=32, double=True, dueling=True, priority_alpha=0.6,
+                      beta_end_step=50_000_000)
+    on = P.build_network("atari", (84, 84, 4), 4, True)
+    tg = P.build_network("atari", (84, 84, 4), 4, True)
+    P.init_params(on, 1)
+    P.sync_target(on, tg)
+    opt = P.RmsProp(on, cfg.learning_rate, cfg.rms_decay, cfg.rms_epsilon)
+    mem = P.PrioritizedReplay(a.cap, (84, 84, 4), P.PriorityConfig(0.6, 0.01, cfg.beta_schedule()))
+    mem.fill_synthetic(1, a.cap)
+    rng = np.random.default_rng(2)
+    for s in range(4):
+        P.learn_step(on, tg, mem, opt, cfg, 50_000 + s, rng)
+    plan = agent._plan_for(on, tg, mem, opt, cfg)
+    k = 32
+    draws = np.empty((a.steps, k + 1))
+    for s in range(a.steps):
+        draws[s, :k] = rng.random(k)
+        draws[s, k] = mem.beta(50_200 + s)
+    d_draws = torch.as_tensor(draws, device="cuda")
+    slot = torch.zeros_like(d_draws[0])
+    saved = plan.h_in
+    graphs = {}
+    for v in settings:
+        apply(v)
+        plan.h_in = slot
+        graphs[v] = agent.capture_graph(lambda: plan.enqueue(io=False), plan.capture_stream)
+        plan.h_in = saved
+    apply("0")
+    sp = torch.cuda.current_stream().cuda_stream
+    res = {v: [] for v in settings}
+    for _ in range(a.rounds):
+        for v in settings:
+            g = graphs[v][1]
+            for s in range(20):
+                slot.copy_(d_draws[s], non_blocking=True)
+                g.launch(sp)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for s in range(a.steps):
+                slot.copy_(d_draws[s], non_blocking=True)
+                g.launch(sp)
+            e1.record()
+            torch.cuda.synchronize()
+            res[v].append(a.steps / (e0.elapsed_time(e1) / 1e3))
+    for v in settings:
+        print(f"ct={v:>5}: " + " ".join(f"{x:7.0f}" for x in res[v]) +
+              f"  | median {np.median(res[v]):7.0f} updates/s", flush=True)
+
+
+if __name__ == "__main__":
+    main()
