@@ -38,18 +38,22 @@ namespace {
 constexpr int CT_BK = 32;                      // k per stage: one tap x 32 channels
 constexpr int CT_BM = 128;                     // A tile rows (output pixels)
 constexpr int CT_THREADS = 192;                // warps 0-3 convert + epilogue, 4 TMA, 5 MMA
-constexpr int CT_EPI_LD = 68;                  // staged partial row stride (floats; conflict-free)
 
 struct ConvTcArgs {
-  CUtensorMap amap;                            // activations, 5-D strided view (SW128)
-  CUtensorMap bmap;                            // W [K][N], raw [32 k][N] boxes
-  int K, C, fw, S;                             // patch length, input channels, filter width, stride
-  int P, ipt, npix;                            // pixels per image, images per tile, B * P
+  CUtensorMap amap;                            // fwd: activations, dgrad: dY (5-D views, SW128)
+  CUtensorMap bmap;                            // fwd: W [K][N] raw [32 k][N]; dgrad: W rows (SW128)
+  int K, C, fw, S;                             // GEMM depth (per stride phase), channels of the
+                                               // k-blocks (fwd: in, dgrad: out), filter width, stride
+  int P, ipt, npix;                            // rows per image, images per tile, B * P
   int klen;                                    // k per cluster rank (multiple of CT_BK)
   int a_bytes;                                 // one A piece: ipt*P rows rounded up to 8, x 128 B
-  const float *bias;
-  int relu;
-  float *y;                                    // [B * P][N]
+  // dgrad: rows are the input pixels (S*yq + py, S*xq + px) of stride phase
+  // (py, px) = blockIdx.z, QH x QW of them per image; taps (py + S i, px + S j)
+  int QW, TW, H, W, cin;                       // phase grid width, taps per phase row, input dims
+  const float *bias;                           // fwd
+  int relu;                                    // fwd
+  const float *mask;                           // dgrad: the layer below's ReLU output (or null)
+  float *y;                                    // fwd: [B * P][N]; dgrad: dX [B][H][W][cin]
 };
 
 __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
@@ -84,19 +88,21 @@ __device__ __forceinline__ uint64_t ct_desc(uint32_t addr) {
 // Stage: A_hi | A_lo (a_bytes each, runtime) | [B_hi ; B_lo] | raw W tile.
 // Two stages of the Atari convs fit twice per SM (conv2 2 x 46 KB, conv3
 // 2 x 50 KB), so the online and target networks' launches share the SMs.
-template <int NB>
+template <int NB, bool DG>
 struct CtPlan {
   static constexpr int B_BYTES = 2 * NB * CT_BK * 4;     // [B_hi ; B_lo]
-  static constexpr int RAW = CT_BK * NB * 4;             // W tile as loaded
-  static constexpr int EPI = CT_BM * CT_EPI_LD * 4;
+  static constexpr int RAW = DG ? 0 : CT_BK * NB * 4;    // fwd: W tile as loaded
+  static constexpr int LD = NB + 4;                      // staged partial row stride (floats)
+  static constexpr int EPI = CT_BM * LD * 4;
   static int stage(int a_bytes) { return 2 * a_bytes + B_BYTES + RAW; }
   static int bytes(int st, int a_bytes) { return std::max(st * stage(a_bytes), EPI) + 1024; }
   static constexpr int TMEM = 4 * NB <= 128 ? 128 : 256;
 };
 
-template <int NB, int CT_ST>
+template <int NB, int CT_ST, bool DG>
 __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_constant__ ConvTcArgs p) {
-  using PL = CtPlan<NB>;
+  using PL = CtPlan<NB, DG>;
+  constexpr int CT_EPI_LD = PL::LD;
   constexpr uint32_t ID_FULL = tc::make_idesc_tf32(2 * NB), ID_HALF = tc::make_idesc_tf32(NB);
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[CT_ST], conv[CT_ST], empty[CT_ST], done;
@@ -144,16 +150,26 @@ __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_con
   if (warp == 4) {
     if (lane == 0) {                          // TMA producer
       const uint32_t a_box = (uint32_t)(p.ipt * p.P * CT_BK * 4);
+      const int py = DG ? (int)blockIdx.z / p.S : 0, px = DG ? (int)blockIdx.z % p.S : 0;
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % CT_ST, use = kb / CT_ST;
         if (use > 0) tc::mbar_wait(&empty[s], (use - 1) & 1);
-        tc::mbar_expect_tx(&full[s], a_box + (uint32_t)PL::RAW);
+        tc::mbar_expect_tx(&full[s], a_box + (uint32_t)(DG ? NB * CT_BK * 4 : PL::RAW));
         const int k0 = kbeg + kb * CT_BK;
         const int tap = k0 / p.C, c0 = k0 - tap * p.C;
-        const int r = tap / p.fw, q = tap - r * p.fw;
-        tma_load_5d(a_hi(s), &p.amap, (q % p.S) * p.C + c0, q / p.S, r % p.S, r / p.S, img0,
-                    &full[s]);
-        tc::tma_load_2d(b_raw(s), &p.bmap, 0, k0, &full[s]);
+        if constexpr (DG) {
+          // tap (i, j) of this phase: filter (py + S i, px + S j) reads dY at
+          // (yq - i, xq - j); rows off the dY grid come back as zeros
+          const int i = tap / p.TW, j = tap - i * p.TW;
+          const int r = py + p.S * i, q = px + p.S * j;
+          tma_load_5d(a_hi(s), &p.amap, c0, -j, 0, -i, img0, &full[s]);
+          tc::tma_load_2d(b_st(s), &p.bmap, c0, (r * p.fw + q) * NB, &full[s]);
+        } else {
+          const int r = tap / p.fw, q = tap - r * p.fw;
+          tma_load_5d(a_hi(s), &p.amap, (q % p.S) * p.C + c0, q / p.S, r % p.S, r / p.S, img0,
+                      &full[s]);
+          tc::tma_load_2d(b_raw(s), &p.bmap, 0, k0, &full[s]);
+        }
       }
     }
   } else if (warp == 5) {
@@ -187,9 +203,21 @@ __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_con
         tc::st_shared_v4(a_lo(s) + 16 * i, make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y),
                                                        tc::tf32_lo(v.z), tc::tf32_lo(v.w)));
       }
+      if constexpr (DG) {
+        // B arrived K-major (W rows (r, s, c), n contiguous): lo rows NB..2NB-1
+        // are hi's bytes shifted by NB rows (the swizzle repeats every 8 rows)
+        for (int i = t; i < NB * CT_BK / 4; i += 128) {
+          const uint32_t src = b_st(s) + 16 * i;
+          float4 v;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(src));
+          tc::st_shared_v4(src + NB * 128, make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y),
+                                                       tc::tf32_lo(v.z), tc::tf32_lo(v.w)));
+        }
+      }
       // B: raw [32 k][NB n] -> row n (hi) and row NB + n (lo), 16-byte column
       // c ^ (n % 8) of the swizzled K-major tile (lanes = consecutive n)
-      for (int u = t; u < NB * (CT_BK / 4); u += 128) {
+      for (int u = t; u < (DG ? 0 : NB * (CT_BK / 4)); u += 128) {
         const int n = u % NB, c = u / NB;
         float v[4];
 #pragma unroll
@@ -283,16 +311,34 @@ __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_con
     for (int h = 0; h < 4; ++h) {
       if (uu[h] >= ue) continue;
       const int row = uu[h] / U4, c4 = uu[h] - row * U4;
-      const float4 b = *reinterpret_cast<const float4 *>(p.bias + 4 * c4);
-      float v[4] = {__fadd_rn(acc[h].x, b.x), __fadd_rn(acc[h].y, b.y),
-                    __fadd_rn(acc[h].z, b.z), __fadd_rn(acc[h].w, b.w)};
-      if (p.relu) {
+      float v[4] = {acc[h].x, acc[h].y, acc[h].z, acc[h].w};
+      int64_t o;
+      if constexpr (DG) {
+        // row -> input pixel of this stride phase
+        const int img = row / p.P, q = row - img * p.P;
+        const int yq = q / p.QW, xq = q - yq * p.QW;
+        const int y = p.S * yq + (int)blockIdx.z / p.S, x = p.S * xq + (int)blockIdx.z % p.S;
+        if (y >= p.H || x >= p.W) continue;
+        o = (((int64_t)(img0 + img) * p.H + y) * p.W + x) * p.cin + 4 * c4;
+        if (p.mask) {
+          const float4 m = *reinterpret_cast<const float4 *>(p.mask + o);
+          if (!(m.x > 0.f)) v[0] = 0.f;
+          if (!(m.y > 0.f)) v[1] = 0.f;
+          if (!(m.z > 0.f)) v[2] = 0.f;
+          if (!(m.w > 0.f)) v[3] = 0.f;
+        }
+      } else {
+        const float4 b = *reinterpret_cast<const float4 *>(p.bias + 4 * c4);
+        v[0] = __fadd_rn(v[0], b.x); v[1] = __fadd_rn(v[1], b.y);
+        v[2] = __fadd_rn(v[2], b.z); v[3] = __fadd_rn(v[3], b.w);
+        if (p.relu) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (v[e] < 0.f) v[e] = 0.f;
+          for (int e = 0; e < 4; ++e)
+            if (v[e] < 0.f) v[e] = 0.f;
+        }
+        o = (int64_t)(pix0 + row) * NB + 4 * c4;
       }
-      *reinterpret_cast<float4 *>(p.y + (int64_t)(pix0 + row) * NB + 4 * c4) =
-          make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4 *>(p.y + o) = make_float4(v[0], v[1], v[2], v[3]);
     }
   }
   if (cl > 1) tc::cluster_sync();             // peers' staged partials read
@@ -346,6 +392,37 @@ bool ct_w_map(CUtensorMap *m, const float *w, int K, int N) {
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// dgrad operands: dY [B][OH][OW][N] as {N, OW, 1, OH, B} with boxes of the
+// phase grid {32, QW, 1, QH, ipt} (reads off the grid fill zeros), and W as
+// rows (r, s, c) of N: boxes {32 n, cin rows}, K-major for the MMA as loaded
+bool ct_dy_map(CUtensorMap *m, const float *dy, const dqn_layer_desc &L, int batch, int ipt,
+               int QH, int QW) {
+  const EncodeTiledFn fn = ct_encode();
+  const int N = L.out_c;
+  if (!fn || ((uintptr_t)dy % 16)) return false;
+  const cuuint64_t dims[5] = {(cuuint64_t)N, (cuuint64_t)L.out_w, 1, (cuuint64_t)L.out_h,
+                              (cuuint64_t)batch};
+  const cuuint64_t strides[4] = {(cuuint64_t)N * 4, (cuuint64_t)L.out_w * N * 4,
+                                 (cuuint64_t)L.out_w * N * 4, (cuuint64_t)L.out_h * L.out_w * N * 4};
+  const cuuint32_t box[5] = {CT_BK, (cuuint32_t)QW, 1, (cuuint32_t)QH, (cuuint32_t)ipt};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float *>(dy), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool ct_wrows_map(CUtensorMap *m, const float *w, int rows, int N, int box_rows) {
+  const EncodeTiledFn fn = ct_encode();
+  if (!fn || ((uintptr_t)w % 16)) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)N * 4};
+  const cuuint32_t box[2] = {CT_BK, (cuuint32_t)box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(w), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // CTAs one launch aims for: K split = ceil(fill / tiles), so the target's
 // batch-32 launches split K further than the online batch-64 ones (measured
 // in the learner: fill 64 / 96 / 128 / 160 / 256 -> 128 best; fixed splits
@@ -354,24 +431,25 @@ bool ct_w_map(CUtensorMap *m, const float *w, int K, int N) {
 int g_ct_cluster = 0;   // diagnostic: 0 auto, > 0 cluster size, -1 engine, -2/-3 one layer only
 int g_ct_stages = 2;    // diagnostic: pipeline stages (2 or 3; 3 measured slower)
 int g_ct_fill = 128;
+int g_ct_dgrad = 1;     // diagnostic: 0 = conv dgrad on the generic engine
+int g_ct_dfill = 256;   // dgrad: CTAs one launch aims for
 #else
-constexpr int g_ct_cluster = 0, g_ct_stages = 2, g_ct_fill = 128;
+constexpr int g_ct_cluster = 0, g_ct_stages = 2, g_ct_fill = 128, g_ct_dgrad = 1, g_ct_dfill = 256;
 #endif
 
-template <int ST>
-int ct_launch(cudaStream_t st, const ConvTcArgs &a, int tiles, int cl) {
-  constexpr int NB = 64;
-  using PL = CtPlan<NB>;
-  auto kern = conv_tc_kernel<NB, ST>;
+template <int NB, int ST, bool DG>
+int ct_launch(cudaStream_t st, const ConvTcArgs &a, dim3 grid, const char *what) {
+  using PL = CtPlan<NB, DG>;
+  auto kern = conv_tc_kernel<NB, ST, DG>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          PL::bytes(ST, CT_BM * 128));
-    if (e != cudaSuccess) return cuda_status(e, "conv_tc_forward");
+    if (e != cudaSuccess) return cuda_status(e, what);
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tiles, cl, 1);
+  cfg.gridDim = grid;
   cfg.blockDim = dim3(CT_THREADS);
   cfg.dynamicSmemBytes = PL::bytes(ST, a.a_bytes);
   cfg.stream = st;
@@ -381,13 +459,27 @@ int ct_launch(cudaStream_t st, const ConvTcArgs &a, int tiles, int cl) {
   attr[1] = priority_attr(st);
   attr[2].id = cudaLaunchAttributeClusterDimension;
   attr[2].val.clusterDim.x = 1;
-  attr[2].val.clusterDim.y = cl;
+  attr[2].val.clusterDim.y = grid.y;
   attr[2].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 3;
   cudaLaunchKernelEx(&cfg, kern, a);
-  DQN_LAUNCH_CHECK("conv_tc_forward");
+  DQN_LAUNCH_CHECK(what);
   return DQN_OK;
+}
+
+// K split across a cluster: about g_ct_fill CTAs per launch, no empty ranks
+int ct_split(ConvTcArgs &a, int tiles, int sw, int fill) {
+  const int chunks = a.K / CT_BK;
+  int cl = (fill + tiles - 1) / tiles;
+  if (g_ct_cluster >= 16)                        // diagnostic: stride-2 layer | stride-1 layer
+    cl = sw == 2 ? (g_ct_cluster >> 4) : (g_ct_cluster & 15);
+  else if (g_ct_cluster > 0)
+    cl = g_ct_cluster;
+  cl = std::max(1, std::min({cl, 8, chunks}));
+  const int per = (chunks + cl - 1) / cl;
+  a.klen = per * CT_BK;
+  return (chunks + per - 1) / per;
 }
 
 }  // namespace
@@ -423,23 +515,54 @@ int conv_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, co
   a.relu = L.relu;
   a.y = y;
   const int tiles = (batch + ipt - 1) / ipt;
-  const int chunks = a.K / CT_BK;
-  // K split so that the launch fills about one wave of 128 CTAs
-  int cl = (g_ct_fill + tiles - 1) / tiles;
-  if (g_ct_cluster < 0)
-    cl = (g_ct_fill + tiles - 1) / tiles;
-  else if (g_ct_cluster >= 16)                       // diagnostic: stride-2 layer | stride-1 layer
-    cl = L.sw == 2 ? (g_ct_cluster >> 4) : (g_ct_cluster & 15);
-  else if (g_ct_cluster > 0)
-    cl = g_ct_cluster;
-  cl = std::max(1, std::min({cl, 8, chunks}));
-  const int per = (chunks + cl - 1) / cl;
-  cl = (chunks + per - 1) / per;                // no empty ranks
-  a.klen = per * CT_BK;
+  const int cl = ct_split(a, tiles, L.sw, g_ct_fill);
 #ifdef DQN_TC_TRACE
-  if (g_ct_stages == 3) return ct_launch<3>(st, a, tiles, cl);
+  if (g_ct_stages == 3) return ct_launch<64, 3, false>(st, a, dim3(tiles, cl, 1), "conv_tc_forward");
 #endif
-  return ct_launch<2>(st, a, tiles, cl);
+  return ct_launch<64, 2, false>(st, a, dim3(tiles, cl, 1), "conv_tc_forward");
+}
+
+// dX of a convolution whose filter tiles its stride (fh % S == 0), as one
+// GEMM per stride phase (blockIdx.z): 32 or 64 input channels, 64-channel dY
+bool conv_tc_dgrad_ok(const dqn_layer_desc &L) {
+  const int S = L.sw;
+  const int QH = (L.in_h + S - 1) / S, QW = (L.in_w + S - 1) / S;
+  return g_ct_dgrad && L.kind == DQN_LAYER_CONV && L.sh == S && S >= 1 && L.fh % S == 0 &&
+         L.fw % S == 0 && L.in_h % S == 0 && L.in_w % S == 0 && L.out_c % CT_BK == 0 &&
+         (L.in_c == 32 || L.in_c == 64) && QH * QW <= CT_BM && QW <= 256 && QH <= 256;
+}
+
+int conv_tc_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
+                  const float *mask, float *dx, int batch) {
+  if (!conv_tc_dgrad_ok(L)) return DQN_ERR_UNSUPPORTED;
+  const int S = L.sw;
+  const int QH = L.in_h / S, QW = L.in_w / S;
+  const int P = QH * QW;
+  const int ipt = std::max(1, std::min(CT_BM / P, std::min(batch, 256)));
+  ConvTcArgs a{};
+  if (!ct_dy_map(&a.amap, dy, L, batch, ipt, QH, QW) ||
+      !ct_wrows_map(&a.bmap, w, L.fh * L.fw * L.in_c, L.out_c, L.in_c))
+    return DQN_ERR_UNSUPPORTED;
+  a.TW = L.fw / S;
+  a.K = (L.fh / S) * a.TW * L.out_c;            // taps of one phase x dY channels
+  a.C = L.out_c;
+  a.fw = L.fw;
+  a.S = S;
+  a.P = P;
+  a.ipt = ipt;
+  a.npix = batch * P;
+  a.a_bytes = ((ipt * P + 7) / 8) * 8 * 128;
+  a.QW = QW;
+  a.H = L.in_h;
+  a.W = L.in_w;
+  a.cin = L.in_c;
+  a.mask = mask;
+  a.y = dx;
+  const int tiles = (batch + ipt - 1) / ipt;
+  const int cl = ct_split(a, tiles * S * S, S, g_ct_dfill);
+  const dim3 grid(tiles, cl, S * S);
+  return L.in_c == 32 ? ct_launch<32, 2, true>(st, a, grid, "conv_tc_dgrad")
+                      : ct_launch<64, 2, true>(st, a, grid, "conv_tc_dgrad");
 }
 
 }  // namespace dqn
@@ -449,4 +572,6 @@ int conv_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, co
 extern "C" void dqn_ct_set_cluster(int cl) { dqn::g_ct_cluster = cl; }
 extern "C" void dqn_ct_set_stages(int st) { dqn::g_ct_stages = st; }
 extern "C" void dqn_ct_set_fill(int f) { dqn::g_ct_fill = f; }
+extern "C" void dqn_ct_set_dgrad(int on) { dqn::g_ct_dgrad = on; }
+extern "C" void dqn_ct_set_dfill(int f) { dqn::g_ct_dfill = f; }
 #endif

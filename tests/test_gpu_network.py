@@ -251,3 +251,34 @@ def test_conv_tc_forward_layers(P, batch):
         err = (got - ref).norm() / ref.norm()
         assert err < 2e-6, (name, batch, float(err))
         assert float((got - ref).abs().max()) <= 1e-5 * float(ref.abs().max()) + 1e-7, name
+
+
+@pytest.mark.parametrize("batch", [1, 3, 32, 33, 130])
+def test_conv_tc_dgrad_layers(P, batch):
+    """conv2 / conv3 input gradients (conv_tc.cu dgrad: dY and W by TMA, one
+    GEMM per stride phase, taps off the dY grid zero-filled by the TMA) against
+    an fp64 transposed convolution of the same dY, masked by the layer
+    below's ReLU."""
+    import torch.nn.functional as F
+    from paper_1804_05834_b200 import synth
+    on = P.build_network("atari", (84, 84, 4), 4, True)
+    P.init_params(on, 6)
+    x8 = synth.frames(5, 0, np.arange(batch) * 3 + 1)
+    q = on.forward(torch.as_tensor(x8, device="cuda"))
+    g = np.random.default_rng(batch).standard_normal(tuple(q.shape)).astype(np.float32)
+    on.backward(g)
+    bind = on.binding(batch)
+    tens = dict(on.named_tensors())
+    shapes = [tuple(u["out_shape"]) for u in on._units]
+    for l, (name, fh, st) in enumerate([("conv2", 4, 2), ("conv3", 3, 1)], start=1):
+        h, w, c = shapes[l - 1]
+        oh, ow, n = shapes[l]
+        dy = bind.dact[l][: batch * oh * ow * n].view(batch, oh, ow, n).double().permute(0, 3, 1, 2)
+        W = tens[f"{name}.weight"].values.double().reshape(fh, fh, c, n).permute(3, 2, 0, 1)
+        ref = F.conv_transpose2d(dy, W, stride=st).permute(0, 2, 3, 1)
+        act = bind.act[l - 1][: batch * h * w * c].view(batch, h, w, c).double()
+        ref = ref * (act > 0)
+        got = bind.dact[l - 1][: batch * h * w * c].view(batch, h, w, c).double()
+        err = (got - ref).norm() / ref.norm()
+        assert err < 2e-6, (name, batch, float(err))
+        assert float((got - ref).abs().max()) <= 1e-5 * float(ref.abs().max()) + 1e-12, name

@@ -25,13 +25,17 @@ for B in (32, 64, 4096):
     x = torch.randint(0, 256, (B, 84, 84, 4), dtype=torch.uint8, device="cuda")
     net.forward_into(x, b)
     torch.cuda.synchronize()
-    for layer, name in ((1, "conv2"), (2, "conv3")):
+    for layer, name, phase in ((1, "conv2", 0), (2, "conv3", 0), (1, "conv2.dgrad", 1),
+                               (2, "conv3.dgrad", 1)):
         res = []
         for cl, stg in ((-1, 2), (0, 2), (0, 3), (1, 2), (2, 2), (4, 2), (8, 2)):
             _lib.lib.dqn_ct_set_cluster(cl)
             _lib.lib.dqn_ct_set_stages(stg)
+            _lib.lib.dqn_ct_set_dgrad(0 if cl < 0 else 1)
+            if phase == 1 and stg == 3:
+                continue
             args = (C.byref(net.desc_for(x)), net.flat_values.data_ptr(), net.flat_grads.data_ptr(),
-                    C.byref(b.struct), layer, 0, flags.data_ptr())
+                    C.byref(b.struct), layer, phase, flags.data_ptr())
             s = torch.cuda.Stream()
             with torch.cuda.stream(s):
                 for _ in range(3):
@@ -52,4 +56,5 @@ for B in (32, 64, 4096):
             us = e0.elapsed_time(e1) * 1e3 / (5 * REPS)
             res.append(f"{'engine' if cl < 0 else ('auto' if cl == 0 else f'cl{cl}')}/{stg} {us:.2f}")
         _lib.lib.dqn_ct_set_cluster(0)
+        _lib.lib.dqn_ct_set_dgrad(1)
         print(f"B={B} {name}: " + " | ".join(res), flush=True)

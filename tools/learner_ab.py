@@ -3,7 +3,7 @@ pre-drawn PER uniforms in HBM, one graph launch per update) under several
 settings of a library-side override, interleaved A/B/A/B so clock and
 placement drift average out.
 
-    python tools/learner_ab.py --ct=-1,0,2:3,0:2:192  # conv_tc cluster[:stages[:fill]]
+    python tools/learner_ab.py --ct=-1,0,2:3,0:2:192,0:2:128:0  # conv_tc cluster[:stages[:fill[:dgrad[:dgrad fill]]]]
                                                  # (-1 = generic engine, 0 = auto)
 Settings are applied before each (re)capture: launch configurations are baked
 into the graph.  Uses the product library; the override entry point is
@@ -35,7 +35,11 @@ def main():
 
     def apply(v):
         cl, _, rest = v.partition(":")
-        st, _, fill = rest.partition(":")
+        st, _, rest = rest.partition(":")
+        fill, _, rest = rest.partition(":")
+        dg, _, dfill = rest.partition(":")
+        _lib.lib.dqn_ct_set_dgrad(int(dg or 1))
+        _lib.lib.dqn_ct_set_dfill(int(dfill or 256))
         _lib.lib.dqn_ct_set_cluster(int(cl))
         _lib.lib.dqn_ct_set_stages(int(st or 2))
         _lib.lib.dqn_ct_set_fill(int(fill or 128))
@@ -51,7 +55,6 @@ def main():
     rng = np.random.default_rng(2)
     for s in range(4):
         P.learn_step(on, tg, mem, opt, cfg, 50_000 + s, rng)
-    plan = agent._plan_for(on, tg, mem, opt, cfg)
     k = 32
     draws = np.empty((a.steps, k + 1))
     for s in range(a.steps):
@@ -59,19 +62,22 @@ def main():
         draws[s, k] = mem.beta(50_200 + s)
     d_draws = torch.as_tensor(draws, device="cuda")
     slot = torch.zeros_like(d_draws[0])
-    saved = plan.h_in
     graphs = {}
     for v in settings:
         apply(v)
+        P.agent._PLANS.clear()
+        P.learn_step(on, tg, mem, opt, cfg, 50_100, rng)       # a plan of this setting
+        plan = agent._plan_for(on, tg, mem, opt, cfg)
+        saved = plan.h_in
         plan.h_in = slot
-        graphs[v] = agent.capture_graph(lambda: plan.enqueue(io=False), plan.capture_stream)
+        graphs[v] = (plan, agent.capture_graph(lambda: plan.enqueue(io=False), plan.capture_stream))
         plan.h_in = saved
     apply("0")
     sp = torch.cuda.current_stream().cuda_stream
     res = {v: [] for v in settings}
     for _ in range(a.rounds):
         for v in settings:
-            g = graphs[v][1]
+            g = graphs[v][1][1]
             for s in range(20):
                 slot.copy_(d_draws[s], non_blocking=True)
                 g.launch(sp)
@@ -85,7 +91,7 @@ def main():
             torch.cuda.synchronize()
             res[v].append(a.steps / (e0.elapsed_time(e1) / 1e3))
     for v in settings:
-        print(f"ct={v:>5}: " + " ".join(f"{x:7.0f}" for x in res[v]) +
+        print(f"{v:>8}: " + " ".join(f"{x:7.0f}" for x in res[v]) +
               f"  | median {np.median(res[v]):7.0f} updates/s", flush=True)
 
 
