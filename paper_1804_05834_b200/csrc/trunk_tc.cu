@@ -30,6 +30,8 @@ bool lin_tc_ok(const dqn_layer_desc &L, int batch);
 int lin_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, const float *params,
                    float *y, int batch);
 bool conv_tc_ok(const dqn_layer_desc &L);
+int conv1_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const uint8_t *x,
+                     const float *params, float *y, int batch);
 int conv_tc_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
                   const float *mask, float *dx, int batch);
 int conv_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, const float *params,
@@ -628,6 +630,12 @@ static int *counters_of(const dqn_binding *b) {
   return reinterpret_cast<int *>(b->scratch + b->scratch_floats - tc::kMaxTiles);
 }
 
+#ifdef DQN_TC_TRACE
+int g_c1_enabled = 1;   // diagnostic: 0 = conv1 forward on the generic engine
+#else
+constexpr int g_c1_enabled = 1;
+#endif
+
 int tc_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const float *params,
                      const dqn_binding *b) {
   const dqn_layer_desc &L = net->layer[l];
@@ -642,6 +650,11 @@ int tc_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const floa
   // fp32-input convolutions: both operands by TMA (conv_tc.cu)
   if (L.kind == DQN_LAYER_CONV && !(l == 0 && net->input_u8) && conv_tc_ok(L)) {
     const int rc = conv_tc_forward(st, L, (const float *)in, params, b->act[l], b->batch);
+    if (rc != DQN_ERR_UNSUPPORTED) return rc;
+  }
+  // the uint8 first convolution: frame slab + W by bulk copies (conv1_tc.cu)
+  if (l == 0 && net->input_u8 && g_c1_enabled) {
+    const int rc = conv1_tc_forward(st, L, (const uint8_t *)in, params, b->act[l], b->batch);
     if (rc != DQN_ERR_UNSUPPORTED) return rc;
   }
   if (l == 0 && net->input_u8)
@@ -694,5 +707,6 @@ extern "C" int dqn_tc_trace(unsigned long long *host, int max_ctas) {
   cudaMemcpyToSymbol(dqn::tc::g_trace_n, &zero, sizeof(zero));
   return (int)n;
 }
+extern "C" void dqn_c1_set(int on) { dqn::g_c1_enabled = on; }
 extern "C" void dqn_tc_skip(int mask) { cudaMemcpyToSymbol(dqn::tc::g_skip, &mask, sizeof(mask)); }
 #endif

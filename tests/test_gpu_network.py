@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from oracle import deepq_oracle as O
-from tests.helpers import rel_norm
+from tests.helpers import follow_device_relu_kinks, rel_norm
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -199,6 +199,8 @@ def test_conv1_wgrad_from_frames(P, batch):
     ref.forward(O.Ring.lift(x8))
     g = np.random.default_rng(batch).standard_normal(q.shape).astype(np.float32)
     on.backward(g)
+    # pre-activations within fp32 rounding of a ReLU kink take the device's side
+    follow_device_relu_kinks(ref, [a.cpu().numpy() for a in on.binding(batch).act])
     ref.backward(g)
     ref.wgrad()
     t1 = dict(on.named_tensors())
@@ -282,3 +284,26 @@ def test_conv_tc_dgrad_layers(P, batch):
         err = (got - ref).norm() / ref.norm()
         assert err < 2e-6, (name, batch, float(err))
         assert float((got - ref).abs().max()) <= 1e-5 * float(ref.abs().max()) + 1e-12, name
+
+
+@pytest.mark.parametrize("batch", [1, 2, 3, 33, 64, 130, 1024])
+def test_conv1_tc_forward(P, batch):
+    """conv1 forward from the uint8 frames (conv1_tc.cu: frame slab and W by
+    bulk copies, integer A, 1/255 on the sum) against an fp64 convolution of
+    the frames / 255."""
+    import torch.nn.functional as F
+    from paper_1804_05834_b200 import synth
+    on = P.build_network("atari", (84, 84, 4), 4, True)
+    P.init_params(on, 8)
+    tens = dict(on.named_tensors())
+    tens["conv1.bias"].values.copy_(torch.linspace(-0.05, 0.05, 32, device="cuda"))
+    x8 = torch.as_tensor(synth.frames(6, 1, np.arange(batch) * 5 + 2), device="cuda")
+    on.forward(x8)
+    bind = on.binding(batch)
+    xin = (x8.double() / 255.0).permute(0, 3, 1, 2)
+    W = tens["conv1.weight"].values.double().reshape(8, 8, 4, 32).permute(3, 2, 0, 1)
+    ref = F.relu(F.conv2d(xin, W, tens["conv1.bias"].values.double(), stride=4)).permute(0, 2, 3, 1)
+    got = bind.act[0][: batch * 20 * 20 * 32].view(batch, 20, 20, 32).double()
+    err = (got - ref).norm() / ref.norm()
+    assert err < 2e-6, (batch, float(err))
+    assert float((got - ref).abs().max()) <= 1e-5 * float(ref.abs().max()), batch

@@ -33,7 +33,18 @@ def main():
     a = ap.parse_args()
     settings = a.ct.split(",")
 
+    prio = {"v": None}
+
     def apply(v):
+        _lib.lib.dqn_c1_set(1)
+        if v.startswith("c1="):                # conv1 forward kernel on (1) / engine (0)
+            _lib.lib.dqn_c1_set(int(v[3:]))
+            v = "0"
+        elif v.startswith("p"):                # stream priorities: p<main>,<side>,<tree>
+            prio["v"] = [int(x) for x in v[1:].split("/")]
+            v = "0"
+        else:
+            prio["v"] = None
         cl, _, rest = v.partition(":")
         st, _, rest = rest.partition(":")
         fill, _, rest = rest.partition(":")
@@ -68,6 +79,11 @@ def main():
         P.agent._PLANS.clear()
         P.learn_step(on, tg, mem, opt, cfg, 50_100, rng)       # a plan of this setting
         plan = agent._plan_for(on, tg, mem, opt, cfg)
+        if prio["v"] is not None:
+            pm, ps, pt = prio["v"]
+            plan.capture_stream = torch.cuda.Stream(priority=pm)
+            plan.side = torch.cuda.Stream(priority=ps)
+            plan.tree_stream = torch.cuda.Stream(priority=pt)
         saved = plan.h_in
         plan.h_in = slot
         graphs[v] = (plan, agent.capture_graph(lambda: plan.enqueue(io=False), plan.capture_stream))
