@@ -113,17 +113,21 @@ def val(r, n):
 # eager launch order of one cfg4 update (agent._StepPlan.enqueue); the name
 # fragment checks the label against the captured kernel
 labels = [("sample+gather (batch 32)", "sample_gather"),
-          ("conv1.fwd (batch 32, target)", "FwdPol<unsigned char"),
-          ("conv2.fwd (batch 32, target)", "FwdPol<float"),
-          ("conv3.fwd (batch 32, target)", "FwdPol<float"),
+          ("conv1.fwd (batch 32, target)", ("conv1_tc", "FwdPol<unsigned char")),
+          ("conv2.fwd (batch 32, target)", ("conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
+          ("conv3.fwd (batch 32, target)", ("conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
           ("fc1.fwd (batch 32, target)", "lin_tc"),
-          ("conv1.fwd (batch 64)", "FwdPol<unsigned char"), ("conv2.fwd (batch 64)", "FwdPol<float"),
-          ("conv3.fwd (batch 64)", "FwdPol<float"), ("fc1.fwd (batch 64)", "lin_tc"),
+          ("conv1.fwd (batch 64)", ("conv1_tc", "FwdPol<unsigned char")),
+          ("conv2.fwd (batch 64)", ("conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
+          ("conv3.fwd (batch 64)", ("conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
+          ("fc1.fwd (batch 64)", "lin_tc"),
           ("duel.fwd+td (Q heads)", "head_q"), ("duel.dgrad+wgrad (TD block)", "head_td_bwd"),
           ("tree update (batch 32)", "tree_update"), ("fc1.wgrad (batch 32)", "lin_wgrad"),
           ("fc1.dgrad (batch 32)", "LinDgrad"), ("conv3.wgrad (batch 32)", "WgradPol<float"),
-          ("conv3.dgrad (batch 32)", "ConvDgradPol"), ("conv2.wgrad (batch 32)", "WgradPol<float"),
-          ("conv2.dgrad (batch 32)", "ConvDgradPol"), ("conv1.wgrad (batch 32)", "conv1_wgrad_u8"),
+          ("conv3.dgrad (batch 32)", ("conv_tc_kernel<64, 2, 1>", "ConvDgradPol")),
+          ("conv2.wgrad (batch 32)", "WgradPol<float"),
+          ("conv2.dgrad (batch 32)", ("conv_tc_kernel<32, 2, 1>", "ConvDgradPol")),
+          ("conv1.wgrad (batch 32)", "conv1_wgrad_u8"),
           ("rmsprop apply", "rms_apply")]
 L = [f"# {tag} — every kernel of one learner update, `ncu --set full`", "",
      "Command: `ncu --profile-from-start off --set full --import-source on --clock-control none "
@@ -136,7 +140,8 @@ traffic = {}
 for i, r in enumerate(data):
     name = clean(r[col["Kernel Name"]])
     lab, frag = labels[i] if i < len(labels) else (f"kernel {i}", "")
-    if frag and frag not in name:
+    frags = frag if isinstance(frag, tuple) else (frag,)
+    if frag and not any(f in name for f in frags):
         lab = f"kernel {i}"
     dr = val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")
     traffic[lab] = {"dram_bytes": dr, "kernel": name, "us_ncu": val(r, "gpu__time_duration.sum")}
