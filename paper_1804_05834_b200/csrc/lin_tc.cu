@@ -426,6 +426,18 @@ inline int lt_rows(int nb) { return nb <= 16 ? 16 : (nb <= 32 ? 32 : 64); }
 
 }  // namespace
 
+// K-split cluster sizes: 16 CTAs above batch 32 (the learner's online [s; s']
+// forward, on the critical path), 4 at batch <= 32 (its target forward, which
+// runs beside it: 16-CTA clusters there tie up whole GPCs the online launch
+// then waits for).  Measured in the learner graph (cfg4): small / big =
+// 16/16 6,676, 8/16 6,961, 4/16 6,989-7,003, 2/16 6,481, 1/16 5,370,
+// 8/8 6,857, 4/8 6,858, 16/8 6,856, 12/16 6,713 updates/s (trace build).
+#ifdef DQN_TC_TRACE
+int g_lt_cl_small = 4, g_lt_cl_big = 16;     // diagnostic overrides
+#else
+constexpr int g_lt_cl_small = 4, g_lt_cl_big = 16;
+#endif
+
 // hidden linear layer at learner batch sizes (<= 64 rows), weights rows >= 128
 bool lin_tc_ok(const dqn_layer_desc &L, int batch) {
   const int F = L.in_h * L.in_w * L.in_c;
@@ -449,15 +461,19 @@ int lin_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, con
   a.bias = params + L.b_off;
   a.relu = L.relu;
   a.out = y;
-  // K split over a 16-CTA cluster: 4 weight tiles x 16 = 64 CTAs for fc1
-  // (measured: 8-CTA clusters 15.6 us, 16-CTA 11.0 us at batch 64)
-  return lt_run<true>(st, a, nb, 16, "lin_tc_forward");
+  // K split over a cluster: 4 weight tiles x 16 = 64 CTAs for fc1 at batch 64
+  // (measured alone: 8-CTA clusters 15.6 us, 16-CTA 11.0 us)
+  return lt_run<true>(st, a, nb, batch <= 32 ? g_lt_cl_small : g_lt_cl_big, "lin_tc_forward");
 }
 
 }  // namespace dqn
 
 
 #ifdef DQN_TC_TRACE
+extern "C" void dqn_lt_set_cluster(int small, int big) {
+  dqn::g_lt_cl_small = small;
+  dqn::g_lt_cl_big = big;
+}
 extern "C" int dqn_lt_trace(unsigned long long *host) {
   return (int)cudaMemcpyFromSymbol(host, dqn::g_lt_trace, sizeof(dqn::g_lt_trace));
 }

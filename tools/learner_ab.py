@@ -37,6 +37,11 @@ def main():
 
     def apply(v):
         _lib.lib.dqn_c1_set(1)
+        _lib.lib.dqn_lt_set_cluster(4, 16)
+        if v.startswith("lt="):                # fc1 forward cluster sizes: lt=<b<=32>/<b>32>
+            a_, b_ = v[3:].split("/")
+            _lib.lib.dqn_lt_set_cluster(int(a_), int(b_))
+            v = "0"
         if v.startswith("c1="):                # conv1 forward kernel on (1) / engine (0)
             _lib.lib.dqn_c1_set(int(v[3:]))
             v = "0"
