@@ -951,7 +951,15 @@ inline int smem_bytes() {
 // Split-K across thread-block clusters (measured in the learner graph: 6,788
 // vs 6,759 updates/s device, +1-2 % end to end).  Same reduction order as
 // the global fixup: identical results.
+#ifdef DQN_TC_TRACE
+inline int &cluster_splitk_override() {   // diagnostic: 1 on, 0 off
+  static int v = 1;
+  return v;
+}
+inline bool cluster_splitk_enabled() { return cluster_splitk_override() != 0; }
+#else
 inline bool cluster_splitk_enabled() { return true; }
+#endif
 
 // split-K reducers per launch (fewer measured -1 to -6 %)
 inline int reducer_budget() { return 60; }

@@ -329,7 +329,11 @@ struct WgradPol : tc::PolBase {
 };
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+#ifdef DQN_TC_TRACE
+int kDgradCap = 16;                 // diagnostic override
+#else
 constexpr int kDgradCap = 16;       // linear dgrad split cap (measured best in the learner)
+#endif
 
 // ------------------------------------------------------------ host helpers
 bool conv_ok(const dqn_layer_desc &L) {
@@ -708,5 +712,7 @@ extern "C" int dqn_tc_trace(unsigned long long *host, int max_ctas) {
   return (int)n;
 }
 extern "C" void dqn_c1_set(int on) { dqn::g_c1_enabled = on; }
+extern "C" void dqn_tc_set_dgrad_cap(int c) { dqn::kDgradCap = c; }
+extern "C" void dqn_tc_set_cluster_splitk(int on) { dqn::tc::cluster_splitk_override() = on; }
 extern "C" void dqn_tc_skip(int mask) { cudaMemcpyToSymbol(dqn::tc::g_skip, &mask, sizeof(mask)); }
 #endif

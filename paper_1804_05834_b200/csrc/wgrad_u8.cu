@@ -426,6 +426,12 @@ bool conv1_wgrad_u8_ok(const dqn_net_desc *net) {
   return w1_smem(L, (PP + 7) / 8 * 8, img_smem) <= 200 * 1024;
 }
 
+#ifdef DQN_TC_TRACE
+int g_w1_cl_max = 8;   // diagnostic: largest cluster
+#else
+constexpr int g_w1_cl_max = 8;
+#endif
+
 int64_t conv1_wgrad_u8_scratch(const dqn_net_desc *net, int batch) {
   const dqn_layer_desc &L = net->layer[0];
   const int R = L.fh * L.fw * L.in_c;
@@ -461,7 +467,7 @@ int conv1_wgrad_u8_tc(cudaStream_t st, const dqn_net_desc *net, const uint8_t *x
   const int ctas = a.units <= 128 ? a.units : 128;
   a.cl = 1;
   for (int c : {8, 4, 2})                   // 8-CTA clusters measured best (vs 1, 2, 4)
-    if (ctas % c == 0 && a.R % c == 0) { a.cl = c; break; }
+    if (c <= g_w1_cl_max && ctas % c == 0 && a.R % c == 0) { a.cl = c; break; }
   a.nclusters = ctas / a.cl;
   const int smem = w1_smem(L, a.PP8, a.img_smem);
   const int MT = a.R / 128;
@@ -474,6 +480,7 @@ int conv1_wgrad_u8_tc(cudaStream_t st, const dqn_net_desc *net, const uint8_t *x
 
 #ifdef DQN_TC_TRACE
 extern "C" void dqn_w1_skip(int m) { cudaMemcpyToSymbol(dqn::g_w1_skip, &m, sizeof(m)); }
+extern "C" void dqn_w1_set_cluster_max(int c) { dqn::g_w1_cl_max = c; }
 extern "C" int dqn_w1_trace(unsigned long long *host) {
   return (int)cudaMemcpyFromSymbol(host, dqn::g_w1_trace, sizeof(dqn::g_w1_trace));
 }

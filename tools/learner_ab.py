@@ -38,6 +38,18 @@ def main():
     def apply(v):
         _lib.lib.dqn_c1_set(1)
         _lib.lib.dqn_lt_set_cluster(4, 16)
+        _lib.lib.dqn_tc_set_cluster_splitk(1)
+        _lib.lib.dqn_w1_set_cluster_max(8)
+        _lib.lib.dqn_tc_set_dgrad_cap(16)
+        if v.startswith("dcap="):              # linear dgrad split cap
+            _lib.lib.dqn_tc_set_dgrad_cap(int(v[5:]))
+            v = "0"
+        if v.startswith("w1cl="):              # conv1 wgrad: largest cluster
+            _lib.lib.dqn_w1_set_cluster_max(int(v[5:]))
+            v = "0"
+        if v == "nocks":                       # engine split-K through global partials only
+            _lib.lib.dqn_tc_set_cluster_splitk(0)
+            v = "0"
         if v.startswith("lt="):                # fc1 forward cluster sizes: lt=<b<=32>/<b>32>
             a_, b_ = v[3:].split("/")
             _lib.lib.dqn_lt_set_cluster(int(a_), int(b_))
