@@ -50,7 +50,7 @@ typedef enum {
 #define DQN_FLAG_BAD_PRIORITY   0x10 /* SumTree.set with negative / non-finite value */
 
 const char *dqn_last_error(void);
-int dqn_abi_version(void);             /* 4 */
+int dqn_abi_version(void);             /* 5 */
 /* 1 if this library was built with the tcgen05 (sm_100a UMMA) conv trunk */
 int dqn_has_tcgen05(void);
 /* kernels launched (or captured) through this library so far, all threads */
@@ -125,11 +125,17 @@ typedef struct {
   int64_t w2_off, b2_off;  /* dueling: advantage branch */
 } dqn_layer_desc;
 
+/* dqn_net_desc.hints: this network's forward runs beside another one that is
+ * on the critical path (the learner's target trunk beside its online trunk):
+ * its launches take fewer SMs (smaller K splits / clusters).  Results differ
+ * from the unhinted forward only by fp32 summation order. */
+#define DQN_NET_HINT_SIDE 1
+
 typedef struct {
   int32_t n_layers;
   int32_t input_u8;        /* 1: input bytes x = f32(u8)/255 (envs.py:300-311); 0: float32 */
   int32_t algo;            /* 0: auto (tcgen05 trunk when the geometry has a kernel), 1: SIMT only */
-  int32_t reserved;
+  int32_t hints;           /* DQN_NET_HINT_*: launch shapes only, never the formulas */
   dqn_layer_desc layer[DQN_MAX_LAYERS];
 } dqn_net_desc;
 

@@ -25,6 +25,7 @@ lib = C.CDLL(str(LIB_PATH))
 # status codes / flags (dqn_b200.h)
 OK, ERR_INVALID_ARG, ERR_GEOMETRY, ERR_INDEX, ERR_EMPTY, ERR_ZERO_TOTAL, ERR_NONFINITE, \
     ERR_CUDA, ERR_UNSUPPORTED = range(9)
+NET_HINT_SIDE = 1          # dqn_net_desc.hints (include/dqn_b200.h)
 FLAG_INDEX, FLAG_ZERO_TOTAL, FLAG_NONFINITE_GRAD, FLAG_NONFINITE_OUT, FLAG_BAD_PRIORITY = \
     0x1, 0x2, 0x4, 0x8, 0x10
 TD_DOUBLE, TD_HUBER, TD_REWARD_CLIP, TD_HEAD_LAST_CTA = 0x1, 0x2, 0x4, 0x8
@@ -42,7 +43,7 @@ class LayerDesc(C.Structure):
 
 
 class NetDesc(C.Structure):
-    _fields_ = [("n_layers", i32), ("input_u8", i32), ("algo", i32), ("reserved", i32),
+    _fields_ = [("n_layers", i32), ("input_u8", i32), ("algo", i32), ("hints", i32),
                 ("layer", LayerDesc * MAX_LAYERS)]
 
 

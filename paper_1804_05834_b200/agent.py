@@ -140,6 +140,10 @@ class _StepPlan:
         # gets a view with its own scratch (split-K partials and counters)
         self.on_wview = online.prefix_binding(self.on_bind, k, own_scratch=True)
         self.tg_bind = target.binding(k)
+        # the target trunk (k rows) beside the online one on [s; s'] (2k rows,
+        # the critical path): leaner launches for it.  Without Double DQN the
+        # two trunks are the same size and share the GPU evenly.
+        self.tg_desc = target.hinted(self.x, _lib.NET_HINT_SIDE) if self.double else None
         # the Q heads, TD block, head backward and head wgrad run as one fused
         # launch (dqn_head_td) when the head fits it (nA <= 18, batch <= 1024)
         units = online._units
@@ -248,11 +252,11 @@ class _StepPlan:
         e_in.record(s0)
         upto = self.head_layer if self.fused_head else None
 
-        def forward(net, x, bind):
-            net.forward_into(x, bind, upto=upto)
+        def forward(net, x, bind, desc=None):
+            net.forward_into(x, bind, upto=upto, desc=desc)
         with torch.cuda.stream(s1):
             s1.wait_event(e_in)
-            forward(tg, self.x[k:], self.tg_bind)
+            forward(tg, self.x[k:], self.tg_bind, self.tg_desc)
             e_tg = ev()
             e_tg.record(s1)
         forward(on, self.x if self.double else self.x[:k], self.on_bind)

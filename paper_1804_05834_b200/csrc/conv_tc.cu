@@ -423,18 +423,22 @@ bool ct_wrows_map(CUtensorMap *m, const float *w, int rows, int N, int box_rows)
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// CTAs one launch aims for: K split = ceil(fill / tiles), so the target's
-// batch-32 launches split K further than the online batch-64 ones (measured
-// in the learner: fill 64 / 96 / 128 / 160 / 256 -> 128 best; fixed splits
-// per layer 6-10 % slower)
+// CTAs one forward launch aims for: K split = ceil(fill / tiles).  128, and
+// 64 for a side trunk (DQN_NET_HINT_SIDE: the learner's target trunk beside
+// its online one).  Measured in the learner: one fill for both 64 /
+// 96 / 128 / 160 / 256 -> 128 best; fixed splits per layer 6-10 % slower;
+// with the online at 128, target fills 32 / 48 / 64 / 80 / 96 / 128 / 192 ->
+// 6,579 / 7,094 / 7,103-7,118 / 7,074 / 7,005 / 7,050 / 7,018 updates/s.
 #ifdef DQN_TC_TRACE
 int g_ct_cluster = 0;   // diagnostic: 0 auto, > 0 cluster size, -1 engine, -2/-3 one layer only
 int g_ct_stages = 2;    // diagnostic: pipeline stages (2 or 3; 3 measured slower)
 int g_ct_fill = 128;
+int g_ct_fill_small = 64;    // diagnostic: fill of a side trunk (DQN_NET_HINT_SIDE)
 int g_ct_dgrad = 1;     // diagnostic: 0 = conv dgrad on the generic engine
 int g_ct_dfill = 256;   // dgrad: CTAs one launch aims for
 #else
 constexpr int g_ct_cluster = 0, g_ct_stages = 2, g_ct_fill = 128, g_ct_dgrad = 1, g_ct_dfill = 256;
+constexpr int g_ct_fill_small = 64;
 #endif
 
 template <int NB, int ST, bool DG>
@@ -494,7 +498,7 @@ bool conv_tc_ok(const dqn_layer_desc &L) {
 }
 
 int conv_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, const float *params,
-                    float *y, int batch) {
+                    float *y, int batch, bool side) {
   if (g_ct_cluster == -1 || (g_ct_cluster == -2 && L.sw != 2) || (g_ct_cluster == -3 && L.sw != 1))
     return DQN_ERR_UNSUPPORTED;   // diagnostic: the generic engine (all / all but stride 2 / 1)
   const int P = L.out_h * L.out_w;
@@ -515,7 +519,7 @@ int conv_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, co
   a.relu = L.relu;
   a.y = y;
   const int tiles = (batch + ipt - 1) / ipt;
-  const int cl = ct_split(a, tiles, L.sw, g_ct_fill);
+  const int cl = ct_split(a, tiles, L.sw, side ? g_ct_fill_small : g_ct_fill);
 #ifdef DQN_TC_TRACE
   if (g_ct_stages == 3) return ct_launch<64, 3, false>(st, a, dim3(tiles, cl, 1), "conv_tc_forward");
 #endif
@@ -572,6 +576,7 @@ int conv_tc_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, con
 extern "C" void dqn_ct_set_cluster(int cl) { dqn::g_ct_cluster = cl; }
 extern "C" void dqn_ct_set_stages(int st) { dqn::g_ct_stages = st; }
 extern "C" void dqn_ct_set_fill(int f) { dqn::g_ct_fill = f; }
+extern "C" void dqn_ct_set_fill_small(int f) { dqn::g_ct_fill_small = f; }
 extern "C" void dqn_ct_set_dgrad(int on) { dqn::g_ct_dgrad = on; }
 extern "C" void dqn_ct_set_dfill(int f) { dqn::g_ct_dfill = f; }
 #endif

@@ -426,9 +426,9 @@ inline int lt_rows(int nb) { return nb <= 16 ? 16 : (nb <= 32 ? 32 : 64); }
 
 }  // namespace
 
-// K-split cluster sizes: 16 CTAs above batch 32 (the learner's online [s; s']
-// forward, on the critical path), 4 at batch <= 32 (its target forward, which
-// runs beside it: 16-CTA clusters there tie up whole GPCs the online launch
+// K-split cluster sizes: 16 CTAs, and 4 for a side trunk (DQN_NET_HINT_SIDE:
+// the learner's target forward, which runs beside the online one on the
+// critical path -- 16-CTA clusters there tie up whole GPCs the online launch
 // then waits for).  Measured in the learner graph (cfg4): small / big =
 // 16/16 6,676, 8/16 6,961, 4/16 6,989-7,003, 2/16 6,481, 1/16 5,370,
 // 8/8 6,857, 4/8 6,858, 16/8 6,856, 12/16 6,713 updates/s (trace build).
@@ -448,7 +448,7 @@ bool lin_tc_ok(const dqn_layer_desc &L, int batch) {
 // y [batch][N] = act(x [batch][F] W[F][N] + b): the weights tile read as
 // [32 k][128 n] and transposed into the K-major A operand in shared memory
 int lin_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, const float *params,
-                   float *y, int batch) {
+                   float *y, int batch, bool side) {
   const int F = L.in_h * L.in_w * L.in_c, N = L.out_c;
   const int nb = lt_rows(batch);
   LinTcArgs a{};
@@ -463,7 +463,7 @@ int lin_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, con
   a.out = y;
   // K split over a cluster: 4 weight tiles x 16 = 64 CTAs for fc1 at batch 64
   // (measured alone: 8-CTA clusters 15.6 us, 16-CTA 11.0 us)
-  return lt_run<true>(st, a, nb, batch <= 32 ? g_lt_cl_small : g_lt_cl_big, "lin_tc_forward");
+  return lt_run<true>(st, a, nb, side ? g_lt_cl_small : g_lt_cl_big, "lin_tc_forward");
 }
 
 }  // namespace dqn

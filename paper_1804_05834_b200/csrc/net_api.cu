@@ -114,7 +114,7 @@ void set_error(const char *fmt, ...) {
 using namespace dqn;
 
 extern "C" const char *dqn_last_error(void) { return g_err; }
-extern "C" int dqn_abi_version(void) { return 4; }
+extern "C" int dqn_abi_version(void) { return 5; }
 extern "C" int dqn_has_tcgen05(void) { return 1; }
 extern "C" int64_t dqn_launch_count(void) { return g_launches.load(); }
 

@@ -28,14 +28,14 @@ bool conv1_wgrad_u8_ok(const dqn_net_desc *net);
 int64_t conv1_wgrad_u8_scratch(const dqn_net_desc *net, int batch);
 bool lin_tc_ok(const dqn_layer_desc &L, int batch);
 int lin_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, const float *params,
-                   float *y, int batch);
+                   float *y, int batch, bool side);
 bool conv_tc_ok(const dqn_layer_desc &L);
 int conv1_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const uint8_t *x,
                      const float *params, float *y, int batch);
 int conv_tc_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
                   const float *mask, float *dx, int batch);
 int conv_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, const float *params,
-                    float *y, int batch);
+                    float *y, int batch, bool side);
 
 namespace {
 
@@ -648,12 +648,14 @@ int tc_layer_forward(cudaStream_t st, const dqn_net_desc *net, int l, const floa
   // kernel (lin_tc.cu; measured +0.3 % in the learner -- its dgrad form was
   // slower than the engine's LinDgradTmaPol there and is not used)
   if (L.kind == DQN_LAYER_LINEAR && l > 0 && lin_tc_ok(L, b->batch)) {
-    const int rc = lin_tc_forward(st, L, (const float *)in, params, b->act[l], b->batch);
+    const int rc = lin_tc_forward(st, L, (const float *)in, params, b->act[l], b->batch,
+                                  (net->hints & DQN_NET_HINT_SIDE) != 0);
     if (rc != DQN_ERR_UNSUPPORTED) return rc;
   }
   // fp32-input convolutions: both operands by TMA (conv_tc.cu)
   if (L.kind == DQN_LAYER_CONV && !(l == 0 && net->input_u8) && conv_tc_ok(L)) {
-    const int rc = conv_tc_forward(st, L, (const float *)in, params, b->act[l], b->batch);
+    const int rc = conv_tc_forward(st, L, (const float *)in, params, b->act[l], b->batch,
+                                   (net->hints & DQN_NET_HINT_SIDE) != 0);
     if (rc != DQN_ERR_UNSUPPORTED) return rc;
   }
   // the uint8 first convolution: frame slab + W by bulk copies (conv1_tc.cu)

@@ -290,17 +290,25 @@ class Network:
             self._views[key] = v
         return v
 
-    def layer_into(self, bind: _Bind, layer: int, phase: int, flags=None) -> None:
+    def layer_into(self, bind: _Bind, layer: int, phase: int, flags=None, desc=None) -> None:
         """One phase (0 fwd, 1 bwd to the layer's input, 2 wgrad) of one layer;
         ``flags`` (default: the network's) receives non-finite outputs and,
-        for wgrad, non-finite gradients as they are written."""
-        _lib.call("dqn_net_layer", _lib.stream_ptr(), C.byref(self.desc_for(bind.x)),
+        for wgrad, non-finite gradients as they are written.  ``desc``: a
+        copy of this network's descriptor with launch hints (``hinted``)."""
+        _lib.call("dqn_net_layer", _lib.stream_ptr(), C.byref(desc or self.desc_for(bind.x)),
                   self.flat_values.data_ptr(), self.flat_grads.data_ptr(), C.byref(bind.struct),
                   layer, phase, (self._flags if flags is None else flags).data_ptr())
 
     def desc_for(self, x):
         import torch
         return self._desc_u8 if x.dtype == torch.uint8 else self._desc
+
+    def hinted(self, x, hints: int):
+        """A copy of the descriptor for inputs like ``x`` with launch hints
+        (``_lib.NET_HINT_SIDE``: this forward runs beside a critical one)."""
+        d = _lib.NetDesc.from_buffer_copy(self.desc_for(x))
+        d.hints = int(hints)
+        return d
 
     # -- phases (network.py:90-126) --------------------------------------------
     def _input(self, values):
@@ -319,19 +327,21 @@ class Network:
             raise GeometryError(f"input shape {tuple(x.shape[1:])} != network input {self.input_shape}")
         return x.contiguous()
 
-    def forward_into(self, x, bind: _Bind, upto: int | None = None, flags=None) -> None:
+    def forward_into(self, x, bind: _Bind, upto: int | None = None, flags=None,
+                     desc=None) -> None:
         """Enqueue the forward phase for a prepared device input (no sync);
         ``upto`` stops before that layer (the learner's fused head takes over);
-        ``flags`` (default: the network's) receives non-finite outputs."""
+        ``flags`` (default: the network's) receives non-finite outputs;
+        ``desc``: a hinted descriptor copy (``hinted``)."""
         bind.x = x
         bind.struct.x = x.data_ptr()
         fl = self._flags if flags is None else flags
         if upto is None:
-            _lib.call("dqn_net_forward", _lib.stream_ptr(), C.byref(self.desc_for(x)),
+            _lib.call("dqn_net_forward", _lib.stream_ptr(), C.byref(desc or self.desc_for(x)),
                       self.flat_values.data_ptr(), C.byref(bind.struct), fl.data_ptr())
             return
         for layer in range(upto):
-            self.layer_into(bind, layer, 0, fl)
+            self.layer_into(bind, layer, 0, fl, desc=desc)
 
     def check_output(self) -> None:
         f = int(self._flags.item())

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in declared_symbols() if not hasattr(lib, s)]
     assert not missing, missing
     assert set(declared_symbols()) == set(_lib.EXPORTED)
-    assert lib.dqn_abi_version() == 4
+    assert lib.dqn_abi_version() == 5
 
 
 def test_struct_layouts_match_header():

@@ -307,3 +307,22 @@ def test_conv1_tc_forward(P, batch):
     err = (got - ref).norm() / ref.norm()
     assert err < 2e-6, (batch, float(err))
     assert float((got - ref).abs().max()) <= 1e-5 * float(ref.abs().max()), batch
+
+
+def test_side_hint_changes_only_the_launch_shapes(P):
+    """dqn_net_desc.hints = DQN_NET_HINT_SIDE (the learner's target trunk):
+    smaller K splits / clusters, so the same outputs up to fp32 summation
+    order, and bit-identical from run to run."""
+    from paper_1804_05834_b200 import _lib, synth
+    net = P.build_network("atari", (84, 84, 4), 4, True)
+    P.init_params(net, 4)
+    x = torch.as_tensor(synth.frames(2, 1, np.arange(32)), device="cuda")
+    bind = net.binding(32)
+    outs = []
+    for desc in (None, net.hinted(x, _lib.NET_HINT_SIDE), net.hinted(x, _lib.NET_HINT_SIDE)):
+        net.forward_into(x, bind, desc=desc)
+        torch.cuda.synchronize()
+        outs.append([a.clone() for a in bind.act])
+    for l in range(len(outs[0])):
+        assert torch.equal(outs[1][l], outs[2][l]), l
+        assert float((outs[1][l] - outs[0][l]).norm() / outs[0][l].norm()) < 1e-6, l

@@ -41,6 +41,11 @@ def main():
         _lib.lib.dqn_tc_set_cluster_splitk(1)
         _lib.lib.dqn_w1_set_cluster_max(8)
         _lib.lib.dqn_tc_set_dgrad_cap(16)
+        _lib.lib.dqn_ct_set_fill_small(64)
+        if v.startswith("fs="):                # conv_tc fill: fs=<batch <= 32>[/<above>]
+            fs_, _, fb_ = v[3:].partition("/")
+            _lib.lib.dqn_ct_set_fill_small(int(fs_))
+            v = "0:2:" + (fb_ or "128")
         if v.startswith("dcap="):              # linear dgrad split cap
             _lib.lib.dqn_tc_set_dgrad_cap(int(v[5:]))
             v = "0"
