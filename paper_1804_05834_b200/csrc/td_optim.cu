@@ -198,6 +198,13 @@ extern "C" int dqn_rmsprop_step(void *stream, float *w, float *g, float *acc, in
 // The apply kernel alone: for gradients whose producers flagged non-finite
 // values as they wrote them (dqn_net_layer phase 2 with flags, dqn_head_td);
 // the step is skipped on any error flag exactly as in dqn_rmsprop_step.
+#ifdef DQN_TC_TRACE
+int g_rms_cap = 148 * 8;
+extern "C" void dqn_rms_set_cap(int c) { g_rms_cap = c; }
+#else
+constexpr int g_rms_cap = 148 * 8;
+#endif
+
 extern "C" int dqn_rmsprop_apply(void *stream, float *w, float *g, float *acc, int64_t n,
                                  float lr, float rho, float one_minus_rho, float eps,
                                  int32_t *flags, int32_t *flag_out) {
@@ -205,7 +212,7 @@ extern "C" int dqn_rmsprop_apply(void *stream, float *w, float *g, float *acc, i
   DQN_CHECK_ARG(((uintptr_t)w | (uintptr_t)g | (uintptr_t)acc) % 16 == 0,
                 "rmsprop: buffers must be 16-byte aligned");
   if (n == 0) return DQN_OK;
-  constexpr int cap = 148 * 8;                          // measured best in the learner graph
+  const int cap = g_rms_cap;                            // measured best in the learner graph
   const int blocks4 = (int)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, cap));
   launch_k(rms_apply_kernel, blocks4, 256, 0, as_stream(stream), w, g, acc, n, lr, rho,
            one_minus_rho, eps, flags, flag_out);

@@ -42,6 +42,10 @@ def main():
         _lib.lib.dqn_w1_set_cluster_max(8)
         _lib.lib.dqn_tc_set_dgrad_cap(16)
         _lib.lib.dqn_ct_set_fill_small(64)
+        _lib.lib.dqn_rms_set_cap(148 * 8)
+        if v.startswith("rms="):               # optimizer grid cap
+            _lib.lib.dqn_rms_set_cap(int(v[4:]))
+            v = "0"
         if v.startswith("fs="):                # conv_tc fill: fs=<batch <= 32>[/<above>]
             fs_, _, fb_ = v[3:].partition("/")
             _lib.lib.dqn_ct_set_fill_small(int(fs_))
