@@ -329,10 +329,15 @@ struct WgradPol : tc::PolBase {
 };
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+#ifndef DQN_WGRAD_CAP
+#define DQN_WGRAD_CAP 8
+#endif
 #ifdef DQN_TC_TRACE
 int kDgradCap = 16;                 // diagnostic override
+int kWgradCap = DQN_WGRAD_CAP;      // diagnostic override
 #else
 constexpr int kDgradCap = 16;       // linear dgrad split cap (measured best in the learner)
+constexpr int kWgradCap = DQN_WGRAD_CAP;   // fp32 conv wgrad split cap at learner sizes
 #endif
 
 // ------------------------------------------------------------ host helpers
@@ -541,10 +546,13 @@ inline void wgrad_split(int M, int N, int K, int bn, bool u8, int &klen, int &sp
   // learner-sized reductions (K <= 64k pixels): the wgrads run beside the
   // dgrad chain, and the model's count for one launch alone (conv3: 25
   // one-block splits over 125 CTAs) takes the SMs the chain needs.  Measured
-  // in the learner's graph (cfg4, batch 32, with conv1's wgrad from the
-  // frames): caps 4 / 8 / 12 / 16 / 128 -> 8 best (+3 % updates/s over 128).
+  // in the learner's graph (cfg4, batch 32): round 2 with the register-fed
+  // forward, caps 4 / 8 / 12 / 16 / 128 -> 8 best.  With the TMA-fed conv
+  // kernels the trace build preferred 12 (+1.7 %), but two product builds
+  // (cap 8 vs 12, bench.py interleaved three times) gave 7,531-7,542 vs
+  // 7,521-7,526: the trace build's engine marks bias engine-side A/Bs.
   // Large batches (K > 64k) keep the model's count.
-  const int cap = K <= 65536 ? (u8 ? 32 : 8) : 128;
+  const int cap = K <= 65536 ? (u8 ? 32 : kWgradCap) : 128;
   split_k(ceil_div(M, tc::BM) * ceil_div(N, bn), K, bn, cap, klen, splits);
 }
 
@@ -715,6 +723,7 @@ extern "C" int dqn_tc_trace(unsigned long long *host, int max_ctas) {
 }
 extern "C" void dqn_c1_set(int on) { dqn::g_c1_enabled = on; }
 extern "C" void dqn_tc_set_dgrad_cap(int c) { dqn::kDgradCap = c; }
+extern "C" void dqn_tc_set_wgrad_cap(int c) { dqn::kWgradCap = c; }
 extern "C" void dqn_tc_set_cluster_splitk(int on) { dqn::tc::cluster_splitk_override() = on; }
 extern "C" void dqn_tc_skip(int mask) { cudaMemcpyToSymbol(dqn::tc::g_skip, &mask, sizeof(mask)); }
 #endif

@@ -6,8 +6,9 @@ placement drift average out.
     python tools/learner_ab.py --ct=-1,0,2:3,0:2:192,0:2:128:0  # conv_tc cluster[:stages[:fill[:dgrad[:dgrad fill]]]]
                                                  # (-1 = generic engine, 0 = auto)
 Settings are applied before each (re)capture: launch configurations are baked
-into the graph.  Uses the product library; the override entry point is
-diagnostic only.
+into the graph.  Uses the trace build (the overrides exist only there); its
+tcgen05-engine time marks slow the engine kernels a little, so confirm an
+engine-side winner with two product builds and bench.py.
 """
 import argparse
 import os
@@ -41,6 +42,10 @@ def main():
         _lib.lib.dqn_tc_set_cluster_splitk(1)
         _lib.lib.dqn_w1_set_cluster_max(8)
         _lib.lib.dqn_tc_set_dgrad_cap(16)
+        _lib.lib.dqn_tc_set_wgrad_cap(8)
+        if v.startswith("wcap="):              # fp32 conv wgrad split cap
+            _lib.lib.dqn_tc_set_wgrad_cap(int(v[5:]))
+            v = "0"
         _lib.lib.dqn_ct_set_fill_small(64)
         _lib.lib.dqn_rms_set_cap(148 * 8)
         if v.startswith("rms="):               # optimizer grid cap
