@@ -6,7 +6,9 @@ placement drift average out.
     python tools/learner_ab.py --ct=-1,0,2:3,0:2:192,0:2:128:0  # conv_tc cluster[:stages[:fill[:dgrad[:dgrad fill]]]]
                                                  # (-1 = generic engine, 0 = auto)
 Settings are applied before each (re)capture: launch configurations are baked
-into the graph.  Uses the trace build (the overrides exist only there); its
+into the graph.  Uses the trace build by default (the overrides exist only
+there; with DQN_B200_LIB pointing at the product library the overrides are
+skipped and only Python-side switches apply); its
 tcgen05-engine time marks slow the engine kernels a little, so confirm an
 engine-side winner with two product builds and bench.py.
 """
@@ -36,40 +38,45 @@ def main():
 
     prio = {"v": None}
 
+    def _set(name, *vals):
+        fn = getattr(_lib.lib, name, None)       # trace-build entry points only
+        if fn is not None:
+            fn(*vals)
+
     def apply(v):
-        _lib.lib.dqn_c1_set(1)
-        _lib.lib.dqn_lt_set_cluster(4, 16)
-        _lib.lib.dqn_tc_set_cluster_splitk(1)
-        _lib.lib.dqn_w1_set_cluster_max(8)
-        _lib.lib.dqn_tc_set_dgrad_cap(16)
-        _lib.lib.dqn_tc_set_wgrad_cap(8)
+        _set("dqn_c1_set", 1)
+        _set("dqn_lt_set_cluster", 4, 16)
+        _set("dqn_tc_set_cluster_splitk", 1)
+        _set("dqn_w1_set_cluster_max", 8)
+        _set("dqn_tc_set_dgrad_cap", 16)
+        _set("dqn_tc_set_wgrad_cap", 8)
         if v.startswith("wcap="):              # fp32 conv wgrad split cap
-            _lib.lib.dqn_tc_set_wgrad_cap(int(v[5:]))
+            _set("dqn_tc_set_wgrad_cap", int(v[5:]))
             v = "0"
-        _lib.lib.dqn_ct_set_fill_small(64)
-        _lib.lib.dqn_rms_set_cap(148 * 8)
+        _set("dqn_ct_set_fill_small", 64)
+        _set("dqn_rms_set_cap", 148 * 8)
         if v.startswith("rms="):               # optimizer grid cap
-            _lib.lib.dqn_rms_set_cap(int(v[4:]))
+            _set("dqn_rms_set_cap", int(v[4:]))
             v = "0"
         if v.startswith("fs="):                # conv_tc fill: fs=<batch <= 32>[/<above>]
             fs_, _, fb_ = v[3:].partition("/")
-            _lib.lib.dqn_ct_set_fill_small(int(fs_))
+            _set("dqn_ct_set_fill_small", int(fs_))
             v = "0:2:" + (fb_ or "128")
         if v.startswith("dcap="):              # linear dgrad split cap
-            _lib.lib.dqn_tc_set_dgrad_cap(int(v[5:]))
+            _set("dqn_tc_set_dgrad_cap", int(v[5:]))
             v = "0"
         if v.startswith("w1cl="):              # conv1 wgrad: largest cluster
-            _lib.lib.dqn_w1_set_cluster_max(int(v[5:]))
+            _set("dqn_w1_set_cluster_max", int(v[5:]))
             v = "0"
         if v == "nocks":                       # engine split-K through global partials only
-            _lib.lib.dqn_tc_set_cluster_splitk(0)
+            _set("dqn_tc_set_cluster_splitk", 0)
             v = "0"
         if v.startswith("lt="):                # fc1 forward cluster sizes: lt=<b<=32>/<b>32>
             a_, b_ = v[3:].split("/")
-            _lib.lib.dqn_lt_set_cluster(int(a_), int(b_))
+            _set("dqn_lt_set_cluster", int(a_), int(b_))
             v = "0"
         if v.startswith("c1="):                # conv1 forward kernel on (1) / engine (0)
-            _lib.lib.dqn_c1_set(int(v[3:]))
+            _set("dqn_c1_set", int(v[3:]))
             v = "0"
         elif v.startswith("p"):                # stream priorities: p<main>,<side>,<tree>
             prio["v"] = [int(x) for x in v[1:].split("/")]
@@ -80,11 +87,11 @@ def main():
         st, _, rest = rest.partition(":")
         fill, _, rest = rest.partition(":")
         dg, _, dfill = rest.partition(":")
-        _lib.lib.dqn_ct_set_dgrad(int(dg or 1))
-        _lib.lib.dqn_ct_set_dfill(int(dfill or 256))
-        _lib.lib.dqn_ct_set_cluster(int(cl))
-        _lib.lib.dqn_ct_set_stages(int(st or 2))
-        _lib.lib.dqn_ct_set_fill(int(fill or 128))
+        _set("dqn_ct_set_dgrad", int(dg or 1))
+        _set("dqn_ct_set_dfill", int(dfill or 256))
+        _set("dqn_ct_set_cluster", int(cl))
+        _set("dqn_ct_set_stages", int(st or 2))
+        _set("dqn_ct_set_fill", int(fill or 128))
     cfg = P.RunConfig(batch_size=32, double=True, dueling=True, priority_alpha=0.6,
                       beta_end_step=50_000_000)
     on = P.build_network("atari", (84, 84, 4), 4, True)
