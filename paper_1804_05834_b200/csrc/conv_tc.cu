@@ -28,6 +28,19 @@
 // order.  K is split across a thread-block cluster; the cluster reduces the
 // partial tiles through distributed shared memory in rank order
 // (deterministic), adds the bias and applies the ReLU.
+//
+// The same kernel computes the input gradient (layers.py:235-248) of a conv
+// whose filter tiles its stride, one GEMM per stride phase (py, px):
+//
+//   dX[S yq + py][S xq + px][c] = sum_{i, j, n} dY[yq - i][xq - j][n] W[py + S i][px + S j][c][n]
+//
+// rows = the phase's input pixels of whole images, K = its taps x dY channels.
+// The dY box of tap (i, j) starts at (-j, -i): the TMA fills the rows that
+// fall off the dY grid with zeros.  W's rows (r, s, c) with n contiguous are
+// K-major for this product and arrive as 128B-swizzle boxes (only their lo
+// pieces are computed); the epilogue applies the ReLU mask of the layer
+// below.  Launch shapes: 2 stages, 2 CTAs per SM; K split sized for ~128 CTAs
+// per forward launch (64 for a DQN_NET_HINT_SIDE trunk), ~256 per dgrad.
 #include "tc_gemm.cuh"
 
 #include <algorithm>
