@@ -67,3 +67,19 @@ def test_product_path_fails_loudly_without_the_library(tmp_path):
     r = subprocess.run([sys.executable, "-c", probe], cwd=root, capture_output=True, text=True,
                        timeout=300)
     assert r.stdout.startswith("GPU") or r.stdout.startswith("RAISED"), r.stdout + r.stderr
+
+
+def test_header_constants_match_the_binding():
+    """Every DQN_FLAG_* / DQN_TD_* / DQN_NET_HINT_* / DQN_LAYER_* value the
+    Python binding uses equals the header's."""
+    from paper_1804_05834_b200 import _lib
+    text = HEADER.read_text()
+    defines = {m.group(1): int(m.group(2), 0)
+               for m in re.finditer(r"#define\s+(DQN_\w+)\s+\(?(0x[0-9a-fA-F]+|\d+)", text)}
+    pairs = {"DQN_NET_HINT_SIDE": _lib.NET_HINT_SIDE}
+    for name in dir(_lib):
+        if name.startswith(("FLAG_", "TD_")) and ("DQN_" + name) in defines:
+            pairs["DQN_" + name] = getattr(_lib, name)
+    assert "DQN_NET_HINT_SIDE" in defines and len(pairs) >= 4, sorted(pairs)
+    for k, v in pairs.items():
+        assert defines[k] == v, (k, defines[k], v)
