@@ -326,3 +326,42 @@ def test_side_hint_changes_only_the_launch_shapes(P):
     for l in range(len(outs[0])):
         assert torch.equal(outs[1][l], outs[2][l]), l
         assert float((outs[1][l] - outs[0][l]).norm() / outs[0][l].norm()) < 1e-6, l
+
+
+@pytest.mark.parametrize("geom", [(27, 3, 3), (16, 4, 2), (12, 3, 1)])
+def test_conv_tc_other_geometries_forward_backward_wgrad(P, geom):
+    """Custom trunks whose 64-filter convolutions take the TMA-fed kernel with
+    other strides / filters / image sizes than the Atari net (stride 3, one
+    and two images per tile, 64-channel input): forward, input gradient and
+    weight gradient against the oracle."""
+    hw, f, s = geom
+    conv = lambda n, ff, ss: P.LayerSpec("convolution", {"filters": n, "filter_h": ff,  # noqa: E731
+                                                          "filter_w": ff, "stride_h": ss,
+                                                          "stride_w": ss})
+    trunk = [conv(32, 1, 1), P.LayerSpec.relu(), conv(64, f, s), P.LayerSpec.relu(),
+             conv(64, f, 1) if (hw - f) // s + 1 >= f else conv(64, 1, 1), P.LayerSpec.relu(),
+             P.LayerSpec.linear(16), P.LayerSpec.relu()]
+    o_trunk = [("conv", 32, 1, 1), ("relu",), ("conv", 64, f, s), ("relu",),
+               ("conv", 64, f, 1) if (hw - f) // s + 1 >= f else ("conv", 64, 1, 1), ("relu",),
+               ("fc", 16), ("relu",)]
+    shape = (hw, hw, 4)
+    on = P.build_network(trunk, shape, 3, True)
+    P.init_params(on, 7)
+    ref = O.QNet(o_trunk, shape, 3, True)
+    ref.init(7)
+    rng = np.random.default_rng(hw)
+    for n, t in on.named_tensors():
+        if n.endswith("bias"):
+            v = (rng.standard_normal(t.shape) * 0.01).astype(np.float32)
+            t.values.copy_(torch.as_tensor(v, device="cuda"))
+            ref.params[n][...] = v
+    x = rng.random((5,) + shape, dtype=np.float32)
+    q = on.forward(x).cpu().numpy()
+    assert rel_norm(q, ref.forward(x)) < TOL
+    g = rng.standard_normal(q.shape).astype(np.float32)
+    dx = on.backward(g).cpu().numpy()
+    assert rel_norm(dx, ref.backward(g)) < TOL
+    on.calculate_gradient()
+    ref.wgrad()
+    for n, t in on.named_tensors():
+        assert rel_norm(t.grad.cpu().numpy(), ref.grads[n]) < 1e-4, n
