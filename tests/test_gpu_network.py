@@ -365,3 +365,29 @@ def test_conv_tc_other_geometries_forward_backward_wgrad(P, geom):
     ref.wgrad()
     for n, t in on.named_tensors():
         assert rel_norm(t.grad.cpu().numpy(), ref.grads[n]) < 1e-4, n
+
+
+@pytest.mark.parametrize("hw,stride", [(64, 4), (36, 2), (44, 4)])
+def test_conv1_tc_other_geometries(P, hw, stride):
+    """The uint8 first layer (8x8 filters over 4 channels, 32 filters) on other
+    frame sizes and strides: conv1_tc tiles of 3-15 output rows; the network's
+    forward and gradients against the oracle."""
+    trunk = [P.LayerSpec("convolution", {"filters": 32, "filter_h": 8, "filter_w": 8,
+                                         "stride_h": stride, "stride_w": stride}),
+             P.LayerSpec.relu(), P.LayerSpec.linear(16), P.LayerSpec.relu()]
+    shape = (hw, hw, 4)
+    on = P.build_network(trunk, shape, 3, False)
+    P.init_params(on, 9)
+    ref = O.QNet([("conv", 32, 8, stride), ("relu",), ("fc", 16), ("relu",)], shape, 3, False)
+    ref.init(9)
+    rng = np.random.default_rng(hw + stride)
+    x8 = rng.integers(0, 256, size=(6,) + shape, dtype=np.uint8)
+    q = on.forward(torch.as_tensor(x8, device="cuda")).cpu().numpy()
+    assert rel_norm(q, ref.forward(O.Ring.lift(x8))) < TOL
+    g = rng.standard_normal(q.shape).astype(np.float32)
+    on.backward(g)
+    ref.backward(g)
+    on.calculate_gradient()
+    ref.wgrad()
+    for n, t in on.named_tensors():
+        assert rel_norm(t.grad.cpu().numpy(), ref.grads[n]) < 1e-4, n
