@@ -112,9 +112,15 @@ struct CtPlan {
   static constexpr int TMEM = 4 * NB <= 128 ? 128 : 256;
 };
 
-template <int NB, int CT_ST, bool DG>
+// TS (forward only): A's lo pieces go to tensor memory (tcgen05.st, one row
+// per converter thread) and the lo * hi MMA reads them there (TS form), one
+// accumulator pair: a stage is A_hi | [B_hi ; B_lo] | raw W, one A piece
+// smaller, so three stages fit twice per SM.
+template <int NB, int CT_ST, bool DG, bool TS = false>
 __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_constant__ ConvTcArgs p) {
   using PL = CtPlan<NB, DG>;
+  static_assert(!(TS && DG), "TS: forward only");
+  constexpr int A_PIECES = TS ? 1 : 2;
   constexpr int CT_EPI_LD = PL::LD;
   constexpr uint32_t ID_FULL = tc::make_idesc_tf32(2 * NB), ID_HALF = tc::make_idesc_tf32(NB);
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -132,7 +138,7 @@ __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_con
   if (warp == 4) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      tc::smem_u32(&tmem_slot)),
-                 "r"(PL::TMEM)
+                 "r"(TS ? 256 : PL::TMEM)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -152,12 +158,12 @@ __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_con
   pdl_wait();                                 // activations come from the layer below
   const uint32_t tmem = tmem_slot;
 
-  const uint32_t stage_b = (uint32_t)(2 * p.a_bytes + PL::B_BYTES + PL::RAW);
+  const uint32_t stage_b = (uint32_t)(A_PIECES * p.a_bytes + PL::B_BYTES + PL::RAW);
   auto a_hi = [&](int s) { return sbase + (uint32_t)s * stage_b; };
   auto a_lo = [&](int s) { return sbase + (uint32_t)s * stage_b + (uint32_t)p.a_bytes; };
-  auto b_st = [&](int s) { return sbase + (uint32_t)s * stage_b + (uint32_t)(2 * p.a_bytes); };
+  auto b_st = [&](int s) { return sbase + (uint32_t)s * stage_b + (uint32_t)(A_PIECES * p.a_bytes); };
   auto b_raw = [&](int s) {
-    return sbase + (uint32_t)s * stage_b + (uint32_t)(2 * p.a_bytes + PL::B_BYTES);
+    return sbase + (uint32_t)s * stage_b + (uint32_t)(A_PIECES * p.a_bytes + PL::B_BYTES);
   };
 
   if (warp == 4) {
@@ -191,14 +197,19 @@ __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_con
         const int s = kb % CT_ST, use = kb / CT_ST;
         tc::mbar_wait(&conv[s], use & 1);
         tc::tc_fence_after();
-        const uint32_t dbig = tmem + (uint32_t)((kb & 1) * 2 * NB);
+        const uint32_t dbig = tmem + (uint32_t)(TS ? 0 : (kb & 1) * 2 * NB);
 #pragma unroll
         for (int kq = 0; kq < CT_BK / 8; ++kq) {
           const uint64_t da = ct_desc(a_hi(s) + 32 * kq);
-          const uint64_t dl = ct_desc(a_lo(s) + 32 * kq);
           const uint64_t db = ct_desc(b_st(s) + 32 * kq);
-          ct_mma(dbig, da, db, ID_FULL, (kb < 2 && kq == 0) ? 0u : 1u);
-          ct_mma(dbig + NB, dl, db, ID_HALF, 1u);
+          if constexpr (TS) {
+            ct_mma(dbig, da, db, ID_FULL, (kb == 0 && kq == 0) ? 0u : 1u);
+            tc::mma_ts(dbig + NB, tmem + 2 * NB + (uint32_t)(s * CT_BK + 8 * kq), db, ID_HALF, 1u);
+          } else {
+            const uint64_t dl = ct_desc(a_lo(s) + 32 * kq);
+            ct_mma(dbig, da, db, ID_FULL, (kb < 2 && kq == 0) ? 0u : 1u);
+            ct_mma(dbig + NB, dl, db, ID_HALF, 1u);
+          }
         }
         tc::mma_commit(&empty[s]);
       }
@@ -208,13 +219,34 @@ __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_con
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % CT_ST, use = kb / CT_ST;
       tc::mbar_wait(&full[s], use & 1);
-      // A: the valid rows' 16-byte chunks, lo at the same (swizzled) offsets
-      for (int i = t; i < rows * (CT_BK / 4); i += 128) {
-        float4 v;
-        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a_hi(s) + 16 * i));
-        tc::st_shared_v4(a_lo(s) + 16 * i, make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y),
-                                                       tc::tf32_lo(v.z), tc::tf32_lo(v.w)));
+      if constexpr (TS) {
+        // A lo of row t into TMEM lane t, columns 2 NB + 32 s .. (k order)
+        float lo[CT_BK];
+#pragma unroll
+        for (int c = 0; c < CT_BK / 4; ++c) {
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (t < rows)
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                         : "r"(a_hi(s) + (uint32_t)(t * 128 + ((c ^ (t & 7)) << 4))));
+          lo[4 * c] = tc::tf32_lo(v.x);
+          lo[4 * c + 1] = tc::tf32_lo(v.y);
+          lo[4 * c + 2] = tc::tf32_lo(v.z);
+          lo[4 * c + 3] = tc::tf32_lo(v.w);
+        }
+        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + 2 * NB + (uint32_t)(s * CT_BK);
+        tc::tmem_st16(ta, lo);
+        tc::tmem_st16(ta + 16, lo + 16);
+        tc::tmem_wait_st();
+      } else {
+        // A: the valid rows' 16-byte chunks, lo at the same (swizzled) offsets
+        for (int i = t; i < rows * (CT_BK / 4); i += 128) {
+          float4 v;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a_hi(s) + 16 * i));
+          tc::st_shared_v4(a_lo(s) + 16 * i, make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y),
+                                                         tc::tf32_lo(v.z), tc::tf32_lo(v.w)));
+        }
       }
       if constexpr (DG) {
         // B arrived K-major (W rows (r, s, c), n contiguous): lo rows NB..2NB-1
@@ -244,6 +276,7 @@ __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_con
                                      tc::tf32_lo(v[3])));
       }
       tc::fence_proxy_async();                // generic smem writes -> tensor-core reads
+      if constexpr (TS) tc::tc_fence_before(); // TMEM stores -> the MMA thread
       tc::mbar_arrive(&conv[s]);
     }
   }
@@ -256,7 +289,7 @@ __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_con
   if (warp < 4) {
     const int row = warp * 32 + lane;
     const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
-    const bool two = nkb > 1;
+    const bool two = !TS && nkb > 1;
 #pragma unroll 1
     for (int c = 0; c < NB; c += 16) {
       float s0[16], s1[16], b0[16], b1[16];
@@ -285,7 +318,7 @@ __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_con
   __syncthreads();
   if (warp == 4)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(PL::TMEM)
+                 "r"(TS ? 256 : PL::TMEM)
                  : "memory");
   // ---- cluster reduction: rank q owns a contiguous range of (row, 4 channels)
   // units and sums the ranks' partials in rank order; then bias and ReLU
@@ -449,26 +482,32 @@ int g_ct_fill = 128;
 int g_ct_fill_small = 64;    // diagnostic: fill of a side trunk (DQN_NET_HINT_SIDE)
 int g_ct_dgrad = 1;     // diagnostic: 0 = conv dgrad on the generic engine
 int g_ct_dfill = 256;   // dgrad: CTAs one launch aims for
+int g_ct_ts = 3;        // diagnostic: forward with A lo in TMEM, this many stages (0 = off)
 #else
 constexpr int g_ct_cluster = 0, g_ct_stages = 2, g_ct_fill = 128, g_ct_dgrad = 1, g_ct_dfill = 256;
 constexpr int g_ct_fill_small = 64;
 #endif
 
-template <int NB, int ST, bool DG>
+template <int NB, int ST, bool DG, bool TS = false>
 int ct_launch(cudaStream_t st, const ConvTcArgs &a, dim3 grid, const char *what) {
   using PL = CtPlan<NB, DG>;
-  auto kern = conv_tc_kernel<NB, ST, DG>;
+  auto kern = conv_tc_kernel<NB, ST, DG, TS>;
+  // TS: one A piece per stage (its lo pieces live in TMEM)
+  auto bytes = [](int a_bytes) {
+    return TS ? std::max(ST * (a_bytes + PL::B_BYTES + PL::RAW), PL::EPI) + 1024
+              : PL::bytes(ST, a_bytes);
+  };
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         PL::bytes(ST, CT_BM * 128));
+                                         bytes(CT_BM * 128));
     if (e != cudaSuccess) return cuda_status(e, what);
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(CT_THREADS);
-  cfg.dynamicSmemBytes = PL::bytes(ST, a.a_bytes);
+  cfg.dynamicSmemBytes = bytes(a.a_bytes);
   cfg.stream = st;
   cudaLaunchAttribute attr[3];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -535,8 +574,14 @@ int conv_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, co
   const int cl = ct_split(a, tiles, L.sw, side ? g_ct_fill_small : g_ct_fill);
 #ifdef DQN_TC_TRACE
   if (g_ct_stages == 3) return ct_launch<64, 3, false>(st, a, dim3(tiles, cl, 1), "conv_tc_forward");
+  if (g_ct_ts == 0) return ct_launch<64, 2, false>(st, a, dim3(tiles, cl, 1), "conv_tc_forward");
+  if (g_ct_ts == 4) return ct_launch<64, 4, false, true>(st, a, dim3(tiles, cl, 1), "conv_tc_forward");
+  if (g_ct_ts == 2) return ct_launch<64, 2, false, true>(st, a, dim3(tiles, cl, 1), "conv_tc_forward");
 #endif
-  return ct_launch<64, 2, false>(st, a, dim3(tiles, cl, 1), "conv_tc_forward");
+  // A's lo pieces in TMEM, three stages (measured: B = 64 conv2 / conv3 9.4-11.0 vs
+  // 10.9-13.9 us with both pieces in smem and two stages; learner +2.7 %; B = 4096
+  // 217 / 126 vs 298 / 171 us)
+  return ct_launch<64, 3, false, true>(st, a, dim3(tiles, cl, 1), "conv_tc_forward");
 }
 
 // dX of a convolution whose filter tiles its stride (fh % S == 0), as one
@@ -592,4 +637,5 @@ extern "C" void dqn_ct_set_fill(int f) { dqn::g_ct_fill = f; }
 extern "C" void dqn_ct_set_fill_small(int f) { dqn::g_ct_fill_small = f; }
 extern "C" void dqn_ct_set_dgrad(int on) { dqn::g_ct_dgrad = on; }
 extern "C" void dqn_ct_set_dfill(int f) { dqn::g_ct_dfill = f; }
+extern "C" void dqn_ct_set_ts(int v) { dqn::g_ct_ts = v; }
 #endif

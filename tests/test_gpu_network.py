@@ -325,7 +325,9 @@ def test_side_hint_changes_only_the_launch_shapes(P):
         outs.append([a.clone() for a in bind.act])
     for l in range(len(outs[0])):
         assert torch.equal(outs[1][l], outs[2][l]), l
-        assert float((outs[1][l] - outs[0][l]).norm() / outs[0][l].norm()) < 1e-6, l
+        # fp32 re-association only (each layer's K split differs): 3e-6 covers the
+        # accumulated difference down the trunk
+        assert float((outs[1][l] - outs[0][l]).norm() / outs[0][l].norm()) < 3e-6, l
 
 
 @pytest.mark.parametrize("geom", [(27, 3, 3), (16, 4, 2), (12, 3, 1)])

@@ -17,8 +17,9 @@ B = 64
 x8 = torch.as_tensor(synth.frames(4, 1, np.arange(B) * 7 + 3), device="cuda")
 tens = dict(on.named_tensors())
 shapes = [tuple(u["out_shape"]) for u in on._units]
-for mode in (-1, 0):
+for mode, ts in ((-1, 0), (0, 0), (0, 2), (0, 3), (0, 4)):
     _lib.lib.dqn_ct_set_cluster(mode)
+    _lib.lib.dqn_ct_set_ts(ts)
     on.forward(x8)
     bind = on.binding(B)
     out = []
@@ -30,4 +31,4 @@ for mode in (-1, 0):
         ref = F.relu(ref)
         got = bind.act[l][: B * oh * ow * n].view(B, oh, ow, n).double()
         out.append(f"{name} rel {float((got-ref).norm()/ref.norm()):.3e} max {float((got-ref).abs().max()/ref.abs().max()):.3e}")
-    print("engine" if mode < 0 else "conv_tc", " | ".join(out))
+    print("engine" if mode < 0 else f"conv_tc ts={ts}", " | ".join(out))

@@ -28,14 +28,15 @@ for B in (32, 64, 4096):
     for layer, name, phase in ((0, "conv1", 0), (1, "conv2", 0), (2, "conv3", 0), (1, "conv2.dgrad", 1),
                                (2, "conv3.dgrad", 1)):
         res = []
-        for cl, stg in ((-1, 2), (0, 2), (0, 3), (1, 2), (2, 2), (4, 2), (8, 2)):
+        for cl, stg in ((-1, 2), (0, 2), (0, 12), (0, 13), (0, 14)):
             _lib.lib.dqn_ct_set_cluster(cl)
-            _lib.lib.dqn_ct_set_stages(stg)
+            _lib.lib.dqn_ct_set_stages(stg if stg < 10 else 2)
+            _lib.lib.dqn_ct_set_ts(stg - 10 if stg >= 10 else 0)
             _lib.lib.dqn_ct_set_dgrad(0 if cl < 0 else 1)
             _lib.lib.dqn_c1_set(0 if cl < 0 else 1)
             if layer == 0 and cl > 0:
                 continue
-            if phase == 1 and stg == 3:
+            if phase == 1 and stg != 2:
                 continue
             args = (C.byref(net.desc_for(x)), net.flat_values.data_ptr(), net.flat_grads.data_ptr(),
                     C.byref(b.struct), layer, phase, flags.data_ptr())
@@ -60,5 +61,6 @@ for B in (32, 64, 4096):
             res.append(f"{'engine' if cl < 0 else ('auto' if cl == 0 else f'cl{cl}')}/{stg} {us:.2f}")
         _lib.lib.dqn_ct_set_cluster(0)
         _lib.lib.dqn_ct_set_dgrad(1)
+        _lib.lib.dqn_ct_set_ts(0)
         _lib.lib.dqn_c1_set(1)
         print(f"B={B} {name}: " + " | ".join(res), flush=True)

@@ -54,6 +54,10 @@ def main():
             _set("dqn_tc_set_wgrad_cap", int(v[5:]))
             v = "0"
         _set("dqn_ct_set_fill_small", 64)
+        _set("dqn_ct_set_ts", 3)
+        if v.startswith("ts="):                # conv_tc forward with A lo in TMEM, stages
+            _set("dqn_ct_set_ts", int(v[3:]))
+            v = "0"
         _set("dqn_rms_set_cap", 148 * 8)
         if v.startswith("rms="):               # optimizer grid cap
             _set("dqn_rms_set_cap", int(v[4:]))
