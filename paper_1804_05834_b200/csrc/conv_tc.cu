@@ -112,14 +112,13 @@ struct CtPlan {
   static constexpr int TMEM = 4 * NB <= 128 ? 128 : 256;
 };
 
-// TS (forward only): A's lo pieces go to tensor memory (tcgen05.st, one row
+// TS: A's lo pieces go to tensor memory (tcgen05.st, one row
 // per converter thread) and the lo * hi MMA reads them there (TS form), one
 // accumulator pair: a stage is A_hi | [B_hi ; B_lo] | raw W, one A piece
 // smaller, so three stages fit twice per SM.
 template <int NB, int CT_ST, bool DG, bool TS = false>
 __global__ void __launch_bounds__(CT_THREADS, 2) conv_tc_kernel(const __grid_constant__ ConvTcArgs p) {
   using PL = CtPlan<NB, DG>;
-  static_assert(!(TS && DG), "TS: forward only");
   constexpr int A_PIECES = TS ? 1 : 2;
   constexpr int CT_EPI_LD = PL::LD;
   constexpr uint32_t ID_FULL = tc::make_idesc_tf32(2 * NB), ID_HALF = tc::make_idesc_tf32(NB);
@@ -483,6 +482,7 @@ int g_ct_fill_small = 64;    // diagnostic: fill of a side trunk (DQN_NET_HINT_S
 int g_ct_dgrad = 1;     // diagnostic: 0 = conv dgrad on the generic engine
 int g_ct_dfill = 256;   // dgrad: CTAs one launch aims for
 int g_ct_ts = 3;        // diagnostic: forward with A lo in TMEM, this many stages (0 = off)
+int g_ct_dts = 3;       // diagnostic: the same for the input gradients
 #else
 constexpr int g_ct_cluster = 0, g_ct_stages = 2, g_ct_fill = 128, g_ct_dgrad = 1, g_ct_dfill = 256;
 constexpr int g_ct_fill_small = 64;
@@ -623,8 +623,18 @@ int conv_tc_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, con
   const int tiles = (batch + ipt - 1) / ipt;
   const int cl = ct_split(a, tiles * S * S, S, g_ct_dfill);
   const dim3 grid(tiles, cl, S * S);
-  return L.in_c == 32 ? ct_launch<32, 2, true>(st, a, grid, "conv_tc_dgrad")
-                      : ct_launch<64, 2, true>(st, a, grid, "conv_tc_dgrad");
+#ifdef DQN_TC_TRACE
+  if (g_ct_dts == 0)
+    return L.in_c == 32 ? ct_launch<32, 2, true>(st, a, grid, "conv_tc_dgrad")
+                        : ct_launch<64, 2, true>(st, a, grid, "conv_tc_dgrad");
+  if (g_ct_dts == 4)
+    return L.in_c == 32 ? ct_launch<32, 4, true, true>(st, a, grid, "conv_tc_dgrad")
+                        : ct_launch<64, 4, true, true>(st, a, grid, "conv_tc_dgrad");
+#endif
+  // A's lo pieces in TMEM, three stages (learner +1.2 %; B = 4096 conv2 / conv3
+  // 432 / 289 vs 528 / 376 us)
+  return L.in_c == 32 ? ct_launch<32, 3, true, true>(st, a, grid, "conv_tc_dgrad")
+                      : ct_launch<64, 3, true, true>(st, a, grid, "conv_tc_dgrad");
 }
 
 }  // namespace dqn
@@ -638,4 +648,5 @@ extern "C" void dqn_ct_set_fill_small(int f) { dqn::g_ct_fill_small = f; }
 extern "C" void dqn_ct_set_dgrad(int on) { dqn::g_ct_dgrad = on; }
 extern "C" void dqn_ct_set_dfill(int f) { dqn::g_ct_dfill = f; }
 extern "C" void dqn_ct_set_ts(int v) { dqn::g_ct_ts = v; }
+extern "C" void dqn_ct_set_dts(int v) { dqn::g_ct_dts = v; }
 #endif

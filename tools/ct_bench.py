@@ -36,8 +36,9 @@ for B in (32, 64, 4096):
             _lib.lib.dqn_c1_set(0 if cl < 0 else 1)
             if layer == 0 and cl > 0:
                 continue
-            if phase == 1 and stg != 2:
+            if phase == 1 and stg not in (2, 13, 14):
                 continue
+            _lib.lib.dqn_ct_set_dts(stg - 10 if (phase == 1 and stg >= 10) else 0)
             args = (C.byref(net.desc_for(x)), net.flat_values.data_ptr(), net.flat_grads.data_ptr(),
                     C.byref(b.struct), layer, phase, flags.data_ptr())
             s = torch.cuda.Stream()
@@ -61,6 +62,7 @@ for B in (32, 64, 4096):
             res.append(f"{'engine' if cl < 0 else ('auto' if cl == 0 else f'cl{cl}')}/{stg} {us:.2f}")
         _lib.lib.dqn_ct_set_cluster(0)
         _lib.lib.dqn_ct_set_dgrad(1)
-        _lib.lib.dqn_ct_set_ts(0)
+        _lib.lib.dqn_ct_set_ts(3)
+        _lib.lib.dqn_ct_set_dts(3)
         _lib.lib.dqn_c1_set(1)
         print(f"B={B} {name}: " + " | ".join(res), flush=True)

@@ -55,6 +55,10 @@ def main():
             v = "0"
         _set("dqn_ct_set_fill_small", 64)
         _set("dqn_ct_set_ts", 3)
+        _set("dqn_ct_set_dts", 3)
+        if v.startswith("dts="):               # conv_tc dgrad with A lo in TMEM, stages
+            _set("dqn_ct_set_dts", int(v[4:]))
+            v = "0"
         if v.startswith("ts="):                # conv_tc forward with A lo in TMEM, stages
             _set("dqn_ct_set_ts", int(v[3:]))
             v = "0"
