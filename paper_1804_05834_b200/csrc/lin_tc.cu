@@ -88,18 +88,26 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
   return d;
 }
 
+// AT (the forward): A's lo pieces go to tensor memory as the converters
+// transpose the weights (one row per thread, tcgen05.st) and the lo * hi MMA
+// reads them there (TS form), one accumulator pair; a stage is then
+// A_hi | [B_hi ; B_lo] | raw, and four stages fit.
 template <int NB, bool AT>
 struct LtPlan {
+  static constexpr bool TS = AT;
   static constexpr int RB = 2 * NB;                       // stacked B rows
   static constexpr int A_BYTES = LT_BM * LT_BK * 4;       // one piece of the A tile
   static constexpr int B_BYTES = RB * LT_BK * 4;
   static constexpr int RAW = AT ? A_BYTES : 0;            // A as loaded ([k][m]) when transposed
-  static constexpr int STAGE = 2 * A_BYTES + B_BYTES + RAW;   // A_hi | A_lo | [B_hi ; B_lo] | raw
-  static constexpr int ST = AT ? 3 : LT_ST;
+  static constexpr int A_PIECES = TS ? 1 : 2;
+  static constexpr int STAGE = A_PIECES * A_BYTES + B_BYTES + RAW;   // A_hi | (A_lo) | [B_hi ; B_lo] | raw
+  static constexpr int ST = AT ? 4 : LT_ST;
   static constexpr int PIPE = ST * STAGE;
   static constexpr int EPI = NB * LT_BM * 4;              // staged partial [NB][128]
   static constexpr int BYTES = (PIPE > EPI ? PIPE : EPI) + 1024;   // + alignment slack
-  static constexpr int TMEM = 4 * NB <= 32 ? 32 : (4 * NB <= 64 ? 64 : (4 * NB <= 128 ? 128 : 256));
+  static constexpr int LO_COL = 2 * NB;                   // TS: A_lo columns after the pair
+  static constexpr int TMEM = TS ? 256
+                                 : (4 * NB <= 32 ? 32 : (4 * NB <= 64 ? 64 : (4 * NB <= 128 ? 128 : 256)));
 };
 
 template <int NB, bool AT>
@@ -145,9 +153,9 @@ __global__ void __launch_bounds__(LT_THREADS, 1) lin_tc_kernel(const __grid_cons
 
   auto a_hi = [&](int s) { return sbase + (uint32_t)(s * PL::STAGE); };
   auto a_lo = [&](int s) { return sbase + (uint32_t)(s * PL::STAGE + PL::A_BYTES); };
-  auto b_st = [&](int s) { return sbase + (uint32_t)(s * PL::STAGE + 2 * PL::A_BYTES); };
+  auto b_st = [&](int s) { return sbase + (uint32_t)(s * PL::STAGE + PL::A_PIECES * PL::A_BYTES); };
   auto a_raw = [&](int s) {
-    return sbase + (uint32_t)(s * PL::STAGE + 2 * PL::A_BYTES + PL::B_BYTES);
+    return sbase + (uint32_t)(s * PL::STAGE + PL::A_PIECES * PL::A_BYTES + PL::B_BYTES);
   };
 
   if (warp == 4) {
@@ -170,14 +178,19 @@ __global__ void __launch_bounds__(LT_THREADS, 1) lin_tc_kernel(const __grid_cons
         const int s = kb % LT_ST, use = kb / LT_ST;
         tc::mbar_wait(&conv[s], use & 1);
         tc::tc_fence_after();
-        const uint32_t dbig = tmem + (uint32_t)((kb & 1) * 2 * NB);
+        const uint32_t dbig = tmem + (uint32_t)(PL::TS ? 0 : (kb & 1) * 2 * NB);
 #pragma unroll
         for (int kq = 0; kq < LT_BK / 8; ++kq) {
           const uint64_t da = sw128_desc(a_hi(s) + 32 * kq);
-          const uint64_t dl = sw128_desc(a_lo(s) + 32 * kq);
           const uint64_t db = sw128_desc(b_st(s) + 32 * kq);
-          mma_ss(dbig, da, db, ID_FULL, (kb < 2 && kq == 0) ? 0u : 1u);
-          mma_ss(dbig + NB, dl, db, ID_HALF, 1u);
+          if constexpr (PL::TS) {
+            mma_ss(dbig, da, db, ID_FULL, (kb == 0 && kq == 0) ? 0u : 1u);
+            tc::mma_ts(dbig + NB, tmem + (uint32_t)(PL::LO_COL + s * LT_BK + 8 * kq), db, ID_HALF, 1u);
+          } else {
+            const uint64_t dl = sw128_desc(a_lo(s) + 32 * kq);
+            mma_ss(dbig, da, db, ID_FULL, (kb < 2 && kq == 0) ? 0u : 1u);
+            mma_ss(dbig + NB, dl, db, ID_HALF, 1u);
+          }
         }
         tc::mma_commit(&empty[s]);
       }
@@ -191,8 +204,12 @@ __global__ void __launch_bounds__(LT_THREADS, 1) lin_tc_kernel(const __grid_cons
         // A from the raw [32 k][128 m] tile: unit (m, 4-k chunk c) -> row m,
         // 16-byte column c ^ (m % 8) of the swizzled K-major hi and lo tiles
         // (lanes = consecutive m: conflict-free reads and writes)
-        for (int u = t; u < LT_BM * LT_BK / 4; u += 128) {
-          const int m = u & (LT_BM - 1), c = u >> 7;
+        // thread t owns row m = t (its TMEM lane): hi chunks to smem, the 32
+        // lo pieces to TMEM columns LO_COL + 32 s ..
+        const int m = t;
+        float lo[LT_BK];
+#pragma unroll
+        for (int c = 0; c < LT_BK / 4; ++c) {
           float v[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -200,9 +217,13 @@ __global__ void __launch_bounds__(LT_THREADS, 1) lin_tc_kernel(const __grid_cons
                          : "=f"(v[i]) : "r"(a_raw(s) + (uint32_t)(((4 * c + i) * LT_BM + m) * 4)));
           const uint32_t off = (uint32_t)(m * 128 + ((c ^ (m & 7)) << 4));
           tc::st_shared_v4(a_hi(s) + off, make_float4(v[0], v[1], v[2], v[3]));
-          tc::st_shared_v4(a_lo(s) + off, make_float4(tc::tf32_lo(v[0]), tc::tf32_lo(v[1]),
-                                                      tc::tf32_lo(v[2]), tc::tf32_lo(v[3])));
+#pragma unroll
+          for (int i = 0; i < 4; ++i) lo[4 * c + i] = tc::tf32_lo(v[i]);
         }
+        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(PL::LO_COL + s * LT_BK);
+        tc::tmem_st16(ta, lo);
+        tc::tmem_st16(ta + 16, lo + 16);
+        tc::tmem_wait_st();
       } else {
         // A: 128 x 32 floats, 16-byte chunks at the same offsets in hi and lo
         for (int i = t; i < LT_BM * LT_BK / 4; i += 128) {
@@ -225,6 +246,7 @@ __global__ void __launch_bounds__(LT_THREADS, 1) lin_tc_kernel(const __grid_cons
                                           tc::tf32_lo(v.w)));
       }
       tc::fence_proxy_async();                // generic smem writes -> tensor-core reads
+      if constexpr (PL::TS) tc::tc_fence_before();   // TMEM stores -> the MMA thread
       tc::mbar_arrive(&conv[s]);
       if (kb == 0) {
         LT_MARK(2)
@@ -241,7 +263,7 @@ __global__ void __launch_bounds__(LT_THREADS, 1) lin_tc_kernel(const __grid_cons
   if (warp < 4) {
     const int row = warp * 32 + lane;
     const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
-    const bool two = nkb > 1;
+    const bool two = !PL::TS && nkb > 1;
 #pragma unroll 1
     for (int c = 0; c < NB; c += 16) {
       float s0[16], s1[16], b0[16], b1[16];
