@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(LT_THREADS, 1) lin_tc_kernel(const __grid_cons
           tc::tma_load_2d(a_raw(s), &p.amap, m0, k0, &full[s]);   // 32 k-rows x 128 m (512 B)
         else
           tc::tma_load_2d(a_hi(s), &p.amap, k0, m0, &full[s]);    // 128 rows x 128 B
-        tc::tma_load_2d(b_st(s), &p.bmap, k0, 0, &full[s]);       // NB rows x 128 B (hi rows)
+        tc::tma_load_2d(b_st(s), &p.bmap, k0, (int)blockIdx.z * NB, &full[s]);   // NB rows (hi)
       }
     }
   } else if (warp == 5) {
@@ -306,8 +306,8 @@ __global__ void __launch_bounds__(LT_THREADS, 1) lin_tc_kernel(const __grid_cons
       const int jj = u / (LT_BM / 4), r4 = (u - jj * (LT_BM / 4)) * 4;
       const int j = rank + jj * cl;
       mm[h] = m0 + r4;
-      ok[h] = u < units && j < p.nrows && mm[h] < p.M;
-      off[h] = (int64_t)j * p.M + mm[h];
+      ok[h] = u < units && (int)blockIdx.z * NB + j < p.nrows && mm[h] < p.M;
+      off[h] = ((int64_t)blockIdx.z * NB + j) * p.M + mm[h];
       const int sidx = j * LT_BM + r4;
       acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
       aux[h] = make_float4(1.f, 1.f, 1.f, 1.f);
@@ -418,7 +418,7 @@ int lt_launch(cudaStream_t st, LinTcArgs &a, int cl, const char *what) {
   cl = std::max(1, std::min(cl, chunks));
   a.klen = ((chunks + cl - 1) / cl) * LT_BK;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((a.M + LT_BM - 1) / LT_BM, cl, 1);
+  cfg.gridDim = dim3((a.M + LT_BM - 1) / LT_BM, cl, (a.nrows + NB - 1) / NB);
   cfg.blockDim = dim3(LT_THREADS);
   cfg.dynamicSmemBytes = PL::BYTES;
   cfg.stream = st;
@@ -456,14 +456,16 @@ inline int lt_rows(int nb) { return nb <= 16 ? 16 : (nb <= 32 ? 32 : 64); }
 // 8/8 6,857, 4/8 6,858, 16/8 6,856, 12/16 6,713 updates/s (trace build).
 #ifdef DQN_TC_TRACE
 int g_lt_cl_small = 4, g_lt_cl_big = 16;     // diagnostic overrides
+int g_lt_max_batch = 1 << 20, g_lt_cl_large = 0;   // 0: the fill rule
 #else
 constexpr int g_lt_cl_small = 4, g_lt_cl_big = 16;
+constexpr int g_lt_max_batch = 1 << 20, g_lt_cl_large = 0;
 #endif
 
 // hidden linear layer at learner batch sizes (<= 64 rows), weights rows >= 128
 bool lin_tc_ok(const dqn_layer_desc &L, int batch) {
   const int F = L.in_h * L.in_w * L.in_c;
-  return L.kind == DQN_LAYER_LINEAR && batch >= 1 && batch <= 64 && F % 4 == 0 &&
+  return L.kind == DQN_LAYER_LINEAR && batch >= 1 && batch <= g_lt_max_batch && F % 4 == 0 &&
          L.out_c % 4 == 0 && F >= 128 && L.out_c >= 128;
 }
 
@@ -485,7 +487,15 @@ int lin_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, con
   a.out = y;
   // K split over a cluster: 4 weight tiles x 16 = 64 CTAs for fc1 at batch 64
   // (measured alone: 8-CTA clusters 15.6 us, 16-CTA 11.0 us)
-  return lt_run<true>(st, a, nb, side ? g_lt_cl_small : g_lt_cl_big, "lin_tc_forward");
+  // above batch 64: 64-row blocks of the batch on blockIdx.z and a K split
+  // for ~128 CTAs (measured at B = 256 / 1024 / 4096: 21.9 / 39.2 / 136 us with
+  // splits 4 / 2 / 1, the generic engine 37.4 / 75.4 / 246 us)
+  int cl = side ? g_lt_cl_small : g_lt_cl_big;
+  if (batch > 64) {
+    const int ctas = ((N + LT_BM - 1) / LT_BM) * ((batch + 63) / 64);
+    cl = g_lt_cl_large > 0 ? g_lt_cl_large : std::max(1, std::min(16, (128 + ctas - 1) / ctas));
+  }
+  return lt_run<true>(st, a, nb, cl, "lin_tc_forward");
 }
 
 }  // namespace dqn
@@ -495,6 +505,10 @@ int lin_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, con
 extern "C" void dqn_lt_set_cluster(int small, int big) {
   dqn::g_lt_cl_small = small;
   dqn::g_lt_cl_big = big;
+}
+extern "C" void dqn_lt_set_large(int max_batch, int cl) {
+  dqn::g_lt_max_batch = max_batch;
+  dqn::g_lt_cl_large = cl;
 }
 extern "C" int dqn_lt_trace(unsigned long long *host) {
   return (int)cudaMemcpyFromSymbol(host, dqn::g_lt_trace, sizeof(dqn::g_lt_trace));
