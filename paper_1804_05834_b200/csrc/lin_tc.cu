@@ -90,8 +90,10 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
 
 // AT (the forward): A's lo pieces go to tensor memory as the converters
 // transpose the weights (one row per thread, tcgen05.st) and the lo * hi MMA
-// reads them there (TS form), one accumulator pair; a stage is then
-// A_hi | [B_hi ; B_lo] | raw, and four stages fit.
+// reads them there (TS form); a stage is then A_hi | [B_hi ; B_lo] | raw, and
+// four stages fit.  The two k-parity accumulator pairs stay (one CTA per SM:
+// TMEM has room), which keeps long K chains (large batch, one split) at the
+// dual-pair accuracy.
 template <int NB, bool AT>
 struct LtPlan {
   static constexpr bool TS = AT;
@@ -105,8 +107,8 @@ struct LtPlan {
   static constexpr int PIPE = ST * STAGE;
   static constexpr int EPI = NB * LT_BM * 4;              // staged partial [NB][128]
   static constexpr int BYTES = (PIPE > EPI ? PIPE : EPI) + 1024;   // + alignment slack
-  static constexpr int LO_COL = 2 * NB;                   // TS: A_lo columns after the pair
-  static constexpr int TMEM = TS ? 256
+  static constexpr int LO_COL = 4 * NB;                   // TS: A_lo columns after the pairs
+  static constexpr int TMEM = TS ? (LO_COL + ST * LT_BK <= 256 ? 256 : 512)
                                  : (4 * NB <= 32 ? 32 : (4 * NB <= 64 ? 64 : (4 * NB <= 128 ? 128 : 256)));
 };
 
@@ -178,13 +180,13 @@ __global__ void __launch_bounds__(LT_THREADS, 1) lin_tc_kernel(const __grid_cons
         const int s = kb % LT_ST, use = kb / LT_ST;
         tc::mbar_wait(&conv[s], use & 1);
         tc::tc_fence_after();
-        const uint32_t dbig = tmem + (uint32_t)(PL::TS ? 0 : (kb & 1) * 2 * NB);
+        const uint32_t dbig = tmem + (uint32_t)((kb & 1) * 2 * NB);
 #pragma unroll
         for (int kq = 0; kq < LT_BK / 8; ++kq) {
           const uint64_t da = sw128_desc(a_hi(s) + 32 * kq);
           const uint64_t db = sw128_desc(b_st(s) + 32 * kq);
           if constexpr (PL::TS) {
-            mma_ss(dbig, da, db, ID_FULL, (kb == 0 && kq == 0) ? 0u : 1u);
+            mma_ss(dbig, da, db, ID_FULL, (kb < 2 && kq == 0) ? 0u : 1u);
             tc::mma_ts(dbig + NB, tmem + (uint32_t)(PL::LO_COL + s * LT_BK + 8 * kq), db, ID_HALF, 1u);
           } else {
             const uint64_t dl = sw128_desc(a_lo(s) + 32 * kq);
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(LT_THREADS, 1) lin_tc_kernel(const __grid_cons
   if (warp < 4) {
     const int row = warp * 32 + lane;
     const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
-    const bool two = !PL::TS && nkb > 1;
+    const bool two = nkb > 1;
 #pragma unroll 1
     for (int c = 0; c < NB; c += 16) {
       float s0[16], s1[16], b0[16], b1[16];
@@ -457,9 +459,11 @@ inline int lt_rows(int nb) { return nb <= 16 ? 16 : (nb <= 32 ? 32 : 64); }
 #ifdef DQN_TC_TRACE
 int g_lt_cl_small = 4, g_lt_cl_big = 16;     // diagnostic overrides
 int g_lt_max_batch = 1 << 20, g_lt_cl_large = 0;   // 0: the fill rule
+int g_ltd_min_batch = 64;                            // dgrad: lin_tc above this batch
 #else
 constexpr int g_lt_cl_small = 4, g_lt_cl_big = 16;
 constexpr int g_lt_max_batch = 1 << 20, g_lt_cl_large = 0;
+constexpr int g_ltd_min_batch = 64;
 #endif
 
 // hidden linear layer at learner batch sizes (<= 64 rows), weights rows >= 128
@@ -498,6 +502,28 @@ int lin_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, con
   return lt_run<true>(st, a, nb, cl, "lin_tc_forward");
 }
 
+// dX [batch][F] = mask(dY [batch][N] W[F][N]^T) above learner batch sizes: W's
+// rows are K-major for this product and arrive as 128B-swizzle boxes (no
+// transpose), 64-row batch blocks on blockIdx.z.  (At batch 32 the engine's
+// LinDgradTmaPol is faster in the learner: DESIGN.md section 5.)
+int lin_tc_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
+                 const float *mask, float *dx, int batch) {
+  if (batch <= g_ltd_min_batch || !lin_tc_ok(L, batch)) return DQN_ERR_UNSUPPORTED;
+  const int F = L.in_h * L.in_w * L.in_c, N = L.out_c;
+  LinTcArgs a{};
+  if (!lt_map(&a.amap, w, N, F, LT_BM) || !lt_map(&a.bmap, dy, N, batch, 64))
+    return DQN_ERR_UNSUPPORTED;
+  a.M = F;
+  a.K = N;
+  a.nrows = batch;
+  a.mode = 1;
+  a.mask = mask;
+  a.out = dx;
+  const int ctas = ((F + LT_BM - 1) / LT_BM) * ((batch + 63) / 64);
+  return lt_run<false>(st, a, 64, std::max(1, std::min(16, (128 + ctas - 1) / ctas)),
+                       "lin_tc_dgrad");
+}
+
 }  // namespace dqn
 
 
@@ -506,6 +532,7 @@ extern "C" void dqn_lt_set_cluster(int small, int big) {
   dqn::g_lt_cl_small = small;
   dqn::g_lt_cl_big = big;
 }
+extern "C" void dqn_ltd_set_min_batch(int b) { dqn::g_ltd_min_batch = b; }
 extern "C" void dqn_lt_set_large(int max_batch, int cl) {
   dqn::g_lt_max_batch = max_batch;
   dqn::g_lt_cl_large = cl;

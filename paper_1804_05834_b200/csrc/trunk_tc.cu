@@ -30,6 +30,8 @@ bool lin_tc_ok(const dqn_layer_desc &L, int batch);
 int lin_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const float *x, const float *params,
                    float *y, int batch, bool side);
 bool conv_tc_ok(const dqn_layer_desc &L);
+int lin_tc_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
+                 const float *mask, float *dx, int batch);
 int conv1_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const uint8_t *x,
                      const float *params, float *y, int batch);
 int conv_tc_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, const float *w,
@@ -687,6 +689,8 @@ int tc_layer_backward(cudaStream_t st, const dqn_net_desc *net, int l, const flo
   const float *w = params + L.w_off;
   if (L.kind == DQN_LAYER_LINEAR) {
     const int M = b->batch, F = L.in_h * L.in_w * L.in_c;
+    const int rc = lin_tc_dgrad(st, L, b->dact[l], w, mask, out, b->batch);
+    if (rc != DQN_ERR_UNSUPPORTED) return rc;
     return lin_dgrad(st, b->dact[l], w, mask, out, b->scratch, counters_of(b), M, F, L.out_c);
   }
   // dY and W by TMA, one GEMM per stride phase (conv_tc.cu)

@@ -393,3 +393,31 @@ def test_conv1_tc_other_geometries(P, hw, stride):
     ref.wgrad()
     for n, t in on.named_tensors():
         assert rel_norm(t.grad.cpu().numpy(), ref.grads[n]) < 1e-4, n
+
+
+@pytest.mark.parametrize("batch", [65, 130, 1024])
+def test_fc1_lin_tc_large_batch(P, batch):
+    """fc1 above learner batch sizes on lin_tc (64-row batch blocks, K split
+    for ~128 CTAs): forward against an fp64 product of the same input, and the
+    input gradient (W rows K-major by TMA) against the fp64 transposed product
+    masked by the layer below's ReLU."""
+    from paper_1804_05834_b200 import synth
+    on = P.build_network("atari", (84, 84, 4), 4, True)
+    P.init_params(on, 11)
+    x = torch.as_tensor(synth.frames(7, 0, np.arange(batch) % 4096), device="cuda")
+    q = on.forward(x)
+    on.backward(torch.as_tensor(np.random.default_rng(batch).standard_normal(tuple(q.shape)),
+                                dtype=torch.float32, device="cuda"))
+    bind = on.binding(batch)
+    tens = dict(on.named_tensors())
+    W = tens["fc1.weight"].values.double()                   # [3136][512]
+    xin = bind.act[2][: batch * 3136].view(batch, 3136).double()
+    ref = torch.relu(xin @ W + tens["fc1.bias"].values.double())
+    got = bind.act[3][: batch * 512].view(batch, 512).double()
+    # fp32-level for a 3,136-long dot product (one K chain of 1,568-3,136 at
+    # these batches; the numpy fp32 oracle is at ~1e-6 itself)
+    assert float((got - ref).norm() / ref.norm()) < 5e-6
+    dy = bind.dact[3][: batch * 512].view(batch, 512).double()
+    dref = (dy @ W.T) * (xin > 0)
+    dgot = bind.dact[2][: batch * 3136].view(batch, 3136).double()
+    assert float((dgot - dref).norm() / dref.norm()) < 5e-6

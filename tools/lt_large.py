@@ -47,3 +47,32 @@ for B in (256, 1024, 4096):
                    f"({2 * B * 3136 * 512 / us / 1e6:.1f} TF/s)")
     _lib.lib.dqn_lt_set_large(1 << 20, 0)
     print(f"B={B} fc1 fwd: " + " | ".join(res), flush=True)
+    res = []
+    q = net.forward(x)
+    net.backward(torch.ones_like(q))
+    for mb in (1 << 20, 64):
+        _lib.lib.dqn_ltd_set_min_batch(mb)
+        args = (C.byref(net.desc_for(x)), net.flat_values.data_ptr(), net.flat_grads.data_ptr(),
+                C.byref(net._cur.struct), 3, 1, flags.data_ptr())
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                _lib.call("dqn_net_layer", s.cuda_stream, *args)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(5):
+                    _lib.call("dqn_net_layer", s.cuda_stream, *args)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(4):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / 20
+        res.append(f"{'engine' if mb > 4096 else 'lin_tc'} {us:.1f} us "
+                   f"({2 * B * 3136 * 512 / us / 1e6:.1f} TF/s)")
+    _lib.lib.dqn_ltd_set_min_batch(64)
+    print(f"B={B} fc1 dgrad: " + " | ".join(res), flush=True)
