@@ -114,19 +114,19 @@ def val(r, n):
 # fragment checks the label against the captured kernel
 labels = [("sample+gather (batch 32)", "sample_gather"),
           ("conv1.fwd (batch 32, target)", ("conv1_tc", "FwdPol<unsigned char")),
-          ("conv2.fwd (batch 32, target)", ("conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
-          ("conv3.fwd (batch 32, target)", ("conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
+          ("conv2.fwd (batch 32, target)", ("conv_tc_kernel<64, 3, 0", "conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
+          ("conv3.fwd (batch 32, target)", ("conv_tc_kernel<64, 3, 0", "conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
           ("fc1.fwd (batch 32, target)", "lin_tc"),
           ("conv1.fwd (batch 64)", ("conv1_tc", "FwdPol<unsigned char")),
-          ("conv2.fwd (batch 64)", ("conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
-          ("conv3.fwd (batch 64)", ("conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
+          ("conv2.fwd (batch 64)", ("conv_tc_kernel<64, 3, 0", "conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
+          ("conv3.fwd (batch 64)", ("conv_tc_kernel<64, 3, 0", "conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
           ("fc1.fwd (batch 64)", "lin_tc"),
           ("duel.fwd+td (Q heads)", "head_q"), ("duel.dgrad+wgrad (TD block)", "head_td_bwd"),
           ("tree update (batch 32)", "tree_update"), ("fc1.wgrad (batch 32)", "lin_wgrad"),
           ("fc1.dgrad (batch 32)", "LinDgrad"), ("conv3.wgrad (batch 32)", "WgradPol<float"),
-          ("conv3.dgrad (batch 32)", ("conv_tc_kernel<64, 2, 1>", "ConvDgradPol")),
+          ("conv3.dgrad (batch 32)", ("conv_tc_kernel<64, 3, 1", "conv_tc_kernel<64, 2, 1>", "ConvDgradPol")),
           ("conv2.wgrad (batch 32)", "WgradPol<float"),
-          ("conv2.dgrad (batch 32)", ("conv_tc_kernel<32, 2, 1>", "ConvDgradPol")),
+          ("conv2.dgrad (batch 32)", ("conv_tc_kernel<32, 3, 1", "conv_tc_kernel<32, 2, 1>", "ConvDgradPol")),
           ("conv1.wgrad (batch 32)", "conv1_wgrad_u8"),
           ("rmsprop apply", "rms_apply")]
 L = [f"# {tag} — every kernel of one learner update, `ncu --set full`", "",
