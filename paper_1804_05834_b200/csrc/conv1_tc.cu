@@ -14,9 +14,11 @@
 // contiguous in the frame (24 rows x 336 B = 8 KB), so one bulk copy brings
 // the slab; a second brings W (256 x 32 fp32).  A k-block of 32 is one filter
 // row r: for output pixel (oy, ox) its 32 values are the 8 pixels x 4
-// channels at slab row 4 oy + r, bytes 16 ox .. 16 ox + 31 -- the converter
-// warps turn each 4-byte pixel into one 16-byte chunk of the swizzled K-major
-// A tile, and transpose W's rows r*32 .. r*32+31 into the K-major B tile.
+// channels at slab row 4 oy + r, bytes 16 ox .. 16 ox + 31.  Each converter
+// thread owns one pixel row and writes those 32 exact integers to its TMEM
+// lane (the A operand of a TS-form MMA: no A tile in shared memory, so six
+// stages fit twice per SM), and the converters transpose W's rows
+// r*32 .. r*32+31 into the K-major B tile in shared memory.
 #include "tc_gemm.cuh"
 
 #include <algorithm>
@@ -27,9 +29,9 @@ namespace {
 constexpr int C1_THREADS = 192;                // warps 0-3 convert + epilogue, 4 loads, 5 MMA
 constexpr int C1_BK = 32;
 constexpr int C1_N = 32;                       // output channels
-constexpr int C1_ST = 3;                       // operand stages
+constexpr int C1_ST = 6;                       // operand stages (B in smem, A in TMEM)
+constexpr int C1_ACOL = 64;                    // TMEM: accumulator [hi | lo] 0..63, A stages after
 constexpr int C1_B_BYTES = 2 * C1_N * 128;     // [W_hi ; W_lo], K-major
-constexpr int C1_UNITS = 7;                    // A chunks per converter thread (<= 896 / 128)
 
 #ifdef DQN_TC_TRACE
 // per-CTA %globaltimer marks (trace build): entry, after pdl_wait, operands
@@ -103,8 +105,9 @@ __global__ void __launch_bounds__(C1_THREADS, 2) conv1_tc_kernel(const __grid_co
   __shared__ uint32_t tmem_slot;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const uint32_t sbase = (tc::smem_u32(smem) + 1023u) & ~1023u;
-  // layout: A stages | B stages | W (K x 32 fp32) | slab
-  const uint32_t a_st = sbase, b_st = a_st + C1_ST * p.a_bytes;
+  // layout: B stages | W (K x 32 fp32) | slab; the A tiles live in TMEM
+  // (columns C1_ACOL + 32 s), the epilogue stages through the B stages
+  const uint32_t a_st = sbase, b_st = sbase;
   const uint32_t w_s = b_st + C1_ST * C1_B_BYTES;
   const int K = p.fh * p.fh * p.C;
   const uint32_t slab = w_s + (uint32_t)K * C1_N * 4;
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(C1_THREADS, 2) conv1_tc_kernel(const __grid_co
   if (warp == 4) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      tc::smem_u32(&tmem_slot)),
-                 "r"(64)
+                 "r"(256)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -157,45 +160,43 @@ __global__ void __launch_bounds__(C1_THREADS, 2) conv1_tc_kernel(const __grid_co
         const int s = kb % C1_ST, use = kb / C1_ST;
         tc::mbar_wait(&conv[s], use & 1);
         tc::tc_fence_after();
-        const uint32_t a = a_st + s * p.a_bytes, b = b_st + s * C1_B_BYTES;
+        const uint32_t b = b_st + s * C1_B_BYTES;
 #pragma unroll
         for (int kq = 0; kq < C1_BK / 8; ++kq)
-          c1_mma(tmem, c1_desc(a + 32 * kq), c1_desc(b + 32 * kq), IDESC,
-                 (kb == 0 && kq == 0) ? 0u : 1u);
+          tc::mma_ts(tmem, tmem + (uint32_t)(C1_ACOL + s * C1_BK + 8 * kq), c1_desc(b + 32 * kq),
+                     IDESC, (kb == 0 && kq == 0) ? 0u : 1u);
         tc::mma_commit(&empty[s]);
       }
       tc::mma_commit(&done);
     }
   } else {                                    // warps 0-3: operand tiles
-    // this thread's A chunks (pixel q, filter column c): slab offset at
-    // filter row 0 and tile offset, fixed over the k-blocks
+    // thread t owns pixel row q = t of the tile (its TMEM lane): the slab
+    // offset of its 8 filter-column pixels at filter row 0
     const uint8_t *sl = smem + (slab - tc::smem_u32(smem));
     const float *ws = reinterpret_cast<const float *>(smem + (w_s - tc::smem_u32(smem)));
-    int in_off[C1_UNITS];
-    uint32_t out_off[C1_UNITS];
-#pragma unroll
-    for (int j = 0; j < C1_UNITS; ++j) {
-      const int u = t + 128 * j;
-      const int q = u >> 3, c = u & 7;
-      const int oy = q / p.OW, ox = q - oy * p.OW;
-      in_off[j] = u < rows * 8 ? p.S * oy * row_bytes + (p.S * ox + c) * 4 : -1;
-      out_off[j] = (uint32_t)(q * 128 + ((c ^ (q & 7)) << 4));
-    }
+    const int q = t, oy = q / p.OW, ox = q - oy * p.OW;
+    const int in0 = q < rows ? p.S * oy * row_bytes + p.S * ox * 4 : -1;
+    const uint32_t ta0 = tmem + ((uint32_t)(warp * 32) << 16) + C1_ACOL;
     tc::mbar_wait(&loaded, 0);
     C1_MARK(2)
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % C1_ST, use = kb / C1_ST;
       if (use > 0) tc::mbar_wait(&empty[s], (use - 1) & 1);
-      const uint32_t a = a_st + s * p.a_bytes, b = b_st + s * C1_B_BYTES;
-      // A: chunk (q, c) = the 4 channel bytes of input pixel (S oy + r, S ox + c)
-      uint32_t v[C1_UNITS];
+      const uint32_t b = b_st + s * C1_B_BYTES;
+      // A row q, filter row kb: the 8 pixels x 4 channel bytes at slab row
+      // S oy + kb, exact integers -> TMEM columns C1_ACOL + 32 s ..
+      float av[C1_BK];
 #pragma unroll
-      for (int j = 0; j < C1_UNITS; ++j)
-        v[j] = in_off[j] >= 0 ? *reinterpret_cast<const uint32_t *>(sl + in_off[j] + kb * row_bytes)
-                              : 0u;
-#pragma unroll
-      for (int j = 0; j < C1_UNITS; ++j)
-        if (in_off[j] >= 0) tc::st_shared_v4(a + out_off[j], c1_bytes(v[j]));
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t v = in0 >= 0 ? *reinterpret_cast<const uint32_t *>(sl + in0 + kb * row_bytes + 4 * c) : 0u;
+        const float4 f = c1_bytes(v);
+        av[4 * c] = f.x;
+        av[4 * c + 1] = f.y;
+        av[4 * c + 2] = f.z;
+        av[4 * c + 3] = f.w;
+      }
+      tc::tmem_st16(ta0 + (uint32_t)(s * C1_BK), av);
+      tc::tmem_st16(ta0 + (uint32_t)(s * C1_BK + 16), av + 16);
       // B: W rows kb*32 .. kb*32+31 transposed: row n (hi), row 32 + n (lo)
       float w[2][4];
 #pragma unroll
@@ -213,7 +214,9 @@ __global__ void __launch_bounds__(C1_THREADS, 2) conv1_tc_kernel(const __grid_co
                          make_float4(tc::tf32_lo(w[h][0]), tc::tf32_lo(w[h][1]),
                                      tc::tf32_lo(w[h][2]), tc::tf32_lo(w[h][3])));
       }
+      tc::tmem_wait_st();
       tc::fence_proxy_async();
+      tc::tc_fence_before();                    // TMEM stores -> the MMA thread
       tc::mbar_arrive(&conv[s]);
     }
   }
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(C1_THREADS, 2) conv1_tc_kernel(const __grid_co
   __syncthreads();
   C1_MARK(4)
   if (warp == 4)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256)
                  : "memory");
 }
 
@@ -304,11 +307,11 @@ int conv1_tc_forward(cudaStream_t st, const dqn_layer_desc &L, const uint8_t *x,
   a.tiles_per_img = L.out_h / gr;
   a.slab_rows = L.sh * (gr - 1) + L.fh;
   const int K = L.fh * L.fw * L.in_c;
-  a.a_bytes = ((gr * L.out_w + 7) / 8) * 8 * 128;
-  if (gr * L.out_w * 8 > C1_UNITS * 128) return DQN_ERR_UNSUPPORTED;
-  const int smem = 1024 + C1_ST * (a.a_bytes + C1_B_BYTES) + K * C1_N * 4 +
+  a.a_bytes = 0;
+  if (gr * L.out_w > 128) return DQN_ERR_UNSUPPORTED;      // one TMEM lane per pixel
+  const int smem = 1024 + C1_ST * C1_B_BYTES + K * C1_N * 4 +
                    ((a.slab_rows * L.in_w * L.in_c + 15) / 16) * 16;
-  if (C1_ST * a.a_bytes < gr * L.out_w * (C1_N + 4) * 4) return DQN_ERR_UNSUPPORTED;  // epilogue stage
+  if (C1_ST * C1_B_BYTES < gr * L.out_w * (C1_N + 4) * 4) return DQN_ERR_UNSUPPORTED;  // epilogue stage
   if (smem > 227 * 1024) return DQN_ERR_UNSUPPORTED;
   static int configured = 0;
   if (smem > configured) {
