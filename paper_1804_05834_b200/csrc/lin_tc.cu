@@ -96,14 +96,14 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
 // dual-pair accuracy.
 template <int NB, bool AT>
 struct LtPlan {
-  static constexpr bool TS = AT;
+  static constexpr bool TS = true;
   static constexpr int RB = 2 * NB;                       // stacked B rows
   static constexpr int A_BYTES = LT_BM * LT_BK * 4;       // one piece of the A tile
   static constexpr int B_BYTES = RB * LT_BK * 4;
   static constexpr int RAW = AT ? A_BYTES : 0;            // A as loaded ([k][m]) when transposed
   static constexpr int A_PIECES = TS ? 1 : 2;
   static constexpr int STAGE = A_PIECES * A_BYTES + B_BYTES + RAW;   // A_hi | (A_lo) | [B_hi ; B_lo] | raw
-  static constexpr int ST = AT ? 4 : LT_ST;
+  static constexpr int ST = AT ? 4 : 6;
   static constexpr int PIPE = ST * STAGE;
   static constexpr int EPI = NB * LT_BM * 4;              // staged partial [NB][128]
   static constexpr int BYTES = (PIPE > EPI ? PIPE : EPI) + 1024;   // + alignment slack
@@ -227,14 +227,23 @@ __global__ void __launch_bounds__(LT_THREADS, 1) lin_tc_kernel(const __grid_cons
         tc::tmem_st16(ta + 16, lo + 16);
         tc::tmem_wait_st();
       } else {
-        // A: 128 x 32 floats, 16-byte chunks at the same offsets in hi and lo
-        for (int i = t; i < LT_BM * LT_BK / 4; i += 128) {
+        // A (W rows by TMA, swizzled K-major): row t's lo pieces to its TMEM lane
+        float lo[LT_BK];
+#pragma unroll
+        for (int c = 0; c < LT_BK / 4; ++c) {
           float4 v;
           asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a_hi(s) + 16 * i));
-          tc::st_shared_v4(a_lo(s) + 16 * i, make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y),
-                                                         tc::tf32_lo(v.z), tc::tf32_lo(v.w)));
+                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                       : "r"(a_hi(s) + (uint32_t)(t * 128 + ((c ^ (t & 7)) << 4))));
+          lo[4 * c] = tc::tf32_lo(v.x);
+          lo[4 * c + 1] = tc::tf32_lo(v.y);
+          lo[4 * c + 2] = tc::tf32_lo(v.z);
+          lo[4 * c + 3] = tc::tf32_lo(v.w);
         }
+        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(PL::LO_COL + s * LT_BK);
+        tc::tmem_st16(ta, lo);
+        tc::tmem_st16(ta + 16, lo + 16);
+        tc::tmem_wait_st();
       }
       // B: hi rows 0..NB-1, lo rows NB..2NB-1 -- the swizzle pattern repeats
       // every 8 rows, so lo is hi's bytes shifted by NB rows
@@ -460,10 +469,12 @@ inline int lt_rows(int nb) { return nb <= 16 ? 16 : (nb <= 32 ? 32 : 64); }
 int g_lt_cl_small = 4, g_lt_cl_big = 16;     // diagnostic overrides
 int g_lt_max_batch = 1 << 20, g_lt_cl_large = 0;   // 0: the fill rule
 int g_ltd_min_batch = 64;                            // dgrad: lin_tc above this batch
+int g_ltd_fill = 128;
 #else
 constexpr int g_lt_cl_small = 4, g_lt_cl_big = 16;
 constexpr int g_lt_max_batch = 1 << 20, g_lt_cl_large = 0;
 constexpr int g_ltd_min_batch = 64;
+constexpr int g_ltd_fill = 128;
 #endif
 
 // hidden linear layer at learner batch sizes (<= 64 rows), weights rows >= 128
@@ -510,8 +521,9 @@ int lin_tc_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, cons
                  const float *mask, float *dx, int batch) {
   if (batch <= g_ltd_min_batch || !lin_tc_ok(L, batch)) return DQN_ERR_UNSUPPORTED;
   const int F = L.in_h * L.in_w * L.in_c, N = L.out_c;
+  const int nb = lt_rows(batch);
   LinTcArgs a{};
-  if (!lt_map(&a.amap, w, N, F, LT_BM) || !lt_map(&a.bmap, dy, N, batch, 64))
+  if (!lt_map(&a.amap, w, N, F, LT_BM) || !lt_map(&a.bmap, dy, N, batch, nb))
     return DQN_ERR_UNSUPPORTED;
   a.M = F;
   a.K = N;
@@ -519,8 +531,8 @@ int lin_tc_dgrad(cudaStream_t st, const dqn_layer_desc &L, const float *dy, cons
   a.mode = 1;
   a.mask = mask;
   a.out = dx;
-  const int ctas = ((F + LT_BM - 1) / LT_BM) * ((batch + 63) / 64);
-  return lt_run<false>(st, a, 64, std::max(1, std::min(16, (128 + ctas - 1) / ctas)),
+  const int ctas = ((F + LT_BM - 1) / LT_BM) * ((batch + nb - 1) / nb);
+  return lt_run<false>(st, a, nb, std::max(1, std::min(16, (g_ltd_fill + ctas - 1) / ctas)),
                        "lin_tc_dgrad");
 }
 
@@ -533,6 +545,7 @@ extern "C" void dqn_lt_set_cluster(int small, int big) {
   dqn::g_lt_cl_big = big;
 }
 extern "C" void dqn_ltd_set_min_batch(int b) { dqn::g_ltd_min_batch = b; }
+extern "C" void dqn_ltd_set_fill(int f) { dqn::g_ltd_fill = f; }
 extern "C" void dqn_lt_set_large(int max_batch, int cl) {
   dqn::g_lt_max_batch = max_batch;
   dqn::g_lt_cl_large = cl;

@@ -56,6 +56,13 @@ def main():
         _set("dqn_ct_set_fill_small", 64)
         _set("dqn_ct_set_ts", 3)
         _set("dqn_ct_set_dts", 3)
+        _set("dqn_ltd_set_min_batch", 64)
+        _set("dqn_ltd_set_fill", 128)
+        if v.startswith("ltdmin="):            # fc1 dgrad on lin_tc above this batch[/fill]
+            mb_, _, fl_ = v[7:].partition("/")
+            _set("dqn_ltd_set_min_batch", int(mb_))
+            _set("dqn_ltd_set_fill", int(fl_ or 128))
+            v = "0"
         if v.startswith("dts="):               # conv_tc dgrad with A lo in TMEM, stages
             _set("dqn_ct_set_dts", int(v[4:]))
             v = "0"
