@@ -89,7 +89,7 @@ class ClockSampler:
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -118,11 +118,17 @@ class ClockSampler:
         rows = [r for r in self.samples if len(r) >= 6 and r[0].replace(".", "").isdigit()]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = sorted(float(r[0]) for r in rows)
+        # the median under load: samples with the GPU busy (an idle GPU drops its
+        # clocks; host-side setup inside a sampled region would otherwise pull the
+        # median down)
+        busy = [r for r in rows if len(r) >= 7 and r[6].replace(".", "").isdigit()
+                and float(r[6]) > 0]
+        use = busy or rows
+        sm = sorted(float(r[0]) for r in use)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in use for i in range(4) if r[2 + i].lower() == "active"})
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(use), "idle_samples": len(rows) - len(busy) if busy else 0}
 
 
 # --------------------------------------------------------------------------
