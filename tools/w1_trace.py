@@ -6,7 +6,7 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-os.environ["DQN_B200_LIB"] = str(ROOT / "paper_1804_05834_b200" / "libdqn_b200_trace.so")
+os.environ.setdefault("DQN_B200_LIB", str(ROOT / "paper_1804_05834_b200" / "libdqn_b200_trace.so"))
 sys.path.insert(0, str(ROOT))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -39,11 +39,14 @@ for skip in [int(v) for v in (sys.argv[1:] or ['0'])]:
       print(f"batch {batch}: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us per launch (back to back)")
       _lib.call("dqn_net_layer", *args)
       torch.cuda.synchronize()
-      buf = (C.c_ulonglong * (256 * 8))()
+      buf = (C.c_ulonglong * (256 * 12))()
       _lib.lib.dqn_w1_trace(buf)
-      t = np.frombuffer(buf, dtype=np.uint64).reshape(256, 8)[:batch].astype(np.int64)
+      t = np.frombuffer(buf, dtype=np.uint64).reshape(256, 12).astype(np.int64)
+      t = t[t[:, 0] > 0]
       t0 = t[:, 0].min()
-      names = ["entry", "pdl", "Bbuilt", "img", "mma", "epi", "clred", "ticket"]
+      print(f"  {len(t)} CTAs")
+      names = ["entry", "pdl", "Bbuilt", "img", "mma", "epi", "clred", "ticket", "final", "issue0", "issue1"]
       for i, n in enumerate(names):
-          v = (t[:, i] - t0) / 1e3
-          print(f"  {n:7s} mean {v.mean():6.2f} max {v.max():6.2f} us")
+          sel = t[:, i] >= t0
+          v = (t[sel, i] - t0) / 1e3
+          print(f"  {n:7s} mean {v.mean():6.2f} max {v.max():6.2f} us  ({sel.sum()} CTAs)")
