@@ -192,10 +192,9 @@ __global__ void __launch_bounds__(512 * MT, 1) conv1_wgrad_u8_kernel(const __gri
   for (int unit = blockIdx.x; unit < a.units; unit += gridDim.x, ++it) {
     const int img = unit / a.PS, pbase = (unit % a.PS) * a.PP;
     const int len = min(a.PP, a.P - pbase), len8 = (len + 7) & ~7, ngroups = len / 4;
-    if (it > 0) {                            // the last unit's MMAs read B / A
-      if (warp == 0) tc::mbar_wait(&done, (it - 1) & 1);
-      __syncthreads();
-    }
+    // (the last unit's A build is done -- its CTA barrier -- so gbase and the
+    // image buffer are free; its MMAs may still read B and A: waited for
+    // below, after this unit's dY loads are in flight)
     // pixels come in groups of 4 consecutive output columns (OW % 4 == 0):
     // group gg starts at output pixel pbase + 4 gg, its pixels SWC bytes apart
     for (int gg = t; gg < ngroups; gg += T) {
@@ -230,6 +229,7 @@ __global__ void __launch_bounds__(512 * MT, 1) conv1_wgrad_u8_kernel(const __gri
             v[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
+        if (it > 0 && u == t) tc::mbar_wait(&done, (it - 1) & 1);   // the last unit's MMAs
         // channel 4q + i over pixels p0..p0+3; lanes rotate i so one store
         // instruction of the warp covers all 8 rows of a core matrix
         const int rot = pq & 3;
@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(512 * MT, 1) conv1_wgrad_u8_kernel(const __gri
           bs[i] = __fadd_rn(bs[i], __fadd_rn(__fadd_rn(c.x, c.y), __fadd_rn(c.z, c.w)));
         }
       }
+      if (it > 0 && t >= nu) tc::mbar_wait(&done, (it - 1) & 1);
     }
     tc::fence_proxy_async();                 // B (generic stores) -> tensor-core reads
     __syncthreads();                         // gbase of this unit visible to every thread
@@ -550,10 +551,11 @@ int g_w1_cl_max = 8;   // diagnostic: largest cluster
 constexpr int g_w1_cl_max = 8;
 #endif
 
-// one CTA per unit up to 64 CTAs (Atari batch 32; the rest of the SMs stay
-// free for the concurrent wgrads); larger batches loop over units inside the
-// CTA, so the reduction stays <= 64 partials
-inline int w1_cpm(int units) { return std::min(units, 64); }
+// one CTA per unit up to 64 units (Atari batch 32 in the learner: the rest of
+// the SMs stay free for the concurrent wgrads); larger batches loop over units
+// inside up to 144 CTAs (clusters of 8 on 148 SMs), so the reduction stays
+// <= 144 partials
+inline int w1_cpm(int units) { return units <= 64 ? units : std::min(units, 144); }
 
 int64_t conv1_wgrad_u8_scratch(const dqn_net_desc *net, int batch) {
   const dqn_layer_desc &L = net->layer[0];
