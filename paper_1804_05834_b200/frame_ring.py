@@ -141,6 +141,10 @@ class FrameDedupMemory(ReplayMemory):
         self.cursor = 0
         self.size = 0
         self._size_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+        # persistent pinned staging for batched plane uploads, reused once the
+        # event recorded after its last copy has completed
+        self._stage = torch.empty((0, self.frame_bytes), dtype=torch.uint8).pin_memory()
+        self._stage_ev = None
         self._scratch = {}
 
     @property
@@ -224,12 +228,18 @@ class FrameDedupMemory(ReplayMemory):
         if new_ids:
             last = {fid: i for i, fid in enumerate(new_ids)}
             keep = sorted(last.values())
-            buf = torch.empty((len(keep), self.frame_bytes), dtype=torch.uint8).pin_memory()
+            if self._stage_ev is not None:
+                self._stage_ev.synchronize()          # the last upload has read the stage
+            if self._stage.shape[0] < len(keep):
+                self._stage = torch.empty((max(len(keep), 2 * self._stage.shape[0]), self.frame_bytes),
+                                          dtype=torch.uint8).pin_memory()
+            buf = self._stage[:len(keep)]
             buf.numpy()[:] = np.frombuffer(b"".join(new_planes[i] for i in keep),
                                            dtype=np.uint8).reshape(len(keep), self.frame_bytes)
             ids_t = torch.as_tensor([new_ids[i] for i in keep], dtype=torch.int64, device="cuda")
-            # (torch's pinned-host allocator keeps buf alive until the copy ran)
             self.frames.index_copy_(0, ids_t, buf.to("cuda", non_blocking=True))
+            self._stage_ev = torch.cuda.Event()
+            self._stage_ev.record()
         # a batch longer than the ring keeps its last `capacity` transitions
         # (scatters with repeated slots would leave an unspecified winner)
         m = min(n, self.capacity)
