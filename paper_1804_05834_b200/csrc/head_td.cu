@@ -55,6 +55,33 @@ struct HeadTdArgs {
 // captured graph's form is fixed by its caller, not by the environment
 inline bool head_two_phase(int td_flags) { return !(td_flags & DQN_TD_HEAD_LAST_CTA); }
 
+// Head weight-gradient epilogue: grads[f][o] += s[o] for the NO outputs of
+// feature f (f == F: the bias row).  Every old value is read before the first
+// write: a read-add-write per output would chain NO L2 round trips.
+template <int NA>
+__device__ __forceinline__ void head_acc_grads(const HeadTdArgs &p, int f, const float (&s)[NA + 1]) {
+  constexpr int NO = NA + 1;
+  const int F = p.F, no = p.dueling ? NO : NA;
+  float *gp[NO];
+  float old[NO];
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+    if (p.dueling)
+      gp[o] = o == 0 ? (f < F ? &p.gwv[f] : &p.gbv[0])
+                     : (f < F ? &p.gwa[(int64_t)f * NA + o - 1] : &p.gba[o - 1]);
+    else
+      gp[o] = f < F ? &p.gwa[(int64_t)f * NA + o] : &p.gba[o];
+    old[o] = o < no ? *gp[o] : 0.f;
+  }
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+    if (o >= no) break;
+    const float v = __fadd_rn(old[o], s[o]);
+    *gp[o] = v;
+    note_grad(p.flags, v);
+  }
+}
+
 // K1: Q heads of both networks (one warp per row: lane-strided fmaf chains,
 // fixed shuffle tree read from lane 0), then -- in the last CTA to finish --
 // the TD block (td_loss_kernel's per-row arithmetic and 256-slot statistics
@@ -208,22 +235,7 @@ __global__ void __launch_bounds__(kHeadCta) head_bwd_wgrad_kernel(const HeadTdAr
     for (int o = 0; o < NO; ++o)
       if (o < no) acc[o] = fmaf(xv, gs[o], acc[o]);
   }
-#pragma unroll
-  for (int o = 0; o < NO; ++o) {
-    if (o >= no) break;
-    const float s = acc[o];
-    if (p.dueling) {
-      if (o == 0) {
-        if (f < F) acc_grad(&p.gwv[f], s, p.flags); else acc_grad(&p.gbv[0], s, p.flags);
-      } else {
-        if (f < F) acc_grad(&p.gwa[(int64_t)f * NA + o - 1], s, p.flags);
-        else acc_grad(&p.gba[o - 1], s, p.flags);
-      }
-    } else {
-      if (f < F) acc_grad(&p.gwa[(int64_t)f * NA + o], s, p.flags);
-      else acc_grad(&p.gba[o], s, p.flags);
-    }
-  }
+  head_acc_grads<NA>(p, f, acc);
 }
 
 // ---- two-phase form for learner batches (k * (nA + 1) <= kGsMax) ----------
@@ -417,21 +429,10 @@ __global__ void __launch_bounds__(kHeadCta) head_td_bwd_kernel(const HeadTdArgs 
   if (rg != 0 || f > F) return;
 #pragma unroll
   for (int o = 0; o < NO; ++o) {
-    if (o >= no) break;
-    float s = s_w[0][fl][o];
-    for (int g = 1; g < kHeadCta / 32; ++g) s = __fadd_rn(s, s_w[g][fl][o]);
-    if (p.dueling) {
-      if (o == 0) {
-        if (f < F) acc_grad(&p.gwv[f], s, p.flags); else acc_grad(&p.gbv[0], s, p.flags);
-      } else {
-        if (f < F) acc_grad(&p.gwa[(int64_t)f * NA + o - 1], s, p.flags);
-        else acc_grad(&p.gba[o - 1], s, p.flags);
-      }
-    } else {
-      if (f < F) acc_grad(&p.gwa[(int64_t)f * NA + o], s, p.flags);
-      else acc_grad(&p.gba[o], s, p.flags);
-    }
+    acc[o] = s_w[0][fl][o];
+    for (int g = 1; g < kHeadCta / 32; ++g) acc[o] = __fadd_rn(acc[o], s_w[g][fl][o]);
   }
+  head_acc_grads<NA>(p, f, acc);
 }
 
 template <int NA>
