@@ -257,15 +257,20 @@ sample_gather_kernel(const double *__restrict__ nodes, int depth, const int64_t 
                             __dmul_rn(__dadd_rn((double)j, u[j]), __ddiv_rn(total, (double)k)),
                             nextafter(total, 0.0));
     if (threadIdx.x == 0) s_slot = i;
-    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.z == 0) {
-      if (out_a) out_a[j] = actions[i];
-      if (out_r) out_r[j] = rewards[i];
-      if (out_t) out_t[j] = terminals[i];
-    }
   }
   __syncthreads();
   const int64_t slot = s_slot;
   const int which = blockIdx.z;
+  // the transition's metadata, by another thread than the one moving the
+  // frame (and after it is started): three reads in flight, then the writes
+  if (threadIdx.x == 1 && blockIdx.x == 0 && blockIdx.z == 0) {
+    const int64_t av = out_a ? actions[slot] : 0;
+    const double rv = out_r ? rewards[slot] : 0.0;
+    const uint8_t tv = out_t ? terminals[slot] : 0;
+    if (out_a) out_a[j] = av;
+    if (out_r) out_r[j] = rv;
+    if (out_t) out_t[j] = tv;
+  }
   if constexpr (TMA) {             // one CTA per frame: the TMA engine moves the slot
     extern __shared__ __align__(128) uint8_t slot_buf[];
     __shared__ uint64_t bar;
