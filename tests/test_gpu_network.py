@@ -186,12 +186,14 @@ def test_small_batch_forward_matches_batched():
     assert out.returncode == 0 and out.stdout.startswith("OK"), out.stdout + out.stderr
 
 
-@pytest.mark.parametrize("batch", [1, 6, 12, 32, 64])
+@pytest.mark.parametrize("batch", [1, 6, 12, 32, 64, 130, 300])
 def test_conv1_wgrad_from_frames(P, batch):
     """conv1's weight gradient straight from the uint8 frames (csrc/wgrad_u8.cu:
-    one CTA per image, cluster + ticketed cross-cluster reduction) against the
-    oracle at batch sizes that give 1, 2, 4 and 8-image clusters; a second
-    accumulation doubles it and two runs are bit-identical (layers.py:250-255)."""
+    one CTA per half image up to 64, then up to 144 CTAs looping over units;
+    cluster push + ticketed cross-cluster reduction) against the oracle at batch
+    sizes that give 1, 2, 4 and 8-CTA clusters, one and several units per CTA
+    (130: uneven); a second accumulation doubles it and two runs are
+    bit-identical (layers.py:250-255)."""
     from paper_1804_05834_b200 import synth
     on, ref = _pair(P, "atari", (84, 84, 4), 4, True, seed=3)
     x8 = synth.frames(9, 0, np.arange(batch))
