@@ -26,7 +26,7 @@
 //     address in registers (the issue loop, ~100 cycles per MMA, is the
 //     kernel's longest phase);
 //   * partials are reduced deterministically: each CTA sends the rows of its
-//     partial that rank k of its 8-CTA cluster owns straight from TMEM
+//     partial that rank k of its (4-CTA) cluster owns straight from TMEM
 //     registers into that rank's shared memory (st.async, counted on the
 //     owner's mbarrier: no cluster barrier around the exchange); the owner
 //     adds them in rank order and writes the cluster partial to global
@@ -545,10 +545,13 @@ bool conv1_wgrad_u8_ok(const dqn_net_desc *net) {
   return w1_smem(L, PP, img_smem, tail_off, tail_bytes, recv_off) <= 200 * 1024;
 }
 
+// largest cluster: 4 (product A/B in the learner, r02g kernel: 8,022 vs 7,987
+// with 8, 7,826 with 2 -- four-CTA clusters leave the concurrent conv2 wgrad's
+// clusters room in the GPCs)
 #ifdef DQN_TC_TRACE
-int g_w1_cl_max = 8;   // diagnostic: largest cluster
+int g_w1_cl_max = 4;   // diagnostic: largest cluster
 #else
-constexpr int g_w1_cl_max = 8;
+constexpr int g_w1_cl_max = 4;
 #endif
 
 // one CTA per unit up to 64 units (Atari batch 32 in the learner: the rest of
@@ -588,7 +591,7 @@ int conv1_wgrad_u8_tc(cudaStream_t st, const dqn_net_desc *net, const uint8_t *x
   a.units = batch * a.PS;
   a.cpm = w1_cpm(a.units);
   a.cl = 1;
-  for (int c : {8, 4, 2})                   // 8-CTA clusters measured best (vs 1, 2, 4)
+  for (int c : {8, 4, 2})                   // up to g_w1_cl_max
     if (c <= g_w1_cl_max && a.cpm % c == 0) { a.cl = c; break; }
   a.ncl = a.cpm / a.cl;
   int smem = w1_smem(L, a.PP, a.img_smem, a.tail_off, a.tail_bytes, a.recv_off);

@@ -47,7 +47,7 @@ def main():
         _set("dqn_c1_set", 1)
         _set("dqn_lt_set_cluster", 4, 16)
         _set("dqn_tc_set_cluster_splitk", 1)
-        _set("dqn_w1_set_cluster_max", 8)
+        _set("dqn_w1_set_cluster_max", 4)
         _set("dqn_tc_set_dgrad_cap", 16)
         _set("dqn_tc_set_wgrad_cap", 8)
         if v.startswith("wcap="):              # fp32 conv wgrad split cap
