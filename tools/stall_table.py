@@ -17,6 +17,7 @@ lines = out.splitlines()
 name = lines[0].split(",", 1)[1].strip().strip('",')
 rows = list(csv.DictReader(io.StringIO("\n".join(lines[1:]))))
 key = "Warp Stall Sampling (All Samples)"
+rows = [r for r in rows if (r.get(key) or "0").isdigit()]   # repeated header lines
 tot = sum(int(r[key] or 0) for r in rows)
 rows.sort(key=lambda r: -int(r[key] or 0))
 L = [f"# {title}", "", f"Kernel `{name}`, {tot} stall samples (ncu source page, SASS).", "",
