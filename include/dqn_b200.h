@@ -351,7 +351,9 @@ int dqn_ring_store(void *stream, uint8_t *states, uint8_t *next_states, int64_t 
  * next states, metadata) in ONE launch: each gather CTA descends its own
  * query, one extra CTA row computes the batch-normalised IS weights.  Same
  * results as the two calls (replay.py:104-115, 215-230); 16-byte aligned
- * frames (slot_bytes % 16 == 0). */
+ * frames (slot_bytes % 16 == 0).  prob == weight == NULL: no weights row --
+ * the gather CTAs write idx, and the caller computes prob / weight with
+ * dqn_tree_sample (same indices), e.g. on another stream beside the trunk. */
 int dqn_sample_gather(void *stream, const double *nodes, int32_t depth, const int64_t *size,
                       const double *u, int32_t k, const double *beta, int64_t *idx,
                       double *prob, double *weight, int32_t *flags, const uint8_t *states,

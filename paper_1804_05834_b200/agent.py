@@ -118,6 +118,8 @@ class _StepPlan:
         self.r = torch.empty(k, dtype=torch.float64, device=dev)
         self.t = torch.empty(k, dtype=torch.bool, device=dev)
         self.idx = torch.empty(k, dtype=torch.int64, device=dev)
+        self.idx_w = torch.empty(k, dtype=torch.int64, device=dev)   # the weights launch's copy
+        self._e_weights = None
         self.prob = torch.empty(k, dtype=torch.float64, device=dev)
         self.w = torch.ones(k, dtype=torch.float64, device=dev)
         # inputs: u[k] + beta (PER) | indices[k] (uniform); pinned staging
@@ -197,7 +199,7 @@ class _StepPlan:
             if hasattr(ring, "sample_gather_fused"):       # frame-deduplicated ring
                 ring.sample_gather_fused(tree, src, k, src[k:], self.idx, self.prob, self.w,
                                          self.flags, self.x, self.x[k:], self.a, self.r, self.t)
-            else:
+            elif not WEIGHTS_BESIDE:
                 _lib.call("dqn_sample_gather", st, tree.nodes.data_ptr(), tree.depth,
                           ring._size_dev.data_ptr(), src.data_ptr(), k,
                           src[k:].data_ptr(), self.idx.data_ptr(), self.prob.data_ptr(),
@@ -206,6 +208,29 @@ class _StepPlan:
                           ring.rewards.data_ptr(), ring.terminals.data_ptr(), self.x.data_ptr(),
                           self.x[k:].data_ptr(), self.a.data_ptr(), self.r.data_ptr(),
                           self.t.data_ptr())
+            else:
+                # the IS weights (a batch-wide max) by their own launch on the
+                # tree stream once the gather is done, beside the trunk: only
+                # the head reads them, and as the fused launch's extra CTA row
+                # they held up conv1
+                _lib.call("dqn_sample_gather", st, tree.nodes.data_ptr(), tree.depth,
+                          ring._size_dev.data_ptr(), src.data_ptr(), k,
+                          src[k:].data_ptr(), self.idx.data_ptr(), None, None,
+                          self.flags.data_ptr(), ring.states.data_ptr(),
+                          ring.next_states.data_ptr(), ring.slot_bytes, ring.actions.data_ptr(),
+                          ring.rewards.data_ptr(), ring.terminals.data_ptr(), self.x.data_ptr(),
+                          self.x[k:].data_ptr(), self.a.data_ptr(), self.r.data_ptr(),
+                          self.t.data_ptr())
+                e_fork = torch.cuda.Event()
+                e_fork.record(torch.cuda.current_stream())
+                with torch.cuda.stream(self.tree_stream):
+                    self.tree_stream.wait_event(e_fork)
+                    _lib.call("dqn_tree_sample", _lib.stream_ptr(), tree.nodes.data_ptr(),
+                              tree.depth, ring._size_dev.data_ptr(), src.data_ptr(), k,
+                              src[k:].data_ptr(), self.idx_w.data_ptr(), self.prob.data_ptr(),
+                              self.w.data_ptr(), self.flags.data_ptr())
+                    self._e_weights = torch.cuda.Event()
+                    self._e_weights.record(self.tree_stream)
         else:
             idx = self.idx
             if self.per:
@@ -267,6 +292,9 @@ class _StepPlan:
             v.x = self.x[:k]
             v.struct.x = self.x.data_ptr()
             v.struct.dx = None                     # conv1 dX is never needed
+        if self._e_weights is not None:           # the IS weights' launch (enqueue)
+            s0.wait_event(self._e_weights)
+            self._e_weights = None
         if self.fused_head:
             # both Q heads + targets/TD/loss + head dX + head wgrad in one launch
             _lib.call("dqn_head_td", st, C.byref(on.desc_for(self.x)), on.flat_values.data_ptr(),
@@ -352,6 +380,7 @@ USE_GRAPH = os.environ.get("DQN_B200_GRAPH", "1") != "0"
 FUSED_HEAD = True       # Q heads + TD block + head backward/wgrad in dqn_head_td
 HEAD_TWO_PHASE = True   # its two-phase form (else the last-CTA-ticket form)
 FUSED_SAMPLE = True     # sum-tree descent + frame gather in one launch
+WEIGHTS_BESIDE = True   # its IS weights by a separate launch on the tree stream
 _GRAPH_LAUNCH = _lib.lib.dqn_graph_launch
 
 

@@ -257,6 +257,10 @@ sample_gather_kernel(const double *__restrict__ nodes, int depth, const int64_t 
                             __dmul_rn(__dadd_rn((double)j, u[j]), __ddiv_rn(total, (double)k)),
                             nextafter(total, 0.0));
     if (threadIdx.x == 0) s_slot = i;
+    // without a weights CTA (weight == nullptr: the IS weights come from a
+    // separate dqn_tree_sample launch off the critical path) the gather CTAs
+    // record the sampled slots themselves
+    if (weight == nullptr && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.z == 0) idx[j] = i;
   }
   __syncthreads();
   const int64_t slot = s_slot;
@@ -909,15 +913,17 @@ extern "C" int dqn_sample_gather(void *stream, const double *nodes, int32_t dept
                                  const uint8_t *terminals, uint8_t *out_states,
                                  uint8_t *out_next_states, int64_t *out_actions,
                                  double *out_rewards, uint8_t *out_terminals) {
-  DQN_CHECK_ARG(nodes && size && u && beta && idx && prob && weight && k >= 1 && depth >= 1 &&
+  DQN_CHECK_ARG(nodes && size && u && beta && idx && (prob == nullptr) == (weight == nullptr) &&
+                    k >= 1 && depth >= 1 &&
                     depth < 40 && states && next_states && out_states && out_next_states &&
                     slot_bytes > 0 && slot_bytes % 16 == 0 && (uintptr_t)states % 16 == 0 &&
                     (uintptr_t)next_states % 16 == 0 && (uintptr_t)out_states % 16 == 0 &&
                     (uintptr_t)out_next_states % 16 == 0 && k < 65535,
                 "sample_gather: bad args (16-byte aligned frames)");
   const int64_t vecs = slot_bytes / 16;
+  const unsigned rows = (unsigned)k + (weight ? 1u : 0u);   // + the weights CTA row
   if (slot_bytes <= 48 * 1024 && tma_gather_enabled()) {
-    launch_k(sample_gather_kernel<true>, dim3(1, (unsigned)k + 1, 2), 32, (size_t)slot_bytes,
+    launch_k(sample_gather_kernel<true>, dim3(1, rows, 2), 32, (size_t)slot_bytes,
              as_stream(stream), nodes, depth, size, u, k, beta, idx, prob, weight, flags,
              reinterpret_cast<const int4 *>(states), reinterpret_cast<const int4 *>(next_states),
              vecs, reinterpret_cast<int4 *>(out_states), reinterpret_cast<int4 *>(out_next_states),
@@ -925,7 +931,7 @@ extern "C" int dqn_sample_gather(void *stream, const double *nodes, int32_t dept
     DQN_LAUNCH_CHECK("sample_gather_tma");
     return DQN_OK;
   }
-  dim3 grid((unsigned)((vecs + kGatherChunk - 1) / kGatherChunk), (unsigned)k + 1, 2);
+  dim3 grid((unsigned)((vecs + kGatherChunk - 1) / kGatherChunk), rows, 2);
   launch_k(sample_gather_kernel<false>, grid, kGatherThreads, 0, as_stream(stream), nodes, depth, size,
            u, k, beta, idx, prob, weight, flags, reinterpret_cast<const int4 *>(states),
            reinterpret_cast<const int4 *>(next_states), vecs,

@@ -50,6 +50,10 @@ def main():
         _set("dqn_w1_set_cluster_max", 4)
         _set("dqn_tc_set_dgrad_cap", 16)
         _set("dqn_tc_set_wgrad_cap", 8)
+        agent.WEIGHTS_BESIDE = True
+        if v == "w8fused":                     # IS weights as the fused sample launch's extra CTA row
+            agent.WEIGHTS_BESIDE = False
+            v = "0"
         if v.startswith("wcap="):              # fp32 conv wgrad split cap
             _set("dqn_tc_set_wgrad_cap", int(v[5:]))
             v = "0"
