@@ -113,6 +113,7 @@ def val(r, n):
 # eager launch order of one cfg4 update (agent._StepPlan.enqueue); the name
 # fragment checks the label against the captured kernel
 labels = [("sample+gather (batch 32)", "sample_gather"),
+          ("IS weights (batch 32, tree stream)", "tree_sample"),
           ("conv1.fwd (batch 32, target)", ("conv1_tc", "FwdPol<unsigned char")),
           ("conv2.fwd (batch 32, target)", ("conv_tc_kernel<64, 3, 0", "conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
           ("conv3.fwd (batch 32, target)", ("conv_tc_kernel<64, 3, 0", "conv_tc_kernel<64, 2, 0>", "FwdPol<float")),
