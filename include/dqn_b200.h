@@ -234,7 +234,8 @@ int dqn_frame_gather(void *stream, const uint8_t *frames, int64_t frame_bytes,
  * launch (replay.py:104-115, 215-230): as dqn_sample_gather (stratified
  * descent per gather CTA, IS-weight CTA row), the stacks assembled from the
  * frame pool as dqn_frame_gather does.  Identical to dqn_tree_sample
- * followed by dqn_frame_gather. */
+ * followed by dqn_frame_gather.  prob == weight == NULL: no weights row, as
+ * for dqn_sample_gather. */
 int dqn_frame_sample_gather(void *stream, const double *nodes, int32_t depth, const int64_t *size,
                             const double *u, int32_t k, const double *beta, int64_t *idx,
                             double *prob, double *weight, int32_t *flags, const uint8_t *frames,

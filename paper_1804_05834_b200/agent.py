@@ -176,6 +176,22 @@ class _StepPlan:
         self.d2h_bytes = (3 * k + 2) * 8 + 4
 
     # -- the device pipeline ----------------------------------------------
+    def _weights_beside(self, tree, ring, src, k: int) -> None:
+        """prob / IS weights of this batch (dqn_tree_sample: the same
+        descents as the gather's) on the tree stream once the gather is
+        enqueued; the head waits for them (enqueue_learn)."""
+        torch = _lib.require_cuda()
+        e_fork = torch.cuda.Event()
+        e_fork.record(torch.cuda.current_stream())
+        with torch.cuda.stream(self.tree_stream):
+            self.tree_stream.wait_event(e_fork)
+            _lib.call("dqn_tree_sample", _lib.stream_ptr(), tree.nodes.data_ptr(), tree.depth,
+                      ring._size_dev.data_ptr(), src.data_ptr(), k, src[k:].data_ptr(),
+                      self.idx_w.data_ptr(), self.prob.data_ptr(), self.w.data_ptr(),
+                      self.flags.data_ptr())
+            self._e_weights = torch.cuda.Event()
+            self._e_weights.record(self.tree_stream)
+
     def enqueue(self, io: bool = True) -> None:
         """Enqueue one update; ``io`` adds the pinned host copies of the
         draws (in) and TdResult + flags (out)."""
@@ -189,16 +205,22 @@ class _StepPlan:
               and (self.fused_sample or not self.per))
         self._host_out = self.h_out if zc else None
         if self.per and self.fused_sample:
-            # descent + IS weights + frame gather in one launch, reading the
-            # draws where they are (pinned host buffer, or a device slot)
+            # descent + frame gather in one launch (the IS weights beside it:
+            # WEIGHTS_BESIDE), reading the draws where they are (pinned host
+            # buffer, or a device slot)
             src = self.h_in
             if not zc and src.device.type == "cpu":
                 self.d_in.copy_(self.h_in, non_blocking=True)
                 src = self.d_in
             tree = self.memory.tree
             if hasattr(ring, "sample_gather_fused"):       # frame-deduplicated ring
-                ring.sample_gather_fused(tree, src, k, src[k:], self.idx, self.prob, self.w,
+                beside = WEIGHTS_BESIDE
+                ring.sample_gather_fused(tree, src, k, src[k:], self.idx,
+                                         None if beside else self.prob,
+                                         None if beside else self.w,
                                          self.flags, self.x, self.x[k:], self.a, self.r, self.t)
+                if beside:
+                    self._weights_beside(tree, ring, src, k)
             elif not WEIGHTS_BESIDE:
                 _lib.call("dqn_sample_gather", st, tree.nodes.data_ptr(), tree.depth,
                           ring._size_dev.data_ptr(), src.data_ptr(), k,
@@ -221,16 +243,7 @@ class _StepPlan:
                           ring.rewards.data_ptr(), ring.terminals.data_ptr(), self.x.data_ptr(),
                           self.x[k:].data_ptr(), self.a.data_ptr(), self.r.data_ptr(),
                           self.t.data_ptr())
-                e_fork = torch.cuda.Event()
-                e_fork.record(torch.cuda.current_stream())
-                with torch.cuda.stream(self.tree_stream):
-                    self.tree_stream.wait_event(e_fork)
-                    _lib.call("dqn_tree_sample", _lib.stream_ptr(), tree.nodes.data_ptr(),
-                              tree.depth, ring._size_dev.data_ptr(), src.data_ptr(), k,
-                              src[k:].data_ptr(), self.idx_w.data_ptr(), self.prob.data_ptr(),
-                              self.w.data_ptr(), self.flags.data_ptr())
-                    self._e_weights = torch.cuda.Event()
-                    self._e_weights.record(self.tree_stream)
+                self._weights_beside(tree, ring, src, k)
         else:
             idx = self.idx
             if self.per:

@@ -142,7 +142,8 @@ frame_gather_kernel(const uint8_t *__restrict__ frames, int64_t frame_bytes,
 // PER batch from the deduplicated ring; replay.py:104-115, 215-230): CTA
 // j descends query j with one warp (eight levels per round trip) and
 // assembles both stacks of that slot and its metadata; the extra CTA j = k
-// computes idx / P / normalised IS weights.
+// computes idx / P / normalised IS weights (prob == weight == nullptr: no
+// extra CTA, the gather CTAs write idx; the caller runs dqn_tree_sample).
 // Same results as dqn_tree_sample followed by dqn_frame_gather.
 __global__ void __launch_bounds__(kFgThreads)
 frame_sample_gather_kernel(const double *nodes, int depth, const int64_t *size_p, const double *u,
@@ -176,6 +177,7 @@ frame_sample_gather_kernel(const double *nodes, int depth, const int64_t *size_p
                             nextafter(total, 0.0));
     if (threadIdx.x == 0) {
       s_slot = i;
+      if (weight == nullptr) idx[j] = i;   // no weights CTA: the caller's dqn_tree_sample has them
       if (out_a) out_a[j] = actions[i];
       if (out_r) out_r[j] = rewards[i];
       if (out_t) out_t[j] = terms[i];
@@ -243,7 +245,8 @@ extern "C" int dqn_frame_sample_gather(void *stream, const double *nodes, int32_
                                        const bool *terminals, uint8_t *out_states,
                                        uint8_t *out_next_states, int64_t *out_actions,
                                        double *out_rewards, bool *out_terminals) {
-  DQN_CHECK_ARG(nodes && size && u && beta && idx && prob && weight && frames && ids &&
+  DQN_CHECK_ARG(nodes && size && u && beta && idx && (prob == nullptr) == (weight == nullptr) &&
+                    frames && ids &&
                     out_states && out_next_states && k >= 1 && k < 65535 && depth >= 1 &&
                     frame_bytes > 0 && stack >= 1 && stack <= 16,
                 "frame_sample_gather: bad args");
@@ -254,7 +257,7 @@ extern "C" int dqn_frame_sample_gather(void *stream, const double *nodes, int32_
   const size_t smem = fg_smem_bytes(frame_bytes, stack);
   if (smem > 48 * 1024 && !fg_configure((const void *)frame_sample_gather_kernel, smem))
     return DQN_ERR_CUDA;
-  launch_k(frame_sample_gather_kernel, dim3(k + 1), kFgThreads, smem, as_stream(stream), nodes,
+  launch_k(frame_sample_gather_kernel, dim3(k + (weight ? 1 : 0)), kFgThreads, smem, as_stream(stream), nodes,
            depth, size, u, k, beta, idx, prob, weight, flags, frames, frame_bytes, ids, stack,
            actions, rewards, terminals, out_states, out_next_states, out_actions, out_rewards,
            out_terminals);
