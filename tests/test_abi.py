@@ -83,3 +83,23 @@ def test_header_constants_match_the_binding():
     assert "DQN_NET_HINT_SIDE" in defines and len(pairs) >= 4, sorted(pairs)
     for k, v in pairs.items():
         assert defines[k] == v, (k, defines[k], v)
+
+
+def test_sample_gather_weights_pointers_both_or_neither():
+    """dqn_sample_gather / dqn_frame_sample_gather: prob and weight are both
+    given (the launch's IS-weights row) or both NULL (the caller computes them
+    with dqn_tree_sample); one without the other is an argument error, found
+    before any device work."""
+    from paper_1804_05834_b200 import _lib
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    p = ctypes.c_void_p(16)                       # never dereferenced: the check comes first
+    sg = lib.dqn_sample_gather
+    sg.restype = ctypes.c_int
+    args = [None, p, ctypes.c_int(20), p, p, ctypes.c_int(32), p, p, p, None, p, p, p,
+            ctypes.c_int64(28224), p, p, p, p, p, p, p, p]
+    assert sg(*args) == 1                         # DQN_ERR_INVALID_ARG (weight NULL, prob not)
+    fg = lib.dqn_frame_sample_gather
+    fg.restype = ctypes.c_int
+    args = [None, p, ctypes.c_int(20), p, p, ctypes.c_int(32), p, p, None, p, p, p,
+            ctypes.c_int64(7056), p, ctypes.c_int(4), p, p, p, p, p, p, p, p]
+    assert fg(*args) == 1                         # prob NULL, weight not
